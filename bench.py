@@ -1,0 +1,324 @@
+#!/usr/bin/env python
+"""Benchmark of the GPU fluid step (BASELINE.json configs 2 and 4).
+
+One step = one D3Q19 SRT fluid time step over the GPU's 512^3 block (fp64), exactly the
+fluid phases of Simulation::step (sim.cpp:689-703) with coupling off:
+  N = 1: periodic ghost fill (K6, pull slots) -> fused pull stream-collide (K1) -> swap
+  N > 1: z-slab of a 512 x 512 x 512N periodic domain per GPU; x/y wrap (K6) ->
+         halo pack + NCCL send/recv on the comm stream (K7) || inner sweep k in [1,n-1) ->
+         unpack -> outer sweep (k = 0, n-1) -> swap     (weak scaling, config 4)
+Inputs: the validation.cpp:46-63 shear wave at tau = 0.8, initialised on the device.
+
+`value` is MLUPS over all GPUs (cells * steps / max-over-ranks device time). `roofline`
+uses 304 algorithmic bytes per lattice update (19 f64 pulled + 19 stored) and the sweep's
+CUDA-event time measured in the timed region. `e2e` drives the same steps through the
+C-ABI from the host with the reference's per-operator error check (one D2H of the stability
+counters per step). `cpu_baseline` times the reference itself (oracle/_ref) on this host.
+
+`--impl reference` runs the unmodified reference CPU path (Simulation::step via
+oracle/_ref) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MLUPS per GPU and % of HBM roofline at 1/2/4/8 B200; coupled step time"
+BYTES_PER_LUP = 304  # 19 f64 loads + 19 f64 stores
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["lbg", "reference"], default="lbg")
+    ap.add_argument("--n", type=int, default=512, help="cells per axis of each GPU's block")
+    ap.add_argument("--tau", type=float, default=0.8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------------- reference CPU path
+REF_CFG = ('{{"scenario":"custom","domain":[{nx},{ny},{nz}],"kernels":"openmp",'
+           '"fluid":{{"tau":{tau},"coupling":false}},"dem":{{"subcycles":1}}}}')
+
+
+def reference_sample(n, tau, budget_s, steps=None, warmup=0):
+    """Simulation::step of the unmodified reference (oracle/_ref) on a 512 x 512 x S periodic
+    slab of the same workload (same per-cell work, bounded memory), OpenMP on all host cores.
+    Returns (MLUPS, sample description, threads, per-step seconds)."""
+    from oracle.pyoracle import RefLib
+    ref = RefLib()
+    threads = os.cpu_count() or 1
+    ref.set_threads(threads)
+    nz = 16
+    sim = ref.sim(REF_CFG.format(nx=n, ny=n, nz=nz, tau=tau))
+    sim.shear_wave()
+    t0 = time.perf_counter()
+    sim.run(1)
+    one = time.perf_counter() - t0
+    if steps is None:
+        steps = max(1, min(200, int(budget_s / max(one, 1e-6))))
+    for _ in range(warmup):
+        sim.run(1)
+    t0 = time.perf_counter()
+    sim.run(steps)
+    dt = time.perf_counter() - t0
+    cells = n * n * nz
+    return (cells * steps / dt / 1e6,
+            f"reference Simulation::step (fluid, coupling off) on a {n}x{n}x{nz} periodic slab, "
+            f"{steps} steps, shear-wave init, OpenMP", threads, dt / steps)
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    try:
+        from oracle.pyoracle import REF_SO
+        if not os.path.exists(REF_SO):
+            raise FileNotFoundError(REF_SO)
+        mlups, sample, threads, per_step = reference_sample(args.n, args.tau, args.cpu_seconds,
+                                                            steps=args.steps, warmup=args.warmup)
+    except Exception as e:  # noqa: BLE001
+        print(json.dumps({"impl": "reference", "unavailable": f"reference build missing: {e}"}))
+        return 0
+    line = {"metric": METRIC, "value": round(mlups, 3), "unit": "MLUPS", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(per_step * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (shear-wave initial state, validation.cpp:46-63)", "impl": "reference",
+            "config": {"workload": f"pure-fluid D3Q19 SRT periodic, {args.n}^3 per GPU (config 2/4)",
+                       "sample": "512x512x16 slab per step (per-cell work identical)"},
+            "cpu_baseline": {"value": round(mlups, 3), "unit": "MLUPS", "cores": threads,
+                             "kind": "reference", "sample": sample},
+            "e2e": {"value": round(mlups, 3), "unit": "MLUPS", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# --------------------------------------------------------------------------- GPU path
+def run_lbg(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2303_11811_b200 import lbdem
+
+    rank, world, local = dist_env()
+    N = world
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n = args.n
+    dims = (n, n, n)
+    domain = (n, n, n * N)
+    blk = lbdem.Block(dims, lo=(0, 0, rank * n), device=local)
+    blk.init_shear_wave(domain)
+    p = lbdem.FluidParams(args.tau)
+    full = lbdem.CellBox((0, 0, 0), dims)
+    inner = lbdem.CellBox((0, 0, 1), (n, n, n - 1))
+    outer = [lbdem.CellBox((0, 0, 0), (n, n, 1)), lbdem.CellBox((0, 0, n - 1), (n, n, n))]
+    if N > 1:
+        uid = [lbdem.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        blk.comm_init(N, rank, uid[0], axis=2, periodic=(1, 1, 1))
+
+    def step():
+        if N == 1:
+            blk.fill_periodic((1, 1, 1), full=False)
+            blk.sweep(p, full)
+        else:
+            blk.fill_periodic((1, 1, 0), full=False)
+            blk.halo_begin()
+            blk.sweep(p, inner)
+            blk.halo_complete()
+            blk.sweep_boxes(p, outer)
+        blk.swap()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step()
+    blk.sync()
+    stream = torch.cuda.ExternalStream(blk.stream, device=torch.device("cuda", local))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    # ---- device-timed region
+    barrier()
+    blk.set_timing(True)
+    blk.timings()  # clear
+    l0 = lbdem.launch_count()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        e1.synchronize()
+    launches = lbdem.launch_count() - l0
+    tm = blk.timings()
+    blk.set_timing(False)
+    blk.sync()  # stability check (NumericError would raise here)
+    barrier()
+    ms_total = max_over_ranks(e0.elapsed_time(e1))
+    ms_step = ms_total / args.steps
+    cells = n * n * n
+    mlups = cells * N * args.steps / (ms_total / 1e3) / 1e6
+
+    sweep_ms, sweep_n = tm["PSM"]
+    sweep_ms_per_step = sweep_ms / args.steps
+    achieved = BYTES_PER_LUP * cells / (sweep_ms_per_step / 1e3) / 1e9  # GB/s
+    pk = peaks()
+    peak, peak_src = (pk["hbm_gbs"], "measured") if pk and pk.get("hbm_gbs") else (6650.0, "fallback")
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "sweep_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            tj = json.load(open(tfile))
+            if tj.get("n") == n:
+                traffic = tj.get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- end to end through the C-ABI (host-driven, per-step error check D2H)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+        blk.sync()  # lbg_sync: D2H of the 3 error counters, raises NumericError/SyncError
+    t1 = time.perf_counter()
+    barrier()
+    e2e_s = max_over_ranks(t1 - t0)
+    e2e_mlups = cells * N * args.steps / e2e_s / 1e6
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if N == 1 and not args.no_cpu_baseline:
+            try:
+                c_mlups, sample, threads, _ = reference_sample(n, args.tau, args.cpu_seconds)
+                cpu = {"value": round(c_mlups, 3), "unit": "MLUPS", "cores": threads,
+                       "kind": "reference", "sample": sample}
+            except Exception as e:  # noqa: BLE001
+                cpu = {"value": None, "unit": "MLUPS", "cores": 0, "kind": "reference",
+                       "sample": f"unavailable: {e}"}
+        out = {
+            "metric": METRIC, "value": round(mlups, 1), "unit": "MLUPS", "n_gpus": N,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (shear-wave initial state, validation.cpp:46-63, device-initialised)",
+            "config": {"workload": (f"config 2: pure-fluid D3Q19 SRT {n}^3 periodic, 1 GPU" if N == 1 else
+                                    f"config 4: pure-fluid D3Q19 SRT weak scaling {n}^3 per GPU, "
+                                    f"{n}x{n}x{n * N} periodic z-slabs, NCCL halo hidden behind the inner sweep"),
+                       "tau": args.tau, "cells_per_gpu": cells, "parallelism": f"z-slab x{N}",
+                       "l2": f"inputs larger than L2 ({2 * 19 * 8 * cells / 1e9:.1f} GB PDF working set)"},
+            "mlups_per_gpu": round(mlups / N, 1),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "kernel": "sweep_box_kernel<false,false> (K1 fused pull stream-collide)",
+                         "bytes_per_lup": BYTES_PER_LUP, "peak_source": peak_src,
+                         "sweep_ms_per_step": round(sweep_ms_per_step, 4),
+                         "sweep_launches": sweep_n},
+            "hbm_roofline_frac_of_step": round(BYTES_PER_LUP * cells / (ms_step / 1e3) / 1e9 / peak, 4),
+            "timings_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in tm.items() if v[1]},
+            "e2e": {"value": round(e2e_mlups, 1), "unit": "MLUPS", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 24,
+                    "how": "per step via the C-ABI (fill_periodic, sweep, swap) + lbg_sync error-counter readback"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out))
+    blk.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_lbg(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,229 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * lbg.h — C-ABI of the B200-native GPU side of the arXiv 2303.11811 coupled
+ * LBM/PSM/DEM solver. Plain pointers and sizes, no C++ or torch types, never throws.
+ *
+ * Every entry point replaces one operator of the reference C++ library
+ * (/root/reference/proj, "lbdem"); the citation next to each declaration names the
+ * reference interface it stands in for. A block (lbg_block) is the device-side twin of
+ * the reference's BlockState fields (sim.hpp:28-52): the double-buffered PdfField, and
+ * with `coupling` the FractionField, SolidVelocityField and CellMomentumScratch.
+ *
+ * Layout contract for host buffers (so parity tests compare raw arrays):
+ *   PDF:       19 q-planes of (nx+2)(ny+2)(nz+2) doubles, PdfField::idx order
+ *              ((k+1)(ny+2)+(j+1))(nx+2)+(i+1)                   (field.hpp:47-49)
+ *   fraction:  interior cells, (k*ny+j)*nx+i                       (field.hpp:95-97)
+ *   Vec3 data: xyz interleaved per cell                            (field.hpp:101-118)
+ * The device layout is private (x-pitch padded for 128-byte row alignment).
+ *
+ * Asynchrony: calls enqueue work on the block's CUDA streams and return. Errors the
+ * reference raises at the end of an operator (NumericError for unstable cells or
+ * overfull cells, SyncError for unknown particle ids) are accumulated in device
+ * counters and reported by lbg_sync(), which maps them to LBG_NUMERIC_ERROR /
+ * LBG_SYNC_ERROR with the reference's messages (lbm.cpp:47-48, psm.cpp:133-135,
+ * psm.cpp:167-168, psm.cpp:301-303). Threading: a block belongs to one host thread at a
+ * time, like a BlockState.
+ */
+#ifndef LBG_H
+#define LBG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; 1-4 map to the reference exceptions (errors.hpp:10-32, CLI exit codes
+ * lbdem_cli.cpp:199-214). */
+typedef enum {
+    LBG_OK = 0,
+    LBG_CONFIG_ERROR = 1,  /* ConfigError  */
+    LBG_NUMERIC_ERROR = 2, /* NumericError */
+    LBG_SYNC_ERROR = 3,    /* SyncError    */
+    LBG_IO_ERROR = 4,      /* IoError      */
+    LBG_CUDA_ERROR = 5,    /* CUDA/NCCL runtime failure (no reference twin) */
+    LBG_INVALID = 6        /* bad argument / missing coupling fields */
+} lbg_status;
+
+typedef struct lbg_block_s* lbg_block;
+
+/* CellBox (field.hpp:13-30): half-open [lo, hi) in block-local cell coordinates. */
+typedef struct {
+    int lo[3];
+    int hi[3];
+} lbg_box;
+
+/* FluidParams (lbm.hpp:21-33). */
+typedef struct {
+    double tau;
+    double f_ext[3];
+} lbg_fluid;
+
+/* BcKind / FaceBc (boundary.hpp:11-17). Face order -x,+x,-y,+y,-z,+z (boundary.hpp:20). */
+enum { LBG_BC_PERIODIC = 0, LBG_BC_NO_SLIP = 1, LBG_BC_VELOCITY = 2, LBG_BC_PRESSURE = 3 };
+typedef struct {
+    int kind;
+    int pad_;
+    double u_wall[3];
+    double rho;
+} lbg_face_bc;
+
+/* ParticleSnapshot (psm.hpp:16-23), id-sorted list of locals + ghosts. */
+typedef struct {
+    int id;
+    int pad_;
+    double x[3];
+    double r;
+    double f_r;
+    double u[3];
+    double omega[3];
+} lbg_snapshot;
+
+/* HydroPartial (psm.hpp:88-92): Neumaier (sum, comp) pairs, vec3.hpp:71-95. */
+typedef struct {
+    int id;
+    int pad_;
+    double f[3];
+    double f_comp[3];
+    double t[3];
+    double t_comp[3];
+} lbg_hydro_partial;
+
+/* End-of-operator error counters (the reference's `bad`, `overfull`, `unknown`). */
+typedef struct {
+    long long unstable_cells; /* lbm.cpp:33-48, psm.cpp:233-261 */
+    long long overfull_cells; /* psm.cpp:132-135 */
+    long long unknown_ids;    /* psm.cpp:166-168, 300-303 */
+} lbg_errors;
+
+/* Hydrodynamic reduction modes for lbg_reduce_hydro. */
+enum {
+    LBG_REDUCE_PARITY = 0, /* per-particle lexicographic Neumaier walk: bitwise == reference */
+    LBG_REDUCE_FAST = 1    /* warp shuffles + shared memory + per-particle atomics (tolerance) */
+};
+
+/* Timing categories, perf.hpp:17-26 (perf::Category order). */
+enum {
+    LBG_CAT_PSM = 0,
+    LBG_CAT_PSM_COMM = 1,
+    LBG_CAT_MAPPING = 2,
+    LBG_CAT_SETU = 3,
+    LBG_CAT_REDF = 4,
+    LBG_CAT_PD = 5,
+    LBG_CAT_PD_COMM = 6,
+    LBG_CAT_OTHER = 7,
+    LBG_NUM_CATS = 8
+};
+
+/* ------------------------------------------------------------------ library */
+const char* lbg_last_error(void);           /* message of the last failing call (thread-local) */
+const char* lbg_version(void);
+int lbg_device_count(void);
+
+/* Pinned host memory for async H2D/D2H (the "pinned async copies" of the north star). */
+lbg_status lbg_host_alloc(size_t bytes, void** out);
+lbg_status lbg_host_free(void* p);
+
+/* ------------------------------------------------------------------ block lifecycle */
+/* BlockState ctor (sim.cpp:15-25) + PdfField(nx,ny,nz) (field.cpp:6-13): zeroed buffers. */
+lbg_status lbg_block_create(int device, const int box_lo[3], const int dims[3], int coupling,
+                            lbg_block* out);
+lbg_status lbg_block_destroy(lbg_block b);
+lbg_status lbg_block_info(lbg_block b, int dims[3], int box_lo[3], int* coupling,
+                          long long* device_bytes);
+/* cudaStream_t of the compute stream, for callers that time with their own events. */
+void* lbg_block_stream(lbg_block b);
+
+/* ------------------------------------------------------------------ PdfField access */
+/* PdfField::src()/at_src() (field.hpp:56-62): whole src/dst buffer incl. ghosts. */
+lbg_status lbg_upload_src(lbg_block b, const double* host);
+lbg_status lbg_download_src(lbg_block b, double* host);
+lbg_status lbg_upload_dst(lbg_block b, const double* host);
+lbg_status lbg_download_dst(lbg_block b, double* host);
+/* Simulation::initialize_fluid (sim.cpp:54-57) via PdfField::fill_src (field.cpp:15-22). */
+lbg_status lbg_fill_equilibrium(lbg_block b, double rho, const double u[3]);
+/* Shear-wave equilibrium state of validation.cpp:46-63 over a global `domain`, computed on
+ * the device (synthetic benchmark input for configs 2/4; not bitwise with glibc sin/cos). */
+lbg_status lbg_init_shear_wave(lbg_block b, const int domain[3]);
+/* PdfField::fill_ghosts_src (field.cpp:24-35), NaN-poisoning tests. */
+lbg_status lbg_fill_ghosts_src(lbg_block b, double v);
+/* PdfField::swap (field.hpp:64). */
+lbg_status lbg_swap(lbg_block b);
+
+/* ------------------------------------------------------------------ fluid operators */
+/* collide_stream_* / psm_collide_stream_* over a CellBox (lbm.cpp:21-59, psm.cpp:218-276).
+ * The plain or coupled kernel is chosen by the block's `coupling` flag, as
+ * Simulation::run_kernel does (sim.cpp:221-236). */
+lbg_status lbg_sweep(lbg_block b, const lbg_fluid* fluid, const lbg_box* range);
+/* Several boxes in one launch (the 6 boundary_shell boxes, field.cpp:55-72). */
+lbg_status lbg_sweep_boxes(lbg_block b, const lbg_fluid* fluid, const lbg_box* boxes, int n);
+/* Unfused pull stream (lbm.cpp:6-17), debug/tests. */
+lbg_status lbg_stream(lbg_block b, const lbg_box* range);
+
+/* fill_periodic_ghosts (boundary.cpp:98-137). full=1 copies all 19 q of all 26 regions
+ * (bitwise identical src buffer); full=0 copies only the ghost slots a pull sweep reads. */
+lbg_status lbg_fill_periodic(lbg_block b, const int periodic[3], int full);
+/* apply_boundaries (boundary.cpp:32-96, 140-146). */
+lbg_status lbg_apply_boundaries(lbg_block b, const lbg_face_bc faces[6], const int touches[6]);
+
+/* ------------------------------------------------------------------ particle coupling */
+/* SubBlockRegistry::build + build_fraction_field + set_solid_velocities
+ * (psm.cpp:55-169): snapshots must be id-sorted; staged through pinned memory and
+ * copied H2D on the block's side stream. `subdivisions` is accepted for API parity
+ * (the device binning is finer and gives the same candidate order). */
+lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisions);
+/* set_solid_velocities alone (psm.cpp:138-169) for a fraction field set by the caller. */
+lbg_status lbg_set_solid_velocities(lbg_block b, const lbg_snapshot* snaps, int n);
+/* finalize_hydro_forces (psm.cpp:278-322): fills out[] id-sorted (one row per particle
+ * with at least one entry), sets *n_out, clears the scratch. Blocks until done. */
+lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int capacity,
+                            int* n_out);
+
+/* Coupling fields (tests / parity; host arrays in the reference layouts above). */
+lbg_status lbg_upload_fraction(lbg_block b, const uint8_t* count, const int* id0,
+                               const int* id1, const double* b0, const double* b1,
+                               const double* btot);
+lbg_status lbg_download_fraction(lbg_block b, uint8_t* count, int* id0, int* id1, double* b0,
+                                 double* b1, double* btot);
+lbg_status lbg_upload_solid_velocity(lbg_block b, const double* v0, const double* v1);
+lbg_status lbg_download_solid_velocity(lbg_block b, double* v0, double* v1);
+lbg_status lbg_upload_scratch(lbg_block b, const double* m0, const double* m1);
+lbg_status lbg_download_scratch(lbg_block b, double* m0, double* m1);
+
+/* ------------------------------------------------------------------ sync / observers */
+/* End-of-phase barrier: waits for the block's streams, returns and clears the error
+ * counters; status LBG_NUMERIC_ERROR / LBG_SYNC_ERROR when any is nonzero. */
+lbg_status lbg_sync(lbg_block b, lbg_errors* out);
+/* total_mass / total_momentum of the src interior (lbm.cpp:69-93), Neumaier-compensated
+ * per block of cells, then combined in fixed order (deterministic, not bitwise). */
+lbg_status lbg_total_mass(lbg_block b, double* out);
+lbg_status lbg_total_momentum(lbg_block b, double out[3]);
+
+/* ------------------------------------------------------------------ halo exchange */
+/* Simulation::begin/complete_halo_exchange (sim.cpp:156-201) for a slab decomposition
+ * along `axis` over `nranks` processes (one GPU each), NCCL send/recv on a dedicated comm
+ * stream; `periodic` is the domain's periodic mask (ring along `axis`, ghost-ring wrap of
+ * received planes along the others). lbg_comm_unique_id is called on rank 0 and broadcast
+ * by the caller. */
+lbg_status lbg_comm_unique_id(char out[128]);
+lbg_status lbg_comm_init(lbg_block b, int nranks, int rank, const char id[128], int axis,
+                         const int periodic[3]);
+lbg_status lbg_comm_destroy(lbg_block b);
+/* Post-collision src boundary planes -> neighbours (non-blocking, comm stream). */
+lbg_status lbg_halo_begin(lbg_block b);
+/* Ghost planes valid for the outer sweep; SyncError without a pending begin (sim.cpp:183). */
+lbg_status lbg_halo_complete(lbg_block b);
+
+/* ------------------------------------------------------------------ instrumentation */
+/* Per-category CUDA-event timing (perf::Category names); off by default. */
+lbg_status lbg_set_timing(lbg_block b, int on);
+/* Sums (and clears) the elapsed device ms per category since the last call. */
+lbg_status lbg_timings(lbg_block b, double ms[LBG_NUM_CATS], long long launches[LBG_NUM_CATS]);
+/* Kernels this library launched (all blocks, process-wide). */
+long long lbg_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LBG_H */

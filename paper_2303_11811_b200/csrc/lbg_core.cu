@@ -1,0 +1,468 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// liblbg core: block lifecycle (BlockState/PdfField, sim.cpp:15-25, field.cpp:6-35),
+// host<->device transfers in the reference layout, the end-of-phase sync with the
+// reference's error semantics, observers and per-category CUDA-event timing
+// (perf::Category, perf.hpp:17-26).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "lbg_internal.cuh"
+
+namespace lbg {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<long long> g_launches{0};
+}  // namespace
+
+lbg_status set_error(lbg_status s, const std::string& msg) {
+    g_last_error = msg;
+    return s;
+}
+
+lbg_status cuda_check(cudaError_t e, const char* what) {
+    return set_error(LBG_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static cudaEvent_t take_event(lbg_block b) {
+    if (!b->event_pool.empty()) {
+        cudaEvent_t e = b->event_pool.back();
+        b->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+Span::Span(lbg_block b_, int cat_) : b(b_), cat(cat_) {
+    if (b->timing) {
+        a = take_event(b);
+        cudaEventRecord(a, b->stream);
+    }
+}
+
+Span::~Span() {
+    if (a) {
+        cudaEvent_t e = take_event(b);
+        cudaEventRecord(e, b->stream);
+        b->spans.push_back({cat, a, e});
+    }
+}
+
+// lbm.hpp:38-45 — host twin of equilibrium() with the reference's operation order
+// (this TU is compiled with -ffp-contract=off for the host side).
+static void equilibrium_host(double rho, const double u[3], double feq[kQ]) {
+    const double u_sq = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+    for (int q = 0; q < kQ; ++q) {
+        const double c0 = cx(q), c1 = cy(q), c2 = cz(q);
+        const double cu = c0 * u[0] + c1 * u[1] + c2 * u[2];
+        feq[q] = wq(q) * (rho + 1.0 * (cu * 3.0 + 0.5 * cu * cu * 9.0 - 0.5 * u_sq * 3.0));
+    }
+}
+
+struct Feq {
+    double v[kQ];
+};
+
+__global__ void fill_interior_kernel(double* __restrict__ buf, Layout L, Feq f) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y;
+    const int k = blockIdx.z;
+    if (i >= L.nx) return;
+    const long long c = L.idx(i, j, k);
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) buf[q * L.plane + c] = f.v[q];
+}
+
+// validation.cpp:46-63 shear-wave initial state, evaluated per cell on the device
+// (synthetic benchmark input; device sin/cos may differ from glibc in the last ulp).
+__global__ void shear_wave_kernel(double* __restrict__ buf, Layout L, int lo0, int lo1, int lo2, int D0,
+                                  int D1, int D2) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y;
+    const int k = blockIdx.z;
+    if (i >= L.nx) return;
+    const double pi = 3.14159265358979323846;
+    const double gx = lo0 + i + 0.5, gy = lo1 + j + 0.5, gz = lo2 + k + 0.5;
+    const double u0 = 0.02 * sin(2.0 * pi * gy / D1);
+    const double u1 = 0.015 * cos(2.0 * pi * gz / D2);
+    const double u2 = 0.01 * sin(2.0 * pi * gx / D0);
+    const double u_sq = (u0 * u0 + u1 * u1) + u2 * u2;
+    const long long c = L.idx(i, j, k);
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+        const double cu = ((double)cx(q) * u0 + (double)cy(q) * u1) + (double)cz(q) * u2;
+        buf[q * L.plane + c] = wq(q) * (1.0 + 1.0 * ((cu * 3.0 + ((0.5 * cu) * cu) * 9.0) - (0.5 * u_sq) * 3.0));
+    }
+}
+
+__global__ void fill_ghosts_kernel(double* __restrict__ buf, Layout L, double v) {
+    // all cells of the (nx+2)(ny+2)(nz+2) box that are not interior
+    const int ii = blockIdx.x * blockDim.x + threadIdx.x;  // 0..nx+1
+    const int jj = blockIdx.y;
+    const int kk = blockIdx.z;
+    if (ii >= L.nx + 2) return;
+    const int i = ii - 1, j = jj - 1, k = kk - 1;
+    const bool interior = i >= 0 && i < L.nx && j >= 0 && j < L.ny && k >= 0 && k < L.nz;
+    if (interior) return;
+    const long long c = L.idx(i, j, k);
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) buf[q * L.plane + c] = v;
+}
+
+// Row-wise Neumaier partial sums of the src interior (lbm.cpp:69-93), combined on the
+// host in lexicographic row order.
+__device__ __forceinline__ void nm_add(double& sum, double& comp, double v) {
+    const double t = sum + v;
+    if (fabs(sum) >= fabs(v))
+        comp += (sum - t) + v;
+    else
+        comp += (v - t) + sum;
+    sum = t;
+}
+
+__global__ void row_moments_kernel(const double* __restrict__ src, Layout L, double* __restrict__ rows) {
+    const int row = blockIdx.x * blockDim.x + threadIdx.x;  // j + k*ny
+    if (row >= L.ny * L.nz) return;
+    const int j = row % L.ny, k = row / L.ny;
+    double s[4] = {0, 0, 0, 0}, c[4] = {0, 0, 0, 0};
+    const long long base = L.row(j, k);
+    for (int i = 0; i < L.nx; ++i) {
+        double rho = 0.0, mx = 0.0, my = 0.0, mz = 0.0;
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+            const double f = src[q * L.plane + base + i];
+            rho += f;
+            mx += f * (double)cx(q);
+            my += f * (double)cy(q);
+            mz += f * (double)cz(q);
+        }
+        nm_add(s[0], c[0], rho);
+        nm_add(s[1], c[1], mx);
+        nm_add(s[2], c[2], my);
+        nm_add(s[3], c[3], mz);
+    }
+    for (int a = 0; a < 4; ++a) {
+        rows[(size_t)row * 8 + 2 * a] = s[a];
+        rows[(size_t)row * 8 + 2 * a + 1] = c[a];
+    }
+}
+
+}  // namespace lbg
+
+using namespace lbg;
+
+extern "C" {
+
+const char* lbg_last_error(void) { return g_last_error.c_str(); }
+const char* lbg_version(void) { return "lbg 0.1 (sm_100a)"; }
+
+int lbg_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+lbg_status lbg_host_alloc(size_t bytes, void** out) {
+    LBG_CUDA(cudaMallocHost(out, bytes));
+    return LBG_OK;
+}
+
+lbg_status lbg_host_free(void* p) {
+    LBG_CUDA(cudaFreeHost(p));
+    return LBG_OK;
+}
+
+long long lbg_launch_count(void) { return g_launches.load(); }
+
+lbg_status lbg_block_create(int device, const int box_lo[3], const int dims[3], int coupling,
+                            lbg_block* out) {
+    *out = nullptr;
+    for (int a = 0; a < 3; ++a)
+        if (dims[a] < 1) return set_error(LBG_CONFIG_ERROR, "block dimensions must be positive");
+    LBG_CUDA(cudaSetDevice(device));
+    auto* b = new lbg_block_s;
+    b->device = device;
+    for (int a = 0; a < 3; ++a) b->lo[a] = box_lo[a];
+    b->coupling = coupling != 0;
+    Layout& L = b->L;
+    L.nx = dims[0];
+    L.ny = dims[1];
+    L.nz = dims[2];
+    L.px = ((kXOff + L.nx + 1) + 15) / 16 * 16;
+    L.py = L.ny + 2;
+    L.pz = L.nz + 2;
+    L.plane = (long long)L.px * L.py * L.pz;
+
+    auto fail = [&](cudaError_t e, const char* what) {
+        lbg_block_destroy(b);
+        return cuda_check(e, what);
+    };
+    const size_t pdf_bytes = sizeof(double) * kQ * (size_t)L.plane;
+    cudaError_t e;
+    for (int s = 0; s < 2; ++s) {
+        if ((e = cudaMalloc(&b->buf[s], pdf_bytes)) != cudaSuccess) return fail(e, "cudaMalloc(pdf)");
+        if ((e = cudaMemset(b->buf[s], 0, pdf_bytes)) != cudaSuccess) return fail(e, "cudaMemset(pdf)");
+        b->device_bytes += pdf_bytes;
+    }
+    if (b->coupling) {
+        const size_t n = (size_t)L.nx * L.ny * L.nz;
+        struct A {
+            void** p;
+            size_t bytes;
+        } allocs[] = {{(void**)&b->count, n},
+                      {(void**)&b->id0, n * 4},
+                      {(void**)&b->id1, n * 4},
+                      {(void**)&b->b0, n * 8},
+                      {(void**)&b->b1, n * 8},
+                      {(void**)&b->btot, n * 8},
+                      {(void**)&b->v0, n * 24},
+                      {(void**)&b->v1, n * 24},
+                      {(void**)&b->m0, n * 24},
+                      {(void**)&b->m1, n * 24}};
+        for (auto& a : allocs) {
+            if ((e = cudaMalloc(a.p, a.bytes)) != cudaSuccess) return fail(e, "cudaMalloc(coupling)");
+            if ((e = cudaMemset(*a.p, 0, a.bytes)) != cudaSuccess) return fail(e, "cudaMemset(coupling)");
+            b->device_bytes += a.bytes;
+        }
+        // FractionField::resize fills id0/id1 with -1 (field.cpp:37-46)
+        cudaMemset(b->id0, 0xff, n * 4);
+        cudaMemset(b->id1, 0xff, n * 4);
+    }
+    if ((e = cudaMalloc(&b->err_d, sizeof(DeviceErrors))) != cudaSuccess) return fail(e, "cudaMalloc(err)");
+    cudaMemset(b->err_d, 0, sizeof(DeviceErrors));
+    if ((e = cudaMallocHost(&b->err_h, sizeof(DeviceErrors))) != cudaSuccess) return fail(e, "cudaMallocHost(err)");
+    int lo_prio = 0, hi_prio = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+    if ((e = cudaStreamCreateWithPriority(&b->stream, cudaStreamNonBlocking, lo_prio)) != cudaSuccess)
+        return fail(e, "cudaStreamCreate");
+    if ((e = cudaStreamCreateWithPriority(&b->side, cudaStreamNonBlocking, hi_prio)) != cudaSuccess)
+        return fail(e, "cudaStreamCreate(side)");
+    if ((e = cudaEventCreateWithFlags(&b->ev_side, cudaEventDisableTiming)) != cudaSuccess)
+        return fail(e, "cudaEventCreate");
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail(e, "block create");
+    *out = b;
+    return LBG_OK;
+}
+
+lbg_status lbg_comm_destroy(lbg_block b);  // lbg_halo.cu
+
+lbg_status lbg_block_destroy(lbg_block b) {
+    if (!b) return LBG_OK;
+    cudaSetDevice(b->device);
+    if (b->stream) cudaStreamSynchronize(b->stream);
+    if (b->side) cudaStreamSynchronize(b->side);
+    if (b->comm) lbg_comm_destroy(b);
+    void* dev[] = {b->buf[0], b->buf[1], b->count, b->id0, b->id1, b->b0, b->b1, b->btot,
+                   b->v0, b->v1, b->m0, b->m1, b->snaps_d, b->bin_count, b->bin_start,
+                   b->bin_items, b->red_rows, b->red_used, b->err_d};
+    for (void* p : dev)
+        if (p) cudaFree(p);
+    void* host[] = {b->snaps_h, b->err_h, b->red_h, b->red_rows_h, b->red_used_h};
+    for (void* p : host)
+        if (p) cudaFreeHost(p);
+    for (auto& s : b->spans) {
+        cudaEventDestroy(s.a);
+        cudaEventDestroy(s.b);
+    }
+    for (auto e : b->event_pool) cudaEventDestroy(e);
+    if (b->ev_side) cudaEventDestroy(b->ev_side);
+    if (b->stream) cudaStreamDestroy(b->stream);
+    if (b->side) cudaStreamDestroy(b->side);
+    delete b;
+    return LBG_OK;
+}
+
+lbg_status lbg_block_info(lbg_block b, int dims[3], int box_lo[3], int* coupling,
+                          long long* device_bytes) {
+    if (!b) return set_error(LBG_INVALID, "null block");
+    if (dims) {
+        dims[0] = b->L.nx;
+        dims[1] = b->L.ny;
+        dims[2] = b->L.nz;
+    }
+    if (box_lo)
+        for (int a = 0; a < 3; ++a) box_lo[a] = b->lo[a];
+    if (coupling) *coupling = b->coupling;
+    if (device_bytes) *device_bytes = b->device_bytes;
+    return LBG_OK;
+}
+
+void* lbg_block_stream(lbg_block b) { return b ? (void*)b->stream : nullptr; }
+
+static lbg_status copy_pdf(lbg_block b, double* dev, const double* host_in, double* host_out) {
+    const Layout& L = b->L;
+    const size_t width = sizeof(double) * (L.nx + 2);
+    const size_t height = (size_t)kQ * L.py * L.pz;
+    double* d0 = dev + (kXOff - 1);
+    LBG_CUDA(cudaSetDevice(b->device));
+    if (host_in) {
+        LBG_CUDA(cudaMemcpy2DAsync(d0, sizeof(double) * L.px, host_in, width, width, height,
+                                   cudaMemcpyHostToDevice, b->stream));
+    } else {
+        LBG_CUDA(cudaMemcpy2DAsync(host_out, width, d0, sizeof(double) * L.px, width, height,
+                                   cudaMemcpyDeviceToHost, b->stream));
+    }
+    LBG_CUDA(cudaStreamSynchronize(b->stream));
+    return LBG_OK;
+}
+
+lbg_status lbg_upload_src(lbg_block b, const double* host) { return copy_pdf(b, b->src(), host, nullptr); }
+lbg_status lbg_download_src(lbg_block b, double* host) { return copy_pdf(b, b->src(), nullptr, host); }
+lbg_status lbg_upload_dst(lbg_block b, const double* host) { return copy_pdf(b, b->dst(), host, nullptr); }
+lbg_status lbg_download_dst(lbg_block b, double* host) { return copy_pdf(b, b->dst(), nullptr, host); }
+
+lbg_status lbg_swap(lbg_block b) {
+    b->cur ^= 1;
+    return LBG_OK;
+}
+
+lbg_status lbg_fill_equilibrium(lbg_block b, double rho, const double u[3]) {
+    Feq f;
+    equilibrium_host(rho, u, f.v);
+    const Layout& L = b->L;
+    LBG_CUDA(cudaSetDevice(b->device));
+    dim3 grid((L.nx + 127) / 128, L.ny, L.nz);
+    fill_interior_kernel<<<grid, 128, 0, b->stream>>>(b->src(), L, f);
+    LBG_LAUNCH_CHECK();
+    return LBG_OK;
+}
+
+lbg_status lbg_init_shear_wave(lbg_block b, const int domain[3]) {
+    const Layout& L = b->L;
+    LBG_CUDA(cudaSetDevice(b->device));
+    dim3 grid((L.nx + 127) / 128, L.ny, L.nz);
+    shear_wave_kernel<<<grid, 128, 0, b->stream>>>(b->src(), L, b->lo[0], b->lo[1], b->lo[2], domain[0],
+                                                   domain[1], domain[2]);
+    LBG_LAUNCH_CHECK();
+    return LBG_OK;
+}
+
+lbg_status lbg_fill_ghosts_src(lbg_block b, double v) {
+    const Layout& L = b->L;
+    LBG_CUDA(cudaSetDevice(b->device));
+    dim3 grid((L.nx + 2 + 127) / 128, L.ny + 2, L.nz + 2);
+    fill_ghosts_kernel<<<grid, 128, 0, b->stream>>>(b->src(), L, v);
+    LBG_LAUNCH_CHECK();
+    return LBG_OK;
+}
+
+lbg_status lbg_sync(lbg_block b, lbg_errors* out) {
+    LBG_CUDA(cudaSetDevice(b->device));
+    LBG_CUDA(cudaStreamSynchronize(b->side));
+    LBG_CUDA(cudaMemcpyAsync(b->err_h, b->err_d, sizeof(DeviceErrors), cudaMemcpyDeviceToHost,
+                             b->stream));
+    LBG_CUDA(cudaMemsetAsync(b->err_d, 0, sizeof(DeviceErrors), b->stream));
+    LBG_CUDA(cudaStreamSynchronize(b->stream));
+    const DeviceErrors e = *b->err_h;
+    if (out) {
+        out->unstable_cells = (long long)e.unstable;
+        out->overfull_cells = (long long)e.overfull;
+        out->unknown_ids = (long long)e.unknown;
+    }
+    if (e.overfull > 0)
+        return set_error(LBG_NUMERIC_ERROR,
+                         "more than two particles overlap a single cell in " +
+                             std::to_string(e.overfull) +
+                             " cells; particle penetration too deep for the coupling");
+    if (e.unknown > 0)
+        return set_error(LBG_SYNC_ERROR, "solid velocity field references " +
+                                             std::to_string(e.unknown) +
+                                             " unknown particle ids (ghost synchronization failed)");
+    if (e.unstable > 0) {
+        if (b->coupling)
+            return set_error(LBG_NUMERIC_ERROR, "fluid instability in PSM kernel: " +
+                                                    std::to_string(e.unstable) +
+                                                    " cells out of range");
+        return set_error(LBG_NUMERIC_ERROR, "fluid instability: " + std::to_string(e.unstable) +
+                                                " cells with rho <= 0 or |u| > " +
+                                                std::to_string(kMaxVelocity));
+    }
+    return LBG_OK;
+}
+
+static void nm_add_host(double& sum, double& comp, double v) {
+    const double t = sum + v;
+    if (std::fabs(sum) >= std::fabs(v))
+        comp += (sum - t) + v;
+    else
+        comp += (v - t) + sum;
+    sum = t;
+}
+
+static lbg_status moments(lbg_block b, double out[4]) {
+    const Layout& L = b->L;
+    const int rows = L.ny * L.nz;
+    LBG_CUDA(cudaSetDevice(b->device));
+    double* d = nullptr;
+    LBG_CUDA(cudaMallocAsync(&d, sizeof(double) * 8 * rows, b->stream));
+    row_moments_kernel<<<(rows + 127) / 128, 128, 0, b->stream>>>(b->src(), L, d);
+    ::lbg::count_launch();
+    std::vector<double> h((size_t)8 * rows);
+    cudaError_t e = cudaMemcpyAsync(h.data(), d, sizeof(double) * 8 * rows, cudaMemcpyDeviceToHost,
+                                    b->stream);
+    cudaFreeAsync(d, b->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(b->stream);
+    if (e != cudaSuccess) return cuda_check(e, "moments");
+    for (int a = 0; a < 4; ++a) {
+        double s = 0.0, c = 0.0;
+        for (int r = 0; r < rows; ++r) {
+            nm_add_host(s, c, h[(size_t)r * 8 + 2 * a]);
+            c += h[(size_t)r * 8 + 2 * a + 1];
+        }
+        out[a] = s + c;
+    }
+    return LBG_OK;
+}
+
+lbg_status lbg_total_mass(lbg_block b, double* out) {
+    double m[4];
+    lbg_status s = moments(b, m);
+    if (s == LBG_OK) *out = m[0];
+    return s;
+}
+
+lbg_status lbg_total_momentum(lbg_block b, double out[3]) {
+    double m[4];
+    lbg_status s = moments(b, m);
+    if (s == LBG_OK)
+        for (int a = 0; a < 3; ++a) out[a] = m[1 + a];
+    return s;
+}
+
+lbg_status lbg_set_timing(lbg_block b, int on) {
+    b->timing = on != 0;
+    return LBG_OK;
+}
+
+lbg_status lbg_timings(lbg_block b, double ms[LBG_NUM_CATS], long long launches[LBG_NUM_CATS]) {
+    LBG_CUDA(cudaSetDevice(b->device));
+    LBG_CUDA(cudaStreamSynchronize(b->stream));
+    for (auto& s : b->spans) {
+        float t = 0.f;
+        LBG_CUDA(cudaEventElapsedTime(&t, s.a, s.b));
+        b->acc_ms[s.cat] += t;
+        b->acc_n[s.cat] += 1;
+        b->event_pool.push_back(s.a);
+        b->event_pool.push_back(s.b);
+    }
+    b->spans.clear();
+    for (int c = 0; c < LBG_NUM_CATS; ++c) {
+        if (ms) ms[c] = b->acc_ms[c];
+        if (launches) launches[c] = b->acc_n[c];
+        b->acc_ms[c] = 0.0;
+        b->acc_n[c] = 0;
+    }
+    return LBG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,170 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Private types of liblbg: the device block, its HBM layout and the D3Q19 tables.
+//
+// HBM layout of one PDF buffer (the reference's PdfField, field.hpp:36-78, re-laid out
+// for sm_100a coalescing):
+//   19 q-planes back to back, plane stride = px * py * pz doubles (py = ny+2, pz = nz+2),
+//   row (j,k) at ((k+1)*py + (j+1)) * px, cell i at row + kXOff + i.
+//   kXOff = 16 puts interior i = 0 on a 128-byte boundary; px is a multiple of 16, so
+//   every interior row starts line-aligned and a warp's 32 consecutive cells are exactly
+//   two 128-B lines per q-plane. The x ghost (i = -1) sits at kXOff - 1.
+// Coupling fields keep the reference's interior lexicographic layout (field.hpp:95-97).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "lbg.h"
+
+namespace lbg {
+
+constexpr int kQ = 19;
+constexpr int kXOff = 16;
+
+// lattice.hpp:18-29 (rest, then opposite pairs) and 32-39 (weights over 36).
+__host__ __device__ constexpr int cx(int q) {
+    constexpr int t[kQ] = {0, 1, -1, 0, 0, 0, 0, 1, -1, 1, -1, 1, -1, 1, -1, 0, 0, 0, 0};
+    return t[q];
+}
+__host__ __device__ constexpr int cy(int q) {
+    constexpr int t[kQ] = {0, 0, 0, 1, -1, 0, 0, 1, -1, -1, 1, 0, 0, 0, 0, 1, -1, 1, -1};
+    return t[q];
+}
+__host__ __device__ constexpr int cz(int q) {
+    constexpr int t[kQ] = {0, 0, 0, 0, 0, 1, -1, 0, 0, 0, 0, 1, -1, -1, 1, 1, -1, -1, 1};
+    return t[q];
+}
+__host__ __device__ constexpr int wnum(int q) {
+    constexpr int t[kQ] = {12, 2, 2, 2, 2, 2, 2, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
+    return t[q];
+}
+// kW[q] = kWeightNum36[q] / 36.0, rounded once exactly like lattice.hpp:35-39.
+__host__ __device__ constexpr double wq(int q) { return wnum(q) / 36.0; }
+__host__ __device__ constexpr int opposite(int q) { return q == 0 ? 0 : (((q - 1) ^ 1) + 1); }
+
+constexpr double kMaxVelocity = 0.57;  // lbm.hpp:19
+
+struct Layout {
+    int nx, ny, nz;
+    int px, py, pz;
+    long long plane;  // doubles per q-plane
+    __host__ __device__ long long row(int j, int k) const {
+        return ((long long)(k + 1) * py + (j + 1)) * px + kXOff;
+    }
+    __host__ __device__ long long idx(int i, int j, int k) const { return row(j, k) + i; }
+    __host__ __device__ long long shift(int q) const {
+        return cx(q) + (long long)cy(q) * px + (long long)cz(q) * px * py;
+    }
+    __host__ __device__ long long frac(int i, int j, int k) const {
+        return ((long long)k * ny + j) * nx + i;
+    }
+};
+
+struct DeviceErrors {
+    unsigned long long unstable;
+    unsigned long long overfull;
+    unsigned long long unknown;
+};
+
+struct TimedSpan {
+    int cat;
+    cudaEvent_t a, b;
+};
+
+struct Comm;  // lbg_halo.cu
+
+}  // namespace lbg
+
+struct lbg_block_s {
+    int device = 0;
+    int lo[3] = {0, 0, 0};
+    bool coupling = false;
+    lbg::Layout L{};
+    double* buf[2] = {nullptr, nullptr};
+    int cur = 0;  // src = buf[cur], dst = buf[cur ^ 1]
+
+    // coupling fields (interior lexicographic)
+    uint8_t* count = nullptr;
+    int* id0 = nullptr;
+    int* id1 = nullptr;
+    double* b0 = nullptr;
+    double* b1 = nullptr;
+    double* btot = nullptr;
+    double* v0 = nullptr;  // xyz per cell
+    double* v1 = nullptr;
+    double* m0 = nullptr;
+    double* m1 = nullptr;
+
+    // particle snapshots: pinned staging + device copy (H2D on the side stream)
+    lbg_snapshot* snaps_h = nullptr;
+    lbg_snapshot* snaps_d = nullptr;
+    int snaps_cap = 0;
+    int n_snaps = 0;
+    // device binning for the mapping kernel (lbg_psm.cu)
+    int* bin_count = nullptr;
+    int* bin_start = nullptr;
+    int* bin_items = nullptr;
+    long long bin_items_cap = 0;
+    long long n_bins_cap = 0;
+    // hydro reduction scratch
+    double* red_rows = nullptr;  // n_snaps x 12
+    int* red_used = nullptr;
+    int red_cap = 0;
+    lbg_hydro_partial* red_h = nullptr;
+    double* red_rows_h = nullptr;
+    int* red_used_h = nullptr;
+
+    lbg::DeviceErrors* err_d = nullptr;
+    lbg::DeviceErrors* err_h = nullptr;  // pinned
+
+    cudaStream_t stream = nullptr;  // compute
+    cudaStream_t side = nullptr;    // H2D/D2H of particle data
+    cudaEvent_t ev_side = nullptr;
+
+    bool timing = false;
+    std::vector<lbg::TimedSpan> spans;
+    std::vector<cudaEvent_t> event_pool;
+    double acc_ms[LBG_NUM_CATS] = {};
+    long long acc_n[LBG_NUM_CATS] = {};
+
+    lbg::Comm* comm = nullptr;
+    long long device_bytes = 0;
+
+    double* src() const { return buf[cur]; }
+    double* dst() const { return buf[cur ^ 1]; }
+};
+
+namespace lbg {
+
+// error plumbing (lbg_core.cu)
+lbg_status set_error(lbg_status s, const std::string& msg);
+lbg_status cuda_check(cudaError_t e, const char* what);
+void count_launch();
+
+// timing spans around a launch (no-ops unless timing is on)
+struct Span {
+    lbg_block b;
+    int cat;
+    cudaEvent_t a = nullptr;
+    Span(lbg_block b_, int cat_);
+    ~Span();
+};
+
+}  // namespace lbg
+
+#define LBG_CUDA(call)                                                      \
+    do {                                                                    \
+        cudaError_t e_ = (call);                                            \
+        if (e_ != cudaSuccess) return ::lbg::cuda_check(e_, #call);         \
+    } while (0)
+
+#define LBG_LAUNCH_CHECK()                                                  \
+    do {                                                                    \
+        ::lbg::count_launch();                                              \
+        cudaError_t e_ = cudaGetLastError();                                \
+        if (e_ != cudaSuccess) return ::lbg::cuda_check(e_, "kernel launch"); \
+    } while (0)

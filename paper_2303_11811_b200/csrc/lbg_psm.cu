@@ -1,0 +1,626 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// K3 — particle -> cell mapping fused with the solid velocity
+//      (SubBlockRegistry::build + build_fraction_field + set_solid_velocities,
+//       psm.cpp:55-169)
+// K4 — hydrodynamic force/torque reduction (finalize_hydro_forces, psm.cpp:278-322)
+//
+// Mapping design (B200): the reference tests every particle against k^3 = 512 host
+// sub-blocks and then every cell against its sub-block list (~67 candidates per cell in
+// config 3). Here the particle list is binned on the device into 8^3-cell bins; each bin's
+// candidate list is sorted ascending by snapshot index (= id order), so a cell sees a
+// superset of the reference's eps > 0 candidates in the same order and the first-two /
+// third-is-overfull rule (psm.cpp:103-130) gives identical entries. One thread per cell
+// writes count/btot for every cell (coalesced, as the reference does) and, per entry, the
+// id, B and the solid velocity u + omega x (c - x) straight from the snapshot it just
+// tested (no id -> index search). Velocities must be the post-sync ones (sim.cpp:249-267),
+// which is why lbg_map is called after the host velocity sync.
+//
+// Reduction design: PARITY mode reproduces the reference's per-particle Neumaier sums in
+// lexicographic cell order bitwise: one warp per particle walks the particle's reach box
+// row by row; lanes load 32 consecutive cells, and the warp replays the hits in lane
+// order through the compensated adder (every lane holds the same accumulator). FAST mode
+// sums per lane, reduces with warp shuffles and adds one atomic per warp and particle.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "lbg_internal.cuh"
+
+namespace lbg {
+
+constexpr int kBin = 8;  // bin edge in cells
+
+struct BinGeom {
+    int nb[3];
+    int lo[3];    // block box lo (global cell coords)
+    int dims[3];  // block dims
+};
+
+__device__ __forceinline__ bool bin_range(const BinGeom& g, const lbg_snapshot& p, int blo[3], int bhi[3]) {
+    // cells whose reach-box test (psm.cpp:66-81: AABB distance <= r + 1/2) can pass
+    const double reach = p.r + 0.5;
+    for (int a = 0; a < 3; ++a) {
+        const double lo = p.x[a] - reach - g.lo[a];
+        const double hi = p.x[a] + reach - g.lo[a];
+        int c0 = (int)floor(lo) - 1, c1 = (int)floor(hi) + 1;  // generous, the cell test is exact
+        c0 = max(c0, 0);
+        c1 = min(c1, g.dims[a] - 1);
+        if (c1 < c0) return false;
+        blo[a] = c0 / kBin;
+        bhi[a] = c1 / kBin;
+    }
+    return true;
+}
+
+__global__ void bin_count_kernel(const lbg_snapshot* __restrict__ s, int n, BinGeom g, int* __restrict__ cnt) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    int lo[3], hi[3];
+    if (!bin_range(g, s[p], lo, hi)) return;
+    for (int z = lo[2]; z <= hi[2]; ++z)
+        for (int y = lo[1]; y <= hi[1]; ++y)
+            for (int x = lo[0]; x <= hi[0]; ++x) atomicAdd(&cnt[(z * g.nb[1] + y) * g.nb[0] + x], 1);
+}
+
+__global__ void bin_fill_kernel(const lbg_snapshot* __restrict__ s, int n, BinGeom g,
+                                const int* __restrict__ start, int* __restrict__ cursor,
+                                int* __restrict__ items) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    int lo[3], hi[3];
+    if (!bin_range(g, s[p], lo, hi)) return;
+    for (int z = lo[2]; z <= hi[2]; ++z)
+        for (int y = lo[1]; y <= hi[1]; ++y)
+            for (int x = lo[0]; x <= hi[0]; ++x) {
+                const int b = (z * g.nb[1] + y) * g.nb[0] + x;
+                const int pos = atomicAdd(&cursor[b], 1);
+                items[start[b] + pos] = p;
+            }
+}
+
+// per-bin ascending order (= id order) makes the candidate sequence deterministic
+__global__ void bin_sort_kernel(const int* __restrict__ start, const int* __restrict__ cnt, int nbins,
+                                int* __restrict__ items) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nbins) return;
+    int* a = items + start[b];
+    const int n = cnt[b];
+    for (int i = 1; i < n; ++i) {
+        const int v = a[i];
+        int j = i - 1;
+        while (j >= 0 && a[j] > v) {
+            a[j + 1] = a[j];
+            --j;
+        }
+        a[j + 1] = v;
+    }
+}
+
+struct MapArgs {
+    const lbg_snapshot* __restrict__ s;
+    BinGeom g;
+    const int* __restrict__ start;
+    const int* __restrict__ cnt;
+    const int* __restrict__ items;
+    uint8_t* __restrict__ count;
+    int* __restrict__ id0;
+    int* __restrict__ id1;
+    double* __restrict__ b0;
+    double* __restrict__ b1;
+    double* __restrict__ btot;
+    double* __restrict__ v0;
+    double* __restrict__ v1;
+    DeviceErrors* err;
+    int with_velocity;
+};
+
+// psm.cpp:28-32 overlap_fraction, psm.cpp:93-136 per-cell entry rule, psm.cpp:157-163 setU
+__global__ void __launch_bounds__(256) map_kernel(const MapArgs a) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y;
+    const int k = blockIdx.z;
+    const BinGeom& g = a.g;
+    bool over = false;
+    if (i < g.dims[0]) {
+        const long long c = ((long long)k * g.dims[1] + j) * g.dims[0] + i;
+        const int b = ((k / kBin) * g.nb[1] + (j / kBin)) * g.nb[0] + (i / kBin);
+        const double cc0 = (double)(g.lo[0] + i) + 0.5;
+        const double cc1 = (double)(g.lo[1] + j) + 0.5;
+        const double cc2 = (double)(g.lo[2] + k) + 0.5;
+        const int* list = a.items + a.start[b];
+        const int n = a.cnt[b];
+        int cnt = 0;
+        double sum = 0.0;
+        for (int t = 0; t < n; ++t) {
+            const lbg_snapshot& p = a.s[list[t]];
+            const double d0 = cc0 - p.x[0], d1 = cc1 - p.x[1], d2 = cc2 - p.x[2];
+            const double dist = sqrt((d0 * d0 + d1 * d1) + d2 * d2);
+            double eps = -(dist - p.r) + p.f_r;
+            eps = eps < 0.0 ? 0.0 : (1.0 < eps ? 1.0 : eps);  // std::clamp
+            if (eps <= 0.0) continue;
+            if (cnt >= 2) {
+                over = true;
+                break;
+            }
+            if (a.with_velocity) {
+                // v = u + cross(omega, c - x)  (vec3.hpp:92-94)
+                const double r0 = cc0 - p.x[0], r1 = cc1 - p.x[1], r2 = cc2 - p.x[2];
+                const double w0 = p.omega[0], w1 = p.omega[1], w2 = p.omega[2];
+                double* v = (cnt == 0 ? a.v0 : a.v1) + 3 * c;
+                v[0] = p.u[0] + (w1 * r2 - w2 * r1);
+                v[1] = p.u[1] + (w2 * r0 - w0 * r2);
+                v[2] = p.u[2] + (w0 * r1 - w1 * r0);
+            }
+            if (cnt == 0) {
+                a.id0[c] = p.id;
+                a.b0[c] = eps;
+            } else {
+                a.id1[c] = p.id;
+                a.b1[c] = eps;
+            }
+            ++cnt;
+            sum += eps;
+        }
+        a.count[c] = (uint8_t)cnt;
+        a.btot[c] = sum < 1.0 ? sum : 1.0;  // std::min(1.0, sum)
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, over);
+    if (m && (threadIdx.x & 31) == 0) atomicAdd(&a.err->overfull, (unsigned long long)__popc(m));
+}
+
+__device__ __forceinline__ int find_snapshot(const lbg_snapshot* s, int n, int id) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (s[mid].id < id)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return (lo < n && s[lo].id == id) ? lo : -1;
+}
+
+// psm.cpp:138-169 — standalone setU over an existing fraction field
+__global__ void __launch_bounds__(256) setu_kernel(const lbg_snapshot* __restrict__ s, int n, BinGeom g,
+                                                   const uint8_t* __restrict__ count,
+                                                   const int* __restrict__ id0, const int* __restrict__ id1,
+                                                   double* __restrict__ v0, double* __restrict__ v1,
+                                                   DeviceErrors* err) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y;
+    const int k = blockIdx.z;
+    int unknown = 0;
+    if (i < g.dims[0]) {
+        const long long c = ((long long)k * g.dims[1] + j) * g.dims[0] + i;
+        const int cnt = count[c];
+        const double cc[3] = {(double)(g.lo[0] + i) + 0.5, (double)(g.lo[1] + j) + 0.5,
+                              (double)(g.lo[2] + k) + 0.5};
+        for (int e = 0; e < cnt; ++e) {
+            const int p = find_snapshot(s, n, e == 0 ? id0[c] : id1[c]);
+            if (p < 0) {
+                ++unknown;
+                continue;
+            }
+            const double r0 = cc[0] - s[p].x[0], r1 = cc[1] - s[p].x[1], r2 = cc[2] - s[p].x[2];
+            const double* w = s[p].omega;
+            double* v = (e == 0 ? v0 : v1) + 3 * c;
+            v[0] = s[p].u[0] + (w[1] * r2 - w[2] * r1);
+            v[1] = s[p].u[1] + (w[2] * r0 - w[0] * r2);
+            v[2] = s[p].u[2] + (w[0] * r1 - w[1] * r0);
+        }
+    }
+    unsigned v = unknown;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (v && (threadIdx.x & 31) == 0) atomicAdd(&err->unknown, (unsigned long long)v);
+}
+
+// ---------------------------------------------------------------- K4 reduction
+__device__ __forceinline__ void nm_add(double& sum, double& comp, double v) {  // vec3.hpp:75-82
+    const double t = sum + v;
+    if (fabs(sum) >= fabs(v))
+        comp += (sum - t) + v;
+    else
+        comp += (v - t) + sum;
+    sum = t;
+}
+
+struct ReduceArgs {
+    const lbg_snapshot* __restrict__ s;
+    int n;
+    BinGeom g;
+    const uint8_t* __restrict__ count;
+    const int* __restrict__ id0;
+    const int* __restrict__ id1;
+    double* __restrict__ m0;
+    double* __restrict__ m1;
+    double* __restrict__ rows;  // n x 12
+    int* __restrict__ used;
+    unsigned long long* __restrict__ visited;  // entries found by the box walks
+    int fast;
+};
+
+// one warp per particle: lexicographic walk of the reach box
+__global__ void __launch_bounds__(128) reduce_kernel(const ReduceArgs a) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= a.n) return;
+    const lbg_snapshot& p = a.s[warp];
+    const BinGeom& g = a.g;
+    const double reach = p.r + 0.5;
+    int lo[3], hi[3];
+    for (int d = 0; d < 3; ++d) {
+        lo[d] = max((int)floor(p.x[d] - reach - g.lo[d]) - 1, 0);
+        hi[d] = min((int)floor(p.x[d] + reach - g.lo[d]) + 1, g.dims[d] - 1);
+    }
+    double fs[3] = {0, 0, 0}, fc[3] = {0, 0, 0}, ts[3] = {0, 0, 0}, tc[3] = {0, 0, 0};
+    unsigned long long hits = 0;
+    const int id = p.id;
+    for (int k = lo[2]; k <= hi[2]; ++k)
+        for (int j = lo[1]; j <= hi[1]; ++j)
+            for (int i0 = lo[0]; i0 <= hi[0]; i0 += 32) {
+                const int i = i0 + lane;
+                int e = -1;
+                long long c = 0;
+                if (i <= hi[0]) {
+                    c = ((long long)k * g.dims[1] + j) * g.dims[0] + i;
+                    const int cnt = a.count[c];
+                    if (cnt > 0 && a.id0[c] == id) e = 0;
+                    else if (cnt > 1 && a.id1[c] == id) e = 1;
+                }
+                double m[3] = {0, 0, 0}, t[3] = {0, 0, 0};
+                if (e >= 0) {
+                    double* mp = (e == 0 ? a.m0 : a.m1) + 3 * c;
+                    m[0] = mp[0];
+                    m[1] = mp[1];
+                    m[2] = mp[2];
+                    mp[0] = mp[1] = mp[2] = 0.0;  // the reference clears the scratch
+                    const double r0 = ((double)(g.lo[0] + i) + 0.5) - p.x[0];
+                    const double r1 = ((double)(g.lo[1] + j) + 0.5) - p.x[1];
+                    const double r2 = ((double)(g.lo[2] + k) + 0.5) - p.x[2];
+                    t[0] = r1 * m[2] - r2 * m[1];  // cross(center - x, m)
+                    t[1] = r2 * m[0] - r0 * m[2];
+                    t[2] = r0 * m[1] - r1 * m[0];
+                }
+                unsigned mask = __ballot_sync(0xffffffffu, e >= 0);
+                hits += __popc(mask);
+                if (a.fast) {
+                    for (int d = 0; d < 3; ++d) {
+                        fs[d] += m[d];
+                        ts[d] += t[d];
+                    }
+                    continue;
+                }
+                while (mask) {  // replay hits in lane (= lexicographic) order
+                    const int src = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    for (int d = 0; d < 3; ++d) nm_add(fs[d], fc[d], __shfl_sync(0xffffffffu, m[d], src));
+                    for (int d = 0; d < 3; ++d) nm_add(ts[d], tc[d], __shfl_sync(0xffffffffu, t[d], src));
+                }
+            }
+    if (a.fast) {
+        for (int d = 0; d < 3; ++d)
+            for (int o = 16; o > 0; o >>= 1) {
+                fs[d] += __shfl_xor_sync(0xffffffffu, fs[d], o);
+                ts[d] += __shfl_xor_sync(0xffffffffu, ts[d], o);
+            }
+    }
+    if (lane == 0) {
+        double* row = a.rows + 12 * (size_t)warp;
+        for (int d = 0; d < 3; ++d) {
+            row[d] = fs[d];
+            row[3 + d] = fc[d];
+            row[6 + d] = ts[d];
+            row[9 + d] = tc[d];
+        }
+        a.used[warp] = hits > 0;
+        if (hits) atomicAdd(a.visited, hits);
+    }
+}
+
+// total entries in the field + unknown-id check (psm.cpp:300-303)
+__global__ void __launch_bounds__(256) entry_census_kernel(const lbg_snapshot* __restrict__ s, int n,
+                                                           long long cells, const uint8_t* __restrict__ count,
+                                                           const int* __restrict__ id0, const int* __restrict__ id1,
+                                                           unsigned long long* __restrict__ total,
+                                                           DeviceErrors* err) {
+    const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned e = 0, unk = 0;
+    if (c < cells) {
+        const int cnt = count[c];
+        e = cnt;
+        if (cnt > 0 && find_snapshot(s, n, id0[c]) < 0) ++unk;
+        if (cnt > 1 && find_snapshot(s, n, id1[c]) < 0) ++unk;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        e += __shfl_xor_sync(0xffffffffu, e, o);
+        unk += __shfl_xor_sync(0xffffffffu, unk, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (e) atomicAdd(total, (unsigned long long)e);
+        if (unk) atomicAdd(&err->unknown, (unsigned long long)unk);
+    }
+}
+
+static BinGeom geom(lbg_block b) {
+    BinGeom g;
+    const int d[3] = {b->L.nx, b->L.ny, b->L.nz};
+    for (int a = 0; a < 3; ++a) {
+        g.dims[a] = d[a];
+        g.lo[a] = b->lo[a];
+        g.nb[a] = (d[a] + kBin - 1) / kBin;
+    }
+    return g;
+}
+
+static lbg_status upload_snapshots(lbg_block b, const lbg_snapshot* snaps, int n) {
+    for (int t = 1; t < n; ++t)
+        if (snaps[t].id <= snaps[t - 1].id)
+            return set_error(LBG_INVALID, "snapshots must be sorted by ascending unique id");
+    if (n > b->snaps_cap) {
+        LBG_CUDA(cudaStreamSynchronize(b->side));
+        LBG_CUDA(cudaStreamSynchronize(b->stream));
+        if (b->snaps_h) cudaFreeHost(b->snaps_h);
+        if (b->snaps_d) cudaFree(b->snaps_d);
+        b->snaps_h = nullptr;
+        b->snaps_d = nullptr;
+        const int cap = std::max(n, 2 * b->snaps_cap);
+        LBG_CUDA(cudaMallocHost(&b->snaps_h, sizeof(lbg_snapshot) * cap));
+        LBG_CUDA(cudaMalloc(&b->snaps_d, sizeof(lbg_snapshot) * cap));
+        b->snaps_cap = cap;
+    }
+    // staging buffer may still feed the previous copy
+    LBG_CUDA(cudaEventSynchronize(b->ev_side));
+    if (n > 0) std::memcpy(b->snaps_h, snaps, sizeof(lbg_snapshot) * n);
+    // the previous step's kernels may still read snaps_d: order the copy after them
+    LBG_CUDA(cudaEventRecord(b->ev_side, b->stream));
+    LBG_CUDA(cudaStreamWaitEvent(b->side, b->ev_side, 0));
+    if (n > 0)
+        LBG_CUDA(cudaMemcpyAsync(b->snaps_d, b->snaps_h, sizeof(lbg_snapshot) * n,
+                                 cudaMemcpyHostToDevice, b->side));
+    LBG_CUDA(cudaEventRecord(b->ev_side, b->side));
+    LBG_CUDA(cudaStreamWaitEvent(b->stream, b->ev_side, 0));
+    b->n_snaps = n;
+    return LBG_OK;
+}
+
+static lbg_status ensure_bins(lbg_block b, long long nbins) {
+    if (nbins <= b->n_bins_cap) return LBG_OK;
+    if (b->bin_count) cudaFree(b->bin_count);
+    if (b->bin_start) cudaFree(b->bin_start);
+    LBG_CUDA(cudaMalloc(&b->bin_count, sizeof(int) * 2 * nbins));  // count + cursor
+    LBG_CUDA(cudaMalloc(&b->bin_start, sizeof(int) * (nbins + 1)));
+    b->n_bins_cap = nbins;
+    return LBG_OK;
+}
+
+}  // namespace lbg
+
+using namespace lbg;
+
+static lbg_status need_coupling(lbg_block b) {
+    if (!b) return set_error(LBG_INVALID, "null block");
+    if (!b->coupling) return set_error(LBG_INVALID, "block was created without coupling fields");
+    return LBG_OK;
+}
+
+extern "C" {
+
+lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisions) {
+    if (lbg_status s = need_coupling(b)) return s;
+    if (subdivisions < 1) return set_error(LBG_CONFIG_ERROR, "subdivisions must be >= 1");
+    LBG_CUDA(cudaSetDevice(b->device));
+    Span span(b, LBG_CAT_MAPPING);
+    if (lbg_status s = upload_snapshots(b, snaps, n)) return s;
+    const BinGeom g = geom(b);
+    const long long nbins = (long long)g.nb[0] * g.nb[1] * g.nb[2];
+    if (lbg_status s = ensure_bins(b, nbins)) return s;
+    int* cnt = b->bin_count;
+    int* cursor = b->bin_count + nbins;
+    LBG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * 2 * nbins, b->stream));
+    if (n > 0) {
+        bin_count_kernel<<<(n + 127) / 128, 128, 0, b->stream>>>(b->snaps_d, n, g, cnt);
+        LBG_LAUNCH_CHECK();
+    }
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, cnt, b->bin_start + 1, (int)nbins, b->stream);
+    void* tmp = nullptr;
+    LBG_CUDA(cudaMallocAsync(&tmp, tmp_bytes, b->stream));
+    LBG_CUDA(cudaMemsetAsync(b->bin_start, 0, sizeof(int), b->stream));
+    cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, cnt, b->bin_start + 1, (int)nbins, b->stream);
+    LBG_LAUNCH_CHECK();
+    LBG_CUDA(cudaFreeAsync(tmp, b->stream));
+    int total = 0;
+    LBG_CUDA(cudaMemcpyAsync(&total, b->bin_start + nbins, sizeof(int), cudaMemcpyDeviceToHost, b->stream));
+    LBG_CUDA(cudaStreamSynchronize(b->stream));
+    if (total > b->bin_items_cap) {
+        if (b->bin_items) cudaFree(b->bin_items);
+        b->bin_items_cap = std::max<long long>(total, 2 * b->bin_items_cap);
+        LBG_CUDA(cudaMalloc(&b->bin_items, sizeof(int) * std::max<long long>(b->bin_items_cap, 1)));
+    }
+    if (b->bin_items == nullptr) {
+        LBG_CUDA(cudaMalloc(&b->bin_items, sizeof(int)));
+        b->bin_items_cap = 1;
+    }
+    if (n > 0) {
+        bin_fill_kernel<<<(n + 127) / 128, 128, 0, b->stream>>>(b->snaps_d, n, g, b->bin_start, cursor,
+                                                                b->bin_items);
+        LBG_LAUNCH_CHECK();
+        bin_sort_kernel<<<(unsigned)((nbins + 127) / 128), 128, 0, b->stream>>>(b->bin_start, cnt, (int)nbins,
+                                                                                b->bin_items);
+        LBG_LAUNCH_CHECK();
+    }
+    MapArgs a{};
+    a.s = b->snaps_d;
+    a.g = g;
+    a.start = b->bin_start;
+    a.cnt = cnt;
+    a.items = b->bin_items;
+    a.count = b->count;
+    a.id0 = b->id0;
+    a.id1 = b->id1;
+    a.b0 = b->b0;
+    a.b1 = b->b1;
+    a.btot = b->btot;
+    a.v0 = b->v0;
+    a.v1 = b->v1;
+    a.err = b->err_d;
+    a.with_velocity = 1;
+    dim3 grid((g.dims[0] + 127) / 128, g.dims[1], g.dims[2]);
+    map_kernel<<<grid, 128, 0, b->stream>>>(a);
+    LBG_LAUNCH_CHECK();
+    return LBG_OK;
+}
+
+lbg_status lbg_set_solid_velocities(lbg_block b, const lbg_snapshot* snaps, int n) {
+    if (lbg_status s = need_coupling(b)) return s;
+    LBG_CUDA(cudaSetDevice(b->device));
+    Span span(b, LBG_CAT_SETU);
+    if (lbg_status s = upload_snapshots(b, snaps, n)) return s;
+    const BinGeom g = geom(b);
+    dim3 grid((g.dims[0] + 127) / 128, g.dims[1], g.dims[2]);
+    setu_kernel<<<grid, 128, 0, b->stream>>>(b->snaps_d, n, g, b->count, b->id0, b->id1, b->v0, b->v1,
+                                            b->err_d);
+    LBG_LAUNCH_CHECK();
+    return LBG_OK;
+}
+
+lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int capacity, int* n_out) {
+    if (lbg_status s = need_coupling(b)) return s;
+    if (n_out) *n_out = 0;
+    LBG_CUDA(cudaSetDevice(b->device));
+    const int n = b->n_snaps;
+    if (n > b->red_cap) {
+        if (b->red_rows) cudaFree(b->red_rows);
+        if (b->red_used) cudaFree(b->red_used);
+        if (b->red_rows_h) cudaFreeHost(b->red_rows_h);
+        if (b->red_used_h) cudaFreeHost(b->red_used_h);
+        b->red_cap = std::max(n, 2 * b->red_cap);
+        LBG_CUDA(cudaMalloc(&b->red_rows, sizeof(double) * 12 * b->red_cap + 16));
+        LBG_CUDA(cudaMalloc(&b->red_used, sizeof(int) * b->red_cap));
+        LBG_CUDA(cudaMallocHost(&b->red_rows_h, sizeof(double) * 12 * b->red_cap + 16));
+        LBG_CUDA(cudaMallocHost(&b->red_used_h, sizeof(int) * b->red_cap));
+    }
+    if (!b->red_rows) {
+        LBG_CUDA(cudaMalloc(&b->red_rows, 16 + sizeof(double) * 12));
+        LBG_CUDA(cudaMallocHost(&b->red_rows_h, 16 + sizeof(double) * 12));
+    }
+    // visited/total counters live after the rows
+    unsigned long long* ctr = (unsigned long long*)(b->red_rows + 12 * (size_t)std::max(b->red_cap, 1));
+    const BinGeom g = geom(b);
+    const long long cells = (long long)g.dims[0] * g.dims[1] * g.dims[2];
+    {
+        Span span(b, LBG_CAT_REDF);
+        LBG_CUDA(cudaMemsetAsync(ctr, 0, 16, b->stream));
+        entry_census_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, b->stream>>>(
+            b->snaps_d, n, cells, b->count, b->id0, b->id1, ctr + 1, b->err_d);
+        LBG_LAUNCH_CHECK();
+        if (n > 0) {
+            ReduceArgs a{};
+            a.s = b->snaps_d;
+            a.n = n;
+            a.g = g;
+            a.count = b->count;
+            a.id0 = b->id0;
+            a.id1 = b->id1;
+            a.m0 = b->m0;
+            a.m1 = b->m1;
+            a.rows = b->red_rows;
+            a.used = b->red_used;
+            a.visited = ctr;
+            a.fast = mode == LBG_REDUCE_FAST;
+            reduce_kernel<<<(n * 32 + 127) / 128, 128, 0, b->stream>>>(a);
+            LBG_LAUNCH_CHECK();
+            LBG_CUDA(cudaMemcpyAsync(b->red_rows_h, b->red_rows, sizeof(double) * 12 * n,
+                                     cudaMemcpyDeviceToHost, b->stream));
+            LBG_CUDA(cudaMemcpyAsync(b->red_used_h, b->red_used, sizeof(int) * n, cudaMemcpyDeviceToHost,
+                                     b->stream));
+        }
+    }
+    unsigned long long ctr_h[2] = {0, 0};
+    LBG_CUDA(cudaMemcpyAsync(ctr_h, ctr, 16, cudaMemcpyDeviceToHost, b->stream));
+    LBG_CUDA(cudaStreamSynchronize(b->stream));
+    if (lbg_status s = lbg_sync(b, nullptr)) {
+        if (s == LBG_SYNC_ERROR)
+            return set_error(LBG_SYNC_ERROR, "hydrodynamic force for unknown particle id");
+        return s;
+    }
+    if (ctr_h[0] != ctr_h[1])
+        return set_error(LBG_INVALID, "fraction entries outside their particle's reach box (" +
+                                          std::to_string(ctr_h[1] - ctr_h[0]) +
+                                          " entries); the field was not produced by lbg_map");
+    int m = 0;
+    for (int p = 0; p < n; ++p) {
+        if (!b->red_used_h[p]) continue;
+        if (m >= capacity) return set_error(LBG_INVALID, "hydro partial output capacity too small");
+        lbg_hydro_partial& h = out[m++];
+        h.id = b->snaps_h[p].id;
+        const double* r = b->red_rows_h + 12 * (size_t)p;
+        for (int d = 0; d < 3; ++d) {
+            h.f[d] = r[d];
+            h.f_comp[d] = r[3 + d];
+            h.t[d] = r[6 + d];
+            h.t_comp[d] = r[9 + d];
+        }
+    }
+    if (n_out) *n_out = m;
+    return LBG_OK;
+}
+
+static lbg_status copy_frac(lbg_block b, bool up, uint8_t* count, int* id0, int* id1, double* b0, double* b1,
+                            double* btot) {
+    if (lbg_status s = need_coupling(b)) return s;
+    LBG_CUDA(cudaSetDevice(b->device));
+    const size_t n = (size_t)b->L.nx * b->L.ny * b->L.nz;
+    const auto kind = up ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+    struct P {
+        void* d;
+        void* h;
+        size_t bytes;
+    } ps[] = {{b->count, count, n}, {b->id0, id0, 4 * n}, {b->id1, id1, 4 * n},
+              {b->b0, b0, 8 * n},   {b->b1, b1, 8 * n},   {b->btot, btot, 8 * n}};
+    for (auto& p : ps) {
+        if (!p.h) continue;
+        LBG_CUDA(cudaMemcpyAsync(up ? p.d : p.h, up ? p.h : p.d, p.bytes, kind, b->stream));
+    }
+    LBG_CUDA(cudaStreamSynchronize(b->stream));
+    return LBG_OK;
+}
+
+lbg_status lbg_upload_fraction(lbg_block b, const uint8_t* count, const int* id0, const int* id1,
+                               const double* b0, const double* b1, const double* btot) {
+    return copy_frac(b, true, (uint8_t*)count, (int*)id0, (int*)id1, (double*)b0, (double*)b1, (double*)btot);
+}
+
+lbg_status lbg_download_fraction(lbg_block b, uint8_t* count, int* id0, int* id1, double* b0, double* b1,
+                                 double* btot) {
+    return copy_frac(b, false, count, id0, id1, b0, b1, btot);
+}
+
+static lbg_status copy_vec_pair(lbg_block b, bool up, double* d0, double* d1, double* h0, double* h1) {
+    if (lbg_status s = need_coupling(b)) return s;
+    LBG_CUDA(cudaSetDevice(b->device));
+    const size_t bytes = sizeof(double) * 3 * (size_t)b->L.nx * b->L.ny * b->L.nz;
+    const auto kind = up ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+    if (h0) LBG_CUDA(cudaMemcpyAsync(up ? d0 : h0, up ? h0 : d0, bytes, kind, b->stream));
+    if (h1) LBG_CUDA(cudaMemcpyAsync(up ? d1 : h1, up ? h1 : d1, bytes, kind, b->stream));
+    LBG_CUDA(cudaStreamSynchronize(b->stream));
+    return LBG_OK;
+}
+
+lbg_status lbg_upload_solid_velocity(lbg_block b, const double* v0, const double* v1) {
+    return copy_vec_pair(b, true, b ? b->v0 : nullptr, b ? b->v1 : nullptr, (double*)v0, (double*)v1);
+}
+lbg_status lbg_download_solid_velocity(lbg_block b, double* v0, double* v1) {
+    return copy_vec_pair(b, false, b ? b->v0 : nullptr, b ? b->v1 : nullptr, v0, v1);
+}
+lbg_status lbg_upload_scratch(lbg_block b, const double* m0, const double* m1) {
+    return copy_vec_pair(b, true, b ? b->m0 : nullptr, b ? b->m1 : nullptr, (double*)m0, (double*)m1);
+}
+lbg_status lbg_download_scratch(lbg_block b, double* m0, double* m1) {
+    return copy_vec_pair(b, false, b ? b->m0 : nullptr, b ? b->m1 : nullptr, m0, m1);
+}
+
+}  // extern "C"

@@ -1,0 +1,413 @@
+"""GPU parity: every liblbg operator against the CPU oracle on identical inputs.
+
+The bar is bitwise equality (fp64, --fmad=false kernels vs the -ffp-contract=off reference
+restatement) for PDFs, ghost fills, BC values, fraction fields, solid velocities, momentum
+scratch and PARITY-mode force partials; FAST-mode partials use the L1-mass tolerance of
+SURVEY.md §8(c): |dF| <= 1e-12 * sum |m|.
+"""
+import numpy as np
+import pytest
+
+from conftest import W, equal_bits, interior, n_bit_mismatch, random_pdf
+from oracle.pyoracle import make_snapshots, new_fraction, new_scratch, new_svel
+
+pytestmark = pytest.mark.gpu
+
+ALL_P = (1, 1, 1)
+
+
+def run_oracle_step(oracle, dims, src, tau, fext, periodic=ALL_P, box=None):
+    src = src.copy()
+    dst = np.zeros_like(src)
+    oracle.fill_periodic(dims, src, periodic)
+    lo, hi = box if box else ((0, 0, 0), dims)
+    bad = oracle.collide_stream(dims, src, dst, tau, fext, lo, hi)
+    return src, dst, bad
+
+
+@pytest.mark.parametrize("dims,fext", [((8, 8, 8), (1e-5, 0.0, -2e-5)),
+                                       ((13, 7, 5), (0.0, 0.0, 0.0)),
+                                       ((40, 3, 9), (2e-6, 1e-6, 0.0))])
+def test_fused_sweep_bitwise(gpu, oracle, dims, fext):
+    src0 = random_pdf(dims, seed=29)
+    tau = 0.8
+    src_o, dst_o, bad = run_oracle_step(oracle, dims, src0, tau, fext)
+    assert bad == 0
+    blk = gpu.Block(dims)
+    blk.upload_src(src0)
+    blk.fill_periodic(ALL_P, full=True)
+    blk.sweep(gpu.FluidParams(tau, fext), gpu.CellBox((0, 0, 0), dims))
+    blk.sync()
+    assert equal_bits(blk.download_src(), src_o), "periodic ghost fill differs"
+    got = blk.download_dst()
+    assert n_bit_mismatch(interior(got), interior(dst_o)) == 0
+
+
+def test_sweep_sub_boxes_and_shell(gpu, oracle):
+    dims = (20, 11, 9)
+    tau, fext = 0.73, (0.0, 3e-6, 0.0)
+    src0 = random_pdf(dims, seed=3)
+    src_o = src0.copy()
+    oracle.fill_periodic(dims, src_o, ALL_P)
+    dst_o = np.zeros_like(src_o)
+    inner = ((1, 1, 1), (dims[0] - 1, dims[1] - 1, dims[2] - 1))
+    oracle.collide_stream(dims, src_o, dst_o, tau, fext, *inner)
+    shell = gpu.boundary_shell(dims)
+    for b in shell:
+        oracle.collide_stream(dims, src_o, dst_o, tau, fext, b.lo, b.hi)
+
+    blk = gpu.Block(dims)
+    blk.upload_src(src0)
+    blk.fill_periodic(ALL_P, full=True)
+    p = gpu.FluidParams(tau, fext)
+    blk.sweep(p, gpu.CellBox(*inner))
+    blk.sweep_boxes(p, shell)
+    blk.sync()
+    assert equal_bits(interior(blk.download_dst()), interior(dst_o))
+
+
+def test_unfused_stream(gpu, oracle):
+    dims = (6, 6, 6)
+    src0 = random_pdf(dims, seed=17)
+    src_o = src0.copy()
+    oracle.fill_periodic(dims, src_o, ALL_P)
+    dst_o = np.zeros_like(src_o)
+    oracle.stream(dims, src_o, dst_o, (0, 0, 0), dims)
+    blk = gpu.Block(dims)
+    blk.upload_src(src0)
+    blk.fill_periodic(ALL_P, full=True)
+    blk.stream_only(gpu.CellBox((0, 0, 0), dims))
+    assert equal_bits(interior(blk.download_dst()), interior(dst_o))
+
+
+@pytest.mark.parametrize("periodic", [(1, 1, 1), (1, 0, 1), (0, 1, 0), (0, 0, 1)])
+def test_periodic_fill_full_bitwise_and_pull_only_equivalent(gpu, oracle, periodic):
+    dims = (9, 5, 7)
+    src0 = random_pdf(dims, seed=5)
+    src_o = src0.copy()
+    oracle.fill_periodic(dims, src_o, periodic)
+    blk = gpu.Block(dims)
+    blk.upload_src(src0)
+    blk.fill_periodic(periodic, full=True)
+    assert equal_bits(blk.download_src(), src_o)
+    # pull-only fill feeds the sweep exactly the same values
+    tau, fext = 0.9, (0.0, 0.0, 1e-6)
+    dst_o = np.zeros_like(src_o)
+    oracle.collide_stream(dims, src_o, dst_o, tau, fext, (0, 0, 0), dims)
+    blk.upload_src(src0)
+    blk.fill_periodic(periodic, full=False)
+    blk.sweep(gpu.FluidParams(tau, fext), gpu.CellBox((0, 0, 0), dims))
+    blk.sync()
+    if all(periodic):
+        assert equal_bits(interior(blk.download_dst()), interior(dst_o))
+
+
+def bed_spec(gpu, zm_vel=(0.0, 0.0, 2.2472e-3), rho_out=1.0):
+    spec = gpu.BcSpec()
+    for f in range(4):
+        spec.faces[f] = gpu.FaceBc(gpu.BcKind.no_slip)
+    spec.faces[4] = gpu.FaceBc(gpu.BcKind.velocity, zm_vel)
+    spec.faces[5] = gpu.FaceBc(gpu.BcKind.pressure, (0.0, 0.0, 0.0), rho_out)
+    return spec
+
+
+def spec_arrays(spec):
+    kinds = [int(f.kind) for f in spec.faces]
+    uw = np.array([f.u_wall for f in spec.faces], dtype=np.float64).ravel()
+    rho = [f.rho for f in spec.faces]
+    return kinds, uw, rho
+
+
+@pytest.mark.parametrize("case", ["bed", "channel_y", "mixed_touch"])
+def test_apply_boundaries_bitwise(gpu, oracle, case):
+    dims = (7, 6, 8)
+    src0 = random_pdf(dims, seed=41)
+    if case == "bed":
+        spec, touches, periodic = bed_spec(gpu), (1, 1, 1, 1, 1, 1), (0, 0, 0)
+    elif case == "channel_y":
+        spec = gpu.BcSpec()
+        spec.faces[2] = gpu.FaceBc(gpu.BcKind.no_slip)
+        spec.faces[3] = gpu.FaceBc(gpu.BcKind.velocity, (0.01, 0.0, 0.002))
+        touches, periodic = (1, 1, 1, 1, 1, 1), (1, 0, 1)
+    else:  # a block touching only some domain faces
+        spec, touches, periodic = bed_spec(gpu, rho_out=1.01), (1, 0, 0, 1, 1, 0), (0, 0, 0)
+    src_o = src0.copy()
+    oracle.fill_periodic(dims, src_o, periodic)
+    oracle.apply_boundaries(dims, src_o, *spec_arrays(spec), touches)
+    blk = gpu.Block(dims)
+    blk.upload_src(src0)
+    blk.fill_periodic(periodic, full=True)
+    blk.apply_boundaries(spec, touches)
+    blk.sync()
+    got = blk.download_src()
+    assert n_bit_mismatch(got, src_o) == 0
+
+
+def test_stability_guard_raises(gpu):
+    dims = (4, 4, 4)
+    blk = gpu.Block(dims)
+    blk.fill_equilibrium(1.0, (0.0, 0.0, 0.0))
+    a = blk.download_src()
+    a[1, 3, 3, 3] = 5.0  # test_lattice_lbm.cpp:324-334
+    blk.upload_src(a)
+    gpu.fill_periodic_ghosts(blk, ALL_P)
+    with pytest.raises(gpu.NumericError, match="fluid instability"):
+        gpu.collide_stream(blk, gpu.FluidParams(0.51), gpu.CellBox((0, 0, 0), dims))
+
+
+def test_config_validation_errors(gpu):
+    blk = gpu.Block((4, 4, 4))
+    with pytest.raises(gpu.ConfigError):
+        blk.sweep(gpu.FluidParams(0.4), gpu.CellBox((0, 0, 0), (4, 4, 4)))
+    spec = gpu.BcSpec()
+    spec.faces[2] = gpu.FaceBc(gpu.BcKind.no_slip)
+    with pytest.raises(gpu.ConfigError):
+        blk.apply_boundaries(spec, (1,) * 6)
+
+
+def shear_wave(oracle, dims):
+    nx, ny, nz = dims
+    a = np.zeros((19, nz + 2, ny + 2, nx + 2))
+    for k in range(nz):
+        for j in range(ny):
+            for i in range(nx):
+                u = (0.02 * np.sin(2.0 * np.pi * (j + 0.5) / ny), 0.015 * np.cos(2.0 * np.pi * (k + 0.5) / nz),
+                     0.01 * np.sin(2.0 * np.pi * (i + 0.5) / nx))
+                a[:, k + 1, j + 1, i + 1] = oracle.equilibrium(1.0, u)
+    return a
+
+
+def test_shear_wave_100_steps_bitwise(gpu, oracle):
+    """SURVEY.md §7 minimum slice: periodic shear wave, tau 0.8, 1 and 100 steps."""
+    dims = (24, 20, 16)
+    src = shear_wave(oracle, dims)
+    blk = gpu.Block(dims)
+    blk.upload_src(src)
+    p = gpu.FluidParams(0.8)
+    o_src = src.copy()
+    for step in range(100):
+        dst = np.zeros_like(o_src)
+        oracle.fill_periodic(dims, o_src, ALL_P)
+        oracle.collide_stream(dims, o_src, dst, 0.8, (0, 0, 0), (0, 0, 0), dims)
+        o_src = dst
+        blk.fill_periodic(ALL_P, full=False)
+        blk.sweep(p, gpu.CellBox((0, 0, 0), dims))
+        blk.swap()
+        if step in (0, 99):
+            blk.sync()
+            assert equal_bits(interior(blk.download_src()), interior(o_src)), f"step {step + 1}"
+    m = blk.total_mass()
+    assert abs(m - oracle.total_mass(dims, o_src)) <= 1e-12 * m
+
+
+# ----------------------------------------------------------------------------- PSM
+def random_fraction(dims, seed, n_ids=4, cover=0.4):
+    rng = np.random.default_rng(seed)
+    nx, ny, nz = dims
+    f = new_fraction(dims)
+    cnt = rng.random((nz, ny, nx))
+    f["count"][:] = np.where(cnt < cover / 2, 2, np.where(cnt < cover, 1, 0)).astype(np.uint8)
+    f["id0"][:] = rng.integers(0, n_ids, (nz, ny, nx))
+    f["id1"][:] = rng.integers(0, n_ids, (nz, ny, nx))
+    f["b0"][:] = rng.random((nz, ny, nx))
+    f["b1"][:] = rng.random((nz, ny, nx)) * (1 - f["b0"])
+    f["btot"][:] = np.minimum(1.0, f["b0"] + np.where(f["count"] > 1, f["b1"], 0.0))
+    sv = new_svel(dims)
+    sv["v0"][:] = 0.02 * (rng.random((nz, ny, nx, 3)) - 0.5)
+    sv["v1"][:] = 0.02 * (rng.random((nz, ny, nx, 3)) - 0.5)
+    return f, sv
+
+
+@pytest.mark.parametrize("fext", [(0.0, 0.0, 0.0), (1e-5, 0.0, -4e-6)])
+def test_psm_sweep_bitwise(gpu, oracle, fext):
+    dims = (12, 10, 9)
+    src0 = random_pdf(dims, seed=67)
+    frac, sv = random_fraction(dims, seed=1)
+    tau = 0.65
+    src_o = src0.copy()
+    oracle.fill_periodic(dims, src_o, ALL_P)
+    dst_o = np.zeros_like(src_o)
+    scr = new_scratch(dims)
+    bad = oracle.psm_collide_stream(dims, src_o, dst_o, tau, fext, (0, 0, 0), dims, frac, sv, scr)
+    assert bad == 0
+    blk = gpu.Block(dims, coupling=True)
+    blk.upload_src(src0)
+    blk.upload_fraction(frac)
+    blk.upload_solid_velocity(sv["v0"], sv["v1"])
+    blk.fill_periodic(ALL_P, full=True)
+    blk.sweep(gpu.FluidParams(tau, fext), gpu.CellBox((0, 0, 0), dims))
+    blk.sync()
+    assert n_bit_mismatch(interior(blk.download_dst()), interior(dst_o)) == 0
+    m0, m1 = blk.download_scratch()
+    c = frac["count"]
+    assert equal_bits(m0[c > 0], scr["m0"][c > 0])
+    assert equal_bits(m1[c > 1], scr["m1"][c > 1])
+
+
+def test_psm_with_zero_fraction_is_plain_srt(gpu, oracle):
+    """test_psm.cpp:269-304 — B = 0 PSM == SRT, bitwise."""
+    dims = (12, 12, 12)
+    src0 = random_pdf(dims, seed=68)
+    p = gpu.FluidParams(0.8, (1e-5, 0.0, 0.0))
+    a = gpu.Block(dims, coupling=True)
+    b = gpu.Block(dims)
+    for blk in (a, b):
+        blk.upload_src(src0)
+        blk.fill_periodic(ALL_P)
+        blk.sweep(p, gpu.CellBox((0, 0, 0), dims))
+        blk.sync()
+    assert equal_bits(a.download_dst(), b.download_dst())
+
+
+def spheres(oracle, centers, radii, ids=None, u=None, w=None):
+    n = len(centers)
+    ids = list(range(n)) if ids is None else ids
+    fr = [oracle.f_of_r(r) for r in radii]
+    return make_snapshots(ids, centers, radii, fr, u, w)
+
+
+@pytest.mark.parametrize("lo", [(0, 0, 0), (16, 8, 24)])
+def test_mapping_and_solid_velocity_bitwise(gpu, oracle, lo):
+    dims = (40, 36, 44)
+    rng = np.random.default_rng(7)
+    centers = [(lo[0] + 10.3, lo[1] + 12.6, lo[2] + 11.2), (lo[0] + 19.0, lo[1] + 12.1, lo[2] + 12.0),
+               (lo[0] + 28.4, lo[1] + 25.5, lo[2] + 30.1), (lo[0] + 1.0, lo[1] + 30.0, lo[2] + 40.5),
+               (lo[0] - 3.0, lo[1] + 2.0, lo[2] + 2.0)]  # last one is a ghost poking in
+    radii = [6.0, 5.0, 8.5, 4.0, 5.5]
+    u = 0.01 * (rng.random((5, 3)) - 0.5)
+    w = 0.002 * (rng.random((5, 3)) - 0.5)
+    s = spheres(oracle, centers, radii, ids=[2, 5, 9, 11, 40], u=u, w=w)
+    f_o, over = oracle.build_fraction_field(lo, dims, s)
+    assert over == 0
+    sv_o, unk = oracle.set_solid_velocities(lo, dims, s, f_o)
+    assert unk == 0
+    blk = gpu.Block(dims, lo=lo, coupling=True)
+    gpu.build_fraction_field(blk, s)
+    f = blk.download_fraction()
+    c = f["count"]
+    assert np.array_equal(c, f_o["count"])
+    assert (c == 2).any()
+    assert equal_bits(f["btot"], f_o["btot"])
+    for e, (idk, bk, vk) in enumerate((("id0", "b0", "v0"), ("id1", "b1", "v1"))):
+        sel = c > e
+        assert np.array_equal(f[idk][sel], f_o[idk][sel])
+        assert equal_bits(f[bk][sel], f_o[bk][sel])
+    v0, v1 = blk.download_solid_velocity()
+    assert equal_bits(v0[c > 0], sv_o["v0"][c > 0])
+    assert equal_bits(v1[c > 1], sv_o["v1"][c > 1])
+
+
+def test_mapping_overfull_raises(gpu, oracle):
+    """test_psm.cpp:166-176 — three particles through one cell."""
+    dims = (40, 40, 40)
+    s = spheres(oracle, [(20.0 + 0.4 * i, 20.0, 20.0) for i in range(3)], [10.0] * 3)
+    blk = gpu.Block(dims, coupling=True)
+    with pytest.raises(gpu.NumericError, match="more than two particles"):
+        gpu.build_fraction_field(blk, s)
+
+
+def test_set_solid_velocities_unknown_id(gpu, oracle):
+    """test_psm.cpp:414-424."""
+    dims = (16, 16, 16)
+    f = new_fraction(dims)
+    f["count"][8, 8, 8] = 1
+    f["id0"][8, 8, 8] = 42
+    f["b0"][8, 8, 8] = 0.5
+    blk = gpu.Block(dims, coupling=True)
+    blk.upload_fraction(f)
+    with pytest.raises(gpu.SyncError, match="unknown particle ids"):
+        gpu.set_solid_velocities(blk, make_snapshots([], np.zeros((0, 3)), [], []))
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_full_coupled_pass_and_reduction(gpu, oracle, mode):
+    """map -> setU -> PSM sweep -> finalize: PARITY mode bitwise, FAST within L1 tolerance."""
+    dims = (32, 30, 34)
+    src0 = random_pdf(dims, seed=90)
+    rng = np.random.default_rng(11)
+    centers = [(9.2, 10.1, 11.7), (17.5, 10.4, 12.2), (22.0, 21.0, 23.3), (8.0, 24.0, 26.0)]
+    s = spheres(oracle, centers, [5.0, 4.5, 6.0, 3.5], ids=[1, 3, 4, 8],
+                u=0.01 * (rng.random((4, 3)) - 0.5), w=0.001 * (rng.random((4, 3)) - 0.5))
+    tau, fext = 0.7, (0.0, 0.0, -1e-5)
+    f_o, _ = oracle.build_fraction_field((0, 0, 0), dims, s)
+    sv_o, _ = oracle.set_solid_velocities((0, 0, 0), dims, s, f_o)
+    src_o = src0.copy()
+    oracle.fill_periodic(dims, src_o, ALL_P)
+    dst_o = np.zeros_like(src_o)
+    scr = new_scratch(dims)
+    oracle.psm_collide_stream(dims, src_o, dst_o, tau, fext, (0, 0, 0), dims, f_o, sv_o, scr)
+    l1 = {}
+    for e, mk in ((0, "m0"), (1, "m1")):
+        sel = f_o["count"] > e
+        ids = f_o["id0" if e == 0 else "id1"][sel]
+        for pid, mv in zip(ids, np.abs(scr[mk][sel])):
+            l1[int(pid)] = l1.get(int(pid), 0) + mv
+    ids_o, rows_o = oracle.finalize_hydro((0, 0, 0), dims, s, f_o, scr)
+
+    blk = gpu.Block(dims, coupling=True)
+    blk.upload_src(src0)
+    blk.map(s)
+    blk.fill_periodic(ALL_P)
+    blk.sweep(gpu.FluidParams(tau, fext), gpu.CellBox((0, 0, 0), dims))
+    blk.sync()
+    assert equal_bits(interior(blk.download_dst()), interior(dst_o))
+    parts = gpu.finalize_hydro_forces(blk, mode)
+    assert [p.id for p in parts] == list(ids_o)
+    for p, r in zip(parts, rows_o):
+        if mode == 0:
+            assert equal_bits(np.concatenate([p.f, p.f_comp, p.t, p.t_comp]), r)
+        else:
+            assert np.all(np.abs((p.f + p.f_comp) - (r[0:3] + r[3:6])) <= 1e-12 * l1[p.id] + 1e-300)
+    m0, m1 = blk.download_scratch()
+    assert not m0.any() and not m1.any()  # finalize clears the scratch
+
+
+def test_finalize_symmetric_pattern(gpu, oracle):
+    """test_psm.cpp:386-412: no cover -> no partials; symmetric pattern -> 6*0.01, zero torque."""
+    dims = (16, 16, 16)
+    s = spheres(oracle, [(8.5, 8.5, 8.5)], [3.0])
+    blk = gpu.Block(dims, coupling=True)
+    blk.map(make_snapshots([0], [(100.0, 100.0, 100.0)], [3.0], [oracle.f_of_r(3.0)]))
+    blk.sync()
+    blk.set_solid_velocities(s)  # registers the snapshot list used by the reduction
+    blk.sync()
+    assert gpu.finalize_hydro_forces(blk) == []
+    f = new_fraction(dims)
+    m0 = np.zeros((16, 16, 16, 3))
+    for c in [(6, 8, 8), (10, 8, 8), (8, 6, 8), (8, 10, 8), (8, 8, 6), (8, 8, 10)]:
+        i, j, k = c
+        f["count"][k, j, i] = 1
+        f["id0"][k, j, i] = 0
+        f["b0"][k, j, i] = 0.5
+        m0[k, j, i] = (0.01, 0.0, 0.0)
+    blk.upload_fraction(f)
+    blk.upload_scratch(m0, np.zeros_like(m0))
+    parts = gpu.finalize_hydro_forces(blk)
+    assert len(parts) == 1
+    assert abs(parts[0].f[0] - 0.06) <= 1e-13 * 0.06
+    assert np.linalg.norm(parts[0].t + parts[0].t_comp) < 1e-14
+
+
+def test_single_rank_halo_equals_periodic_fill(gpu, oracle):
+    """K7 with one rank and a periodic z axis is the local z wrap of the ghost planes."""
+    dims = (10, 8, 6)
+    src0 = random_pdf(dims, seed=12)
+    tau = 0.8
+    src_o = src0.copy()
+    oracle.fill_periodic(dims, src_o, ALL_P)
+    dst_o = np.zeros_like(src_o)
+    oracle.collide_stream(dims, src_o, dst_o, tau, (0, 0, 0), (0, 0, 0), dims)
+    blk = gpu.Block(dims)
+    blk.comm_init(1, 0, b"\0" * 128, axis=2, periodic=ALL_P)
+    blk.upload_src(src0)
+    blk.fill_periodic((1, 1, 0), full=False)
+    blk.halo_begin()
+    p = gpu.FluidParams(tau)
+    blk.sweep(p, gpu.CellBox((0, 0, 1), (dims[0], dims[1], dims[2] - 1)))
+    blk.halo_complete()
+    blk.sweep_boxes(p, [gpu.CellBox((0, 0, 0), (dims[0], dims[1], 1)),
+                        gpu.CellBox((0, 0, dims[2] - 1), dims)])
+    blk.sync()
+    assert equal_bits(interior(blk.download_dst()), interior(dst_o))
+    with pytest.raises(gpu.SyncError):
+        blk.halo_complete()
