@@ -3,8 +3,8 @@
 
 One step = one D3Q19 SRT fluid time step over the GPU's 512^3 block (fp64), exactly the
 fluid phases of Simulation::step (sim.cpp:689-703) with coupling off:
-  N = 1: periodic ghost fill (K6, pull slots) -> fused pull stream-collide (K1) -> swap
-  N > 1: z-slab of a 512 x 512 x 512N periodic domain per GPU; x/y wrap (K6) ->
+  N = 1: fused pull stream-collide (K1) with the periodic wrap in-kernel -> swap
+  N > 1: z-slab of a 512 x 512 x 512N periodic domain per GPU; x/y wrapped in-kernel;
          halo pack + NCCL send/recv on the comm stream (K7) || inner sweep k in [1,n-1) ->
          unpack -> outer sweep (k = 0, n-1) -> swap     (weak scaling, config 4)
 Inputs: the validation.cpp:46-63 shear wave at tau = 0.8, initialised on the device.
@@ -192,12 +192,13 @@ def run_lbg(args):
         dist.broadcast_object_list(uid, src=0)
         blk.comm_init(N, rank, uid[0], axis=2, periodic=(1, 1, 1))
 
+    # x, y (and z on one GPU) are periodic and spanned by the block: wrapped in-kernel
+    blk.set_periodic_wrap((1, 1, 1) if N == 1 else (1, 1, 0))
+
     def step():
         if N == 1:
-            blk.fill_periodic((1, 1, 1), full=False)
             blk.sweep(p, full)
         else:
-            blk.fill_periodic((1, 1, 0), full=False)
             blk.halo_begin()
             blk.sweep(p, inner)
             blk.halo_complete()
@@ -301,7 +302,7 @@ def run_lbg(args):
             "timings_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in tm.items() if v[1]},
             "e2e": {"value": round(e2e_mlups, 1), "unit": "MLUPS", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 24,
-                    "how": "per step via the C-ABI (fill_periodic, sweep, swap) + lbg_sync error-counter readback"},
+                    "how": "per step via the C-ABI (sweep [+ halo], swap) + lbg_sync error-counter readback"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

@@ -158,6 +158,11 @@ lbg_status lbg_swap(lbg_block b);
 lbg_status lbg_sweep(lbg_block b, const lbg_fluid* fluid, const lbg_box* range);
 /* Several boxes in one launch (the 6 boundary_shell boxes, field.cpp:55-72). */
 lbg_status lbg_sweep_boxes(lbg_block b, const lbg_fluid* fluid, const lbg_box* boxes, int n);
+/* Periodic axes the sweep wraps in-kernel: for an axis the block spans completely (one
+ * block along it), the pull of a population that would come from the ghost layer reads the
+ * wrapped interior cell instead — the value fill_periodic_ghosts would have put there — so
+ * the ghost fill for that axis is not needed. Bitwise identical interior results. */
+lbg_status lbg_set_periodic_wrap(lbg_block b, const int wrap[3]);
 /* Unfused pull stream (lbm.cpp:6-17), debug/tests. */
 lbg_status lbg_stream(lbg_block b, const lbg_box* range);
 

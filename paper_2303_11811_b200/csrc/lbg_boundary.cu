@@ -24,6 +24,7 @@ struct GhostArgs {
     Layout L;
     int periodic[3];
     int full;
+    int wrap[3];  // axes the sweep wraps in-kernel (lbg_set_periodic_wrap)
     long long nA, nB, nC;  // shell region sizes
 };
 
@@ -77,7 +78,14 @@ __global__ void __launch_bounds__(256) periodic_fill_kernel(const GhostArgs a) {
     const long long si = L.idx(s[0], s[1], s[2]);
 #pragma unroll
     for (int q = 0; q < kQ; ++q) {
-        if (!a.full && !interior(L, g[0] + cx(q), g[1] + cy(q), g[2] + cz(q))) continue;
+        if (!a.full) {
+            // pulled by cell g + c_q; along in-kernel-wrapped axes that cell always exists
+            const int t0 = g[0] + cx(q), t1 = g[1] + cy(q), t2 = g[2] + cz(q);
+            const bool in0 = a.wrap[0] || (t0 >= 0 && t0 < L.nx);
+            const bool in1 = a.wrap[1] || (t1 >= 0 && t1 < L.ny);
+            const bool in2 = a.wrap[2] || (t2 >= 0 && t2 < L.nz);
+            if (!(in0 && in1 && in2)) continue;
+        }
         a.src[q * L.plane + gi] = a.src[q * L.plane + si];
     }
 }
@@ -183,6 +191,7 @@ lbg_status lbg_fill_periodic(lbg_block b, const int periodic[3], int full) {
     a.L = b->L;
     for (int d = 0; d < 3; ++d) a.periodic[d] = periodic[d] != 0;
     a.full = full != 0;
+    for (int d = 0; d < 3; ++d) a.wrap[d] = b->wrap[d];
     const Layout& L = b->L;
     a.nA = 2LL * (L.nx + 2) * (L.ny + 2);
     a.nB = 2LL * (L.nx + 2) * L.nz;

@@ -237,6 +237,11 @@ lbg_status lbg_block_create(int device, const int box_lo[3], const int dims[3], 
         // FractionField::resize fills id0/id1 with -1 (field.cpp:37-46)
         cudaMemset(b->id0, 0xff, n * 4);
         cudaMemset(b->id1, 0xff, n * 4);
+        if ((e = cudaMalloc(&b->cov_list, sizeof(unsigned) * n)) != cudaSuccess) return fail(e, "cudaMalloc(cov)");
+        if ((e = cudaMalloc(&b->cov_n, sizeof(int))) != cudaSuccess) return fail(e, "cudaMalloc(cov_n)");
+        cudaMemset(b->cov_n, 0, sizeof(int));
+        b->cov_dirty = false;  // all-zero count: empty list
+        b->device_bytes += sizeof(unsigned) * n;
     }
     if ((e = cudaMalloc(&b->err_d, sizeof(DeviceErrors))) != cudaSuccess) return fail(e, "cudaMalloc(err)");
     cudaMemset(b->err_d, 0, sizeof(DeviceErrors));
@@ -264,7 +269,7 @@ lbg_status lbg_block_destroy(lbg_block b) {
     if (b->comm) lbg_comm_destroy(b);
     void* dev[] = {b->buf[0], b->buf[1], b->count, b->id0, b->id1, b->b0, b->b1, b->btot,
                    b->v0, b->v1, b->m0, b->m1, b->snaps_d, b->bin_count, b->bin_start,
-                   b->bin_items, b->red_rows, b->red_used, b->err_d};
+                   b->bin_items, b->red_rows, b->red_used, b->err_d, b->cov_list, b->cov_n};
     for (void* p : dev)
         if (p) cudaFree(p);
     void* host[] = {b->snaps_h, b->err_h, b->red_h, b->red_rows_h, b->red_used_h};
@@ -320,6 +325,12 @@ lbg_status lbg_upload_src(lbg_block b, const double* host) { return copy_pdf(b, 
 lbg_status lbg_download_src(lbg_block b, double* host) { return copy_pdf(b, b->src(), nullptr, host); }
 lbg_status lbg_upload_dst(lbg_block b, const double* host) { return copy_pdf(b, b->dst(), host, nullptr); }
 lbg_status lbg_download_dst(lbg_block b, double* host) { return copy_pdf(b, b->dst(), nullptr, host); }
+
+lbg_status lbg_set_periodic_wrap(lbg_block b, const int wrap[3]) {
+    if (!b || !wrap) return set_error(LBG_INVALID, "null argument");
+    for (int a = 0; a < 3; ++a) b->wrap[a] = wrap[a] != 0;
+    return LBG_OK;
+}
 
 lbg_status lbg_swap(lbg_block b) {
     b->cur ^= 1;

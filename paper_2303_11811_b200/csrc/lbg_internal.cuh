@@ -98,6 +98,14 @@ struct lbg_block_s {
     double* v1 = nullptr;
     double* m0 = nullptr;
     double* m1 = nullptr;
+    // covered cells (count > 0), compacted by the mapping kernel / after a fraction upload;
+    // the PSM operator runs over this list so the SRT sweep keeps its low register count
+    unsigned* cov_list = nullptr;
+    int* cov_n = nullptr;  // device counter
+    bool cov_dirty = true;
+
+    // periodic axes the sweep wraps in-kernel (no ghost read), lbg_set_periodic_wrap
+    int wrap[3] = {0, 0, 0};
 
     // particle snapshots: pinned staging + device copy (H2D on the side stream)
     lbg_snapshot* snaps_h = nullptr;
@@ -139,6 +147,21 @@ struct lbg_block_s {
 };
 
 namespace lbg {
+
+// covered-cell list rebuild from `count` (lbg_psm.cu)
+lbg_status rebuild_covered(lbg_block b);
+
+// warp-aggregated append of `pred` lanes' values to list[*n ...]
+__device__ __forceinline__ void warp_append(bool pred, unsigned v, unsigned* list, int* n) {
+    const unsigned m = __ballot_sync(0xffffffffu, pred);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(n, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (pred) list[base + __popc(m & ((1u << lane) - 1))] = v;
+}
 
 // error plumbing (lbg_core.cu)
 lbg_status set_error(lbg_status s, const std::string& msg);

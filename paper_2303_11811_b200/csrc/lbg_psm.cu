@@ -115,6 +115,8 @@ struct MapArgs {
     double* __restrict__ v1;
     DeviceErrors* err;
     int with_velocity;
+    unsigned* cov_list;
+    int* cov_n;
 };
 
 // psm.cpp:28-32 overlap_fraction, psm.cpp:93-136 per-cell entry rule, psm.cpp:157-163 setU
@@ -124,6 +126,8 @@ __global__ void __launch_bounds__(256) map_kernel(const MapArgs a) {
     const int k = blockIdx.z;
     const BinGeom& g = a.g;
     bool over = false;
+    bool covered = false;
+    unsigned cell = 0;
     if (i < g.dims[0]) {
         const long long c = ((long long)k * g.dims[1] + j) * g.dims[0] + i;
         const int b = ((k / kBin) * g.nb[1] + (j / kBin)) * g.nb[0] + (i / kBin);
@@ -166,9 +170,19 @@ __global__ void __launch_bounds__(256) map_kernel(const MapArgs a) {
         }
         a.count[c] = (uint8_t)cnt;
         a.btot[c] = sum < 1.0 ? sum : 1.0;  // std::min(1.0, sum)
+        covered = cnt > 0;
+        cell = (unsigned)c;
     }
+    warp_append(covered, cell, a.cov_list, a.cov_n);
     const unsigned m = __ballot_sync(0xffffffffu, over);
     if (m && (threadIdx.x & 31) == 0) atomicAdd(&a.err->overfull, (unsigned long long)__popc(m));
+}
+
+// covered-cell list from an externally set fraction field
+__global__ void __launch_bounds__(256) covered_kernel(const uint8_t* __restrict__ count, long long cells,
+                                                      unsigned* __restrict__ list, int* __restrict__ n) {
+    const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    warp_append(c < cells && count[c] > 0, (unsigned)c, list, n);
 }
 
 __device__ __forceinline__ int find_snapshot(const lbg_snapshot* s, int n, int id) {
@@ -396,6 +410,15 @@ static lbg_status ensure_bins(lbg_block b, long long nbins) {
     return LBG_OK;
 }
 
+lbg_status rebuild_covered(lbg_block b) {
+    const long long cells = (long long)b->L.nx * b->L.ny * b->L.nz;
+    LBG_CUDA(cudaMemsetAsync(b->cov_n, 0, sizeof(int), b->stream));
+    covered_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, b->stream>>>(b->count, cells, b->cov_list, b->cov_n);
+    LBG_LAUNCH_CHECK();
+    b->cov_dirty = false;
+    return LBG_OK;
+}
+
 }  // namespace lbg
 
 using namespace lbg;
@@ -468,9 +491,13 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
     a.v1 = b->v1;
     a.err = b->err_d;
     a.with_velocity = 1;
+    a.cov_list = b->cov_list;
+    a.cov_n = b->cov_n;
+    LBG_CUDA(cudaMemsetAsync(b->cov_n, 0, sizeof(int), b->stream));
     dim3 grid((g.dims[0] + 127) / 128, g.dims[1], g.dims[2]);
     map_kernel<<<grid, 128, 0, b->stream>>>(a);
     LBG_LAUNCH_CHECK();
+    b->cov_dirty = false;
     return LBG_OK;
 }
 
@@ -591,6 +618,7 @@ static lbg_status copy_frac(lbg_block b, bool up, uint8_t* count, int* id0, int*
 
 lbg_status lbg_upload_fraction(lbg_block b, const uint8_t* count, const int* id0, const int* id1,
                                const double* b0, const double* b1, const double* btot) {
+    if (b) b->cov_dirty = true;
     return copy_frac(b, true, (uint8_t*)count, (int*)id0, (int*)id1, (double*)b0, (double*)b1, (double*)btot);
 }
 

@@ -7,12 +7,19 @@
 // stored = 304 B for the plain sweep; the coupled sweep adds the 1-byte count per cell and,
 // per covered cell, 8 B btot + per entry (8 B b + 24 B v read, 24 B m written).
 //
-// Launch shapes:
-//   box  — one CellBox, 3-D grid; thread x maps to global i with the chunk origin aligned to
-//          32 cells, so every warp's loads/stores of a q-plane are two 128-B lines
-//          (the pulled x-neighbour costs one extra sector per warp, served by L1/L2).
-//   flat — up to 8 boxes in one launch (the 6 boundary_shell boxes of field.cpp:55-72),
-//          flattened cell index; used for thin boxes where a 3-D grid would idle lanes.
+// Kernels:
+//   K1 sweep_box   — one CellBox, 3-D grid; thread x maps to global i with the chunk origin
+//                    aligned to 32 cells, so a warp's loads/stores of a q-plane are two 128-B
+//                    lines (the pulled x-neighbour costs one extra sector per warp, from L2).
+//   K1 sweep_flat  — up to 8 boxes in one launch (the boundary_shell boxes, field.cpp:55-72).
+//   K2 psm_list    — the covered cells (count > 0) of a coupled block, from the compacted list
+//                    the mapping kernel writes. In a coupled block K1 skips covered cells, so
+//                    the SRT kernel keeps ~70 registers (3 CTAs/SM) instead of the ~210 the
+//                    fused PSM operator needs (the A100 kernel of the paper ran at 196 regs,
+//                    12.5% occupancy); only the covered minority pays for them.
+// Periodic wrap: for axes in b->wrap the pull reads the wrapped interior cell directly
+// (what fill_periodic_ghosts would have copied into the ghost slot), so a fully periodic
+// single-GPU step is one launch with no ghost fill.
 // Unstable cells (lbm.hpp:106) are counted with a warp ballot into the block's error
 // counter; lbg_sync() raises NumericError like the reference does after the sweep.
 #include "lbg_cell.cuh"
@@ -27,6 +34,7 @@ struct SweepArgs {
     double inv_tau;
     Force F;
     DeviceErrors* err;
+    int wrap[3];
     // coupling (interior lexicographic)
     const uint8_t* __restrict__ count;
     const double* __restrict__ b0;
@@ -36,46 +44,72 @@ struct SweepArgs {
     const double* __restrict__ v1;
     double* __restrict__ m0;
     double* __restrict__ m1;
+    const unsigned* __restrict__ cov_list;
+    const int* __restrict__ cov_n;
     // box launch
     int lo[3], hi[3];
     int i0;  // aligned chunk origin
-    // flat launch
+    // flat launch / list range test
     int nbox;
     int blo[8][3];
     int bext[8][3];
     long long bstart[9];
 };
 
-template <bool kForced, bool kCoupled>
-__device__ __forceinline__ bool process_cell(const SweepArgs& a, int i, int j, int k) {
+// pull the 19 populations of cell (i,j,k), wrapping periodic axes in-kernel
+__device__ __forceinline__ void pull(const SweepArgs& a, int i, int j, int k, long long base,
+                                     double (&f)[kQ]) {
+    const Layout& L = a.L;
+    const long long sy = L.px, sz = (long long)L.px * L.py;
+    const long long xl = (a.wrap[0] && i == 0) ? L.nx : 0;  // source i-1 = -1 -> nx-1
+    const long long xh = (a.wrap[0] && i == L.nx - 1) ? -(long long)L.nx : 0;
+    const long long yl = (a.wrap[1] && j == 0) ? L.ny * sy : 0;
+    const long long yh = (a.wrap[1] && j == L.ny - 1) ? -L.ny * sy : 0;
+    const long long zl = (a.wrap[2] && k == 0) ? L.nz * sz : 0;
+    const long long zh = (a.wrap[2] && k == L.nz - 1) ? -L.nz * sz : 0;
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+        const long long corr = (cx(q) == 1 ? xl : (cx(q) == -1 ? xh : 0)) +
+                               (cy(q) == 1 ? yl : (cy(q) == -1 ? yh : 0)) +
+                               (cz(q) == 1 ? zl : (cz(q) == -1 ? zh : 0));
+        f[q] = a.src[q * L.plane + base - L.shift(q) + corr];
+    }
+}
+
+// plain cell; in a coupled block covered cells are left to K2 (kSkipCovered)
+template <bool kForced, bool kSkipCovered>
+__device__ __forceinline__ bool srt_cell_at(const SweepArgs& a, int i, int j, int k) {
+    if constexpr (kSkipCovered) {
+        if (a.count[a.L.frac(i, j, k)] != 0) return true;
+    }
+    const long long base = a.L.idx(i, j, k);
+    double f[kQ];
+    pull(a, i, j, k, base, f);
+    const bool ok = srt_cell<kForced>(f, a.inv_tau, a.F);
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) a.dst[q * a.L.plane + base] = f[q];
+    return ok;
+}
+
+// covered cell, psm.cpp:236-258
+__device__ __forceinline__ bool psm_cell_at(const SweepArgs& a, int i, int j, int k) {
     const Layout& L = a.L;
     const long long base = L.idx(i, j, k);
+    const long long fc = L.frac(i, j, k);
+    const int cnt = a.count[fc];
     double f[kQ];
-#pragma unroll
-    for (int q = 0; q < kQ; ++q) f[q] = a.src[q * L.plane + base - L.shift(q)];
-
-    bool ok;
-    if constexpr (kCoupled) {
-        const long long fc = L.frac(i, j, k);
-        const int cnt = a.count[fc];
-        if (cnt == 0) {
-            ok = srt_cell<kForced>(f, a.inv_tau, a.F);
-        } else {
-            const double be[2] = {a.b0[fc], cnt > 1 ? a.b1[fc] : 0.0};
-            double ue[2][3];
-            for (int c = 0; c < 3; ++c) {
-                ue[0][c] = a.v0[3 * fc + c];
-                ue[1][c] = cnt > 1 ? a.v1[3 * fc + c] : 0.0;
-            }
-            double m[2][3];
-            ok = psm_cell(f, a.inv_tau, a.F, cnt, a.btot[fc], be, ue, m);
-            for (int c = 0; c < 3; ++c) a.m0[3 * fc + c] = m[0][c];
-            if (cnt > 1)
-                for (int c = 0; c < 3; ++c) a.m1[3 * fc + c] = m[1][c];
-        }
-    } else {
-        ok = srt_cell<kForced>(f, a.inv_tau, a.F);
+    pull(a, i, j, k, base, f);
+    const double be[2] = {a.b0[fc], cnt > 1 ? a.b1[fc] : 0.0};
+    double ue[2][3];
+    for (int c = 0; c < 3; ++c) {
+        ue[0][c] = a.v0[3 * fc + c];
+        ue[1][c] = cnt > 1 ? a.v1[3 * fc + c] : 0.0;
     }
+    double m[2][3];
+    const bool ok = psm_cell(f, a.inv_tau, a.F, cnt, a.btot[fc], be, ue, m);
+    for (int c = 0; c < 3; ++c) a.m0[3 * fc + c] = m[0][c];
+    if (cnt > 1)
+        for (int c = 0; c < 3; ++c) a.m1[3 * fc + c] = m[1][c];
 #pragma unroll
     for (int q = 0; q < kQ; ++q) a.dst[q * L.plane + base] = f[q];
     return ok;
@@ -86,32 +120,64 @@ __device__ __forceinline__ void count_bad(DeviceErrors* err, bool bad) {
     if (m && (threadIdx.x & 31) == 0) atomicAdd(&err->unstable, (unsigned long long)__popc(m));
 }
 
-template <bool kForced, bool kCoupled>
+template <bool kForced, bool kSkipCovered>
 __global__ void __launch_bounds__(256) sweep_box_kernel(const SweepArgs a) {
     const int i = a.i0 + blockIdx.x * blockDim.x + threadIdx.x;
     const int j = a.lo[1] + blockIdx.y * blockDim.y + threadIdx.y;
     const int k = a.lo[2] + blockIdx.z;
     const bool active = i >= a.lo[0] && i < a.hi[0] && j < a.hi[1];
     bool ok = true;
-    if (active) ok = process_cell<kForced, kCoupled>(a, i, j, k);
+    if (active) ok = srt_cell_at<kForced, kSkipCovered>(a, i, j, k);
     count_bad(a.err, !ok);
 }
 
-template <bool kForced, bool kCoupled>
+__device__ __forceinline__ void flat_cell(const SweepArgs& a, long long t, int& i, int& j, int& k) {
+    int b = 0;
+    while (t >= a.bstart[b + 1]) ++b;
+    const long long r = t - a.bstart[b];
+    const int ex = a.bext[b][0], ey = a.bext[b][1];
+    i = a.blo[b][0] + (int)(r % ex);
+    j = a.blo[b][1] + (int)((r / ex) % ey);
+    k = a.blo[b][2] + (int)(r / ((long long)ex * ey));
+}
+
+template <bool kForced, bool kSkipCovered>
 __global__ void __launch_bounds__(256) sweep_flat_kernel(const SweepArgs a) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     bool ok = true;
     if (t < a.bstart[a.nbox]) {
-        int b = 0;
-        while (t >= a.bstart[b + 1]) ++b;
-        const long long r = t - a.bstart[b];
-        const int ex = a.bext[b][0], ey = a.bext[b][1];
-        const int i = a.blo[b][0] + (int)(r % ex);
-        const int j = a.blo[b][1] + (int)((r / ex) % ey);
-        const int k = a.blo[b][2] + (int)(r / ((long long)ex * ey));
-        ok = process_cell<kForced, kCoupled>(a, i, j, k);
+        int i, j, k;
+        flat_cell(a, t, i, j, k);
+        ok = srt_cell_at<kForced, kSkipCovered>(a, i, j, k);
     }
     count_bad(a.err, !ok);
+}
+
+__device__ __forceinline__ bool in_boxes(const SweepArgs& a, int i, int j, int k) {
+    for (int b = 0; b < a.nbox; ++b)
+        if (i >= a.blo[b][0] && i < a.blo[b][0] + a.bext[b][0] && j >= a.blo[b][1] &&
+            j < a.blo[b][1] + a.bext[b][1] && k >= a.blo[b][2] && k < a.blo[b][2] + a.bext[b][2])
+            return true;
+    return false;
+}
+
+// K2: grid-stride over the covered-cell list (length read on the device)
+__global__ void __launch_bounds__(128) psm_list_kernel(const SweepArgs a) {
+    const int n = *a.cov_n;
+    const int stride = gridDim.x * blockDim.x;
+    const Layout& L = a.L;
+    for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
+        const int t = base + threadIdx.x;
+        bool ok = true;
+        if (t < n) {
+            const unsigned c = a.cov_list[t];
+            const int i = (int)(c % (unsigned)L.nx);
+            const int j = (int)((c / (unsigned)L.nx) % (unsigned)L.ny);
+            const int k = (int)(c / ((unsigned)L.nx * (unsigned)L.ny));
+            if (in_boxes(a, i, j, k)) ok = psm_cell_at(a, i, j, k);
+        }
+        count_bad(a.err, !ok);
+    }
 }
 
 // lbm.cpp:6-17 — unfused pull stream.
@@ -145,6 +211,7 @@ static SweepArgs make_args(lbg_block b, const lbg_fluid* fl) {
     a.inv_tau = 1.0 / fl->tau;  // kDt / params.tau (lbm.cpp:30)
     a.F = {fl->f_ext[0], fl->f_ext[1], fl->f_ext[2]};
     a.err = b->err_d;
+    for (int c = 0; c < 3; ++c) a.wrap[c] = b->wrap[c];
     if (b->coupling) {
         a.count = b->count;
         a.b0 = b->b0;
@@ -154,23 +221,50 @@ static SweepArgs make_args(lbg_block b, const lbg_fluid* fl) {
         a.v1 = b->v1;
         a.m0 = b->m0;
         a.m1 = b->m1;
+        a.cov_list = b->cov_list;
+        a.cov_n = b->cov_n;
     }
     return a;
 }
 
-template <bool kForced, bool kCoupled>
+static lbg_status add_boxes(SweepArgs& a, const Layout& L, const lbg_box* boxes, int n) {
+    a.nbox = 0;
+    a.bstart[0] = 0;
+    for (int t = 0; t < n; ++t) {
+        if (empty_box(boxes[t])) continue;
+        if (!valid_box(L, boxes[t])) return set_error(LBG_INVALID, "sweep range outside the block");
+        long long vol = 1;
+        for (int c = 0; c < 3; ++c) {
+            a.blo[a.nbox][c] = boxes[t].lo[c];
+            a.bext[a.nbox][c] = boxes[t].hi[c] - boxes[t].lo[c];
+            vol *= a.bext[a.nbox][c];
+        }
+        a.bstart[a.nbox + 1] = a.bstart[a.nbox] + vol;
+        ++a.nbox;
+    }
+    return LBG_OK;
+}
+
+template <bool kForced, bool kSkip>
 static void launch_box(const SweepArgs& a, cudaStream_t s) {
     constexpr int BX = 128, BY = 2;
     dim3 block(BX, BY, 1);
     dim3 grid((a.hi[0] - a.i0 + BX - 1) / BX, (a.hi[1] - a.lo[1] + BY - 1) / BY, a.hi[2] - a.lo[2]);
-    sweep_box_kernel<kForced, kCoupled><<<grid, block, 0, s>>>(a);
+    sweep_box_kernel<kForced, kSkip><<<grid, block, 0, s>>>(a);
 }
 
-template <bool kForced, bool kCoupled>
+template <bool kForced, bool kSkip>
 static void launch_flat(const SweepArgs& a, cudaStream_t s) {
     const long long n = a.bstart[a.nbox];
     const int T = 256;
-    sweep_flat_kernel<kForced, kCoupled><<<(unsigned)((n + T - 1) / T), T, 0, s>>>(a);
+    sweep_flat_kernel<kForced, kSkip><<<(unsigned)((n + T - 1) / T), T, 0, s>>>(a);
+}
+
+static void launch_psm_list(lbg_block b, const SweepArgs& a) {
+    // persistent grid: 4 CTAs of 128 per SM, the list length is read on the device
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, b->device);
+    psm_list_kernel<<<sms * 4, 128, 0, b->stream>>>(a);
 }
 
 }  // namespace lbg
@@ -185,6 +279,10 @@ static lbg_status check_fluid(const lbg_fluid* fl) {
     return LBG_OK;
 }
 
+static bool forced(const lbg_fluid* fl) {
+    return fl->f_ext[0] != 0.0 || fl->f_ext[1] != 0.0 || fl->f_ext[2] != 0.0;
+}
+
 extern "C" {
 
 lbg_status lbg_sweep(lbg_block b, const lbg_fluid* fl, const lbg_box* range) {
@@ -193,18 +291,23 @@ lbg_status lbg_sweep(lbg_block b, const lbg_fluid* fl, const lbg_box* range) {
     if (empty_box(*range)) return LBG_OK;  // run_kernel skips empty ranges (sim.cpp:222)
     if (!valid_box(b->L, *range)) return set_error(LBG_INVALID, "sweep range outside the block");
     LBG_CUDA(cudaSetDevice(b->device));
+    if (b->coupling && b->cov_dirty)
+        if (lbg_status s = rebuild_covered(b)) return s;
     SweepArgs a = make_args(b, fl);
     for (int c = 0; c < 3; ++c) {
         a.lo[c] = range->lo[c];
         a.hi[c] = range->hi[c];
     }
     a.i0 = (range->lo[0] / 32) * 32;
-    const bool forced = fl->f_ext[0] != 0.0 || fl->f_ext[1] != 0.0 || fl->f_ext[2] != 0.0;
+    if (lbg_status s = add_boxes(a, b->L, range, 1)) return s;
     Span span(b, LBG_CAT_PSM);
+    const bool fo = forced(fl);
     if (b->coupling) {
-        forced ? launch_box<true, true>(a, b->stream) : launch_box<false, true>(a, b->stream);
+        fo ? launch_box<true, true>(a, b->stream) : launch_box<false, true>(a, b->stream);
+        LBG_LAUNCH_CHECK();
+        launch_psm_list(b, a);
     } else {
-        forced ? launch_box<true, false>(a, b->stream) : launch_box<false, false>(a, b->stream);
+        fo ? launch_box<true, false>(a, b->stream) : launch_box<false, false>(a, b->stream);
     }
     LBG_LAUNCH_CHECK();
     return LBG_OK;
@@ -215,28 +318,19 @@ lbg_status lbg_sweep_boxes(lbg_block b, const lbg_fluid* fl, const lbg_box* boxe
     if (lbg_status s = check_fluid(fl)) return s;
     if (n > 8) return set_error(LBG_INVALID, "at most 8 boxes per launch");
     LBG_CUDA(cudaSetDevice(b->device));
+    if (b->coupling && b->cov_dirty)
+        if (lbg_status s = rebuild_covered(b)) return s;
     SweepArgs a = make_args(b, fl);
-    a.nbox = 0;
-    a.bstart[0] = 0;
-    for (int t = 0; t < n; ++t) {
-        if (empty_box(boxes[t])) continue;
-        if (!valid_box(b->L, boxes[t])) return set_error(LBG_INVALID, "sweep range outside the block");
-        long long vol = 1;
-        for (int c = 0; c < 3; ++c) {
-            a.blo[a.nbox][c] = boxes[t].lo[c];
-            a.bext[a.nbox][c] = boxes[t].hi[c] - boxes[t].lo[c];
-            vol *= a.bext[a.nbox][c];
-        }
-        a.bstart[a.nbox + 1] = a.bstart[a.nbox] + vol;
-        ++a.nbox;
-    }
+    if (lbg_status s = add_boxes(a, b->L, boxes, n)) return s;
     if (a.nbox == 0) return LBG_OK;
-    const bool forced = fl->f_ext[0] != 0.0 || fl->f_ext[1] != 0.0 || fl->f_ext[2] != 0.0;
     Span span(b, LBG_CAT_PSM);
+    const bool fo = forced(fl);
     if (b->coupling) {
-        forced ? launch_flat<true, true>(a, b->stream) : launch_flat<false, true>(a, b->stream);
+        fo ? launch_flat<true, true>(a, b->stream) : launch_flat<false, true>(a, b->stream);
+        LBG_LAUNCH_CHECK();
+        launch_psm_list(b, a);
     } else {
-        forced ? launch_flat<true, false>(a, b->stream) : launch_flat<false, false>(a, b->stream);
+        fo ? launch_flat<true, false>(a, b->stream) : launch_flat<false, false>(a, b->stream);
     }
     LBG_LAUNCH_CHECK();
     return LBG_OK;

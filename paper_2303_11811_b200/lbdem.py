@@ -317,6 +317,10 @@ class Block:
         arr = (_abi.Box * max(len(boxes), 1))(*[b.c() for b in boxes])
         check(_lib().lbg_sweep_boxes(self.h, C.byref(fl), arr, len(boxes)))
 
+    def set_periodic_wrap(self, wrap):
+        """Periodic axes the sweep wraps in-kernel (replaces the ghost fill for them)."""
+        check(_lib().lbg_set_periodic_wrap(self.h, (C.c_int * 3)(*[int(bool(w)) for w in wrap])))
+
     def stream_only(self, box: CellBox):
         bx = box.c()
         check(_lib().lbg_stream(self.h, C.byref(bx)))

@@ -82,6 +82,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "lbg_sweep": (st, [blk, C.POINTER(Fluid), C.POINTER(Box)]),
         "lbg_sweep_boxes": (st, [blk, C.POINTER(Fluid), C.POINTER(Box), C.c_int]),
         "lbg_stream": (st, [blk, C.POINTER(Box)]),
+        "lbg_set_periodic_wrap": (st, [blk, i3]),
         "lbg_fill_periodic": (st, [blk, i3, C.c_int]),
         "lbg_apply_boundaries": (st, [blk, C.POINTER(FaceBc), i3]),
         "lbg_map": (st, [blk, C.POINTER(Snapshot), C.c_int, C.c_int]),

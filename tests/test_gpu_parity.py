@@ -102,6 +102,37 @@ def test_periodic_fill_full_bitwise_and_pull_only_equivalent(gpu, oracle, period
         assert equal_bits(interior(blk.download_dst()), interior(dst_o))
 
 
+@pytest.mark.parametrize("wrap", [(1, 1, 1), (1, 0, 1), (0, 1, 0), (0, 0, 1)])
+@pytest.mark.parametrize("coupled", [False, True])
+def test_in_kernel_periodic_wrap_bitwise(gpu, oracle, wrap, coupled):
+    """lbg_set_periodic_wrap: wrapped pulls == pulls from periodically filled ghosts."""
+    dims = (13, 9, 7)
+    src0 = random_pdf(dims, seed=21)
+    tau, fext = 0.77, (1e-6, 0.0, -2e-6)
+    src_o = src0.copy()
+    oracle.fill_periodic(dims, src_o, ALL_P)
+    dst_o = np.zeros_like(src_o)
+    blk = gpu.Block(dims, coupling=coupled)
+    if coupled:
+        frac, sv = random_fraction(dims, seed=4)
+        scr = new_scratch(dims)
+        oracle.psm_collide_stream(dims, src_o, dst_o, tau, fext, (0, 0, 0), dims, frac, sv, scr)
+        blk.upload_fraction(frac)
+        blk.upload_solid_velocity(sv["v0"], sv["v1"])
+    else:
+        oracle.collide_stream(dims, src_o, dst_o, tau, fext, (0, 0, 0), dims)
+    blk.upload_src(src0)
+    blk.set_periodic_wrap(wrap)  # before the fill: the pull-only fill honours the wrap
+    blk.fill_periodic(tuple(1 - w for w in wrap), full=False)
+    blk.sweep(gpu.FluidParams(tau, fext), gpu.CellBox((0, 0, 0), dims))
+    blk.sync()
+    assert n_bit_mismatch(interior(blk.download_dst()), interior(dst_o)) == 0
+    if coupled:
+        m0, _ = blk.download_scratch()
+        c = frac["count"]
+        assert equal_bits(m0[c > 0], scr["m0"][c > 0])
+
+
 def bed_spec(gpu, zm_vel=(0.0, 0.0, 2.2472e-3), rho_out=1.0):
     spec = gpu.BcSpec()
     for f in range(4):
@@ -411,3 +442,15 @@ def test_single_rank_halo_equals_periodic_fill(gpu, oracle):
     assert equal_bits(interior(blk.download_dst()), interior(dst_o))
     with pytest.raises(gpu.SyncError):
         blk.halo_complete()
+    # the bench's weak-scaling step shape: x/y wrapped in-kernel, z through the halo
+    blk2 = gpu.Block(dims)
+    blk2.comm_init(1, 0, b"\0" * 128, axis=2, periodic=ALL_P)
+    blk2.upload_src(src0)
+    blk2.set_periodic_wrap((1, 1, 0))
+    blk2.halo_begin()
+    blk2.sweep(p, gpu.CellBox((0, 0, 1), (dims[0], dims[1], dims[2] - 1)))
+    blk2.halo_complete()
+    blk2.sweep_boxes(p, [gpu.CellBox((0, 0, 0), (dims[0], dims[1], 1)),
+                         gpu.CellBox((0, 0, dims[2] - 1), dims)])
+    blk2.sync()
+    assert equal_bits(interior(blk2.download_dst()), interior(dst_o))
