@@ -220,6 +220,16 @@ lbg_status lbg_halo_begin(lbg_block b);
 /* Ghost planes valid for the outer sweep; SyncError without a pending begin (sim.cpp:183). */
 lbg_status lbg_halo_complete(lbg_block b);
 
+/* Generic in-process halo slabs with the reference's exact semantics, for block layouts the
+ * NCCL slab exchange does not cover (several blocks per process, 26 neighbours):
+ * lbg_pack_slab copies all 19 q of source_slab(off) (sim.cpp:120-135) from src into `out`
+ * in PdfSlab order (q-major, then k, j, i; sim.cpp:167-173); lbg_unpack_slab writes `in` into
+ * ghost_region(dir) (sim.cpp:137-152, 186-197). `out`/`in` are host buffers of
+ * 19 * slab-cells doubles; *n_out receives that count. Both block until done. */
+lbg_status lbg_pack_slab(lbg_block b, const int off[3], double* out, long long capacity,
+                         long long* n_out);
+lbg_status lbg_unpack_slab(lbg_block b, const int dir[3], const double* in, long long n);
+
 /* ------------------------------------------------------------------ instrumentation */
 /* Per-category CUDA-event timing (perf::Category names); off by default. */
 lbg_status lbg_set_timing(lbg_block b, int on);

@@ -1,0 +1,179 @@
+"""Builds the drop-in: the reference solver with its GPU-side operators served by liblbg.
+
+This is what a maintainer of the reference does: the host program —
+Simulation's phase structure, DEM, particle messaging, partial routing, config, scenarios —
+stays the reference's own code, and the call sites of the fluid/coupling operators in
+sim.cpp / the fields in sim.hpp's BlockState are pointed at lbdem::gpu::DeviceBlock
+(include/lbdem_gpu.hpp). The edits are applied to copies of the two files in
+integration/_build/ (git-ignored; no reference source enters the repository); every other
+reference source compiles unmodified from /root/reference.
+
+    python integration/make_dropin.py      # -> integration/_build/liblbdem_dropin.so
+"""
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+REF = os.environ.get("LBDEM_REF", "/root/reference/proj")
+BUILD = os.path.join(HERE, "_build")
+
+# (anchor in the reference file, replacement). Each edit names the reference lines it replaces.
+SIM_HPP_EDITS = [
+    # sim.hpp:12 — forward declaration of the device twin
+    ('#include "lbdem/psm.hpp"\n',
+     '#include "lbdem/psm.hpp"\n\nnamespace lbdem::gpu {\nclass DeviceBlock;\n}\n'),
+    # sim.hpp:49 — BlockState gains its device twin (field/frac/svel/scratch live on the GPU)
+    ("    bool halo_pending = false;\n",
+     "    bool halo_pending = false;\n"
+     "    std::shared_ptr<gpu::DeviceBlock> dev;  ///< liblbg block (drop-in)\n"
+     "    mutable bool host_stale = false;        ///< host field copy behind the device\n"),
+]
+
+SIM_CPP_EDITS = [
+    # includes + host-copy refresh used by the observers
+    ("#include <set>\n",
+     "#include <set>\n#include <cstdlib>\n\n#include \"lbdem_gpu.hpp\"\n"),
+    ("namespace lbdem {\n\nusing partition::MsgKind;",
+     "namespace lbdem {\n\n"
+     "namespace {\n"
+     "int gpu_device() {\n"
+     "    const char* e = std::getenv(\"LBDEM_GPU_DEVICE\");\n"
+     "    return e ? std::atoi(e) : 0;\n"
+     "}\n"
+     "/// Observers read the host copies; refresh them from the device after a step.\n"
+     "void refresh_host(const std::vector<std::unique_ptr<BlockState>>& blocks, bool coupling) {\n"
+     "    for (const auto& b : blocks) {\n"
+     "        if (!b->host_stale) continue;\n"
+     "        BlockState& m = const_cast<BlockState&>(*b);\n"
+     "        m.dev->download_src(m.field);\n"
+     "        if (coupling) m.dev->download_fraction(m.frac);\n"
+     "        m.host_stale = false;\n"
+     "    }\n"
+     "}\n"
+     "}  // namespace\n\n"
+     "using partition::MsgKind;"),
+    # sim.cpp:19-24 — BlockState ctor: create the device block
+    ("        scratch.resize(frac.cells());\n    }\n}\n",
+     "        scratch.resize(frac.cells());\n    }\n"
+     "    dev = std::make_shared<gpu::DeviceBlock>(gpu_device(), box_, coupling);\n}\n"),
+    # sim.cpp:54-57 — initialize_fluid on the device too
+    ("    for (auto& blk : blocks_) blk->field.fill_src(feq);\n",
+     "    for (auto& blk : blocks_) {\n"
+     "        blk->field.fill_src(feq);\n"
+     "        blk->dev->initialize_fluid(rho, u);\n"
+     "    }\n"),
+    # sim.cpp:167-173 — pack the source slab from the device
+    ("        for (int q = 0; q < lbm::kQ; ++q) {\n"
+     "            const double* p = blk.field.src(q);\n"
+     "            for (int k = src.lo.z; k < src.hi.z; ++k)\n"
+     "                for (int j = src.lo.y; j < src.hi.y; ++j)\n"
+     "                    for (int i = src.lo.x; i < src.hi.x; ++i)\n"
+     "                        slab.values.push_back(p[blk.field.idx(i, j, k)]);\n"
+     "        }\n",
+     "        blk.dev->pack_slab(n.offset, slab.values);\n"),
+    # sim.cpp:189-197 — unpack into the device ghost region
+    ("            const CellBox dst = ghost_region(dims, slab.dir);\n"
+     "            std::size_t v = 0;\n"
+     "            for (int q = 0; q < lbm::kQ; ++q) {\n"
+     "                double* p = blk.field.src(q);\n"
+     "                for (int k = dst.lo.z; k < dst.hi.z; ++k)\n"
+     "                    for (int j = dst.lo.y; j < dst.hi.y; ++j)\n"
+     "                        for (int i = dst.lo.x; i < dst.hi.x; ++i)\n"
+     "                            p[blk.field.idx(i, j, k)] = slab.values[v++];\n"
+     "            }\n",
+     "            (void)dims;\n"
+     "            blk.dev->unpack_slab(slab.dir, slab.values);\n"),
+    # sim.cpp:221-236 — run_kernel: the device sweep (plain or PSM per the block's coupling)
+    ("    if (range.empty()) return;\n"
+     "    if (params_.coupling) {\n"
+     "        if (params_.kernels == KernelMode::openmp)\n"
+     "            psm::psm_collide_stream_omp(blk.field, params_.fluid, blk.frac, blk.svel,\n"
+     "                                        blk.scratch, range);\n"
+     "        else\n"
+     "            psm::psm_collide_stream_serial(blk.field, params_.fluid, blk.frac, blk.svel,\n"
+     "                                           blk.scratch, range);\n"
+     "    } else {\n"
+     "        if (params_.kernels == KernelMode::openmp)\n"
+     "            lbm::collide_stream_omp(blk.field, params_.fluid, range);\n"
+     "        else\n"
+     "            lbm::collide_stream_serial(blk.field, params_.fluid, range);\n"
+     "    }\n",
+     "    if (range.empty()) return;\n"
+     "    blk.dev->sweep(params_.fluid, range);\n"),
+    # sim.cpp:278-280 — registry + build_fraction_field -> device mapping
+    ("        blk.registry.build(blk.box, blk.snapshots, params_.subdivisions);\n"
+     "        psm::build_fraction_field(blk.frac, blk.box, blk.registry, blk.snapshots,\n"
+     "                                  params_.kernels == KernelMode::openmp);\n",
+     "        blk.dev->map(blk.snapshots, params_.subdivisions);\n"
+     "        blk.dev->sync();\n"),
+    # sim.cpp:296-297 — set_solid_velocities on the device (post velocity-sync snapshots)
+    ("        psm::set_solid_velocities(blk.svel, blk.frac, blk.box, blk.snapshots,\n"
+     "                                  params_.kernels == KernelMode::openmp);\n",
+     "        blk.dev->set_solid_velocities(blk.snapshots);\n"
+     "        blk.dev->sync();\n"),
+    # sim.cpp:302 — inner kernel + end-of-operator check
+    ("        run_kernel(blk, {{1, 1, 1}, {d.x - 1, d.y - 1, d.z - 1}});\n",
+     "        run_kernel(blk, {{1, 1, 1}, {d.x - 1, d.y - 1, d.z - 1}});\n"
+     "        blk.dev->sync();\n"),
+    # sim.cpp:312-317 — BCs, outer shell in one launch, swap
+    ("    lbm::apply_boundaries(blk.field, params_.bc, blk.domain_faces);\n"
+     "    {\n"
+     "        ScopedTimer t(blk.timings, Category::kPsm);\n"
+     "        for (const CellBox& box : boundary_shell(blk.dims())) run_kernel(blk, box);\n"
+     "    }\n"
+     "    blk.field.swap();\n",
+     "    blk.dev->apply_boundaries(params_.bc, blk.domain_faces);\n"
+     "    {\n"
+     "        ScopedTimer t(blk.timings, Category::kPsm);\n"
+     "        blk.dev->sweep_boxes(params_.fluid, boundary_shell(blk.dims()));\n"
+     "        blk.dev->sync();\n"
+     "    }\n"
+     "    blk.dev->swap();\n"
+     "    blk.host_stale = true;\n"),
+    # sim.cpp:321 — finalize_hydro_forces on the device (PARITY: bitwise partials)
+    ("    auto partials = psm::finalize_hydro_forces(blk.frac, blk.scratch, blk.box, blk.snapshots);\n",
+     "    auto partials = blk.dev->finalize_hydro_forces();\n"),
+    # sim.cpp:740-772 — observers read refreshed host copies
+    ("double Simulation::total_fluid_mass() const {\n",
+     "double Simulation::total_fluid_mass() const {\n    refresh_host(blocks_, params_.coupling);\n"),
+    ("Vec3 Simulation::total_fluid_momentum() const {\n",
+     "Vec3 Simulation::total_fluid_momentum() const {\n    refresh_host(blocks_, params_.coupling);\n"),
+    ("void Simulation::macroscopic_at(const Vec3i& cell, double& rho, Vec3& u) const {\n",
+     "void Simulation::macroscopic_at(const Vec3i& cell, double& rho, Vec3& u) const {\n"
+     "    refresh_host(blocks_, params_.coupling);\n"),
+    ("double Simulation::pdf_at(const Vec3i& cell, int q) const {\n",
+     "double Simulation::pdf_at(const Vec3i& cell, int q) const {\n    refresh_host(blocks_, params_.coupling);\n"),
+    ("double Simulation::fraction_at(const Vec3i& cell) const {\n",
+     "double Simulation::fraction_at(const Vec3i& cell) const {\n    refresh_host(blocks_, params_.coupling);\n"),
+]
+
+
+def patch(src, edits, name):
+    text = open(src).read()
+    for anchor, repl in edits:
+        if text.count(anchor) != 1:
+            sys.exit(f"{name}: anchor not found exactly once:\n{anchor}")
+        text = text.replace(anchor, repl)
+    return text
+
+
+def main():
+    if not os.path.isdir(REF):
+        if os.path.exists(os.path.join(BUILD, "liblbdem_dropin.so")):
+            return 0
+        sys.exit(f"reference sources not found at {REF}")
+    os.makedirs(os.path.join(BUILD, "include", "lbdem"), exist_ok=True)
+    os.makedirs(os.path.join(BUILD, "src"), exist_ok=True)
+    hpp = patch(os.path.join(REF, "include/lbdem/sim.hpp"), SIM_HPP_EDITS, "sim.hpp")
+    cpp = patch(os.path.join(REF, "src/sim.cpp"), SIM_CPP_EDITS, "sim.cpp")
+    for path, text in ((os.path.join(BUILD, "include/lbdem/sim.hpp"), hpp), (os.path.join(BUILD, "src/sim.cpp"), cpp)):
+        if not os.path.exists(path) or open(path).read() != text:
+            open(path, "w").write(text)
+    subprocess.check_call(["make", "-s", "-j8", "-C", HERE, f"REF={REF}"])
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

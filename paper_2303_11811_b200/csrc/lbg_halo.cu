@@ -112,6 +112,23 @@ __global__ void __launch_bounds__(256) halo_unpack_kernel(const HaloArgs h) {
     }
 }
 
+// generic slab copy between the src buffer and a packed [q][k][j][i] buffer
+__global__ void __launch_bounds__(256) slab_copy_kernel(double* __restrict__ src, Layout L, int lo0, int lo1,
+                                                        int lo2, int e0, int e1, int e2,
+                                                        double* __restrict__ buf, int to_buf) {
+    const long long cells = (long long)e0 * e1 * e2;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= cells * kQ) return;
+    const int q = (int)(t / cells);
+    const long long r = t % cells;
+    const int i = lo0 + (int)(r % e0), j = lo1 + (int)((r / e0) % e1), k = lo2 + (int)(r / ((long long)e0 * e1));
+    double* p = src + q * L.plane + L.idx(i, j, k);
+    if (to_buf)
+        buf[t] = *p;
+    else
+        *p = buf[t];
+}
+
 static lbg_status nccl_check(ncclResult_t r, const char* what) {
     if (r == ncclSuccess) return LBG_OK;
     return set_error(LBG_CUDA_ERROR, std::string(what) + ": " + ncclGetErrorString(r));
@@ -268,6 +285,64 @@ lbg_status lbg_halo_complete(lbg_block b) {
     }
     c.pending = false;
     return LBG_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// source_slab (sim.cpp:120-135) for pack, ghost_region (sim.cpp:137-152) for unpack
+void slab_box(const lbg::Layout& L, const int off[3], bool ghost, int lo[3], int ext[3]) {
+    const int n[3] = {L.nx, L.ny, L.nz};
+    for (int a = 0; a < 3; ++a) {
+        if (off[a] == 1) {
+            lo[a] = ghost ? n[a] : n[a] - 1;
+            ext[a] = 1;
+        } else if (off[a] == -1) {
+            lo[a] = ghost ? -1 : 0;
+            ext[a] = 1;
+        } else {
+            lo[a] = 0;
+            ext[a] = n[a];
+        }
+    }
+}
+
+lbg_status slab_io(lbg_block b, const int off[3], bool ghost, double* host, long long capacity,
+                   long long* n_out, bool to_host) {
+    using namespace lbg;
+    if (!b || !off || !host) return set_error(LBG_INVALID, "null argument");
+    int lo[3], ext[3];
+    slab_box(b->L, off, ghost, lo, ext);
+    const long long n = (long long)kQ * ext[0] * ext[1] * ext[2];
+    if (n_out) *n_out = n;
+    if (capacity < n) return set_error(LBG_INVALID, "slab buffer too small");
+    LBG_CUDA(cudaSetDevice(b->device));
+    double* d = nullptr;
+    LBG_CUDA(cudaMallocAsync(&d, sizeof(double) * n, b->stream));
+    if (!to_host) LBG_CUDA(cudaMemcpyAsync(d, host, sizeof(double) * n, cudaMemcpyHostToDevice, b->stream));
+    slab_copy_kernel<<<(unsigned)((n + 255) / 256), 256, 0, b->stream>>>(b->src(), b->L, lo[0], lo[1], lo[2],
+                                                                         ext[0], ext[1], ext[2], d, to_host);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess && to_host)
+        e = cudaMemcpyAsync(host, d, sizeof(double) * n, cudaMemcpyDeviceToHost, b->stream);
+    cudaFreeAsync(d, b->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(b->stream);
+    if (e != cudaSuccess) return cuda_check(e, "slab copy");
+    return LBG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+lbg_status lbg_pack_slab(lbg_block b, const int off[3], double* out, long long capacity, long long* n_out) {
+    return slab_io(b, off, false, out, capacity, n_out, true);
+}
+
+lbg_status lbg_unpack_slab(lbg_block b, const int dir[3], const double* in, long long n) {
+    return slab_io(b, dir, true, const_cast<double*>(in), n, nullptr, false);
 }
 
 }  // extern "C"
