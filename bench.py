@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--n", type=int, default=512, help="cells per axis of each GPU's block")
     ap.add_argument("--tau", type=float, default=0.8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-coupled", action="store_true", help="skip the config-3 coupled-step timing")
+    ap.add_argument("--coupled-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     return ap.parse_args()
 
@@ -164,6 +166,54 @@ def run_reference(args):
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
+
+
+# --------------------------------------------------------------------------- coupled step
+CONFIG3 = ('{"scenario":"fluidized_bed_dense","domain":[256,256,256],"particles":{"count":10000},'
+           '"physical":{"diameter_cells":10},"fluid":{"bc":{"xm":"no_slip","xp":"no_slip",'
+           '"ym":"no_slip","yp":"no_slip","zm":"velocity","zp":"pressure"}},'
+           '"dem":{"k_n":230,"d_n":520,"k_t":65,"d_t":260,"subcycles":10}}')
+CATS = ("PSM", "PSM-comm", "mapping", "setU", "redF", "PD", "PD-comm", "other")
+
+
+def coupled_step(steps, with_reference, ref_steps=1):
+    """Config 3: ~10^4 spheres d = 10 in 256^3, bed BCs, four-way coupled
+    with the reference's host DEM. GPU side through the drop-in build (the reference
+    Simulation with its fluid/coupling operators on liblbg); the same config on the
+    unmodified reference (oracle/_ref, OpenMP on all host cores) for comparison. Times are
+    the reference's own per-category wall-clock TimingReport (perf.hpp:17-51)."""
+    sys.path.insert(0, os.path.join(ROOT, "integration"))
+    import dropin
+    out = {"workload": "config 3: 10^4 spheres (d = 10) in 256^3, no-slip walls, velocity inflow, "
+                       "pressure outflow, 10 DEM sub-cycles per fluid step (host DEM = reference code)"}
+    sim = dropin.DropinSim(CONFIG3, (256, 256, 256))
+    sim.run(1)  # warm-up (allocations, first mapping)
+    sim.reset_timers()
+    t0 = time.perf_counter()
+    sim.run(steps)
+    dt = time.perf_counter() - t0
+    cat = sim.timings()
+    out.update({"ms_per_step": round(dt * 1e3 / steps, 2), "steps": steps,
+                "categories_ms_per_step": {c: round(v * 1e3 / steps, 3) for c, v in zip(CATS, cat)},
+                "particles": len(sim.particles()),
+                "mlups": round(256 ** 3 * steps / dt / 1e6, 1)})
+    sim.close()
+    if with_reference:
+        from oracle.pyoracle import RefLib
+        ref = RefLib()
+        threads = os.cpu_count() or 1
+        ref.set_threads(threads)
+        rs = ref.sim(CONFIG3)
+        rs.reset_timers()
+        t0 = time.perf_counter()
+        rs.run(ref_steps)
+        rdt = time.perf_counter() - t0
+        rc = rs.timings()
+        out["reference"] = {"ms_per_step": round(rdt * 1e3 / ref_steps, 1), "steps": ref_steps,
+                            "threads": threads, "kind": "reference",
+                            "categories_ms_per_step": {c: round(v * 1e3 / ref_steps, 2) for c, v in zip(CATS, rc)}}
+        out["speedup_vs_reference"] = round(out["reference"]["ms_per_step"] / out["ms_per_step"], 2)
+    return out
 
 
 # --------------------------------------------------------------------------- GPU path
@@ -307,8 +357,14 @@ def run_lbg(args):
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
-        print(json.dumps(out))
     blk.close()
+    if rank == 0:
+        if N == 1 and not args.no_coupled:
+            try:
+                out["coupled_step"] = coupled_step(args.coupled_steps, not args.no_cpu_baseline)
+            except Exception as e:  # noqa: BLE001
+                out["coupled_step"] = {"unavailable": f"{type(e).__name__}: {e}"}
+        print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
     return 0
