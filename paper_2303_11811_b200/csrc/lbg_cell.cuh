@@ -145,4 +145,99 @@ __device__ __forceinline__ bool psm_cell(double (&f)[kQ], double inv_tau, Force 
     return ok;
 }
 
+// moments of srt_cell (folded, identical operations)
+__device__ __forceinline__ void moments(const double (&f)[kQ], double& rho, double& ux, double& uy,
+                                        double& uz) {
+    rho = f[0];
+#pragma unroll
+    for (int q = 1; q < kQ; ++q) rho += f[q];
+    ux = ((((((((f[1] - f[2]) + f[7]) - f[8]) + f[9]) - f[10]) + f[11]) - f[12]) + f[13]) - f[14];
+    uy = ((((((((f[3] - f[4]) + f[7]) - f[8]) - f[9]) + f[10]) + f[15]) - f[16]) + f[17]) - f[18];
+    uz = ((((((((f[5] - f[6]) + f[11]) - f[12]) - f[13]) + f[14]) + f[15]) - f[16]) - f[17]) + f[18];
+}
+
+// equilibrium(rho, u) via the exact +-cu pairs (any velocity; signed zeros in cu cannot
+// reach feq because A + B and B - A with B = +0 are +0 either way)
+__device__ __forceinline__ void feq_all(double rho, double ux, double uy, double uz, double (&feq)[kQ]) {
+    const double T = (0.5 * ((ux * ux + uy * uy) + uz * uz)) * 3.0;
+    feq[0] = wq(0) * (rho - T);
+    feq_pair(wq(1), ux, rho, T, feq[1], feq[2]);
+    feq_pair(wq(3), uy, rho, T, feq[3], feq[4]);
+    feq_pair(wq(5), uz, rho, T, feq[5], feq[6]);
+    feq_pair(wq(7), ux + uy, rho, T, feq[7], feq[8]);
+    feq_pair(wq(9), ux - uy, rho, T, feq[9], feq[10]);
+    feq_pair(wq(11), ux + uz, rho, T, feq[11], feq[12]);
+    feq_pair(wq(13), ux - uz, rho, T, feq[13], feq[14]);
+    feq_pair(wq(15), uy + uz, rho, T, feq[15], feq[16]);
+    feq_pair(wq(17), uy - uz, rho, T, feq[17], feq[18]);
+}
+
+// cu of direction q for velocity u, equal to (c . u) of the reference for nonzero results
+template <int q>
+__device__ __forceinline__ double cu_of(double ux, double uy, double uz) {
+    constexpr int a = cx(q), b = cy(q), c = cz(q);
+    if constexpr (a == 0 && b == 0 && c == 0) return 0.0;
+    else if constexpr (b == 0 && c == 0) return a > 0 ? ux : -ux;
+    else if constexpr (a == 0 && c == 0) return b > 0 ? uy : -uy;
+    else if constexpr (a == 0 && b == 0) return c > 0 ? uz : -uz;
+    else if constexpr (c == 0) return a > 0 ? (b > 0 ? ux + uy : ux - uy) : (b > 0 ? -(ux - uy) : -(ux + uy));
+    else if constexpr (b == 0) return a > 0 ? (c > 0 ? ux + uz : ux - uz) : (c > 0 ? -(ux - uz) : -(ux + uz));
+    else return b > 0 ? (c > 0 ? uy + uz : uy - uz) : (c > 0 ? -(uy - uz) : -(uy + uz));
+}
+
+// psm_cell (psm.cpp:174-216) with the register footprint cut down: the fluid equilibrium
+// enters only through d_q = f_q - feq_f,q (feq_f - f == -d exactly), the particle
+// equilibria are rebuilt pairwise per entry, and the unforced path drops the force term
+// (it adds a signed zero to a value it cannot change). Momentum sums keep every term.
+template <bool kForced>
+__device__ __forceinline__ bool psm_cell_opt(double (&f)[kQ], double inv_tau, Force F, int cnt,
+                                             double b_tot, const double be[2], const double ue[2][3],
+                                             double m_out[2][3]) {
+    double rho, ux, uy, uz;
+    moments(f, rho, ux, uy, uz);
+    const double usq = (ux * ux + uy * uy) + uz * uz;
+    const bool ok = rho > 0.0 && usq <= kMaxVelocity * kMaxVelocity && isfinite(rho);
+    double d[kQ];
+    feq_all(rho, ux, uy, uz, d);
+    double fout[kQ];
+    const double fluid_w = 1.0 - b_tot;
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+        const double coll = inv_tau * (d[q] - f[q]);  // inv_tau * (feq_f - f)
+        d[q] = f[q] - d[q];
+        fout[q] = coll;
+    }
+    if constexpr (kForced) {
+#define LBG_PF(q) fout[q] = f[q] + fluid_w * (fout[q] + forcing<q>(cu_of<q>(ux, uy, uz), ux, uy, uz, F.x, F.y, F.z))
+        LBG_PF(0); LBG_PF(1); LBG_PF(2); LBG_PF(3); LBG_PF(4); LBG_PF(5); LBG_PF(6);
+        LBG_PF(7); LBG_PF(8); LBG_PF(9); LBG_PF(10); LBG_PF(11); LBG_PF(12);
+        LBG_PF(13); LBG_PF(14); LBG_PF(15); LBG_PF(16); LBG_PF(17); LBG_PF(18);
+#undef LBG_PF
+    } else {
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) fout[q] = f[q] + fluid_w * fout[q];
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {  // static entry index keeps be/ue/m_out in registers
+        if (e >= cnt) break;
+        double fp[kQ];
+        feq_all(rho, ue[e][0], ue[e][1], ue[e][2], fp);
+        double mx = 0.0, my = 0.0, mz = 0.0;
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+            const double c_solid = d[opposite(q)] - (f[q] - fp[q]);
+            fout[q] += be[e] * c_solid;
+            mx -= c_solid * (double)cx(q);
+            my -= c_solid * (double)cy(q);
+            mz -= c_solid * (double)cz(q);
+        }
+        m_out[e][0] = be[e] * mx;
+        m_out[e][1] = be[e] * my;
+        m_out[e][2] = be[e] * mz;
+    }
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) f[q] = fout[q];
+    return ok;
+}
+
 }  // namespace lbg

@@ -269,6 +269,11 @@ __global__ void __launch_bounds__(128) reduce_kernel(const ReduceArgs a) {
         lo[d] = max((int)floor(p.x[d] - reach - g.lo[d]) - 1, 0);
         hi[d] = min((int)floor(p.x[d] + reach - g.lo[d]) + 1, g.dims[d] - 1);
     }
+    // PARITY: lane l < 6 owns one compensated chain (f.x f.y f.z t.x t.y t.z) and replays the
+    // segment's hits in lane order from shared memory — the 6 chains run in parallel
+    __shared__ double seg[4][32][6];
+    double (*sg)[6] = seg[(threadIdx.x >> 5) & 3];
+    double csum = 0.0, ccomp = 0.0;
     double fs[3] = {0, 0, 0}, fc[3] = {0, 0, 0}, ts[3] = {0, 0, 0}, tc[3] = {0, 0, 0};
     unsigned long long hits = 0;
     const int id = p.id;
@@ -307,13 +312,33 @@ __global__ void __launch_bounds__(128) reduce_kernel(const ReduceArgs a) {
                     }
                     continue;
                 }
-                while (mask) {  // replay hits in lane (= lexicographic) order
-                    const int src = __ffs(mask) - 1;
-                    mask &= mask - 1;
-                    for (int d = 0; d < 3; ++d) nm_add(fs[d], fc[d], __shfl_sync(0xffffffffu, m[d], src));
-                    for (int d = 0; d < 3; ++d) nm_add(ts[d], tc[d], __shfl_sync(0xffffffffu, t[d], src));
+                if (!mask) continue;
+                if (e >= 0) {
+                    sg[lane][0] = m[0];
+                    sg[lane][1] = m[1];
+                    sg[lane][2] = m[2];
+                    sg[lane][3] = t[0];
+                    sg[lane][4] = t[1];
+                    sg[lane][5] = t[2];
                 }
+                __syncwarp();
+                if (lane < 6) {
+                    while (mask) {  // replay hits in lane (= lexicographic) order
+                        const int src = __ffs(mask) - 1;
+                        mask &= mask - 1;
+                        nm_add(csum, ccomp, sg[src][lane]);
+                    }
+                }
+                __syncwarp();
             }
+    if (!a.fast) {  // gather the six chains to lane 0's layout
+        for (int d = 0; d < 3; ++d) {
+            fs[d] = __shfl_sync(0xffffffffu, csum, d);
+            fc[d] = __shfl_sync(0xffffffffu, ccomp, d);
+            ts[d] = __shfl_sync(0xffffffffu, csum, 3 + d);
+            tc[d] = __shfl_sync(0xffffffffu, ccomp, 3 + d);
+        }
+    }
     if (a.fast) {
         for (int d = 0; d < 3; ++d)
             for (int o = 16; o > 0; o >>= 1) {

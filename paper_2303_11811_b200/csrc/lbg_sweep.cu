@@ -92,6 +92,7 @@ __device__ __forceinline__ bool srt_cell_at(const SweepArgs& a, int i, int j, in
 }
 
 // covered cell, psm.cpp:236-258
+template <bool kForced>
 __device__ __forceinline__ bool psm_cell_at(const SweepArgs& a, int i, int j, int k) {
     const Layout& L = a.L;
     const long long base = L.idx(i, j, k);
@@ -106,7 +107,7 @@ __device__ __forceinline__ bool psm_cell_at(const SweepArgs& a, int i, int j, in
         ue[1][c] = cnt > 1 ? a.v1[3 * fc + c] : 0.0;
     }
     double m[2][3];
-    const bool ok = psm_cell(f, a.inv_tau, a.F, cnt, a.btot[fc], be, ue, m);
+    const bool ok = psm_cell_opt<kForced>(f, a.inv_tau, a.F, cnt, a.btot[fc], be, ue, m);
     for (int c = 0; c < 3; ++c) a.m0[3 * fc + c] = m[0][c];
     if (cnt > 1)
         for (int c = 0; c < 3; ++c) a.m1[3 * fc + c] = m[1][c];
@@ -162,6 +163,7 @@ __device__ __forceinline__ bool in_boxes(const SweepArgs& a, int i, int j, int k
 }
 
 // K2: grid-stride over the covered-cell list (length read on the device)
+template <bool kForced>
 __global__ void __launch_bounds__(128) psm_list_kernel(const SweepArgs a) {
     const int n = *a.cov_n;
     const int stride = gridDim.x * blockDim.x;
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(128) psm_list_kernel(const SweepArgs a) {
             const int i = (int)(c % (unsigned)L.nx);
             const int j = (int)((c / (unsigned)L.nx) % (unsigned)L.ny);
             const int k = (int)(c / ((unsigned)L.nx * (unsigned)L.ny));
-            if (in_boxes(a, i, j, k)) ok = psm_cell_at(a, i, j, k);
+            if (in_boxes(a, i, j, k)) ok = psm_cell_at<kForced>(a, i, j, k);
         }
         count_bad(a.err, !ok);
     }
@@ -260,11 +262,14 @@ static void launch_flat(const SweepArgs& a, cudaStream_t s) {
     sweep_flat_kernel<kForced, kSkip><<<(unsigned)((n + T - 1) / T), T, 0, s>>>(a);
 }
 
-static void launch_psm_list(lbg_block b, const SweepArgs& a) {
+static void launch_psm_list(lbg_block b, const SweepArgs& a, bool forced) {
     // persistent grid: 4 CTAs of 128 per SM, the list length is read on the device
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, b->device);
-    psm_list_kernel<<<sms * 4, 128, 0, b->stream>>>(a);
+    if (forced)
+        psm_list_kernel<true><<<sms * 4, 128, 0, b->stream>>>(a);
+    else
+        psm_list_kernel<false><<<sms * 4, 128, 0, b->stream>>>(a);
 }
 
 }  // namespace lbg
@@ -305,7 +310,7 @@ lbg_status lbg_sweep(lbg_block b, const lbg_fluid* fl, const lbg_box* range) {
     if (b->coupling) {
         fo ? launch_box<true, true>(a, b->stream) : launch_box<false, true>(a, b->stream);
         LBG_LAUNCH_CHECK();
-        launch_psm_list(b, a);
+        launch_psm_list(b, a, fo);
     } else {
         fo ? launch_box<true, false>(a, b->stream) : launch_box<false, false>(a, b->stream);
     }
@@ -328,7 +333,7 @@ lbg_status lbg_sweep_boxes(lbg_block b, const lbg_fluid* fl, const lbg_box* boxe
     if (b->coupling) {
         fo ? launch_flat<true, true>(a, b->stream) : launch_flat<false, true>(a, b->stream);
         LBG_LAUNCH_CHECK();
-        launch_psm_list(b, a);
+        launch_psm_list(b, a, fo);
     } else {
         fo ? launch_flat<true, false>(a, b->stream) : launch_flat<false, false>(a, b->stream);
     }
