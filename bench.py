@@ -79,6 +79,10 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            t0 = time.time()  # nvidia-smi needs a moment: start timing once it samples
+            while not self.rows and time.time() - t0 < 3.0:
+                time.sleep(0.02)
+            self.rows.clear()
         except Exception:
             self.proc = None
         return self
@@ -186,18 +190,28 @@ def coupled_step(steps, with_reference, ref_steps=1):
     import dropin
     out = {"workload": "config 3: 10^4 spheres (d = 10) in 256^3, no-slip walls, velocity inflow, "
                        "pressure outflow, 10 DEM sub-cycles per fluid step (host DEM = reference code)"}
-    sim = dropin.DropinSim(CONFIG3, (256, 256, 256))
-    sim.run(1)  # warm-up (allocations, first mapping)
-    sim.reset_timers()
-    t0 = time.perf_counter()
-    sim.run(steps)
-    dt = time.perf_counter() - t0
-    cat = sim.timings()
-    out.update({"ms_per_step": round(dt * 1e3 / steps, 2), "steps": steps,
-                "categories_ms_per_step": {c: round(v * 1e3 / steps, 3) for c, v in zip(CATS, cat)},
-                "particles": len(sim.particles()),
-                "mlups": round(256 ** 3 * steps / dt / 1e6, 1)})
-    sim.close()
+    for mode in ("scratch", "fused"):
+        # scratch: reference semantics, partials bitwise (PARITY reduction);
+        # fused: force/torque summed inside the PSM kernel (FAST, tolerance-level partials)
+        os.environ["LBDEM_GPU_FORCE"] = mode
+        sim = dropin.DropinSim(CONFIG3, (256, 256, 256))
+        sim.run(1)  # warm-up (allocations, first mapping)
+        sim.reset_timers()
+        t0 = time.perf_counter()
+        sim.run(steps)
+        dt = time.perf_counter() - t0
+        cat = sim.timings()
+        rec = {"ms_per_step": round(dt * 1e3 / steps, 2), "steps": steps,
+               "categories_ms_per_step": {c: round(v * 1e3 / steps, 3) for c, v in zip(CATS, cat)},
+               "gpu_side_ms_per_step": round(sum(cat[i] for i in (0, 1, 2, 3, 4)) * 1e3 / steps, 3),
+               "particles": len(sim.particles()),
+               "mlups": round(256 ** 3 * steps / dt / 1e6, 1)}
+        sim.close()
+        if mode == "scratch":
+            out.update(rec)
+        else:
+            out["fused_force_mode"] = rec
+    os.environ.pop("LBDEM_GPU_FORCE", None)
     if with_reference:
         from oracle.pyoracle import RefLib
         ref = RefLib()
@@ -279,6 +293,7 @@ def run_lbg(args):
     blk.timings()  # clear
     l0 = lbdem.launch_count()
     with ClockSampler(local) as clk:
+        barrier()  # all ranks' samplers are running
         e0.record(stream)
         for _ in range(args.steps):
             step()

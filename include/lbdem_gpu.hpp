@@ -21,7 +21,9 @@
 //   end-of-operator throws                      sync()  (NumericError / SyncError, same texts)
 #pragma once
 
+#include <algorithm>
 #include <array>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -56,11 +58,20 @@ inline lbg_fluid to_fluid(const lbm::FluidParams& p) { return {p.tau, {p.f_ext.x
 
 class DeviceBlock {
 public:
-    DeviceBlock(int device, const CellBox& box, bool coupling) {
+    /// force_mode: LBG_FORCE_SCRATCH (reference semantics, bitwise partials) or
+    /// LBG_FORCE_FUSED (force/torque summed inside the PSM kernel; tolerance-level partials).
+    /// -1 reads LBDEM_GPU_FORCE=fused|scratch from the environment (default scratch).
+    DeviceBlock(int device, const CellBox& box, bool coupling, int force_mode = -1) {
         const Vec3i d = box.hi - box.lo;
         const int lo[3] = {box.lo.x, box.lo.y, box.lo.z};
         const int dims[3] = {d.x, d.y, d.z};
         check(lbg_block_create(device, lo, dims, coupling ? 1 : 0, &b_));
+        if (force_mode < 0) {
+            const char* e = std::getenv("LBDEM_GPU_FORCE");
+            force_mode = (e && std::string(e) == "fused") ? LBG_FORCE_FUSED : LBG_FORCE_SCRATCH;
+        }
+        if (coupling) check(lbg_set_force_mode(b_, force_mode));
+        fused_ = coupling && force_mode == LBG_FORCE_FUSED;
     }
     ~DeviceBlock() { lbg_block_destroy(b_); }
     DeviceBlock(const DeviceBlock&) = delete;
@@ -138,7 +149,8 @@ public:
     }
     void swap() { check(lbg_swap(b_)); }
 
-    std::vector<psm::HydroPartial> finalize_hydro_forces(int mode = LBG_REDUCE_PARITY) {
+    std::vector<psm::HydroPartial> finalize_hydro_forces(int mode = -1) {
+        if (mode < 0) mode = fused_ ? LBG_REDUCE_FAST : LBG_REDUCE_PARITY;
         std::vector<lbg_hydro_partial> out(cs_.size() + 1);
         int n = 0;
         check(lbg_reduce_hydro(b_, mode, out.data(), static_cast<int>(out.size()), &n));
@@ -171,6 +183,7 @@ private:
     }
 
     lbg_block b_ = nullptr;
+    bool fused_ = false;
     std::vector<lbg_snapshot> cs_;
 };
 

@@ -103,6 +103,14 @@ enum {
     LBG_REDUCE_FAST = 1    /* warp shuffles + shared memory + per-particle atomics (tolerance) */
 };
 
+/* Where the PSM kernel puts the per-entry momentum transfer. */
+enum {
+    LBG_FORCE_SCRATCH = 0, /* CellMomentumScratch m0/m1 (field.hpp:112-118), reduced by
+                              lbg_reduce_hydro; PARITY-capable (reference semantics) */
+    LBG_FORCE_FUSED = 1    /* summed per particle inside the sweep (warp-aggregated by particle,
+                              one atomic per warp group); lbg_reduce_hydro(FAST) returns the sums */
+};
+
 /* Timing categories, perf.hpp:17-26 (perf::Category order). */
 enum {
     LBG_CAT_PSM = 0,
@@ -180,8 +188,11 @@ lbg_status lbg_apply_boundaries(lbg_block b, const lbg_face_bc faces[6], const i
 lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisions);
 /* set_solid_velocities alone (psm.cpp:138-169) for a fraction field set by the caller. */
 lbg_status lbg_set_solid_velocities(lbg_block b, const lbg_snapshot* snaps, int n);
+/* LBG_FORCE_SCRATCH (default) or LBG_FORCE_FUSED; takes effect from the next lbg_map. */
+lbg_status lbg_set_force_mode(lbg_block b, int mode);
 /* finalize_hydro_forces (psm.cpp:278-322): fills out[] id-sorted (one row per particle
- * with at least one entry), sets *n_out, clears the scratch. Blocks until done. */
+ * with at least one entry), sets *n_out, clears the scratch. Blocks until done.
+ * In LBG_FORCE_FUSED mode only LBG_REDUCE_FAST is available (comp terms are zero). */
 lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int capacity,
                             int* n_out);
 
@@ -204,6 +215,11 @@ lbg_status lbg_sync(lbg_block b, lbg_errors* out);
  * per block of cells, then combined in fixed order (deterministic, not bitwise). */
 lbg_status lbg_total_mass(lbg_block b, double* out);
 lbg_status lbg_total_momentum(lbg_block b, double out[3]);
+/* The fluid part of io::sample_scalars (output.cpp:22-45), one device pass over the src
+ * interior: out = {mass, momentum x, y, z (bare moment, lbm.cpp:82-93), fluid kinetic energy
+ * sum 0.5 rho |u|^2 and max |u| with the observable u = m + f_ext/2 (lbm.hpp:55-63)}.
+ * Compensated, deterministic for a given device; not bitwise equal to the serial order. */
+lbg_status lbg_observe(lbg_block b, const double f_ext[3], double out[6]);
 
 /* ------------------------------------------------------------------ halo exchange */
 /* Simulation::begin/complete_halo_exchange (sim.cpp:156-201) for a slab decomposition

@@ -157,11 +157,127 @@ __global__ void row_moments_kernel(const double* __restrict__ src, Layout L, dou
     }
 }
 
+// ---- per-step observers (output.cpp:22-61 sample_scalars; lbm.cpp:69-93), on the device.
+// Each thread walks a fixed strided set of cells with Neumaier accumulators, the CTA combines
+// the (sum, comp) pairs in a fixed tree, and the host adds the CTA partials in order:
+// deterministic for a given grid (not bitwise equal to the reference's serial order).
+constexpr int kObsThreads = 256;
+constexpr int kObsVals = 5;  // mass, px, py, pz, fluid KE
+
+__device__ __forceinline__ void two_sum_add(double& s, double& c, double s2, double c2) {
+    const double t = s + s2;
+    const double bp = t - s;
+    const double err = (s - (t - bp)) + (s2 - bp);
+    s = t;
+    c = (c + c2) + err;
+}
+
+__global__ void __launch_bounds__(kObsThreads) observe_kernel(const double* __restrict__ src, Layout L,
+                                                               double fx, double fy, double fz,
+                                                               double* __restrict__ part) {
+    double s[kObsVals] = {0, 0, 0, 0, 0}, c[kObsVals] = {0, 0, 0, 0, 0};
+    double max_u2 = 0.0;
+    const long long cells = (long long)L.nx * L.ny * L.nz;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < cells;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(t % L.nx), j = (int)((t / L.nx) % L.ny), k = (int)(t / ((long long)L.nx * L.ny));
+        const long long base = L.idx(i, j, k);
+        double rho = 0.0, mx = 0.0, my = 0.0, mz = 0.0;
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+            const double f = src[q * L.plane + base];
+            rho += f;
+            mx += f * (double)cx(q);
+            my += f * (double)cy(q);
+            mz += f * (double)cz(q);
+        }
+        // lbm.hpp:55-63: observable velocity carries the half-force shift
+        const double ux = mx / 1.0 + (1.0 / (2.0 * 1.0)) * fx;
+        const double uy = my / 1.0 + (1.0 / (2.0 * 1.0)) * fy;
+        const double uz = mz / 1.0 + (1.0 / (2.0 * 1.0)) * fz;
+        const double u2 = (ux * ux + uy * uy) + uz * uz;
+        const double v[kObsVals] = {rho, mx, my, mz, 0.5 * rho * u2};
+#pragma unroll
+        for (int a = 0; a < kObsVals; ++a) nm_add(s[a], c[a], v[a]);
+        max_u2 = fmax(max_u2, u2);
+    }
+    __shared__ double sh[kObsThreads / 32][2 * kObsVals + 1];
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int a = 0; a < kObsVals; ++a) {
+            const double s2 = __shfl_down_sync(0xffffffffu, s[a], o);
+            const double c2 = __shfl_down_sync(0xffffffffu, c[a], o);
+            two_sum_add(s[a], c[a], s2, c2);
+        }
+        max_u2 = fmax(max_u2, __shfl_down_sync(0xffffffffu, max_u2, o));
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        for (int a = 0; a < kObsVals; ++a) {
+            sh[w][2 * a] = s[a];
+            sh[w][2 * a + 1] = c[a];
+        }
+        sh[w][2 * kObsVals] = max_u2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double* out = part + (size_t)blockIdx.x * (2 * kObsVals + 1);
+        for (int a = 0; a < kObsVals; ++a) {
+            double ss = sh[0][2 * a], cc = sh[0][2 * a + 1];
+            for (int v = 1; v < kObsThreads / 32; ++v) two_sum_add(ss, cc, sh[v][2 * a], sh[v][2 * a + 1]);
+            out[2 * a] = ss;
+            out[2 * a + 1] = cc;
+        }
+        double m = sh[0][2 * kObsVals];
+        for (int v = 1; v < kObsThreads / 32; ++v) m = fmax(m, sh[v][2 * kObsVals]);
+        out[2 * kObsVals] = m;
+    }
+}
+
 }  // namespace lbg
 
 using namespace lbg;
 
 extern "C" {
+
+lbg_status lbg_observe(lbg_block b, const double f_ext[3], double out[6]) {
+    if (!b || !out) return set_error(LBG_INVALID, "null argument");
+    LBG_CUDA(cudaSetDevice(b->device));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, b->device);
+    const int blocks = sms * 4;
+    const size_t per = 2 * kObsVals + 1;
+    if (!b->obs_d) {
+        LBG_CUDA(cudaMalloc(&b->obs_d, sizeof(double) * per * blocks));
+        LBG_CUDA(cudaMallocHost(&b->obs_h, sizeof(double) * per * blocks));
+    }
+    const double fx = f_ext ? f_ext[0] : 0.0, fy = f_ext ? f_ext[1] : 0.0, fz = f_ext ? f_ext[2] : 0.0;
+    {
+        Span span(b, LBG_CAT_OTHER);
+        observe_kernel<<<blocks, kObsThreads, 0, b->stream>>>(b->src(), b->L, fx, fy, fz, b->obs_d);
+        LBG_LAUNCH_CHECK();
+        LBG_CUDA(cudaMemcpyAsync(b->obs_h, b->obs_d, sizeof(double) * per * blocks, cudaMemcpyDeviceToHost,
+                                 b->stream));
+    }
+    LBG_CUDA(cudaStreamSynchronize(b->stream));
+    double s[kObsVals] = {0, 0, 0, 0, 0}, c[kObsVals] = {0, 0, 0, 0, 0}, mx = 0.0;
+    for (int k = 0; k < blocks; ++k) {
+        const double* p = b->obs_h + per * k;
+        for (int a = 0; a < kObsVals; ++a) {
+            const double t = s[a] + p[2 * a];
+            if (std::fabs(s[a]) >= std::fabs(p[2 * a]))
+                c[a] += (s[a] - t) + p[2 * a];
+            else
+                c[a] += (p[2 * a] - t) + s[a];
+            s[a] = t;
+            c[a] += p[2 * a + 1];
+        }
+        mx = std::max(mx, p[2 * kObsVals]);
+    }
+    for (int a = 0; a < kObsVals; ++a) out[a] = s[a] + c[a];
+    out[5] = std::sqrt(mx);
+    return LBG_OK;
+}
 
 const char* lbg_last_error(void) { return g_last_error.c_str(); }
 const char* lbg_version(void) { return "lbg 0.1 (sm_100a)"; }
@@ -269,10 +385,10 @@ lbg_status lbg_block_destroy(lbg_block b) {
     if (b->comm) lbg_comm_destroy(b);
     void* dev[] = {b->buf[0], b->buf[1], b->count, b->id0, b->id1, b->b0, b->b1, b->btot,
                    b->v0, b->v1, b->m0, b->m1, b->snaps_d, b->bin_count, b->bin_start,
-                   b->bin_items, b->red_rows, b->red_used, b->err_d, b->cov_list, b->cov_n};
+                   b->bin_items, b->red_rows, b->red_used, b->err_d, b->cov_list, b->cov_n, b->facc, b->fused_used, b->scan_tmp, b->obs_d};
     for (void* p : dev)
         if (p) cudaFree(p);
-    void* host[] = {b->snaps_h, b->err_h, b->red_h, b->red_rows_h, b->red_used_h};
+    void* host[] = {b->snaps_h, b->err_h, b->red_h, b->red_rows_h, b->red_used_h, b->obs_h};
     for (void* p : host)
         if (p) cudaFreeHost(p);
     for (auto& s : b->spans) {

@@ -107,6 +107,14 @@ struct lbg_block_s {
     // periodic axes the sweep wraps in-kernel (no ghost read), lbg_set_periodic_wrap
     int wrap[3] = {0, 0, 0};
 
+    // force mode: LBG_FORCE_SCRATCH (reference: per-cell m scratch + finalize walk) or
+    // LBG_FORCE_FUSED (the PSM kernel accumulates per-particle force/torque with warp
+    // aggregation + atomics; the scratch is never written)
+    int force_mode = 0;
+    double* facc = nullptr;  // n_snaps x 6 (f xyz, t xyz)
+    int* fused_used = nullptr;
+    int facc_cap = 0;
+
     // particle snapshots: pinned staging + device copy (H2D on the side stream)
     lbg_snapshot* snaps_h = nullptr;
     lbg_snapshot* snaps_d = nullptr;
@@ -118,6 +126,8 @@ struct lbg_block_s {
     int* bin_items = nullptr;
     long long bin_items_cap = 0;
     long long n_bins_cap = 0;
+    void* scan_tmp = nullptr;
+    size_t scan_tmp_bytes = 0;
     // hydro reduction scratch
     double* red_rows = nullptr;  // n_snaps x 12
     int* red_used = nullptr;
@@ -141,6 +151,8 @@ struct lbg_block_s {
 
     lbg::Comm* comm = nullptr;
     long long device_bytes = 0;
+    double* obs_d = nullptr;  // observer partials (lbg_observe)
+    double* obs_h = nullptr;
 
     double* src() const { return buf[cur]; }
     double* dst() const { return buf[cur ^ 1]; }

@@ -454,7 +454,29 @@ static lbg_status need_coupling(lbg_block b) {
     return LBG_OK;
 }
 
+// per-particle accumulators of LBG_FORCE_FUSED, zeroed once per step (at the mapping)
+static lbg_status prepare_fused(lbg_block b, int n) {
+    if (b->force_mode != LBG_FORCE_FUSED) return LBG_OK;
+    if (n > b->facc_cap || !b->facc) {
+        if (b->facc) cudaFree(b->facc);
+        if (b->fused_used) cudaFree(b->fused_used);
+        b->facc_cap = std::max(n, std::max(1, 2 * b->facc_cap));
+        LBG_CUDA(cudaMalloc(&b->facc, sizeof(double) * 6 * b->facc_cap));
+        LBG_CUDA(cudaMalloc(&b->fused_used, sizeof(int) * b->facc_cap));
+    }
+    LBG_CUDA(cudaMemsetAsync(b->facc, 0, sizeof(double) * 6 * b->facc_cap, b->stream));
+    LBG_CUDA(cudaMemsetAsync(b->fused_used, 0, sizeof(int) * b->facc_cap, b->stream));
+    return LBG_OK;
+}
+
 extern "C" {
+
+lbg_status lbg_set_force_mode(lbg_block b, int mode) {
+    if (lbg_status s = need_coupling(b)) return s;
+    if (mode != LBG_FORCE_SCRATCH && mode != LBG_FORCE_FUSED) return set_error(LBG_INVALID, "bad force mode");
+    b->force_mode = mode;
+    return LBG_OK;
+}
 
 lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisions) {
     if (lbg_status s = need_coupling(b)) return s;
@@ -462,6 +484,7 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
     LBG_CUDA(cudaSetDevice(b->device));
     Span span(b, LBG_CAT_MAPPING);
     if (lbg_status s = upload_snapshots(b, snaps, n)) return s;
+    if (lbg_status s = prepare_fused(b, n)) return s;
     const BinGeom g = geom(b);
     const long long nbins = (long long)g.nb[0] * g.nb[1] * g.nb[2];
     if (lbg_status s = ensure_bins(b, nbins)) return s;
@@ -472,25 +495,30 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
         bin_count_kernel<<<(n + 127) / 128, 128, 0, b->stream>>>(b->snaps_d, n, g, cnt);
         LBG_LAUNCH_CHECK();
     }
+    // persistent scan workspace (no per-call allocation)
     size_t tmp_bytes = 0;
     cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, cnt, b->bin_start + 1, (int)nbins, b->stream);
-    void* tmp = nullptr;
-    LBG_CUDA(cudaMallocAsync(&tmp, tmp_bytes, b->stream));
-    LBG_CUDA(cudaMemsetAsync(b->bin_start, 0, sizeof(int), b->stream));
-    cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, cnt, b->bin_start + 1, (int)nbins, b->stream);
-    LBG_LAUNCH_CHECK();
-    LBG_CUDA(cudaFreeAsync(tmp, b->stream));
-    int total = 0;
-    LBG_CUDA(cudaMemcpyAsync(&total, b->bin_start + nbins, sizeof(int), cudaMemcpyDeviceToHost, b->stream));
-    LBG_CUDA(cudaStreamSynchronize(b->stream));
-    if (total > b->bin_items_cap) {
-        if (b->bin_items) cudaFree(b->bin_items);
-        b->bin_items_cap = std::max<long long>(total, 2 * b->bin_items_cap);
-        LBG_CUDA(cudaMalloc(&b->bin_items, sizeof(int) * std::max<long long>(b->bin_items_cap, 1)));
+    if (tmp_bytes > b->scan_tmp_bytes) {
+        if (b->scan_tmp) cudaFree(b->scan_tmp);
+        LBG_CUDA(cudaMalloc(&b->scan_tmp, tmp_bytes));
+        b->scan_tmp_bytes = tmp_bytes;
     }
-    if (b->bin_items == nullptr) {
-        LBG_CUDA(cudaMalloc(&b->bin_items, sizeof(int)));
-        b->bin_items_cap = 1;
+    LBG_CUDA(cudaMemsetAsync(b->bin_start, 0, sizeof(int), b->stream));
+    cub::DeviceScan::InclusiveSum(b->scan_tmp, tmp_bytes, cnt, b->bin_start + 1, (int)nbins, b->stream);
+    LBG_LAUNCH_CHECK();
+    // host upper bound of the registrations (bins a particle's reach box can touch), so the
+    // item list is sized without reading the scan back: the whole mapping stays asynchronous
+    long long bound = 1;
+    for (int p = 0; p < n; ++p) {
+        long long nb = 1;
+        for (int d = 0; d < 3; ++d)
+            nb *= std::min<long long>(g.nb[d], (long long)((2.0 * (snaps[p].r + 0.5) + 4.0) / kBin) + 2);
+        bound += nb;
+    }
+    if (bound > b->bin_items_cap) {
+        if (b->bin_items) cudaFree(b->bin_items);
+        b->bin_items_cap = std::max<long long>(bound, 2 * b->bin_items_cap);
+        LBG_CUDA(cudaMalloc(&b->bin_items, sizeof(int) * b->bin_items_cap));
     }
     if (n > 0) {
         bin_fill_kernel<<<(n + 127) / 128, 128, 0, b->stream>>>(b->snaps_d, n, g, b->bin_start, cursor,
@@ -539,9 +567,49 @@ lbg_status lbg_set_solid_velocities(lbg_block b, const lbg_snapshot* snaps, int 
     return LBG_OK;
 }
 
+// LBG_FORCE_FUSED: the sweep already summed; copy the accumulators out
+static lbg_status reduce_fused(lbg_block b, lbg_hydro_partial* out, int capacity, int* n_out) {
+    const int n = b->n_snaps;
+    std::vector<double> acc((size_t)6 * std::max(n, 1));
+    std::vector<int> used((size_t)std::max(n, 1));
+    {
+        Span span(b, LBG_CAT_REDF);
+        if (n > 0) {
+            LBG_CUDA(cudaMemcpyAsync(acc.data(), b->facc, sizeof(double) * 6 * n, cudaMemcpyDeviceToHost, b->stream));
+            LBG_CUDA(cudaMemcpyAsync(used.data(), b->fused_used, sizeof(int) * n, cudaMemcpyDeviceToHost, b->stream));
+        }
+    }
+    if (lbg_status s = lbg_sync(b, nullptr)) {
+        if (s == LBG_SYNC_ERROR) return set_error(LBG_SYNC_ERROR, "hydrodynamic force for unknown particle id");
+        return s;
+    }
+    int m = 0;
+    for (int p = 0; p < n; ++p) {
+        if (!used[p]) continue;
+        if (m >= capacity) return set_error(LBG_INVALID, "hydro partial output capacity too small");
+        lbg_hydro_partial& h = out[m++];
+        h.id = b->snaps_h[p].id;
+        for (int d = 0; d < 3; ++d) {
+            h.f[d] = acc[6 * (size_t)p + d];
+            h.t[d] = acc[6 * (size_t)p + 3 + d];
+            h.f_comp[d] = 0.0;
+            h.t_comp[d] = 0.0;
+        }
+    }
+    if (n_out) *n_out = m;
+    return LBG_OK;
+}
+
 lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int capacity, int* n_out) {
     if (lbg_status s = need_coupling(b)) return s;
     if (n_out) *n_out = 0;
+    if (b->force_mode == LBG_FORCE_FUSED) {
+        if (mode != LBG_REDUCE_FAST)
+            return set_error(LBG_INVALID, "PARITY reduction needs LBG_FORCE_SCRATCH (the fused sweep "
+                                          "does not keep per-cell momenta)");
+        LBG_CUDA(cudaSetDevice(b->device));
+        return reduce_fused(b, out, capacity, n_out);
+    }
     LBG_CUDA(cudaSetDevice(b->device));
     const int n = b->n_snaps;
     if (n > b->red_cap) {

@@ -46,6 +46,14 @@ struct SweepArgs {
     double* __restrict__ m1;
     const unsigned* __restrict__ cov_list;
     const int* __restrict__ cov_n;
+    const int* __restrict__ id0;
+    const int* __restrict__ id1;
+    // fused force reduction (LBG_FORCE_FUSED)
+    const lbg_snapshot* __restrict__ snaps;
+    int n_snaps;
+    int blk_lo[3];
+    double* __restrict__ facc;
+    int* __restrict__ fused_used;
     // box launch
     int lo[3], hi[3];
     int i0;  // aligned chunk origin
@@ -91,13 +99,15 @@ __device__ __forceinline__ bool srt_cell_at(const SweepArgs& a, int i, int j, in
     return ok;
 }
 
-// covered cell, psm.cpp:236-258
-template <bool kForced>
-__device__ __forceinline__ bool psm_cell_at(const SweepArgs& a, int i, int j, int k) {
+// covered cell, psm.cpp:236-258; with kFused the per-entry momentum goes to m_out instead of
+// the scratch
+template <bool kForced, bool kFused>
+__device__ __forceinline__ bool psm_cell_at(const SweepArgs& a, int i, int j, int k, int& cnt,
+                                            double (&m)[2][3]) {
     const Layout& L = a.L;
     const long long base = L.idx(i, j, k);
     const long long fc = L.frac(i, j, k);
-    const int cnt = a.count[fc];
+    cnt = a.count[fc];
     double f[kQ];
     pull(a, i, j, k, base, f);
     const double be[2] = {a.b0[fc], cnt > 1 ? a.b1[fc] : 0.0};
@@ -106,11 +116,12 @@ __device__ __forceinline__ bool psm_cell_at(const SweepArgs& a, int i, int j, in
         ue[0][c] = a.v0[3 * fc + c];
         ue[1][c] = cnt > 1 ? a.v1[3 * fc + c] : 0.0;
     }
-    double m[2][3];
     const bool ok = psm_cell_opt<kForced>(f, a.inv_tau, a.F, cnt, a.btot[fc], be, ue, m);
-    for (int c = 0; c < 3; ++c) a.m0[3 * fc + c] = m[0][c];
-    if (cnt > 1)
-        for (int c = 0; c < 3; ++c) a.m1[3 * fc + c] = m[1][c];
+    if constexpr (!kFused) {
+        for (int c = 0; c < 3; ++c) a.m0[3 * fc + c] = m[0][c];
+        if (cnt > 1)
+            for (int c = 0; c < 3; ++c) a.m1[3 * fc + c] = m[1][c];
+    }
 #pragma unroll
     for (int q = 0; q < kQ; ++q) a.dst[q * L.plane + base] = f[q];
     return ok;
@@ -162,8 +173,55 @@ __device__ __forceinline__ bool in_boxes(const SweepArgs& a, int i, int j, int k
     return false;
 }
 
+__device__ __forceinline__ int snapshot_of(const SweepArgs& a, int id) {
+    int lo = 0, hi = a.n_snaps;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a.snaps[mid].id < id)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return (lo < a.n_snaps && a.snaps[lo].id == id) ? lo : -1;
+}
+
+// LBG_FORCE_FUSED: lanes holding an entry of the same particle form a group (match_any);
+// the group leader sums the group's force and torque (cross(c - x_p, m), psm.cpp:296) by
+// shuffles in lane order and issues one atomicAdd per component.
+__device__ __forceinline__ void fused_accumulate(const SweepArgs& a, int p, const double (&m)[3],
+                                                 const double (&cc)[3]) {
+    double v[6] = {0, 0, 0, 0, 0, 0};
+    if (p >= 0) {
+        const lbg_snapshot& s = a.snaps[p];
+        const double r0 = cc[0] - s.x[0], r1 = cc[1] - s.x[1], r2 = cc[2] - s.x[2];
+        v[0] = m[0];
+        v[1] = m[1];
+        v[2] = m[2];
+        v[3] = r1 * m[2] - r2 * m[1];
+        v[4] = r2 * m[0] - r0 * m[2];
+        v[5] = r0 * m[1] - r1 * m[0];
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, p);
+    if (p < 0) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(peers) - 1;
+    double s[6] = {0, 0, 0, 0, 0, 0};
+    unsigned rest = peers;
+    while (rest) {
+        const int src = __ffs(rest) - 1;
+        rest &= rest - 1;
+#pragma unroll
+        for (int d = 0; d < 6; ++d) s[d] += __shfl_sync(peers, v[d], src);
+    }
+    if (lane == leader) {
+#pragma unroll
+        for (int d = 0; d < 6; ++d) atomicAdd(&a.facc[6 * p + d], s[d]);
+        a.fused_used[p] = 1;
+    }
+}
+
 // K2: grid-stride over the covered-cell list (length read on the device)
-template <bool kForced>
+template <bool kForced, bool kFused>
 __global__ void __launch_bounds__(128) psm_list_kernel(const SweepArgs a) {
     const int n = *a.cov_n;
     const int stride = gridDim.x * blockDim.x;
@@ -171,14 +229,67 @@ __global__ void __launch_bounds__(128) psm_list_kernel(const SweepArgs a) {
     for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
         const int t = base + threadIdx.x;
         bool ok = true;
+        int cnt = 0;
+        double m[2][3];
+        double cc[3] = {0, 0, 0};
+        int p0 = -1, p1 = -1;
         if (t < n) {
             const unsigned c = a.cov_list[t];
             const int i = (int)(c % (unsigned)L.nx);
             const int j = (int)((c / (unsigned)L.nx) % (unsigned)L.ny);
             const int k = (int)(c / ((unsigned)L.nx * (unsigned)L.ny));
-            if (in_boxes(a, i, j, k)) ok = psm_cell_at<kForced>(a, i, j, k);
+            if (in_boxes(a, i, j, k)) {
+                ok = psm_cell_at<kForced, kFused>(a, i, j, k, cnt, m);
+                if constexpr (kFused) {
+                    cc[0] = (double)(a.blk_lo[0] + i) + 0.5;
+                    cc[1] = (double)(a.blk_lo[1] + j) + 0.5;
+                    cc[2] = (double)(a.blk_lo[2] + k) + 0.5;
+                    p0 = snapshot_of(a, a.id0[c]);
+                    if (cnt > 1) p1 = snapshot_of(a, a.id1[c]);
+                    if (p0 < 0 || (cnt > 1 && p1 < 0)) atomicAdd(&a.err->unknown, 1ull);
+                }
+            }
         }
         count_bad(a.err, !ok);
+        if constexpr (kFused) {
+            fused_accumulate(a, p0, m[0], cc);
+            fused_accumulate(a, p1, m[1], cc);
+        }
+    }
+}
+
+// Thin boxes of a coupled block (the boundary shell): covered cells are handled inline
+// instead of re-scanning the whole covered list for the few shell cells.
+template <bool kForced, bool kFused>
+__global__ void __launch_bounds__(128) sweep_flat_coupled_kernel(const SweepArgs a) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    bool ok = true;
+    int cnt = 0;
+    double m[2][3];
+    double cc[3] = {0, 0, 0};
+    int p0 = -1, p1 = -1;
+    if (t < a.bstart[a.nbox]) {
+        int i, j, k;
+        flat_cell(a, t, i, j, k);
+        const long long fc = a.L.frac(i, j, k);
+        if (a.count[fc] == 0) {
+            ok = srt_cell_at<kForced, false>(a, i, j, k);
+        } else {
+            ok = psm_cell_at<kForced, kFused>(a, i, j, k, cnt, m);
+            if constexpr (kFused) {
+                cc[0] = (double)(a.blk_lo[0] + i) + 0.5;
+                cc[1] = (double)(a.blk_lo[1] + j) + 0.5;
+                cc[2] = (double)(a.blk_lo[2] + k) + 0.5;
+                p0 = snapshot_of(a, a.id0[fc]);
+                if (cnt > 1) p1 = snapshot_of(a, a.id1[fc]);
+                if (p0 < 0 || (cnt > 1 && p1 < 0)) atomicAdd(&a.err->unknown, 1ull);
+            }
+        }
+    }
+    count_bad(a.err, !ok);
+    if constexpr (kFused) {
+        fused_accumulate(a, p0, m[0], cc);
+        fused_accumulate(a, p1, m[1], cc);
     }
 }
 
@@ -225,6 +336,13 @@ static SweepArgs make_args(lbg_block b, const lbg_fluid* fl) {
         a.m1 = b->m1;
         a.cov_list = b->cov_list;
         a.cov_n = b->cov_n;
+        a.id0 = b->id0;
+        a.id1 = b->id1;
+        a.snaps = b->snaps_d;
+        a.n_snaps = b->n_snaps;
+        for (int c = 0; c < 3; ++c) a.blk_lo[c] = b->lo[c];
+        a.facc = b->facc;
+        a.fused_used = b->fused_used;
     }
     return a;
 }
@@ -266,10 +384,13 @@ static void launch_psm_list(lbg_block b, const SweepArgs& a, bool forced) {
     // persistent grid: 4 CTAs of 128 per SM, the list length is read on the device
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, b->device);
+    const bool fused = b->force_mode == LBG_FORCE_FUSED;
     if (forced)
-        psm_list_kernel<true><<<sms * 4, 128, 0, b->stream>>>(a);
+        fused ? psm_list_kernel<true, true><<<sms * 4, 128, 0, b->stream>>>(a)
+              : psm_list_kernel<true, false><<<sms * 4, 128, 0, b->stream>>>(a);
     else
-        psm_list_kernel<false><<<sms * 4, 128, 0, b->stream>>>(a);
+        fused ? psm_list_kernel<false, true><<<sms * 4, 128, 0, b->stream>>>(a)
+              : psm_list_kernel<false, false><<<sms * 4, 128, 0, b->stream>>>(a);
 }
 
 }  // namespace lbg
@@ -331,9 +452,15 @@ lbg_status lbg_sweep_boxes(lbg_block b, const lbg_fluid* fl, const lbg_box* boxe
     Span span(b, LBG_CAT_PSM);
     const bool fo = forced(fl);
     if (b->coupling) {
-        fo ? launch_flat<true, true>(a, b->stream) : launch_flat<false, true>(a, b->stream);
-        LBG_LAUNCH_CHECK();
-        launch_psm_list(b, a, fo);
+        const long long n_cells = a.bstart[a.nbox];
+        const unsigned grid = (unsigned)((n_cells + 127) / 128);
+        const bool fu = b->force_mode == LBG_FORCE_FUSED;
+        if (fo)
+            fu ? sweep_flat_coupled_kernel<true, true><<<grid, 128, 0, b->stream>>>(a)
+               : sweep_flat_coupled_kernel<true, false><<<grid, 128, 0, b->stream>>>(a);
+        else
+            fu ? sweep_flat_coupled_kernel<false, true><<<grid, 128, 0, b->stream>>>(a)
+               : sweep_flat_coupled_kernel<false, false><<<grid, 128, 0, b->stream>>>(a);
     } else {
         fo ? launch_flat<true, false>(a, b->stream) : launch_flat<false, false>(a, b->stream);
     }

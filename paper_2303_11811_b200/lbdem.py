@@ -335,6 +335,11 @@ class Block:
         arr, n = snapshot_array(snaps)
         check(_lib().lbg_map(self.h, arr, n, subdivisions))
 
+    def set_force_mode(self, mode):
+        """lbg.FORCE_SCRATCH (reference scratch + finalize) or lbg.FORCE_FUSED (the PSM
+        kernel sums per-particle force/torque with warp aggregation + atomics)."""
+        check(_lib().lbg_set_force_mode(self.h, int(mode)))
+
     def set_solid_velocities(self, snaps):
         arr, n = snapshot_array(snaps)
         check(_lib().lbg_set_solid_velocities(self.h, arr, n))
@@ -403,6 +408,13 @@ class Block:
         v = (C.c_double * 3)()
         check(_lib().lbg_total_momentum(self.h, v))
         return np.array(list(v))
+
+    def observe(self, f_ext=(0.0, 0.0, 0.0)) -> dict:
+        """Fluid part of io::sample_scalars (output.cpp:22-45) as one device reduction."""
+        out = (C.c_double * 6)()
+        check(_lib().lbg_observe(self.h, (C.c_double * 3)(*f_ext), out))
+        v = list(out)
+        return {"mass": v[0], "momentum": np.array(v[1:4]), "fluid_ke": v[4], "max_u": v[5]}
 
     # halo
     def comm_init(self, nranks, rank, uid: bytes, axis=2, periodic=(1, 1, 1)):

@@ -16,6 +16,7 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include", "lbg.h")
 OK, CONFIG_ERROR, NUMERIC_ERROR, SYNC_ERROR, IO_ERROR, CUDA_ERROR, INVALID = range(7)
 BC_PERIODIC, BC_NO_SLIP, BC_VELOCITY, BC_PRESSURE = range(4)
 REDUCE_PARITY, REDUCE_FAST = 0, 1
+FORCE_SCRATCH, FORCE_FUSED = 0, 1
 CATEGORIES = ("PSM", "PSM-comm", "mapping", "setU", "redF", "PD", "PD-comm", "other")  # perf.hpp:17-26
 
 
@@ -87,6 +88,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "lbg_apply_boundaries": (st, [blk, C.POINTER(FaceBc), i3]),
         "lbg_map": (st, [blk, C.POINTER(Snapshot), C.c_int, C.c_int]),
         "lbg_set_solid_velocities": (st, [blk, C.POINTER(Snapshot), C.c_int]),
+        "lbg_set_force_mode": (st, [blk, C.c_int]),
         "lbg_reduce_hydro": (st, [blk, C.c_int, C.POINTER(HydroPartial), C.c_int, C.POINTER(C.c_int)]),
         "lbg_upload_fraction": (st, [blk, vp, vp, vp, vp, vp, vp]),
         "lbg_download_fraction": (st, [blk, vp, vp, vp, vp, vp, vp]),
@@ -97,6 +99,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "lbg_sync": (st, [blk, C.POINTER(Errors)]),
         "lbg_total_mass": (st, [blk, d3]),
         "lbg_total_momentum": (st, [blk, d3]),
+        "lbg_observe": (st, [blk, d3, d3]),
         "lbg_comm_unique_id": (st, [C.c_char_p]),
         "lbg_comm_init": (st, [blk, C.c_int, C.c_int, C.c_char_p, C.c_int, i3]),
         "lbg_comm_destroy": (st, [blk]),

@@ -1,0 +1,23 @@
+"""Per-step timing probe of the config-3 coupled step through the drop-in (diagnostics)."""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "integration"))
+import bench  # noqa: E402
+import dropin  # noqa: E402
+
+for mode in sys.argv[1:] or ["scratch"]:
+    os.environ["LBDEM_GPU_FORCE"] = mode
+    sim = dropin.DropinSim(bench.CONFIG3, (256, 256, 256))
+    for s in range(int(os.environ.get("PROBE_STEPS", "6"))):
+        sim.reset_timers()
+        t0 = time.perf_counter()
+        sim.run(1)
+        dt = time.perf_counter() - t0
+        print(json.dumps({"mode": mode, "step": s, "ms": round(dt * 1e3, 2),
+                          "cats": [round(v * 1e3, 2) for v in sim.timings()]}), flush=True)
+    sim.close()

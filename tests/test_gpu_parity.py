@@ -174,6 +174,33 @@ def test_apply_boundaries_bitwise(gpu, oracle, case):
     assert n_bit_mismatch(got, src_o) == 0
 
 
+def test_device_observers_match_sample_scalars(gpu, oracle):
+    """lbg_observe == the fluid part of io::sample_scalars (output.cpp:22-45): mass and bare
+    momentum as total_mass/total_momentum (lbm.cpp:69-93), KE with the half-force-shifted
+    velocity; compensated device reduction, relative 1e-14 of the oracle's serial sums."""
+    dims = (40, 33, 27)
+    src = random_pdf(dims, seed=55)
+    fext = (2e-5, -1e-5, 3e-6)
+    blk = gpu.Block(dims)
+    blk.upload_src(src)
+    obs = blk.observe(fext)
+    mass = oracle.total_mass(dims, src)
+    mom = oracle.total_momentum(dims, src)
+    f = interior(src)
+    cxyz = np.array([[0, 1, -1, 0, 0, 0, 0, 1, -1, 1, -1, 1, -1, 1, -1, 0, 0, 0, 0],
+                     [0, 0, 0, 1, -1, 0, 0, 1, -1, -1, 1, 0, 0, 0, 0, 1, -1, 1, -1],
+                     [0, 0, 0, 0, 0, 1, -1, 0, 0, 0, 0, 1, -1, -1, 1, 1, -1, -1, 1]], float)
+    rho = f.sum(axis=0)
+    u = np.einsum("aq,qkji->akji", cxyz, f) + 0.5 * np.array(fext)[:, None, None, None]
+    u2 = (u * u).sum(axis=0)
+    ke = float(np.sum(0.5 * rho * u2, dtype=np.float64))
+    assert abs(obs["mass"] - mass) <= 1e-14 * abs(mass)
+    assert np.all(np.abs(obs["momentum"] - mom) <= 1e-13 * np.abs(f).sum())
+    assert abs(obs["fluid_ke"] - ke) <= 1e-12 * ke
+    assert abs(obs["max_u"] - np.sqrt(u2.max())) <= 1e-15
+    assert abs(blk.total_mass() - mass) <= 1e-14 * mass
+
+
 def test_stability_guard_raises(gpu):
     dims = (4, 4, 4)
     blk = gpu.Block(dims)
@@ -391,6 +418,54 @@ def test_full_coupled_pass_and_reduction(gpu, oracle, mode):
             assert np.all(np.abs((p.f + p.f_comp) - (r[0:3] + r[3:6])) <= 1e-12 * l1[p.id] + 1e-300)
     m0, m1 = blk.download_scratch()
     assert not m0.any() and not m1.any()  # finalize clears the scratch
+
+
+def test_fused_force_mode_within_l1_tolerance(gpu, oracle):
+    """LBG_FORCE_FUSED: force/torque summed inside the PSM kernel (warp aggregation by particle
+    + atomics); PDFs stay bitwise, partials within |dF| <= 1e-12 * sum|m| (and the same for
+    the torque with sum |r x m|)."""
+    dims = (32, 30, 34)
+    src0 = random_pdf(dims, seed=91)
+    rng = np.random.default_rng(12)
+    centers = [(9.2, 10.1, 11.7), (17.5, 10.4, 12.2), (22.0, 21.0, 23.3), (8.0, 24.0, 26.0)]
+    s = spheres(oracle, centers, [5.0, 4.5, 6.0, 3.5], ids=[1, 3, 4, 8],
+                u=0.01 * (rng.random((4, 3)) - 0.5), w=0.001 * (rng.random((4, 3)) - 0.5))
+    tau, fext = 0.7, (0.0, 0.0, -1e-5)
+    f_o, _ = oracle.build_fraction_field((0, 0, 0), dims, s)
+    sv_o, _ = oracle.set_solid_velocities((0, 0, 0), dims, s, f_o)
+    src_o = src0.copy()
+    oracle.fill_periodic(dims, src_o, ALL_P)
+    dst_o = np.zeros_like(src_o)
+    scr = new_scratch(dims)
+    oracle.psm_collide_stream(dims, src_o, dst_o, tau, fext, (0, 0, 0), dims, f_o, sv_o, scr)
+    l1f, l1t = {}, {}
+    for e, mk in ((0, "m0"), (1, "m1")):
+        sel = f_o["count"] > e
+        ids = f_o["id0" if e == 0 else "id1"][sel]
+        kk, jj, ii = np.nonzero(sel)
+        for pid, mv, i, j, k in zip(ids, scr[mk][sel], ii, jj, kk):
+            x = s["x"][list(s["id"]).index(pid)]
+            r = np.array([i + 0.5, j + 0.5, k + 0.5]) - x
+            l1f[int(pid)] = l1f.get(int(pid), 0) + np.abs(mv)
+            l1t[int(pid)] = l1t.get(int(pid), 0) + np.abs(np.cross(r, mv))
+    ids_o, rows_o = oracle.finalize_hydro((0, 0, 0), dims, s, f_o, scr)
+    blk = gpu.Block(dims, coupling=True)
+    blk.set_force_mode(1)
+    blk.upload_src(src0)
+    blk.map(s)
+    blk.fill_periodic(ALL_P)
+    p = gpu.FluidParams(tau, fext)
+    blk.sweep(p, gpu.CellBox((1, 1, 1), (dims[0] - 1, dims[1] - 1, dims[2] - 1)))
+    blk.sweep_boxes(p, gpu.boundary_shell(dims))  # two launches accumulate into one sum
+    blk.sync()
+    assert equal_bits(interior(blk.download_dst()), interior(dst_o))
+    with pytest.raises(ValueError):
+        gpu.finalize_hydro_forces(blk, 0)  # PARITY needs the scratch
+    parts = gpu.finalize_hydro_forces(blk, 1)
+    assert [q.id for q in parts] == list(ids_o)
+    for q, r in zip(parts, rows_o):
+        assert np.all(np.abs(q.f - (r[0:3] + r[3:6])) <= 1e-12 * l1f[q.id])
+        assert np.all(np.abs(q.t - (r[6:9] + r[9:12])) <= 1e-12 * l1t[q.id] + 1e-300)
 
 
 def test_finalize_symmetric_pattern(gpu, oracle):
