@@ -11,9 +11,11 @@ Inputs: the validation.cpp:46-63 shear wave at tau = 0.8, initialised on the dev
 
 `value` is MLUPS over all GPUs (cells * steps / max-over-ranks device time). `roofline`
 uses 304 algorithmic bytes per lattice update (19 f64 pulled + 19 stored) and the sweep's
-CUDA-event time measured in the timed region. `e2e` drives the same steps through the
-C-ABI from the host with the reference's per-operator error check (one D2H of the stability
-counters per step). `cpu_baseline` times the reference itself (oracle/_ref) on this host.
+CUDA-event time measured in the timed region. `e2e` is the same K steps run as a job through
+the C-ABI with host buffers: the state uploaded from pinned host memory, every step closed by
+the reference's per-operator error check (one D2H of the stability counters), the final state
+downloaded. `coupled_step` times config 3 (10^4 spheres, host DEM) through the drop-in build.
+`cpu_baseline` times the reference itself (oracle/_ref) on this host.
 
 `--impl reference` runs the unmodified reference CPU path (Simulation::step via
 oracle/_ref) on a bounded sample of the same workload.
@@ -324,16 +326,36 @@ def run_lbg(args):
         except Exception:
             traffic = None
 
-    # ---- end to end through the C-ABI (host-driven, per-step error check D2H)
+    # ---- end to end through the C-ABI with host buffers: the job a caller with a host
+    # PdfField runs — upload the state from pinned host memory (reference idx() layout),
+    # K steps each closed by the reference's end-of-operator check (lbg_sync: D2H of the
+    # error counters, raises NumericError), download the final state to the host buffer.
+    import ctypes as C
+    import numpy as np
+    from paper_2303_11811_b200 import lbg as abi
+    pdf_bytes = 8 * 19 * (n + 2) ** 3
+    hp = C.c_void_p()
+    lbdem.check(abi.load().lbg_host_alloc(pdf_bytes, C.byref(hp)))
+    host = np.ctypeslib.as_array(C.cast(hp, C.POINTER(C.c_double)), shape=(19, n + 2, n + 2, n + 2))
+    lbdem.check(abi.load().lbg_download_src(blk.h, hp))  # the current state as the job's input
     barrier()
     t0 = time.perf_counter()
+    lbdem.check(abi.load().lbg_upload_src(blk.h, hp))
+    tl0 = time.perf_counter()
     for _ in range(args.steps):
         step()
         blk.sync()  # lbg_sync: D2H of the 3 error counters, raises NumericError/SyncError
+    tl1 = time.perf_counter()
+    lbdem.check(abi.load().lbg_download_src(blk.h, hp))
     t1 = time.perf_counter()
     barrier()
     e2e_s = max_over_ranks(t1 - t0)
+    loop_s = max_over_ranks(tl1 - tl0)
     e2e_mlups = cells * N * args.steps / e2e_s / 1e6
+    loop_mlups = cells * N * args.steps / loop_s / 1e6
+    finite = bool(np.isfinite(host[:, n // 2, n // 2, 1:5]).all())
+    del host
+    abi.load().lbg_host_free(hp)
 
     out = None
     if rank == 0:
@@ -365,9 +387,14 @@ def run_lbg(args):
                          "sweep_launches": sweep_n},
             "hbm_roofline_frac_of_step": round(BYTES_PER_LUP * cells / (ms_step / 1e3) / 1e9 / peak, 4),
             "timings_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in tm.items() if v[1]},
-            "e2e": {"value": round(e2e_mlups, 1), "unit": "MLUPS", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 24,
-                    "how": "per step via the C-ABI (sweep [+ halo], swap) + lbg_sync error-counter readback"},
+            "e2e": {"value": round(e2e_mlups, 1), "unit": "MLUPS",
+                    "h2d_bytes_per_step": round(pdf_bytes / args.steps),
+                    "d2h_bytes_per_step": round(pdf_bytes / args.steps) + 24,
+                    "how": (f"job of {args.steps} steps through the C-ABI with host buffers: lbg_upload_src "
+                            "from pinned host memory (reference layout), per step sweep [+ halo] + swap + "
+                            "lbg_sync (error-counter D2H, NumericError check), lbg_download_src; wall clock, "
+                            "max over ranks"),
+                    "steady_state_loop_mlups": round(loop_mlups, 1), "result_finite": finite},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
