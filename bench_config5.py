@@ -1,0 +1,70 @@
+#!/usr/bin/env python
+"""Config 5 (BASELINE.json): fluidized-bed four-way coupled PSM + DEM, weak scaling over
+the GPUs of one box, through the drop-in build (the reference Simulation with its GPU-side
+operators on liblbg; host DEM = the reference's code).
+
+    python bench_config5.py --gpus N [--steps K] [--edge 512] [--per-gpu 12500]
+
+Weak scaling as SURVEY §8(d): domain (edge*N) x edge x edge, block grid {N,1,1} (x-slabs, so
+the bottom-settled bed splits evenly), edge^3 cells and `per_gpu` spheres (d = 10) per GPU,
+one block per GPU (LBDEM_GPU_SPREAD=1), one reference worker thread per block, no host PDF
+mirror (LBDEM_GPU_HOST_MIRROR=0). Prints one JSON line with the reference's own
+per-category TimingReport (perf.hpp:17-51) and MLUPS = cells * steps / wall time.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "integration"))
+
+CATS = ("PSM", "PSM-comm", "mapping", "setU", "redF", "PD", "PD-comm", "other")
+CFG = ('{{"scenario":"fluidized_bed_dense","domain":[{nx},{n},{n}],"blocks":[{g},1,1],'
+       '"workers":{g},"particles":{{"count":{p}}},"physical":{{"diameter_cells":10}},'
+       '"fluid":{{"bc":{{"xm":"no_slip","xp":"no_slip","ym":"no_slip","yp":"no_slip",'
+       '"zm":"velocity","zp":"pressure"}}}},'
+       '"dem":{{"k_n":230,"d_n":520,"k_t":65,"d_t":260,"subcycles":10,"settle_subcycles":{settle}}}}}')
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--edge", type=int, default=512)
+    ap.add_argument("--per-gpu", type=int, default=12500)
+    ap.add_argument("--settle", type=int, default=100)
+    ap.add_argument("--force", choices=["scratch", "fused"], default="fused")
+    args = ap.parse_args()
+    os.environ["LBDEM_GPU_SPREAD"] = "1"
+    os.environ["LBDEM_GPU_HOST_MIRROR"] = "0"
+    os.environ["LBDEM_GPU_FORCE"] = args.force
+    import torch  # noqa: F401  (CUDA plumbing)
+    import dropin
+    g, n = args.gpus, args.edge
+    cfg = CFG.format(nx=n * g, n=n, g=g, p=args.per_gpu * g, settle=args.settle)
+    t0 = time.perf_counter()
+    sim = dropin.DropinSim(cfg, (n * g, n, n))
+    setup = time.perf_counter() - t0
+    sim.run(1)
+    sim.reset_timers()
+    t0 = time.perf_counter()
+    sim.run(args.steps)
+    dt = time.perf_counter() - t0
+    cat = sim.timings()
+    cells = n * n * n * g
+    print(json.dumps({
+        "workload": f"config 5 weak: {n * g}x{n}x{n} fluidized bed, {args.per_gpu * g} spheres d=10, "
+                    f"blocks {{{g},1,1}}, one per GPU, host DEM (reference), force mode {args.force}",
+        "n_gpus": g, "steps": args.steps, "ms_per_step": round(dt * 1e3 / args.steps, 2),
+        "mlups": round(cells * args.steps / dt / 1e6, 1),
+        "mlups_per_gpu": round(cells * args.steps / dt / 1e6 / g, 1),
+        "categories_ms_per_step": {c: round(v * 1e3 / args.steps, 3) for c, v in zip(CATS, cat)},
+        "particles": args.per_gpu * g, "setup_s": round(setup, 1)}))
+    sim.close()
+
+
+if __name__ == "__main__":
+    main()

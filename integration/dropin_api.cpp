@@ -119,6 +119,7 @@ int dropin_sim_shear_wave(void* h) {
         for (int b = 0; b < r.sim->num_blocks(); ++b) {
             BlockState& blk = r.sim->block(b);
             const Vec3i d = blk.dims();
+            if (blk.field.nx() != d.x) throw ConfigError("shear-wave init needs LBDEM_GPU_HOST_MIRROR=1");
             for (int k = 0; k < d.z; ++k)
                 for (int j = 0; j < d.y; ++j)
                     for (int i = 0; i < d.x; ++i) {

@@ -38,12 +38,23 @@ SIM_CPP_EDITS = [
     ("namespace lbdem {\n\nusing partition::MsgKind;",
      "namespace lbdem {\n\n"
      "namespace {\n"
-     "int gpu_device() {\n"
+     "/// Device of block `id`: LBDEM_GPU_DEVICE (default 0), or with LBDEM_GPU_SPREAD=1 the\n"
+     "/// blocks are dealt round-robin over all visible GPUs (one worker thread per block).\n"
+     "int gpu_device(int id) {\n"
+     "    const char* s = std::getenv(\"LBDEM_GPU_SPREAD\");\n"
+     "    if (s && std::atoi(s) != 0) return id % std::max(1, lbg_device_count());\n"
      "    const char* e = std::getenv(\"LBDEM_GPU_DEVICE\");\n"
      "    return e ? std::atoi(e) : 0;\n"
      "}\n"
+     "/// LBDEM_GPU_HOST_MIRROR=0: no host PdfField/coupling copies (large runs; observers off).\n"
+     "bool host_mirror() {\n"
+     "    const char* e = std::getenv(\"LBDEM_GPU_HOST_MIRROR\");\n"
+     "    return !(e && std::atoi(e) == 0);\n"
+     "}\n"
+     "int mirror_dim(int d) { return host_mirror() ? d : 1; }\n"
      "/// Observers read the host copies; refresh them from the device after a step.\n"
      "void refresh_host(const std::vector<std::unique_ptr<BlockState>>& blocks, bool coupling) {\n"
+     "    if (!host_mirror()) throw std::runtime_error(\"observer needs LBDEM_GPU_HOST_MIRROR=1\");\n"
      "    for (const auto& b : blocks) {\n"
      "        if (!b->host_stale) continue;\n"
      "        BlockState& m = const_cast<BlockState&>(*b);\n"
@@ -54,14 +65,19 @@ SIM_CPP_EDITS = [
      "}\n"
      "}  // namespace\n\n"
      "using partition::MsgKind;"),
-    # sim.cpp:19-24 — BlockState ctor: create the device block
+    # sim.cpp:15-25 — BlockState ctor: optional host mirror, create the device block
+    ("      field(box_.hi.x - box_.lo.x, box_.hi.y - box_.lo.y, box_.hi.z - box_.lo.z) {\n"
+     "    if (coupling) {\n",
+     "      field(mirror_dim(box_.hi.x - box_.lo.x), mirror_dim(box_.hi.y - box_.lo.y),\n"
+     "            mirror_dim(box_.hi.z - box_.lo.z)) {\n"
+     "    if (coupling && host_mirror()) {\n"),
     ("        scratch.resize(frac.cells());\n    }\n}\n",
      "        scratch.resize(frac.cells());\n    }\n"
-     "    dev = std::make_shared<gpu::DeviceBlock>(gpu_device(), box_, coupling);\n}\n"),
+     "    dev = std::make_shared<gpu::DeviceBlock>(gpu_device(id_), box_, coupling);\n}\n"),
     # sim.cpp:54-57 — initialize_fluid on the device too
     ("    for (auto& blk : blocks_) blk->field.fill_src(feq);\n",
      "    for (auto& blk : blocks_) {\n"
-     "        blk->field.fill_src(feq);\n"
+     "        if (host_mirror()) blk->field.fill_src(feq);\n"
      "        blk->dev->initialize_fluid(rho, u);\n"
      "    }\n"),
     # sim.cpp:167-173 — pack the source slab from the device
