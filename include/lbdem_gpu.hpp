@@ -108,6 +108,18 @@ public:
         check(lbg_unpack_slab(b_, d, values.data(), static_cast<long long>(values.size())));
     }
 
+    /// Device-side halo (no host staging): stage this block's source slabs for its neighbour
+    /// offsets (begin_halo_exchange), then fetch a neighbour's slab into a ghost region.
+    void stage_slabs(const std::vector<Vec3i>& offsets) {
+        std::vector<std::array<int, 3>> o;
+        for (const Vec3i& v : offsets) o.push_back({v.x, v.y, v.z});
+        check(lbg_halo_stage(b_, reinterpret_cast<const int(*)[3]>(o.data()), static_cast<int>(o.size())));
+    }
+    void fetch_slab(const Vec3i& dir, const DeviceBlock& from) {
+        const int d[3] = {dir.x, dir.y, dir.z};
+        check(lbg_halo_fetch(b_, d, from.b_));
+    }
+
     void map(const std::vector<psm::ParticleSnapshot>& snaps, int subdivisions) {
         to_c(snaps);
         check(lbg_map(b_, cs_.data(), static_cast<int>(cs_.size()), subdivisions));

@@ -245,6 +245,30 @@ lbg_status lbg_halo_complete(lbg_block b);
 lbg_status lbg_pack_slab(lbg_block b, const int off[3], double* out, long long capacity,
                          long long* n_out);
 lbg_status lbg_unpack_slab(lbg_block b, const int dir[3], const double* in, long long n);
+/* The same exchange without the host: lbg_halo_stage packs source_slab(off) of every listed
+ * neighbour offset into device staging buffers (begin_halo_exchange, async); a receiver then
+ * calls lbg_halo_fetch(dst, dir, src) for each of its neighbour entries (src block at offset
+ * dir): src's staged source_slab(-dir) is copied device-to-device (peer copy over NVLink when
+ * the blocks live on different GPUs) and unpacked into dst's ghost_region(dir). All 19 q,
+ * identical values to the message-bus path. */
+lbg_status lbg_halo_stage(lbg_block b, const int (*offs)[3], int n);
+lbg_status lbg_halo_fetch(lbg_block dst, const int dir[3], lbg_block src);
+
+/* The slab halo fused into the outer sweep over NVLink peer memory (one process per GPU,
+ * >= 2 ranks, plain-fluid blocks). lbg_p2p_handles exports 192 bytes of CUDA IPC handles
+ * (both PDF buffers + a flag word array); the caller all-gathers them (rank order) and passes
+ * them to lbg_p2p_connect. After every rank's state is set and a host barrier,
+ * lbg_p2p_prime fills the slab-axis ghost planes once from the neighbours. Then each step:
+ * lbg_sweep (inner planes 1..n-2) -> lbg_sweep_outer_p2p (waits for the neighbours' previous
+ * outer sweep, computes the two boundary planes and stores their outbound populations
+ * directly into the neighbours' ghost planes, then publishes the step) -> lbg_swap. Replaces
+ * lbg_halo_begin/complete (no pack, no NCCL, no unpack). */
+lbg_status lbg_p2p_handles(lbg_block b, void* out, size_t* bytes);
+lbg_status lbg_p2p_connect(lbg_block b, int nranks, int rank, const void* all_handles, int axis,
+                           const int periodic[3]);
+lbg_status lbg_p2p_prime(lbg_block b);
+lbg_status lbg_sweep_outer_p2p(lbg_block b, const lbg_fluid* fluid);
+lbg_status lbg_p2p_destroy(lbg_block b);
 
 /* ------------------------------------------------------------------ instrumentation */
 /* Per-category CUDA-event timing (perf::Category names); off by default. */

@@ -52,6 +52,11 @@ SIM_CPP_EDITS = [
      "    return !(e && std::atoi(e) == 0);\n"
      "}\n"
      "int mirror_dim(int d) { return host_mirror() ? d : 1; }\n"
+     "/// PDF halo device to device (default) or through the MessageBus (LBDEM_GPU_HALO=host).\n"
+     "bool device_halo() {\n"
+     "    const char* e = std::getenv(\"LBDEM_GPU_HALO\");\n"
+     "    return !(e && std::string(e) == \"host\");\n"
+     "}\n"
      "/// Observers read the host copies; refresh them from the device after a step.\n"
      "void refresh_host(const std::vector<std::unique_ptr<BlockState>>& blocks, bool coupling) {\n"
      "    if (!host_mirror()) throw std::runtime_error(\"observer needs LBDEM_GPU_HOST_MIRROR=1\");\n"
@@ -79,6 +84,27 @@ SIM_CPP_EDITS = [
      "    for (auto& blk : blocks_) {\n"
      "        if (host_mirror()) blk->field.fill_src(feq);\n"
      "        blk->dev->initialize_fluid(rho, u);\n"
+     "    }\n"),
+    # sim.cpp:156-158 — halo begin: stage the source slabs on the device (no host copy); the
+    # message-bus path below stays available with LBDEM_GPU_HALO=host
+    ("void Simulation::begin_halo_exchange(int b) {\n    BlockState& blk = *blocks_[b];\n",
+     "void Simulation::begin_halo_exchange(int b) {\n    BlockState& blk = *blocks_[b];\n"
+     "    if (device_halo()) {\n"
+     "        std::vector<Vec3i> offs;\n"
+     "        for (const auto& n : decomp_.blocks[b].neighbors) offs.push_back(n.offset);\n"
+     "        blk.dev->stage_slabs(offs);\n"
+     "        blk.halo_pending = true;\n"
+     "        return;\n"
+     "    }\n"),
+    # sim.cpp:181-186 — halo complete: each neighbour entry (s, o) fills ghost_region(o) with
+    # s's staged source_slab(-o), device to device (peer copy across GPUs)
+    ("    if (!blk.halo_pending) throw SyncError(\"halo completion without a pending exchange\");\n",
+     "    if (!blk.halo_pending) throw SyncError(\"halo completion without a pending exchange\");\n"
+     "    if (device_halo()) {\n"
+     "        for (const auto& n : decomp_.blocks[b].neighbors)\n"
+     "            blk.dev->fetch_slab(n.offset, *blocks_[n.block]->dev);\n"
+     "        blk.halo_pending = false;\n"
+     "        return;\n"
      "    }\n"),
     # sim.cpp:167-173 — pack the source slab from the device
     ("        for (int q = 0; q < lbm::kQ; ++q) {\n"

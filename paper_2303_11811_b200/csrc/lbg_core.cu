@@ -376,6 +376,7 @@ lbg_status lbg_block_create(int device, const int box_lo[3], const int dims[3], 
 }
 
 lbg_status lbg_comm_destroy(lbg_block b);  // lbg_halo.cu
+lbg_status lbg_p2p_destroy(lbg_block b);   // lbg_p2p.cu
 
 lbg_status lbg_block_destroy(lbg_block b) {
     if (!b) return LBG_OK;
@@ -383,6 +384,7 @@ lbg_status lbg_block_destroy(lbg_block b) {
     if (b->stream) cudaStreamSynchronize(b->stream);
     if (b->side) cudaStreamSynchronize(b->side);
     if (b->comm) lbg_comm_destroy(b);
+    if (b->p2p) lbg_p2p_destroy(b);
     void* dev[] = {b->buf[0], b->buf[1], b->count, b->id0, b->id1, b->b0, b->b1, b->btot,
                    b->v0, b->v1, b->m0, b->m1, b->snaps_d, b->bin_count, b->bin_start,
                    b->bin_items, b->red_rows, b->red_used, b->err_d, b->cov_list, b->cov_n, b->facc, b->fused_used, b->scan_tmp, b->obs_d};
@@ -397,6 +399,10 @@ lbg_status lbg_block_destroy(lbg_block b) {
     }
     for (auto e : b->event_pool) cudaEventDestroy(e);
     if (b->ev_side) cudaEventDestroy(b->ev_side);
+    if (b->ev_stage) cudaEventDestroy(b->ev_stage);
+    for (double* p : b->stage)
+        if (p) cudaFree(p);
+    if (b->recv_buf) cudaFree(b->recv_buf);
     if (b->stream) cudaStreamDestroy(b->stream);
     if (b->side) cudaStreamDestroy(b->side);
     delete b;
@@ -496,6 +502,8 @@ lbg_status lbg_sync(lbg_block b, lbg_errors* out) {
         out->overfull_cells = (long long)e.overfull;
         out->unknown_ids = (long long)e.unknown;
     }
+    if (e.p2p_timeout > 0)
+        return set_error(LBG_CUDA_ERROR, "P2P halo: neighbour did not publish its step (wait timed out)");
     if (e.overfull > 0)
         return set_error(LBG_NUMERIC_ERROR,
                          "more than two particles overlap a single cell in " +

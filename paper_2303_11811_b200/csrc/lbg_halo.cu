@@ -345,4 +345,58 @@ lbg_status lbg_unpack_slab(lbg_block b, const int dir[3], const double* in, long
     return slab_io(b, dir, true, const_cast<double*>(in), n, nullptr, false);
 }
 
+lbg_status lbg_halo_stage(lbg_block b, const int (*offs)[3], int n) {
+    using namespace lbg;
+    if (!b || (n > 0 && !offs)) return set_error(LBG_INVALID, "null argument");
+    LBG_CUDA(cudaSetDevice(b->device));
+    if (!b->ev_stage) LBG_CUDA(cudaEventCreateWithFlags(&b->ev_stage, cudaEventDisableTiming));
+    Span span(b, LBG_CAT_PSM_COMM);
+    for (int t = 0; t < n; ++t) {
+        int lo[3], ext[3];
+        slab_box(b->L, offs[t], false, lo, ext);
+        const size_t cnt = (size_t)kQ * ext[0] * ext[1] * ext[2];
+        const int key = (offs[t][0] + 1) * 9 + (offs[t][1] + 1) * 3 + (offs[t][2] + 1);
+        if (b->stage_cap[key] < cnt) {
+            if (b->stage[key]) cudaFree(b->stage[key]);
+            LBG_CUDA(cudaMalloc(&b->stage[key], sizeof(double) * cnt));
+            b->stage_cap[key] = cnt;
+        }
+        slab_copy_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, b->stream>>>(
+            b->src(), b->L, lo[0], lo[1], lo[2], ext[0], ext[1], ext[2], b->stage[key], 1);
+        LBG_LAUNCH_CHECK();
+    }
+    LBG_CUDA(cudaEventRecord(b->ev_stage, b->stream));
+    return LBG_OK;
+}
+
+lbg_status lbg_halo_fetch(lbg_block dst, const int dir[3], lbg_block src) {
+    using namespace lbg;
+    if (!dst || !src || !dir) return set_error(LBG_INVALID, "null argument");
+    const int back[3] = {-dir[0], -dir[1], -dir[2]};
+    const int key = (back[0] + 1) * 9 + (back[1] + 1) * 3 + (back[2] + 1);
+    int lo[3], ext[3];
+    slab_box(dst->L, dir, true, lo, ext);
+    const size_t cnt = (size_t)kQ * ext[0] * ext[1] * ext[2];
+    if (!src->stage[key] || src->stage_cap[key] < cnt)
+        return set_error(LBG_SYNC_ERROR, "halo completion without a pending exchange");
+    LBG_CUDA(cudaSetDevice(dst->device));
+    Span span(dst, LBG_CAT_PSM_COMM);
+    LBG_CUDA(cudaStreamWaitEvent(dst->stream, src->ev_stage, 0));
+    const double* from = src->stage[key];
+    if (src->device != dst->device) {
+        if (dst->recv_cap < cnt) {
+            if (dst->recv_buf) cudaFree(dst->recv_buf);
+            LBG_CUDA(cudaMalloc(&dst->recv_buf, sizeof(double) * cnt));
+            dst->recv_cap = cnt;
+        }
+        LBG_CUDA(cudaMemcpyPeerAsync(dst->recv_buf, dst->device, from, src->device, sizeof(double) * cnt,
+                                     dst->stream));
+        from = dst->recv_buf;
+    }
+    slab_copy_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, dst->stream>>>(
+        dst->src(), dst->L, lo[0], lo[1], lo[2], ext[0], ext[1], ext[2], const_cast<double*>(from), 0);
+    LBG_LAUNCH_CHECK();
+    return LBG_OK;
+}
+
 }  // extern "C"

@@ -68,6 +68,7 @@ struct DeviceErrors {
     unsigned long long unstable;
     unsigned long long overfull;
     unsigned long long unknown;
+    unsigned long long p2p_timeout;  // lbg_p2p.cu wait gave up
 };
 
 struct TimedSpan {
@@ -76,6 +77,7 @@ struct TimedSpan {
 };
 
 struct Comm;  // lbg_halo.cu
+struct P2P;   // lbg_p2p.cu
 
 }  // namespace lbg
 
@@ -150,9 +152,18 @@ struct lbg_block_s {
     long long acc_n[LBG_NUM_CATS] = {};
 
     lbg::Comm* comm = nullptr;
+    lbg::P2P* p2p = nullptr;
     long long device_bytes = 0;
     double* obs_d = nullptr;  // observer partials (lbg_observe)
     double* obs_h = nullptr;
+
+    // device-side generic halo (lbg_halo_stage / lbg_halo_fetch): staged source slabs per
+    // neighbour offset (index (ox+1)*9+(oy+1)*3+(oz+1)), a receive buffer, a staging event
+    double* stage[27] = {};
+    size_t stage_cap[27] = {};
+    double* recv_buf = nullptr;
+    size_t recv_cap = 0;
+    cudaEvent_t ev_stage = nullptr;
 
     double* src() const { return buf[cur]; }
     double* dst() const { return buf[cur ^ 1]; }

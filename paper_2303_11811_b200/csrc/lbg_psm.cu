@@ -277,13 +277,22 @@ __global__ void __launch_bounds__(128) reduce_kernel(const ReduceArgs a) {
     double fs[3] = {0, 0, 0}, fc[3] = {0, 0, 0}, ts[3] = {0, 0, 0}, tc[3] = {0, 0, 0};
     unsigned long long hits = 0;
     const int id = p.id;
+    // rows no wider than 32 cells are packed R per warp iteration (lane = r*W + i offset);
+    // lane order stays lexicographic (row j before row j+1)
+    const int W = hi[0] - lo[0] + 1;
+    const bool packed = W <= 32;
+    const int R = packed ? 32 / W : 1;
+    const int r_of = packed ? lane / W : 0;
+    const int i_of = packed ? lane % W : lane;
+    const int istep = packed ? W : 32;
     for (int k = lo[2]; k <= hi[2]; ++k)
-        for (int j = lo[1]; j <= hi[1]; ++j)
-            for (int i0 = lo[0]; i0 <= hi[0]; i0 += 32) {
-                const int i = i0 + lane;
+        for (int j0 = lo[1]; j0 <= hi[1]; j0 += R)
+            for (int i0 = lo[0]; i0 <= hi[0]; i0 += istep) {
+                const int i = i0 + i_of;
+                const int j = j0 + r_of;
                 int e = -1;
                 long long c = 0;
-                if (i <= hi[0]) {
+                if (r_of < R && j <= hi[1] && i <= hi[0]) {
                     c = ((long long)k * g.dims[1] + j) * g.dims[0] + i;
                     const int cnt = a.count[c];
                     if (cnt > 0 && a.id0[c] == id) e = 0;

@@ -91,8 +91,13 @@ class FluidStepper:
 
     def __init__(self, decomp: SlabDecomposition, rank: int, params: lbdem.FluidParams,
                  bc: lbdem.BcSpec | None = None, coupling: bool = False, device: int = 0,
-                 uid: bytes | None = None):
+                 uid: bytes | None = None, halo: str = "nccl", allgather=None):
+        """halo: "nccl" (pack -> ncclSend/Recv on the comm stream -> unpack, hidden behind
+        the inner sweep) or "p2p" (the outer sweep stores the outbound populations straight
+        into the neighbours' ghost planes over NVLink; plain fluid, >= 2 ranks). For "p2p",
+        `allgather(bytes) -> list[bytes]` exchanges the CUDA IPC handles in rank order."""
         self.decomp, self.rank, self.params = decomp, rank, params
+        self.halo = halo
         self.bc = bc or lbdem.BcSpec()
         self.bc.validate()
         params.validate()
@@ -107,7 +112,14 @@ class FluidStepper:
         self.fill = tuple(0 if self.has_bc is False else w for w in decomp.wrap_axes())
         self.block.set_periodic_wrap(self.wrap)
         self.exchange = decomp.nranks > 1 or (decomp.periodic[decomp.axis] and not decomp.wrap_axes()[decomp.axis])
-        if self.exchange:
+        self.p2p = halo == "p2p" and decomp.nranks > 1
+        if self.p2p:
+            if coupling or self.has_bc:
+                raise lbdem.ConfigError("the P2P halo is the plain periodic-fluid path")
+            handles = allgather(self.block.p2p_handles())
+            self.block.p2p_connect(decomp.nranks, rank, b"".join(handles), axis=decomp.axis,
+                                   periodic=decomp.periodic)
+        elif self.exchange:
             self.block.comm_init(decomp.nranks, rank, uid or b"\0" * 128, axis=decomp.axis,
                                  periodic=decomp.periodic)
         a = decomp.axis
@@ -123,8 +135,19 @@ class FluidStepper:
         self.outer = outer
         self.full = lbdem.CellBox((0, 0, 0), dims)
 
+    def prime(self) -> None:
+        """P2P mode: fill the slab-axis ghost planes once from the neighbours (call after
+        every rank set its state and passed a host barrier)."""
+        if self.p2p:
+            self.block.p2p_prime()
+
     def step(self) -> None:
         b = self.block
+        if self.p2p:
+            b.sweep(self.params, self.inner)
+            b.sweep_outer_p2p(self.params)
+            b.swap()
+            return
         if not self.exchange and not self.has_bc:
             b.sweep(self.params, self.full)
         else:

@@ -421,6 +421,24 @@ class Block:
         check(_lib().lbg_comm_init(self.h, nranks, rank, uid, axis,
                                    (C.c_int * 3)(*[int(bool(p)) for p in periodic])))
 
+    # fused P2P halo (lbg_p2p.cu)
+    def p2p_handles(self) -> bytes:
+        buf = C.create_string_buffer(192)
+        n = C.c_size_t()
+        check(_lib().lbg_p2p_handles(self.h, buf, C.byref(n)))
+        return buf.raw[: n.value]
+
+    def p2p_connect(self, nranks, rank, all_handles: bytes, axis=2, periodic=(1, 1, 1)):
+        check(_lib().lbg_p2p_connect(self.h, nranks, rank, all_handles, axis,
+                                     (C.c_int * 3)(*[int(bool(p)) for p in periodic])))
+
+    def p2p_prime(self):
+        check(_lib().lbg_p2p_prime(self.h))
+
+    def sweep_outer_p2p(self, params: FluidParams):
+        fl = params.c()
+        check(_lib().lbg_sweep_outer_p2p(self.h, C.byref(fl)))
+
     def halo_begin(self):
         check(_lib().lbg_halo_begin(self.h))
 

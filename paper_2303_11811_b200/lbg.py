@@ -105,6 +105,15 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "lbg_comm_destroy": (st, [blk]),
         "lbg_halo_begin": (st, [blk]),
         "lbg_halo_complete": (st, [blk]),
+        "lbg_pack_slab": (st, [blk, i3, vp, C.c_longlong, C.POINTER(C.c_longlong)]),
+        "lbg_unpack_slab": (st, [blk, i3, vp, C.c_longlong]),
+        "lbg_halo_stage": (st, [blk, i3, C.c_int]),
+        "lbg_halo_fetch": (st, [blk, i3, blk]),
+        "lbg_p2p_handles": (st, [blk, vp, C.POINTER(C.c_size_t)]),
+        "lbg_p2p_connect": (st, [blk, C.c_int, C.c_int, C.c_char_p, C.c_int, i3]),
+        "lbg_p2p_prime": (st, [blk]),
+        "lbg_sweep_outer_p2p": (st, [blk, C.POINTER(Fluid)]),
+        "lbg_p2p_destroy": (st, [blk]),
         "lbg_set_timing": (st, [blk, C.c_int]),
         "lbg_timings": (st, [blk, d3, C.POINTER(C.c_longlong)]),
         "lbg_launch_count": (C.c_longlong, []),

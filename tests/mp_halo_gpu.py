@@ -34,7 +34,14 @@ def main():
     uid = [lbdem.comm_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
     params = lbdem.FluidParams(0.7, (1e-6, -2e-6, 0.0))
-    st = FluidStepper(dec, rank, params, device=local, uid=uid[0])
+    halo = os.environ.get("SLAB_HALO", "nccl")
+
+    def allgather(b: bytes):
+        out = [None] * world
+        dist.all_gather_object(out, b)
+        return out
+
+    st = FluidStepper(dec, rank, params, device=local, uid=uid[0], halo=halo, allgather=allgather)
     dims, lo = dec.block_dims(), dec.block_lo(rank)
     glob = random_pdf(domain, seed=321, ghosts=False)
     sl = [slice(None)] * 4
@@ -43,6 +50,10 @@ def main():
     mine = np.zeros((19, dims[2] + 2, dims[1] + 2, dims[0] + 2))
     mine[:, 1:-1, 1:-1, 1:-1] = glob[tuple(sl)]
     st.block.upload_src(mine)
+    dist.barrier()
+    st.prime()
+    torch.cuda.synchronize()
+    dist.barrier()
     for _ in range(steps):
         st.step()
     st.block.sync()

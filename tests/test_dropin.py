@@ -64,9 +64,12 @@ def test_particle_bed_matches_reference(dropin, ref, blocks, workers):
     assert equal_bits(a.pdfs(), b.pdfs())
 
 
-def test_decomposition_invariance_2x2x2(dropin):
-    """Acceptance criterion 11 on the GPU: 2x2x2 device blocks (26-neighbour halo through the
-    generic slab ops) reproduce the single-block known answer bitwise."""
+@pytest.mark.parametrize("halo", ["device", "host"])
+def test_decomposition_invariance_2x2x2(dropin, halo, monkeypatch):
+    """Acceptance criterion 11 on the GPU: 2x2x2 device blocks (26-neighbour halo, device to
+    device via lbg_halo_stage/fetch or through the MessageBus with host slabs) reproduce the
+    single-block known answer bitwise."""
+    monkeypatch.setenv("LBDEM_GPU_HALO", halo)
     ka = json.load(open(os.path.join(GOLDEN, "config1_known_answers.json")))
     cfg = json.loads(ka["config"])
     cfg["blocks"] = [2, 2, 2]

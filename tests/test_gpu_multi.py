@@ -15,12 +15,12 @@ def _ngpus():
     return torch.cuda.device_count()
 
 
-@pytest.mark.parametrize("axis", [2, 0])
-def test_slab_halo_nccl_bitwise(axis):
+@pytest.mark.parametrize("axis,halo", [(2, "nccl"), (0, "nccl"), (2, "p2p"), (0, "p2p")])
+def test_slab_halo_bitwise(axis, halo):
     n = _ngpus()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
-    env = dict(os.environ, SLAB_AXIS=str(axis), SLAB_STEPS="4")
+    env = dict(os.environ, SLAB_AXIS=str(axis), SLAB_STEPS="4", SLAB_HALO=halo)
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                         f"--nproc-per-node={min(n, 4)}", "--master-addr=127.0.0.1",
                         "--master-port=29531", os.path.join(HERE, "mp_halo_gpu.py")],
