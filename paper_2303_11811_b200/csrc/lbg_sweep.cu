@@ -222,7 +222,7 @@ __device__ __forceinline__ void fused_accumulate(const SweepArgs& a, int p, cons
 
 // K2: grid-stride over the covered-cell list (length read on the device)
 template <bool kForced, bool kFused>
-__global__ void __launch_bounds__(128, 4) psm_list_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__(128) psm_list_kernel(const SweepArgs a) {
     const int n = *a.cov_n;
     const int stride = gridDim.x * blockDim.x;
     const Layout& L = a.L;
