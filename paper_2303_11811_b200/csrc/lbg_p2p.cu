@@ -123,10 +123,11 @@ __global__ void __launch_bounds__(256) outer_p2p_kernel(const OuterArgs a) {
     }
     const unsigned m = __ballot_sync(0xffffffffu, !ok);
     if (m && (threadIdx.x & 31) == 0) atomicAdd(&a.err->unstable, (unsigned long long)__popc(m));
-    // last CTA publishes the step to both neighbours
-    __threadfence_system();
+    // last CTA publishes the step to both neighbours (CTA barrier, then one system fence by
+    // the CTA's first thread: the grid-sync pattern, cumulative over the CTA's stores)
     __syncthreads();
     if (threadIdx.x == 0) {
+        __threadfence_system();
         const unsigned long long done = atomicAdd(a.ctr, 1ull) + 1;
         if (done == gridDim.x) {
             *a.ctr = 0;
