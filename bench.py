@@ -184,7 +184,13 @@ CONFIG3 = ('{"scenario":"fluidized_bed_dense","domain":[256,256,256],"particles"
 CATS = ("PSM", "PSM-comm", "mapping", "setU", "redF", "PD", "PD-comm", "other")
 
 
-def coupled_step(steps, with_reference, ref_steps=1):
+def config3(blocks=(1, 1, 1), workers=1):
+    c = json.loads(CONFIG3)
+    c["blocks"], c["workers"] = list(blocks), workers
+    return json.dumps(c)
+
+
+def coupled_step(steps, with_reference, ref_steps=1, blocks=(1, 1, 1), workers=1):
     """Config 3: ~10^4 spheres d = 10 in 256^3, bed BCs, four-way coupled
     with the reference's host DEM. GPU side through the drop-in build (the reference
     Simulation with its fluid/coupling operators on liblbg); the same config on the
@@ -192,13 +198,15 @@ def coupled_step(steps, with_reference, ref_steps=1):
     the reference's own per-category wall-clock TimingReport (perf.hpp:17-51)."""
     sys.path.insert(0, os.path.join(ROOT, "integration"))
     import dropin
+    cfg = config3(blocks, workers)
     out = {"workload": "config 3: 10^4 spheres (d = 10) in 256^3, no-slip walls, velocity inflow, "
-                       "pressure outflow, 10 DEM sub-cycles per fluid step (host DEM = reference code)"}
+                       "pressure outflow, 10 DEM sub-cycles per fluid step (host DEM = reference code)",
+           "blocks": list(blocks), "workers": workers}
     for mode in ("scratch", "fused"):
         # scratch: reference semantics, partials bitwise (PARITY reduction);
         # fused: force/torque summed inside the PSM kernel (FAST, tolerance-level partials)
         os.environ["LBDEM_GPU_FORCE"] = mode
-        sim = dropin.DropinSim(CONFIG3, (256, 256, 256))
+        sim = dropin.DropinSim(cfg, (256, 256, 256))
         sim.run(1)  # warm-up (allocations, first mapping)
         sim.reset_timers()
         t0 = time.perf_counter()
@@ -221,7 +229,7 @@ def coupled_step(steps, with_reference, ref_steps=1):
         ref = RefLib()
         threads = os.cpu_count() or 1
         ref.set_threads(threads)
-        rs = ref.sim(CONFIG3)
+        rs = ref.sim(cfg)
         rs.reset_timers()
         t0 = time.perf_counter()
         rs.run(ref_steps)

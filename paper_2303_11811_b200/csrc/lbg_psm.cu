@@ -277,6 +277,83 @@ __global__ void __launch_bounds__(128) reduce_kernel(const ReduceArgs a) {
     double fs[3] = {0, 0, 0}, fc[3] = {0, 0, 0}, ts[3] = {0, 0, 0}, tc[3] = {0, 0, 0};
     unsigned long long hits = 0;
     const int id = p.id;
+    if (!a.fast) {
+        // Two phases per chunk of 8 x 32 cells of a box plane (lexicographic order t):
+        //  A) every lane tests 8 cells with independent loads (count, ids) and the hits are
+        //     compacted in t order into a shared list;
+        //  B) the hits' momenta are loaded 32 at a time (lane h -> hit h, lever arm, torque)
+        //     and lanes 0..5 replay them in order through their compensated chains.
+        __shared__ unsigned hl[4][256];
+        unsigned* list = hl[(threadIdx.x >> 5) & 3];
+        constexpr int U = 8;
+        const int W = hi[0] - lo[0] + 1, H = hi[1] - lo[1] + 1;
+        const int plane = W * H;
+        for (int k = lo[2]; k <= hi[2]; ++k) {
+            for (int base = 0; base < plane; base += 32 * U) {
+                int hit[U];
+                unsigned cell[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int t = base + u * 32 + lane;
+                    hit[u] = -1;
+                    cell[u] = 0;
+                    if (t < plane) {
+                        const int j = lo[1] + t / W, i = lo[0] + t % W;
+                        const long long c = ((long long)k * g.dims[1] + j) * g.dims[0] + i;
+                        cell[u] = (unsigned)c;
+                        const int cnt = a.count[c];
+                        if (cnt > 0) {
+                            const int i0v = a.id0[c];
+                            const int i1v = cnt > 1 ? a.id1[c] : -1;
+                            hit[u] = i0v == id ? 0 : (i1v == id ? 1 : -1);
+                        }
+                    }
+                }
+                int n = 0;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const unsigned mk = __ballot_sync(0xffffffffu, hit[u] >= 0);
+                    if (hit[u] >= 0) list[n + __popc(mk & ((1u << lane) - 1))] = cell[u] | ((unsigned)hit[u] << 31);
+                    n += __popc(mk);
+                }
+                hits += n;
+                __syncwarp();
+                for (int h0 = 0; h0 < n; h0 += 32) {
+                    const int h = h0 + lane;
+                    if (h < n) {
+                        const unsigned v = list[h];
+                        const long long c = v & 0x7fffffffu;
+                        double* mp = ((v >> 31) ? a.m1 : a.m0) + 3 * c;
+                        const double m0v = mp[0], m1v = mp[1], m2v = mp[2];
+                        mp[0] = mp[1] = mp[2] = 0.0;  // the reference clears the scratch
+                        const int i = (int)(c % g.dims[0]);
+                        const int j = (int)((c / g.dims[0]) % g.dims[1]);
+                        const double r0 = ((double)(g.lo[0] + i) + 0.5) - p.x[0];
+                        const double r1 = ((double)(g.lo[1] + j) + 0.5) - p.x[1];
+                        const double r2 = ((double)(g.lo[2] + k) + 0.5) - p.x[2];
+                        sg[lane][0] = m0v;
+                        sg[lane][1] = m1v;
+                        sg[lane][2] = m2v;
+                        sg[lane][3] = r1 * m2v - r2 * m1v;  // cross(center - x, m)
+                        sg[lane][4] = r2 * m0v - r0 * m2v;
+                        sg[lane][5] = r0 * m1v - r1 * m0v;
+                    }
+                    __syncwarp();
+                    if (lane < 6) {
+                        const int cntr = min(32, n - h0);
+                        for (int s = 0; s < cntr; ++s) nm_add(csum, ccomp, sg[s][lane]);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        for (int d = 0; d < 3; ++d) {
+            fs[d] = __shfl_sync(0xffffffffu, csum, d);
+            fc[d] = __shfl_sync(0xffffffffu, ccomp, d);
+            ts[d] = __shfl_sync(0xffffffffu, csum, 3 + d);
+            tc[d] = __shfl_sync(0xffffffffu, ccomp, 3 + d);
+        }
+    } else {
     // rows no wider than 32 cells are packed R per warp iteration (lane = r*W + i offset);
     // lane order stays lexicographic (row j before row j+1)
     const int W = hi[0] - lo[0] + 1;
@@ -312,41 +389,13 @@ __global__ void __launch_bounds__(128) reduce_kernel(const ReduceArgs a) {
                     t[1] = r2 * m[0] - r0 * m[2];
                     t[2] = r0 * m[1] - r1 * m[0];
                 }
-                unsigned mask = __ballot_sync(0xffffffffu, e >= 0);
+                const unsigned mask = __ballot_sync(0xffffffffu, e >= 0);
                 hits += __popc(mask);
-                if (a.fast) {
-                    for (int d = 0; d < 3; ++d) {
-                        fs[d] += m[d];
-                        ts[d] += t[d];
-                    }
-                    continue;
+                for (int d = 0; d < 3; ++d) {  // FAST: per-lane sums, shuffle-reduced below
+                    fs[d] += m[d];
+                    ts[d] += t[d];
                 }
-                if (!mask) continue;
-                if (e >= 0) {
-                    sg[lane][0] = m[0];
-                    sg[lane][1] = m[1];
-                    sg[lane][2] = m[2];
-                    sg[lane][3] = t[0];
-                    sg[lane][4] = t[1];
-                    sg[lane][5] = t[2];
-                }
-                __syncwarp();
-                if (lane < 6) {
-                    while (mask) {  // replay hits in lane (= lexicographic) order
-                        const int src = __ffs(mask) - 1;
-                        mask &= mask - 1;
-                        nm_add(csum, ccomp, sg[src][lane]);
-                    }
-                }
-                __syncwarp();
             }
-    if (!a.fast) {  // gather the six chains to lane 0's layout
-        for (int d = 0; d < 3; ++d) {
-            fs[d] = __shfl_sync(0xffffffffu, csum, d);
-            fc[d] = __shfl_sync(0xffffffffu, ccomp, d);
-            ts[d] = __shfl_sync(0xffffffffu, csum, 3 + d);
-            tc[d] = __shfl_sync(0xffffffffu, ccomp, 3 + d);
-        }
     }
     if (a.fast) {
         for (int d = 0; d < 3; ++d)

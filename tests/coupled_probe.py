@@ -10,9 +10,17 @@ sys.path.insert(0, os.path.join(ROOT, "integration"))
 import bench  # noqa: E402
 import dropin  # noqa: E402
 
+blocks = os.environ.get("PROBE_BLOCKS")  # e.g. "2,2,2": the reference's own worker parallelism
+cfg = bench.CONFIG3
+if blocks:
+    import json as _j
+    c = _j.loads(cfg)
+    c["blocks"] = [int(v) for v in blocks.split(",")]
+    c["workers"] = int(os.environ.get("PROBE_WORKERS", "8"))
+    cfg = _j.dumps(c)
 for mode in sys.argv[1:] or ["scratch"]:
     os.environ["LBDEM_GPU_FORCE"] = mode
-    sim = dropin.DropinSim(bench.CONFIG3, (256, 256, 256))
+    sim = dropin.DropinSim(cfg, (256, 256, 256))
     for s in range(int(os.environ.get("PROBE_STEPS", "6"))):
         sim.reset_timers()
         t0 = time.perf_counter()
