@@ -400,6 +400,11 @@ lbg_status lbg_block_destroy(lbg_block b) {
     for (auto e : b->event_pool) cudaEventDestroy(e);
     if (b->ev_side) cudaEventDestroy(b->ev_side);
     if (b->ev_stage) cudaEventDestroy(b->ev_stage);
+    for (int s = 0; s < 2; ++s) {
+        if (b->xfer[s]) cudaFree(b->xfer[s]);
+        if (b->ev_copy[s]) cudaEventDestroy(b->ev_copy[s]);
+        if (b->ev_done[s]) cudaEventDestroy(b->ev_done[s]);
+    }
     for (double* p : b->stage)
         if (p) cudaFree(p);
     if (b->recv_buf) cudaFree(b->recv_buf);
@@ -426,12 +431,78 @@ lbg_status lbg_block_info(lbg_block b, int dims[3], int box_lo[3], int* coupling
 
 void* lbg_block_stream(lbg_block b) { return b ? (void*)b->stream : nullptr; }
 
+// packed reference rows (stride nx+2) <-> pitched device rows (stride px, offset kXOff-1)
+__global__ void repitch_kernel(double* __restrict__ dev, const double* __restrict__ packed_in,
+                               double* __restrict__ packed_out, long long row0, long long rows, int w,
+                               int px) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= rows * w) return;
+    const long long r = t / w;
+    const int c = (int)(t % w);
+    double* d = dev + (row0 + r) * px + (kXOff - 1) + c;
+    if (packed_in)
+        *d = packed_in[t];
+    else
+        packed_out[t] = *d;
+}
+
+// Large transfers from/to PINNED host memory: linear chunk copies on the side stream (full
+// PCIe rate) double-buffered against the re-pitch kernel on the compute stream, instead of one
+// row-by-row 2-D copy.
+static lbg_status copy_pdf_pinned(lbg_block b, double* dev, const double* host_in, double* host_out) {
+    const Layout& L = b->L;
+    const int w = L.nx + 2;
+    const long long rows = (long long)kQ * L.py * L.pz;
+    const long long chunk_rows = std::max<long long>(1, (256ll << 20) / (8ll * w));
+    const size_t chunk_bytes = sizeof(double) * (size_t)chunk_rows * w;
+    if (!b->xfer[0]) {
+        for (int s = 0; s < 2; ++s) {
+            LBG_CUDA(cudaMalloc(&b->xfer[s], chunk_bytes));
+            LBG_CUDA(cudaEventCreateWithFlags(&b->ev_copy[s], cudaEventDisableTiming));
+            LBG_CUDA(cudaEventCreateWithFlags(&b->ev_done[s], cudaEventDisableTiming));
+            LBG_CUDA(cudaEventRecord(b->ev_done[s], b->stream));
+        }
+    }
+    for (long long r0 = 0, c = 0; r0 < rows; r0 += chunk_rows, ++c) {
+        const int s = (int)(c & 1);
+        const long long nr = std::min(chunk_rows, rows - r0);
+        const size_t bytes = sizeof(double) * (size_t)nr * w;
+        const unsigned grid = (unsigned)((nr * w + 255) / 256);
+        if (host_in) {
+            LBG_CUDA(cudaStreamWaitEvent(b->side, b->ev_done[s], 0));
+            LBG_CUDA(cudaMemcpyAsync(b->xfer[s], host_in + r0 * w, bytes, cudaMemcpyHostToDevice, b->side));
+            LBG_CUDA(cudaEventRecord(b->ev_copy[s], b->side));
+            LBG_CUDA(cudaStreamWaitEvent(b->stream, b->ev_copy[s], 0));
+            repitch_kernel<<<grid, 256, 0, b->stream>>>(dev, b->xfer[s], nullptr, r0, nr, w, L.px);
+            LBG_LAUNCH_CHECK();
+            LBG_CUDA(cudaEventRecord(b->ev_done[s], b->stream));
+        } else {
+            LBG_CUDA(cudaStreamWaitEvent(b->stream, b->ev_done[s], 0));
+            repitch_kernel<<<grid, 256, 0, b->stream>>>(dev, nullptr, b->xfer[s], r0, nr, w, L.px);
+            LBG_LAUNCH_CHECK();
+            LBG_CUDA(cudaEventRecord(b->ev_copy[s], b->stream));
+            LBG_CUDA(cudaStreamWaitEvent(b->side, b->ev_copy[s], 0));
+            LBG_CUDA(cudaMemcpyAsync(host_out + r0 * w, b->xfer[s], bytes, cudaMemcpyDeviceToHost, b->side));
+            LBG_CUDA(cudaEventRecord(b->ev_done[s], b->side));
+        }
+    }
+    LBG_CUDA(cudaStreamSynchronize(b->side));
+    LBG_CUDA(cudaStreamSynchronize(b->stream));
+    return LBG_OK;
+}
+
 static lbg_status copy_pdf(lbg_block b, double* dev, const double* host_in, double* host_out) {
     const Layout& L = b->L;
     const size_t width = sizeof(double) * (L.nx + 2);
     const size_t height = (size_t)kQ * L.py * L.pz;
     double* d0 = dev + (kXOff - 1);
     LBG_CUDA(cudaSetDevice(b->device));
+    cudaPointerAttributes attr{};
+    const void* hp = host_in ? (const void*)host_in : (const void*)host_out;
+    if (width * height > (64u << 20) && cudaPointerGetAttributes(&attr, hp) == cudaSuccess &&
+        attr.type == cudaMemoryTypeHost)
+        return copy_pdf_pinned(b, dev, host_in, host_out);
+    cudaGetLastError();  // pageable pointers are not an error
     if (host_in) {
         LBG_CUDA(cudaMemcpy2DAsync(d0, sizeof(double) * L.px, host_in, width, width, height,
                                    cudaMemcpyHostToDevice, b->stream));

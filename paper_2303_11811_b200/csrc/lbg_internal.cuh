@@ -165,6 +165,11 @@ struct lbg_block_s {
     size_t recv_cap = 0;
     cudaEvent_t ev_stage = nullptr;
 
+    // pinned-host PDF transfers: double-buffered device staging (lbg_core.cu)
+    double* xfer[2] = {nullptr, nullptr};
+    cudaEvent_t ev_copy[2] = {nullptr, nullptr};
+    cudaEvent_t ev_done[2] = {nullptr, nullptr};
+
     double* src() const { return buf[cur]; }
     double* dst() const { return buf[cur ^ 1]; }
 };
