@@ -227,7 +227,8 @@ def coupled_step(steps, with_reference, ref_steps=1, blocks=(1, 1, 1), workers=1
     if with_reference:
         from oracle.pyoracle import RefLib
         ref = RefLib()
-        threads = os.cpu_count() or 1
+        # all host cores: OpenMP teams inside each block worker share them
+        threads = max(1, (os.cpu_count() or 1) // max(1, workers))
         ref.set_threads(threads)
         rs = ref.sim(cfg)
         rs.reset_timers()
@@ -236,7 +237,8 @@ def coupled_step(steps, with_reference, ref_steps=1, blocks=(1, 1, 1), workers=1
         rdt = time.perf_counter() - t0
         rc = rs.timings()
         out["reference"] = {"ms_per_step": round(rdt * 1e3 / ref_steps, 1), "steps": ref_steps,
-                            "threads": threads, "kind": "reference",
+                            "threads": threads * max(1, workers), "workers": workers,
+                            "omp_threads_per_worker": threads, "kind": "reference",
                             "categories_ms_per_step": {c: round(v * 1e3 / ref_steps, 2) for c, v in zip(CATS, rc)}}
         out["speedup_vs_reference"] = round(out["reference"]["ms_per_step"] / out["ms_per_step"], 2)
     return out
@@ -416,7 +418,14 @@ def run_lbg(args):
     if rank == 0:
         if N == 1 and not args.no_coupled:
             try:
-                out["coupled_step"] = coupled_step(args.coupled_steps, not args.no_cpu_baseline)
+                # the reference's own parallelism lever: 2x2x2 blocks, one worker thread each
+                # (host DEM per block in parallel), same blocks/workers for the reference run
+                workers = min(8, os.cpu_count() or 8)
+                out["coupled_step"] = coupled_step(args.coupled_steps, not args.no_cpu_baseline,
+                                                   blocks=(2, 2, 2), workers=workers)
+                single = coupled_step(args.coupled_steps, False)
+                out["coupled_step"]["single_block"] = {k: single[k] for k in (
+                    "ms_per_step", "categories_ms_per_step", "gpu_side_ms_per_step", "fused_force_mode")}
             except Exception as e:  # noqa: BLE001
                 out["coupled_step"] = {"unavailable": f"{type(e).__name__}: {e}"}
         print(json.dumps(out))

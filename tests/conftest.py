@@ -26,7 +26,11 @@ def ref():
     from oracle.pyoracle import REF_SO, RefLib
     if not os.path.exists(REF_SO):
         pytest.skip("oracle/_ref not built (needs /root/reference at build time)")
-    return RefLib()
+    lib = RefLib()
+    # the reference nests OpenMP inside its block-worker threads; bound the team so
+    # multi-worker configs do not oversubscribe many-core hosts (spinning OMP teams)
+    lib.set_threads(max(1, min(8, (os.cpu_count() or 2) // 2)))
+    return lib
 
 
 def random_pdf(dims, seed, lo=0.95, span=0.1, ghosts=True):
