@@ -240,4 +240,62 @@ __device__ __forceinline__ bool psm_cell_opt(double (&f)[kQ], double inv_tau, Fo
     return ok;
 }
 
+// psm_cell for a cell with exactly one entry, scheduled pair by pair: everything direction
+// q needs (f_q, feq_q, d_q̄, fp_q) lives in the (q, q̄) pair, so the output populations are
+// produced and stored pair by pair instead of being held in registers. Same arithmetic as
+// psm_cell_opt term for term (psm.cpp:174-216 with cnt == 1); the momentum sum keeps the q
+// order because pairs are visited in q order. Returns ok; m_out = B * sum C c_qbar.
+template <bool kForced>
+__device__ __forceinline__ bool psm_cell_one(const double (&f)[kQ], double inv_tau, Force F,
+                                             double b_tot, double be, double vx, double vy, double vz,
+                                             double* __restrict__ dst, long long plane, long long base,
+                                             double (&m_out)[3]) {
+    double rho, ux, uy, uz;
+    moments(f, rho, ux, uy, uz);
+    const double usq = (ux * ux + uy * uy) + uz * uz;
+    const bool ok = rho > 0.0 && usq <= kMaxVelocity * kMaxVelocity && isfinite(rho);
+    const double T = (0.5 * usq) * 3.0;
+    const double Tp = (0.5 * ((vx * vx + vy * vy) + vz * vz)) * 3.0;
+    const double fluid_w = 1.0 - b_tot;
+    double mx = 0.0, my = 0.0, mz = 0.0;
+    // fout_q = (f_q + w_f * (inv_tau * (feq_q - f_q) [+ F_q])) + B * ((f_qb - feq_qb) - (f_q - fp_q))
+    auto out = [&](int q, double fq, double feq_q, double fqb, double feq_qb, double fp_q, double force) {
+        const double coll = inv_tau * (feq_q - fq);
+        const double base_out = fq + fluid_w * (kForced ? coll + force : coll);
+        const double c_solid = (fqb - feq_qb) - (fq - fp_q);
+        mx -= c_solid * (double)cx(q);
+        my -= c_solid * (double)cy(q);
+        mz -= c_solid * (double)cz(q);
+        dst[q * plane + base] = base_out + be * c_solid;
+    };
+    {
+        const double feq0 = wq(0) * (rho - T);
+        const double fp0 = wq(0) * (rho - Tp);
+        out(0, f[0], feq0, f[0], feq0, fp0, kForced ? forcing<0>(0.0, ux, uy, uz, F.x, F.y, F.z) : 0.0);
+    }
+#define LBG_PAIR(qa, qb, cuf, cup)                                                                   \
+    {                                                                                                \
+        double fa, fb, pa, pb;                                                                       \
+        feq_pair(wq(qa), (cuf), rho, T, fa, fb);                                                     \
+        feq_pair(wq(qa), (cup), rho, Tp, pa, pb);                                                    \
+        const double cu_a = (cuf);                                                                   \
+        out(qa, f[qa], fa, f[qb], fb, pa, kForced ? forcing<qa>(cu_a, ux, uy, uz, F.x, F.y, F.z) : 0.0); \
+        out(qb, f[qb], fb, f[qa], fa, pb, kForced ? forcing<qb>(-cu_a, ux, uy, uz, F.x, F.y, F.z) : 0.0); \
+    }
+    LBG_PAIR(1, 2, ux, vx)
+    LBG_PAIR(3, 4, uy, vy)
+    LBG_PAIR(5, 6, uz, vz)
+    LBG_PAIR(7, 8, ux + uy, vx + vy)
+    LBG_PAIR(9, 10, ux - uy, vx - vy)
+    LBG_PAIR(11, 12, ux + uz, vx + vz)
+    LBG_PAIR(13, 14, ux - uz, vx - vz)
+    LBG_PAIR(15, 16, uy + uz, vy + vz)
+    LBG_PAIR(17, 18, uy - uz, vy - vz)
+#undef LBG_PAIR
+    m_out[0] = be * mx;
+    m_out[1] = be * my;
+    m_out[2] = be * mz;
+    return ok;
+}
+
 }  // namespace lbg

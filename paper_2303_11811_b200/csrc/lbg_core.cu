@@ -354,8 +354,8 @@ lbg_status lbg_block_create(int device, const int box_lo[3], const int dims[3], 
         cudaMemset(b->id0, 0xff, n * 4);
         cudaMemset(b->id1, 0xff, n * 4);
         if ((e = cudaMalloc(&b->cov_list, sizeof(unsigned) * n)) != cudaSuccess) return fail(e, "cudaMalloc(cov)");
-        if ((e = cudaMalloc(&b->cov_n, sizeof(int))) != cudaSuccess) return fail(e, "cudaMalloc(cov_n)");
-        cudaMemset(b->cov_n, 0, sizeof(int));
+        if ((e = cudaMalloc(&b->cov_n, 2 * sizeof(int))) != cudaSuccess) return fail(e, "cudaMalloc(cov_n)");
+        cudaMemset(b->cov_n, 0, 2 * sizeof(int));
         b->cov_dirty = false;  // all-zero count: empty list
         b->device_bytes += sizeof(unsigned) * n;
     }

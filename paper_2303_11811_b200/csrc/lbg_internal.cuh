@@ -191,6 +191,20 @@ __device__ __forceinline__ void warp_append(bool pred, unsigned v, unsigned* lis
     if (pred) list[base + __popc(m & ((1u << lane) - 1))] = v;
 }
 
+// covered cells split by entry count: one-entry cells fill the list from the front
+// (counter n[0]), two-entry cells from the back (counter n[1], slot cap-1-i)
+__device__ __forceinline__ void covered_append(int cnt, unsigned v, unsigned* list, long long cap, int* n) {
+    warp_append(cnt == 1, v, list, n);
+    const unsigned m = __ballot_sync(0xffffffffu, cnt == 2);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(n + 1, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (cnt == 2) list[cap - 1 - (base + __popc(m & ((1u << lane) - 1)))] = v;
+}
+
 // error plumbing (lbg_core.cu)
 lbg_status set_error(lbg_status s, const std::string& msg);
 lbg_status cuda_check(cudaError_t e, const char* what);

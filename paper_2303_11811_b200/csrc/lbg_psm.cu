@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(256) map_kernel(const MapArgs a) {
     const int k = blockIdx.z;
     const BinGeom& g = a.g;
     bool over = false;
-    bool covered = false;
+    int covered = 0;  // entry count for the covered-cell lists
     unsigned cell = 0;
     if (i < g.dims[0]) {
         const long long c = ((long long)k * g.dims[1] + j) * g.dims[0] + i;
@@ -170,10 +170,10 @@ __global__ void __launch_bounds__(256) map_kernel(const MapArgs a) {
         }
         a.count[c] = (uint8_t)cnt;
         a.btot[c] = sum < 1.0 ? sum : 1.0;  // std::min(1.0, sum)
-        covered = cnt > 0;
+        covered = cnt;
         cell = (unsigned)c;
     }
-    warp_append(covered, cell, a.cov_list, a.cov_n);
+    covered_append(covered, cell, a.cov_list, (long long)g.dims[0] * g.dims[1] * g.dims[2], a.cov_n);
     const unsigned m = __ballot_sync(0xffffffffu, over);
     if (m && (threadIdx.x & 31) == 0) atomicAdd(&a.err->overfull, (unsigned long long)__popc(m));
 }
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(256) map_kernel(const MapArgs a) {
 __global__ void __launch_bounds__(256) covered_kernel(const uint8_t* __restrict__ count, long long cells,
                                                       unsigned* __restrict__ list, int* __restrict__ n) {
     const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    warp_append(c < cells && count[c] > 0, (unsigned)c, list, n);
+    covered_append(c < cells ? count[c] : 0, (unsigned)c, list, cells, n);
 }
 
 __device__ __forceinline__ int find_snapshot(const lbg_snapshot* s, int n, int id) {
@@ -495,7 +495,7 @@ static lbg_status ensure_bins(lbg_block b, long long nbins) {
 
 lbg_status rebuild_covered(lbg_block b) {
     const long long cells = (long long)b->L.nx * b->L.ny * b->L.nz;
-    LBG_CUDA(cudaMemsetAsync(b->cov_n, 0, sizeof(int), b->stream));
+    LBG_CUDA(cudaMemsetAsync(b->cov_n, 0, 2 * sizeof(int), b->stream));
     covered_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, b->stream>>>(b->count, cells, b->cov_list, b->cov_n);
     LBG_LAUNCH_CHECK();
     b->cov_dirty = false;
@@ -604,7 +604,7 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
     a.with_velocity = 1;
     a.cov_list = b->cov_list;
     a.cov_n = b->cov_n;
-    LBG_CUDA(cudaMemsetAsync(b->cov_n, 0, sizeof(int), b->stream));
+    LBG_CUDA(cudaMemsetAsync(b->cov_n, 0, 2 * sizeof(int), b->stream));
     dim3 grid((g.dims[0] + 127) / 128, g.dims[1], g.dims[2]);
     map_kernel<<<grid, 128, 0, b->stream>>>(a);
     LBG_LAUNCH_CHECK();

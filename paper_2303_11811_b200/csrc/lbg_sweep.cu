@@ -44,8 +44,9 @@ struct SweepArgs {
     const double* __restrict__ v1;
     double* __restrict__ m0;
     double* __restrict__ m1;
-    const unsigned* __restrict__ cov_list;
-    const int* __restrict__ cov_n;
+    const unsigned* __restrict__ cov_list;  // one-entry cells from the front, two-entry from the back
+    const int* __restrict__ cov_n;          // [0] one-entry count, [1] two-entry count
+    long long cov_cap;
     const int* __restrict__ id0;
     const int* __restrict__ id1;
     // fused force reduction (LBG_FORCE_FUSED)
@@ -220,10 +221,50 @@ __device__ __forceinline__ void fused_accumulate(const SweepArgs& a, int p, cons
     }
 }
 
-// K2: grid-stride over the covered-cell list (length read on the device)
+// K2a: one-entry covered cells (front of the list), pair-scheduled operator (psm_cell_one)
+template <bool kForced, bool kFused>
+__global__ void __launch_bounds__(128) psm_one_kernel(const SweepArgs a) {
+    const int n = a.cov_n[0];
+    const int stride = gridDim.x * blockDim.x;
+    const Layout& L = a.L;
+    for (int base0 = blockIdx.x * blockDim.x; base0 < n; base0 += stride) {
+        const int t = base0 + threadIdx.x;
+        bool ok = true;
+        double m[3] = {0, 0, 0};
+        double cc[3] = {0, 0, 0};
+        int p0 = -1;
+        if (t < n) {
+            const unsigned c = a.cov_list[t];
+            const int i = (int)(c % (unsigned)L.nx);
+            const int j = (int)((c / (unsigned)L.nx) % (unsigned)L.ny);
+            const int k = (int)(c / ((unsigned)L.nx * (unsigned)L.ny));
+            if (in_boxes(a, i, j, k)) {
+                const long long base = L.idx(i, j, k);
+                double f[kQ];
+                pull(a, i, j, k, base, f);
+                ok = psm_cell_one<kForced>(f, a.inv_tau, a.F, a.btot[c], a.b0[c], a.v0[3 * (size_t)c],
+                                           a.v0[3 * (size_t)c + 1], a.v0[3 * (size_t)c + 2], a.dst, L.plane,
+                                           base, m);
+                if constexpr (kFused) {
+                    cc[0] = (double)(a.blk_lo[0] + i) + 0.5;
+                    cc[1] = (double)(a.blk_lo[1] + j) + 0.5;
+                    cc[2] = (double)(a.blk_lo[2] + k) + 0.5;
+                    p0 = snapshot_of(a, a.id0[c]);
+                    if (p0 < 0) atomicAdd(&a.err->unknown, 1ull);
+                } else {
+                    for (int d = 0; d < 3; ++d) a.m0[3 * (size_t)c + d] = m[d];
+                }
+            }
+        }
+        count_bad(a.err, !ok);
+        if constexpr (kFused) fused_accumulate(a, p0, m, cc);
+    }
+}
+
+// K2b: two-entry covered cells (back of the list), general operator (psm_cell_opt)
 template <bool kForced, bool kFused>
 __global__ void __launch_bounds__(128) psm_list_kernel(const SweepArgs a) {
-    const int n = *a.cov_n;
+    const int n = a.cov_n[1];
     const int stride = gridDim.x * blockDim.x;
     const Layout& L = a.L;
     for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
@@ -234,7 +275,7 @@ __global__ void __launch_bounds__(128) psm_list_kernel(const SweepArgs a) {
         double cc[3] = {0, 0, 0};
         int p0 = -1, p1 = -1;
         if (t < n) {
-            const unsigned c = a.cov_list[t];
+            const unsigned c = a.cov_list[a.cov_cap - 1 - t];
             const int i = (int)(c % (unsigned)L.nx);
             const int j = (int)((c / (unsigned)L.nx) % (unsigned)L.ny);
             const int k = (int)(c / ((unsigned)L.nx * (unsigned)L.ny));
@@ -336,6 +377,7 @@ static SweepArgs make_args(lbg_block b, const lbg_fluid* fl) {
         a.m1 = b->m1;
         a.cov_list = b->cov_list;
         a.cov_n = b->cov_n;
+        a.cov_cap = (long long)b->L.nx * b->L.ny * b->L.nz;
         a.id0 = b->id0;
         a.id1 = b->id1;
         a.snaps = b->snaps_d;
@@ -385,6 +427,15 @@ static void launch_psm_list(lbg_block b, const SweepArgs& a, bool forced) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, b->device);
     const bool fused = b->force_mode == LBG_FORCE_FUSED;
+    // one-entry cells (the bulk): lean pair-scheduled kernel, more CTAs per SM
+    if (forced)
+        fused ? psm_one_kernel<true, true><<<sms * 8, 128, 0, b->stream>>>(a)
+              : psm_one_kernel<true, false><<<sms * 8, 128, 0, b->stream>>>(a);
+    else
+        fused ? psm_one_kernel<false, true><<<sms * 8, 128, 0, b->stream>>>(a)
+              : psm_one_kernel<false, false><<<sms * 8, 128, 0, b->stream>>>(a);
+    count_launch();
+    // two-entry cells (particle contacts)
     if (forced)
         fused ? psm_list_kernel<true, true><<<sms * 4, 128, 0, b->stream>>>(a)
               : psm_list_kernel<true, false><<<sms * 4, 128, 0, b->stream>>>(a);
