@@ -390,7 +390,9 @@ lbg_status lbg_block_destroy(lbg_block b) {
                    b->bin_items, b->red_rows, b->red_used, b->err_d, b->cov_list, b->cov_n, b->facc, b->fused_used, b->scan_tmp, b->obs_d};
     for (void* p : dev)
         if (p) cudaFree(p);
-    void* host[] = {b->snaps_h, b->err_h, b->red_h, b->red_rows_h, b->red_used_h, b->obs_h};
+    void* host[] = {b->snaps_h, b->err_h, b->red_rows_h, b->red_used_h, b->obs_h};
+    for (void* p : {(void*)b->ekeys[0], (void*)b->ekeys[1], b->sort_tmp, (void*)b->seg})
+        if (p) cudaFree(p);
     for (void* p : host)
         if (p) cudaFreeHost(p);
     for (auto& s : b->spans) {

@@ -134,9 +134,15 @@ struct lbg_block_s {
     double* red_rows = nullptr;  // n_snaps x 12
     int* red_used = nullptr;
     int red_cap = 0;
-    lbg_hydro_partial* red_h = nullptr;
     double* red_rows_h = nullptr;
     int* red_used_h = nullptr;
+    // sorted-entry PARITY reduction: entry keys (in/out), radix-sort workspace, segments
+    unsigned long long* ekeys[2] = {nullptr, nullptr};
+    long long ekeys_cap = 0;
+    void* sort_tmp = nullptr;
+    size_t sort_tmp_bytes = 0;
+    int* seg = nullptr;  // start[n], end[n]
+    int seg_cap = 0;
 
     lbg::DeviceErrors* err_d = nullptr;
     lbg::DeviceErrors* err_h = nullptr;  // pinned

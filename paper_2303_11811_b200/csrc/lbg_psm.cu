@@ -17,10 +17,11 @@
 // which is why lbg_map is called after the host velocity sync.
 //
 // Reduction design: PARITY mode reproduces the reference's per-particle Neumaier sums in
-// lexicographic cell order bitwise: one warp per particle walks the particle's reach box
-// row by row; lanes load 32 consecutive cells, and the warp replays the hits in lane
-// order through the compensated adder (every lane holds the same accumulator). FAST mode
-// sums per lane, reduces with warp shuffles and adds one atomic per warp and particle.
+// lexicographic cell order bitwise: every fraction entry of the covered-cell lists becomes a
+// (particle, cell, slot) key, a radix sort puts each particle's entries in the reference's
+// visiting order, and six threads per particle run the compensated chains (f.x..t.z) over
+// the particle's segment. FAST sums the same segments plainly; the fused force mode
+// (lbg_sweep.cu) sums inside the PSM kernel with warp aggregation + atomics instead.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -241,204 +242,91 @@ __device__ __forceinline__ void nm_add(double& sum, double& comp, double v) {  /
     sum = t;
 }
 
-struct ReduceArgs {
-    const lbg_snapshot* __restrict__ s;
-    int n;
-    BinGeom g;
-    const uint8_t* __restrict__ count;
-    const int* __restrict__ id0;
-    const int* __restrict__ id1;
-    double* __restrict__ m0;
-    double* __restrict__ m1;
-    double* __restrict__ rows;  // n x 12
-    int* __restrict__ used;
-    unsigned long long* __restrict__ visited;  // entries found by the box walks
-    int fast;
-};
-
-// one warp per particle: lexicographic walk of the reach box
-__global__ void __launch_bounds__(128) reduce_kernel(const ReduceArgs a) {
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= a.n) return;
-    const lbg_snapshot& p = a.s[warp];
-    const BinGeom& g = a.g;
-    const double reach = p.r + 0.5;
-    int lo[3], hi[3];
-    for (int d = 0; d < 3; ++d) {
-        lo[d] = max((int)floor(p.x[d] - reach - g.lo[d]) - 1, 0);
-        hi[d] = min((int)floor(p.x[d] + reach - g.lo[d]) + 1, g.dims[d] - 1);
-    }
-    // PARITY: lane l < 6 owns one compensated chain (f.x f.y f.z t.x t.y t.z) and replays the
-    // segment's hits in lane order from shared memory — the 6 chains run in parallel
-    __shared__ double seg[4][32][6];
-    double (*sg)[6] = seg[(threadIdx.x >> 5) & 3];
-    double csum = 0.0, ccomp = 0.0;
-    double fs[3] = {0, 0, 0}, fc[3] = {0, 0, 0}, ts[3] = {0, 0, 0}, tc[3] = {0, 0, 0};
-    unsigned long long hits = 0;
-    const int id = p.id;
-    if (!a.fast) {
-        // Two phases per chunk of 8 x 32 cells of a box plane (lexicographic order t):
-        //  A) every lane tests 8 cells with independent loads (count, ids) and the hits are
-        //     compacted in t order into a shared list;
-        //  B) the hits' momenta are loaded 32 at a time (lane h -> hit h, lever arm, torque)
-        //     and lanes 0..5 replay them in order through their compensated chains.
-        __shared__ unsigned hl[4][256];
-        unsigned* list = hl[(threadIdx.x >> 5) & 3];
-        constexpr int U = 8;
-        const int W = hi[0] - lo[0] + 1, H = hi[1] - lo[1] + 1;
-        const int plane = W * H;
-        for (int k = lo[2]; k <= hi[2]; ++k) {
-            for (int base = 0; base < plane; base += 32 * U) {
-                int hit[U];
-                unsigned cell[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int t = base + u * 32 + lane;
-                    hit[u] = -1;
-                    cell[u] = 0;
-                    if (t < plane) {
-                        const int j = lo[1] + t / W, i = lo[0] + t % W;
-                        const long long c = ((long long)k * g.dims[1] + j) * g.dims[0] + i;
-                        cell[u] = (unsigned)c;
-                        const int cnt = a.count[c];
-                        if (cnt > 0) {
-                            const int i0v = a.id0[c];
-                            const int i1v = cnt > 1 ? a.id1[c] : -1;
-                            hit[u] = i0v == id ? 0 : (i1v == id ? 1 : -1);
-                        }
-                    }
-                }
-                int n = 0;
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const unsigned mk = __ballot_sync(0xffffffffu, hit[u] >= 0);
-                    if (hit[u] >= 0) list[n + __popc(mk & ((1u << lane) - 1))] = cell[u] | ((unsigned)hit[u] << 31);
-                    n += __popc(mk);
-                }
-                hits += n;
-                __syncwarp();
-                for (int h0 = 0; h0 < n; h0 += 32) {
-                    const int h = h0 + lane;
-                    if (h < n) {
-                        const unsigned v = list[h];
-                        const long long c = v & 0x7fffffffu;
-                        double* mp = ((v >> 31) ? a.m1 : a.m0) + 3 * c;
-                        const double m0v = mp[0], m1v = mp[1], m2v = mp[2];
-                        mp[0] = mp[1] = mp[2] = 0.0;  // the reference clears the scratch
-                        const int i = (int)(c % g.dims[0]);
-                        const int j = (int)((c / g.dims[0]) % g.dims[1]);
-                        const double r0 = ((double)(g.lo[0] + i) + 0.5) - p.x[0];
-                        const double r1 = ((double)(g.lo[1] + j) + 0.5) - p.x[1];
-                        const double r2 = ((double)(g.lo[2] + k) + 0.5) - p.x[2];
-                        sg[lane][0] = m0v;
-                        sg[lane][1] = m1v;
-                        sg[lane][2] = m2v;
-                        sg[lane][3] = r1 * m2v - r2 * m1v;  // cross(center - x, m)
-                        sg[lane][4] = r2 * m0v - r0 * m2v;
-                        sg[lane][5] = r0 * m1v - r1 * m0v;
-                    }
-                    __syncwarp();
-                    if (lane < 6) {
-                        const int cntr = min(32, n - h0);
-                        for (int s = 0; s < cntr; ++s) nm_add(csum, ccomp, sg[s][lane]);
-                    }
-                    __syncwarp();
-                }
-            }
+// ---- sorted-entry PARITY reduction -------------------------------------------------------
+// Every fraction entry (cell c, slot e) of the covered-cell lists becomes a 64-bit key
+// (particle index << 32 | c << 1 | e); a radix sort orders the entries by particle, then
+// lexicographic cell — exactly finalize_hydro_forces' visiting order per particle
+// (psm.cpp:288-308) — and six threads per particle (f.x f.y f.z t.x t.y t.z) run the
+// Neumaier chains over the particle's segment. No walk over empty cells, any fraction field.
+__global__ void __launch_bounds__(256) entry_keys_kernel(const unsigned* __restrict__ cov_list,
+                                                         const int* __restrict__ cov_n, long long cap,
+                                                         const int* __restrict__ id0, const int* __restrict__ id1,
+                                                         const lbg_snapshot* __restrict__ s, int n_snaps,
+                                                         unsigned long long* __restrict__ keys,
+                                                         DeviceErrors* err) {
+    const long long n1 = cov_n[0], n2 = cov_n[1];
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n1 + n2) return;
+    const bool one = t < n1;
+    const unsigned c = one ? cov_list[t] : cov_list[cap - 1 - (t - n1)];
+    unsigned long long* out = one ? keys + t : keys + n1 + 2 * (t - n1);
+    for (int e = 0; e < (one ? 1 : 2); ++e) {
+        const int p = find_snapshot(s, n_snaps, e == 0 ? id0[c] : id1[c]);
+        if (p < 0) {
+            atomicAdd(&err->unknown, 1ull);
+            out[e] = ((unsigned long long)n_snaps << 32) | ((unsigned long long)c << 1) | (unsigned long long)e;
+        } else {
+            out[e] = ((unsigned long long)p << 32) | ((unsigned long long)c << 1) | (unsigned long long)e;
         }
-        for (int d = 0; d < 3; ++d) {
-            fs[d] = __shfl_sync(0xffffffffu, csum, d);
-            fc[d] = __shfl_sync(0xffffffffu, ccomp, d);
-            ts[d] = __shfl_sync(0xffffffffu, csum, 3 + d);
-            tc[d] = __shfl_sync(0xffffffffu, ccomp, 3 + d);
-        }
-    } else {
-    // rows no wider than 32 cells are packed R per warp iteration (lane = r*W + i offset);
-    // lane order stays lexicographic (row j before row j+1)
-    const int W = hi[0] - lo[0] + 1;
-    const bool packed = W <= 32;
-    const int R = packed ? 32 / W : 1;
-    const int r_of = packed ? lane / W : 0;
-    const int i_of = packed ? lane % W : lane;
-    const int istep = packed ? W : 32;
-    for (int k = lo[2]; k <= hi[2]; ++k)
-        for (int j0 = lo[1]; j0 <= hi[1]; j0 += R)
-            for (int i0 = lo[0]; i0 <= hi[0]; i0 += istep) {
-                const int i = i0 + i_of;
-                const int j = j0 + r_of;
-                int e = -1;
-                long long c = 0;
-                if (r_of < R && j <= hi[1] && i <= hi[0]) {
-                    c = ((long long)k * g.dims[1] + j) * g.dims[0] + i;
-                    const int cnt = a.count[c];
-                    if (cnt > 0 && a.id0[c] == id) e = 0;
-                    else if (cnt > 1 && a.id1[c] == id) e = 1;
-                }
-                double m[3] = {0, 0, 0}, t[3] = {0, 0, 0};
-                if (e >= 0) {
-                    double* mp = (e == 0 ? a.m0 : a.m1) + 3 * c;
-                    m[0] = mp[0];
-                    m[1] = mp[1];
-                    m[2] = mp[2];
-                    mp[0] = mp[1] = mp[2] = 0.0;  // the reference clears the scratch
-                    const double r0 = ((double)(g.lo[0] + i) + 0.5) - p.x[0];
-                    const double r1 = ((double)(g.lo[1] + j) + 0.5) - p.x[1];
-                    const double r2 = ((double)(g.lo[2] + k) + 0.5) - p.x[2];
-                    t[0] = r1 * m[2] - r2 * m[1];  // cross(center - x, m)
-                    t[1] = r2 * m[0] - r0 * m[2];
-                    t[2] = r0 * m[1] - r1 * m[0];
-                }
-                const unsigned mask = __ballot_sync(0xffffffffu, e >= 0);
-                hits += __popc(mask);
-                for (int d = 0; d < 3; ++d) {  // FAST: per-lane sums, shuffle-reduced below
-                    fs[d] += m[d];
-                    ts[d] += t[d];
-                }
-            }
-    }
-    if (a.fast) {
-        for (int d = 0; d < 3; ++d)
-            for (int o = 16; o > 0; o >>= 1) {
-                fs[d] += __shfl_xor_sync(0xffffffffu, fs[d], o);
-                ts[d] += __shfl_xor_sync(0xffffffffu, ts[d], o);
-            }
-    }
-    if (lane == 0) {
-        double* row = a.rows + 12 * (size_t)warp;
-        for (int d = 0; d < 3; ++d) {
-            row[d] = fs[d];
-            row[3 + d] = fc[d];
-            row[6 + d] = ts[d];
-            row[9 + d] = tc[d];
-        }
-        a.used[warp] = hits > 0;
-        if (hits) atomicAdd(a.visited, hits);
     }
 }
 
-// total entries in the field + unknown-id check (psm.cpp:300-303)
-__global__ void __launch_bounds__(256) entry_census_kernel(const lbg_snapshot* __restrict__ s, int n,
-                                                           long long cells, const uint8_t* __restrict__ count,
-                                                           const int* __restrict__ id0, const int* __restrict__ id1,
-                                                           unsigned long long* __restrict__ total,
-                                                           DeviceErrors* err) {
-    const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned e = 0, unk = 0;
-    if (c < cells) {
-        const int cnt = count[c];
-        e = cnt;
-        if (cnt > 0 && find_snapshot(s, n, id0[c]) < 0) ++unk;
-        if (cnt > 1 && find_snapshot(s, n, id1[c]) < 0) ++unk;
+__global__ void __launch_bounds__(256) segment_kernel(const unsigned long long* __restrict__ keys, long long n,
+                                                      int n_snaps, int* __restrict__ start, int* __restrict__ end) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned p = (unsigned)(keys[i] >> 32);
+    if (p >= (unsigned)n_snaps) return;  // unknown id (SyncError is raised)
+    if (i == 0 || (unsigned)(keys[i - 1] >> 32) != p) start[p] = (int)i;
+    if (i == n - 1 || (unsigned)(keys[i + 1] >> 32) != p) end[p] = (int)(i + 1);
+}
+
+__global__ void __launch_bounds__(192) chain_kernel(const unsigned long long* __restrict__ keys,
+                                                    const int* __restrict__ start, const int* __restrict__ end,
+                                                    const lbg_snapshot* __restrict__ s, int n_snaps, BinGeom g,
+                                                    const double* __restrict__ m0, const double* __restrict__ m1,
+                                                    double* __restrict__ rows, int* __restrict__ used, int fast) {
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int p = tid / 6, d = tid % 6;
+    if (p >= n_snaps) return;
+    const int i0 = start[p], i1 = end[p];
+    double sum = 0.0, comp = 0.0;
+    const double x0 = s[p].x[0], x1 = s[p].x[1], x2 = s[p].x[2];
+    for (int i = i0; i < i1; ++i) {
+        const unsigned long long key = keys[i];
+        const long long c = (long long)((key >> 1) & 0x7fffffffull);
+        const double* mp = ((key & 1ull) ? m1 : m0) + 3 * c;
+        double v;
+        if (d < 3) {
+            v = mp[d];
+        } else {
+            const int ci = (int)(c % g.dims[0]), cj = (int)((c / g.dims[0]) % g.dims[1]),
+                      ck = (int)(c / ((long long)g.dims[0] * g.dims[1]));
+            const double r0 = ((double)(g.lo[0] + ci) + 0.5) - x0;
+            const double r1 = ((double)(g.lo[1] + cj) + 0.5) - x1;
+            const double r2 = ((double)(g.lo[2] + ck) + 0.5) - x2;
+            const double a0 = mp[0], a1 = mp[1], a2 = mp[2];
+            v = d == 3 ? r1 * a2 - r2 * a1 : (d == 4 ? r2 * a0 - r0 * a2 : r0 * a1 - r1 * a0);
+        }
+        if (fast)
+            sum += v;
+        else
+            nm_add(sum, comp, v);
     }
-    for (int o = 16; o > 0; o >>= 1) {
-        e += __shfl_xor_sync(0xffffffffu, e, o);
-        unk += __shfl_xor_sync(0xffffffffu, unk, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        if (e) atomicAdd(total, (unsigned long long)e);
-        if (unk) atomicAdd(&err->unknown, (unsigned long long)unk);
-    }
+    const int slot = d < 3 ? d : 6 + (d - 3);
+    rows[12 * (size_t)p + slot] = sum;
+    rows[12 * (size_t)p + slot + 3] = comp;
+    if (d == 0) used[p] = i1 > i0;
+}
+
+// the reference clears the scratch of every visited entry (psm.cpp:305)
+__global__ void __launch_bounds__(256) clear_entries_kernel(const unsigned long long* __restrict__ keys, long long n,
+                                                            double* __restrict__ m0, double* __restrict__ m1) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const long long c = (long long)((keys[i] >> 1) & 0x7fffffffull);
+    double* mp = ((keys[i] & 1ull) ? m1 : m0) + 3 * c;
+    mp[0] = mp[1] = mp[2] = 0.0;
 }
 
 static BinGeom geom(lbg_block b) {
@@ -685,50 +573,76 @@ lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int c
         LBG_CUDA(cudaMalloc(&b->red_rows, 16 + sizeof(double) * 12));
         LBG_CUDA(cudaMallocHost(&b->red_rows_h, 16 + sizeof(double) * 12));
     }
-    // visited/total counters live after the rows
-    unsigned long long* ctr = (unsigned long long*)(b->red_rows + 12 * (size_t)std::max(b->red_cap, 1));
     const BinGeom g = geom(b);
     const long long cells = (long long)g.dims[0] * g.dims[1] * g.dims[2];
+    if (b->cov_dirty)
+        if (lbg_status s = rebuild_covered(b)) return s;
     {
         Span span(b, LBG_CAT_REDF);
-        LBG_CUDA(cudaMemsetAsync(ctr, 0, 16, b->stream));
-        entry_census_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, b->stream>>>(
-            b->snaps_d, n, cells, b->count, b->id0, b->id1, ctr + 1, b->err_d);
-        LBG_LAUNCH_CHECK();
-        if (n > 0) {
-            ReduceArgs a{};
-            a.s = b->snaps_d;
-            a.n = n;
-            a.g = g;
-            a.count = b->count;
-            a.id0 = b->id0;
-            a.id1 = b->id1;
-            a.m0 = b->m0;
-            a.m1 = b->m1;
-            a.rows = b->red_rows;
-            a.used = b->red_used;
-            a.visited = ctr;
-            a.fast = mode == LBG_REDUCE_FAST;
-            reduce_kernel<<<(n * 32 + 127) / 128, 128, 0, b->stream>>>(a);
+        int cn[2] = {0, 0};
+        LBG_CUDA(cudaMemcpyAsync(cn, b->cov_n, sizeof(cn), cudaMemcpyDeviceToHost, b->stream));
+        LBG_CUDA(cudaStreamSynchronize(b->stream));
+        const long long ne = (long long)cn[0] + 2LL * cn[1];
+        if (ne > b->ekeys_cap) {
+            for (auto& k : b->ekeys)
+                if (k) cudaFree(k);
+            b->ekeys_cap = std::max(ne, 2 * b->ekeys_cap);
+            LBG_CUDA(cudaMalloc(&b->ekeys[0], sizeof(unsigned long long) * b->ekeys_cap));
+            LBG_CUDA(cudaMalloc(&b->ekeys[1], sizeof(unsigned long long) * b->ekeys_cap));
+        }
+        if (std::max(n, 1) > b->seg_cap) {
+            if (b->seg) cudaFree(b->seg);
+            b->seg_cap = std::max(std::max(n, 1), 2 * b->seg_cap);
+            LBG_CUDA(cudaMalloc(&b->seg, sizeof(int) * 2 * b->seg_cap));
+        }
+        if (ne > 0) {
+            entry_keys_kernel<<<(unsigned)((cn[0] + cn[1] + 255) / 256), 256, 0, b->stream>>>(
+                b->cov_list, b->cov_n, cells, b->id0, b->id1, b->snaps_d, n, b->ekeys[0], b->err_d);
             LBG_LAUNCH_CHECK();
+            int bits = 1;
+            while ((1ll << bits) < n + 1) ++bits;
+            size_t tmp = 0;
+            cub::DeviceRadixSort::SortKeys(nullptr, tmp, b->ekeys[0], b->ekeys[1], (int)ne, 0, 32 + bits,
+                                           b->stream);  // unknown ids carry index n: still < 2^bits
+            if (tmp > b->sort_tmp_bytes) {
+                if (b->sort_tmp) cudaFree(b->sort_tmp);
+                LBG_CUDA(cudaMalloc(&b->sort_tmp, tmp));
+                b->sort_tmp_bytes = tmp;
+            }
+            cub::DeviceRadixSort::SortKeys(b->sort_tmp, tmp, b->ekeys[0], b->ekeys[1], (int)ne, 0, 32 + bits,
+                                           b->stream);
+            LBG_LAUNCH_CHECK();
+        }
+        if (n > 0) {
+            int* start = b->seg;
+            int* end = b->seg + b->seg_cap;
+            LBG_CUDA(cudaMemsetAsync(start, 0, sizeof(int) * n, b->stream));
+            LBG_CUDA(cudaMemsetAsync(end, 0, sizeof(int) * n, b->stream));
+            if (ne > 0) {
+                segment_kernel<<<(unsigned)((ne + 255) / 256), 256, 0, b->stream>>>(b->ekeys[1], ne, n, start, end);
+                LBG_LAUNCH_CHECK();
+            }
+            chain_kernel<<<(unsigned)((6LL * n + 191) / 192), 192, 0, b->stream>>>(
+                b->ekeys[1], start, end, b->snaps_d, n, g, b->m0, b->m1, b->red_rows, b->red_used,
+                mode == LBG_REDUCE_FAST);
+            LBG_LAUNCH_CHECK();
+            if (ne > 0) {
+                clear_entries_kernel<<<(unsigned)((ne + 255) / 256), 256, 0, b->stream>>>(b->ekeys[1], ne, b->m0,
+                                                                                         b->m1);
+                LBG_LAUNCH_CHECK();
+            }
             LBG_CUDA(cudaMemcpyAsync(b->red_rows_h, b->red_rows, sizeof(double) * 12 * n,
                                      cudaMemcpyDeviceToHost, b->stream));
             LBG_CUDA(cudaMemcpyAsync(b->red_used_h, b->red_used, sizeof(int) * n, cudaMemcpyDeviceToHost,
                                      b->stream));
         }
     }
-    unsigned long long ctr_h[2] = {0, 0};
-    LBG_CUDA(cudaMemcpyAsync(ctr_h, ctr, 16, cudaMemcpyDeviceToHost, b->stream));
     LBG_CUDA(cudaStreamSynchronize(b->stream));
     if (lbg_status s = lbg_sync(b, nullptr)) {
         if (s == LBG_SYNC_ERROR)
             return set_error(LBG_SYNC_ERROR, "hydrodynamic force for unknown particle id");
         return s;
     }
-    if (ctr_h[0] != ctr_h[1])
-        return set_error(LBG_INVALID, "fraction entries outside their particle's reach box (" +
-                                          std::to_string(ctr_h[1] - ctr_h[0]) +
-                                          " entries); the field was not produced by lbg_map");
     int m = 0;
     for (int p = 0; p < n; ++p) {
         if (!b->red_used_h[p]) continue;
