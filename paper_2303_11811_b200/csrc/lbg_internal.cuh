@@ -103,8 +103,13 @@ struct lbg_block_s {
     // covered cells (count > 0), compacted by the mapping kernel / after a fraction upload;
     // the PSM operator runs over this list so the SRT sweep keeps its low register count
     unsigned* cov_list = nullptr;
-    int* cov_n = nullptr;  // device counter
+    int* cov_n = nullptr;  // device counters [2]
     bool cov_dirty = true;
+    // aligned 32-cell row segments holding covered cells (first cell index): segments with
+    // one-entry cells only from the front (seg_n[0]), with a two-entry cell from the back
+    unsigned* seg_list = nullptr;
+    int* seg_n = nullptr;
+    long long seg_cap = 0;
 
     // periodic axes the sweep wraps in-kernel (no ghost read), lbg_set_periodic_wrap
     int wrap[3] = {0, 0, 0};
@@ -141,8 +146,9 @@ struct lbg_block_s {
     long long ekeys_cap = 0;
     void* sort_tmp = nullptr;
     size_t sort_tmp_bytes = 0;
-    int* seg = nullptr;  // start[n], end[n]
-    int seg_cap = 0;
+    int* red_seg = nullptr;  // start[n], end[n]
+    int red_seg_cap = 0;
+    int* cn_h = nullptr;  // pinned copy of cov_n
 
     lbg::DeviceErrors* err_d = nullptr;
     lbg::DeviceErrors* err_h = nullptr;  // pinned

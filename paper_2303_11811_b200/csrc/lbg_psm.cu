@@ -118,6 +118,9 @@ struct MapArgs {
     int with_velocity;
     unsigned* cov_list;
     int* cov_n;
+    unsigned* seg_list;
+    int* seg_n;
+    long long seg_cap;
 };
 
 // psm.cpp:28-32 overlap_fraction, psm.cpp:93-136 per-cell entry rule, psm.cpp:157-163 setU
@@ -175,6 +178,14 @@ __global__ void __launch_bounds__(256) map_kernel(const MapArgs a) {
         cell = (unsigned)c;
     }
     covered_append(covered, cell, a.cov_list, (long long)g.dims[0] * g.dims[1] * g.dims[2], a.cov_n);
+    // this warp is one aligned 32-cell row segment: register it for the PSM sweep (K2)
+    const int segmax = __reduce_max_sync(0xffffffffu, covered);
+    if ((threadIdx.x & 31) == 0 && segmax > 0) {
+        if (segmax == 1)
+            a.seg_list[atomicAdd(&a.seg_n[0], 1)] = cell;
+        else
+            a.seg_list[a.seg_cap - 1 - atomicAdd(&a.seg_n[1], 1)] = cell;
+    }
     const unsigned m = __ballot_sync(0xffffffffu, over);
     if (m && (threadIdx.x & 31) == 0) atomicAdd(&a.err->overfull, (unsigned long long)__popc(m));
 }
@@ -184,6 +195,24 @@ __global__ void __launch_bounds__(256) covered_kernel(const uint8_t* __restrict_
                                                       unsigned* __restrict__ list, int* __restrict__ n) {
     const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     covered_append(c < cells ? count[c] : 0, (unsigned)c, list, cells, n);
+}
+
+// segment lists from an externally set fraction field (one thread per 32-cell row segment)
+__global__ void __launch_bounds__(256) segments_kernel(const uint8_t* __restrict__ count, int nx, long long rows,
+                                                       unsigned* __restrict__ seg_list, int* __restrict__ seg_n,
+                                                       long long seg_cap) {
+    const int per_row = (nx + 31) / 32;
+    const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= rows * per_row) return;
+    const long long row = s / per_row;
+    const int i0 = (int)(s % per_row) * 32;
+    const long long c0 = row * nx + i0;
+    int mx = 0;
+    for (int i = 0; i < 32 && i0 + i < nx; ++i) mx = max(mx, (int)count[c0 + i]);
+    if (mx == 1)
+        seg_list[atomicAdd(&seg_n[0], 1)] = (unsigned)c0;
+    else if (mx >= 2)
+        seg_list[seg_cap - 1 - atomicAdd(&seg_n[1], 1)] = (unsigned)c0;
 }
 
 __device__ __forceinline__ int find_snapshot(const lbg_snapshot* s, int n, int id) {
@@ -386,6 +415,12 @@ lbg_status rebuild_covered(lbg_block b) {
     LBG_CUDA(cudaMemsetAsync(b->cov_n, 0, 2 * sizeof(int), b->stream));
     covered_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, b->stream>>>(b->count, cells, b->cov_list, b->cov_n);
     LBG_LAUNCH_CHECK();
+    const long long rows = (long long)b->L.ny * b->L.nz;
+    const long long nseg = rows * ((b->L.nx + 31) / 32);
+    LBG_CUDA(cudaMemsetAsync(b->seg_n, 0, 2 * sizeof(int), b->stream));
+    segments_kernel<<<(unsigned)((nseg + 255) / 256), 256, 0, b->stream>>>(b->count, b->L.nx, rows, b->seg_list,
+                                                                           b->seg_n, b->seg_cap);
+    LBG_LAUNCH_CHECK();
     b->cov_dirty = false;
     return LBG_OK;
 }
@@ -492,7 +527,11 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
     a.with_velocity = 1;
     a.cov_list = b->cov_list;
     a.cov_n = b->cov_n;
+    a.seg_list = b->seg_list;
+    a.seg_n = b->seg_n;
+    a.seg_cap = b->seg_cap;
     LBG_CUDA(cudaMemsetAsync(b->cov_n, 0, 2 * sizeof(int), b->stream));
+    LBG_CUDA(cudaMemsetAsync(b->seg_n, 0, 2 * sizeof(int), b->stream));
     dim3 grid((g.dims[0] + 127) / 128, g.dims[1], g.dims[2]);
     map_kernel<<<grid, 128, 0, b->stream>>>(a);
     LBG_LAUNCH_CHECK();
@@ -579,21 +618,27 @@ lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int c
         if (lbg_status s = rebuild_covered(b)) return s;
     {
         Span span(b, LBG_CAT_REDF);
-        int cn[2] = {0, 0};
-        LBG_CUDA(cudaMemcpyAsync(cn, b->cov_n, sizeof(cn), cudaMemcpyDeviceToHost, b->stream));
+        if (!b->cn_h) LBG_CUDA(cudaMallocHost(&b->cn_h, 2 * sizeof(int)));  // pinned: no staged copy
+        LBG_CUDA(cudaMemcpyAsync(b->cn_h, b->cov_n, 2 * sizeof(int), cudaMemcpyDeviceToHost, b->stream));
         LBG_CUDA(cudaStreamSynchronize(b->stream));
+        const int cn[2] = {b->cn_h[0], b->cn_h[1]};
         const long long ne = (long long)cn[0] + 2LL * cn[1];
-        if (ne > b->ekeys_cap) {
-            for (auto& k : b->ekeys)
-                if (k) cudaFree(k);
-            b->ekeys_cap = std::max(ne, 2 * b->ekeys_cap);
+        if (!b->ekeys[0]) {
+            // sized once for the worst case (two entries per cell): steady-state steps never
+            // allocate (cudaFree/cudaMalloc serialise all block-worker threads of a process)
+            b->ekeys_cap = std::max(2 * cells, 1LL);
             LBG_CUDA(cudaMalloc(&b->ekeys[0], sizeof(unsigned long long) * b->ekeys_cap));
             LBG_CUDA(cudaMalloc(&b->ekeys[1], sizeof(unsigned long long) * b->ekeys_cap));
+            size_t tmp = 0;
+            cub::DeviceRadixSort::SortKeys(nullptr, tmp, b->ekeys[0], b->ekeys[1], (int)b->ekeys_cap, 0, 64,
+                                           b->stream);
+            LBG_CUDA(cudaMalloc(&b->sort_tmp, tmp));
+            b->sort_tmp_bytes = tmp;
         }
-        if (std::max(n, 1) > b->seg_cap) {
-            if (b->seg) cudaFree(b->seg);
-            b->seg_cap = std::max(std::max(n, 1), 2 * b->seg_cap);
-            LBG_CUDA(cudaMalloc(&b->seg, sizeof(int) * 2 * b->seg_cap));
+        if (std::max(n, 1) > b->red_seg_cap) {
+            if (b->red_seg) cudaFree(b->red_seg);
+            b->red_seg_cap = std::max(std::max(n, 1), 2 * b->red_seg_cap);
+            LBG_CUDA(cudaMalloc(&b->red_seg, sizeof(int) * 2 * b->red_seg_cap));
         }
         if (ne > 0) {
             entry_keys_kernel<<<(unsigned)((cn[0] + cn[1] + 255) / 256), 256, 0, b->stream>>>(
@@ -614,8 +659,8 @@ lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int c
             LBG_LAUNCH_CHECK();
         }
         if (n > 0) {
-            int* start = b->seg;
-            int* end = b->seg + b->seg_cap;
+            int* start = b->red_seg;
+            int* end = b->red_seg + b->red_seg_cap;
             LBG_CUDA(cudaMemsetAsync(start, 0, sizeof(int) * n, b->stream));
             LBG_CUDA(cudaMemsetAsync(end, 0, sizeof(int) * n, b->stream));
             if (ne > 0) {

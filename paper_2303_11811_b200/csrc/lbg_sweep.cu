@@ -12,11 +12,13 @@
 //                    aligned to 32 cells, so a warp's loads/stores of a q-plane are two 128-B
 //                    lines (the pulled x-neighbour costs one extra sector per warp, from L2).
 //   K1 sweep_flat  — up to 8 boxes in one launch (the boundary_shell boxes, field.cpp:55-72).
-//   K2 psm_list    — the covered cells (count > 0) of a coupled block, from the compacted list
-//                    the mapping kernel writes. In a coupled block K1 skips covered cells, so
-//                    the SRT kernel keeps ~70 registers (3 CTAs/SM) instead of the ~210 the
-//                    fused PSM operator needs (the A100 kernel of the paper ran at 196 regs,
-//                    12.5% occupancy); only the covered minority pays for them.
+//   K2 psm_seg     — the aligned 32-cell row segments that hold covered cells (count > 0),
+//                    from the segment lists the mapping kernel writes; K1 skips exactly those
+//                    segments, so each DRAM sector is swept by one kernel. Segments with only
+//                    one-entry cells use the pair-scheduled operator (~80 registers), segments
+//                    with a two-entry cell the general one (~170); the fluid majority keeps the
+//                    70-register SRT kernel (the paper's fused A100 kernel ran at 196 registers,
+//                    12.5 % occupancy).
 // Periodic wrap: for axes in b->wrap the pull reads the wrapped interior cell directly
 // (what fill_periodic_ghosts would have copied into the ghost slot), so a fully periodic
 // single-GPU step is one launch with no ghost fill.
@@ -47,6 +49,9 @@ struct SweepArgs {
     const unsigned* __restrict__ cov_list;  // one-entry cells from the front, two-entry from the back
     const int* __restrict__ cov_n;          // [0] one-entry count, [1] two-entry count
     long long cov_cap;
+    const unsigned* __restrict__ seg_list;  // covered 32-cell row segments: max count 1 front, 2 back
+    const int* __restrict__ seg_n;
+    long long seg_cap;
     const int* __restrict__ id0;
     const int* __restrict__ id1;
     // fused force reduction (LBG_FORCE_FUSED)
@@ -140,7 +145,13 @@ __global__ void __launch_bounds__(256) sweep_box_kernel(const SweepArgs a) {
     const int k = a.lo[2] + blockIdx.z;
     const bool active = i >= a.lo[0] && i < a.hi[0] && j < a.hi[1];
     bool ok = true;
-    if (active) ok = srt_cell_at<kForced, kSkipCovered>(a, i, j, k);
+    if constexpr (kSkipCovered) {
+        // a warp is one aligned 32-cell row segment; a segment holding any covered cell is
+        // swept whole by K2 (psm_seg kernels), so no DRAM sector is touched by both kernels
+        const bool cov = i < a.L.nx && j < a.L.ny && a.count[a.L.frac(i, j, k)] != 0;
+        if (__any_sync(0xffffffffu, cov)) return;
+    }
+    if (active) ok = srt_cell_at<kForced, false>(a, i, j, k);
     count_bad(a.err, !ok);
 }
 
@@ -221,72 +232,50 @@ __device__ __forceinline__ void fused_accumulate(const SweepArgs& a, int p, cons
     }
 }
 
-// K2a: one-entry covered cells (front of the list), pair-scheduled operator (psm_cell_one)
-template <bool kForced, bool kFused>
-__global__ void __launch_bounds__(128) psm_one_kernel(const SweepArgs a) {
-    const int n = a.cov_n[0];
-    const int stride = gridDim.x * blockDim.x;
+// K2: one warp per covered 32-cell row segment (segment lists written by the mapping kernel).
+// Each lane takes its cell through SRT (count 0), the pair-scheduled one-entry operator
+// (count 1) or — in segments holding a two-entry cell (kTwo) — the general operator. K1 skips
+// exactly these segments, so every DRAM sector of the PDF planes is read and written once.
+template <bool kForced, bool kFused, bool kTwo>
+__global__ void __launch_bounds__(128) psm_seg_kernel(const SweepArgs a) {
+    const int nseg = kTwo ? a.seg_n[1] : a.seg_n[0];
+    const int lane = threadIdx.x & 31;
+    const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
     const Layout& L = a.L;
-    for (int base0 = blockIdx.x * blockDim.x; base0 < n; base0 += stride) {
-        const int t = base0 + threadIdx.x;
+    for (int s = warp; s < nseg; s += nwarps) {
+        const unsigned c0 = kTwo ? a.seg_list[a.seg_cap - 1 - s] : a.seg_list[s];
+        const int i = (int)(c0 % (unsigned)L.nx) + lane;
+        const int j = (int)((c0 / (unsigned)L.nx) % (unsigned)L.ny);
+        const int k = (int)(c0 / ((unsigned)L.nx * (unsigned)L.ny));
         bool ok = true;
-        double m[3] = {0, 0, 0};
+        int cnt = 0;
+        double m[2][3] = {{0, 0, 0}, {0, 0, 0}};
         double cc[3] = {0, 0, 0};
-        int p0 = -1;
-        if (t < n) {
-            const unsigned c = a.cov_list[t];
-            const int i = (int)(c % (unsigned)L.nx);
-            const int j = (int)((c / (unsigned)L.nx) % (unsigned)L.ny);
-            const int k = (int)(c / ((unsigned)L.nx * (unsigned)L.ny));
-            if (in_boxes(a, i, j, k)) {
+        int p0 = -1, p1 = -1;
+        if (i < L.nx && in_boxes(a, i, j, k)) {
+            const long long fc = L.frac(i, j, k);
+            cnt = a.count[fc];
+            if (cnt == 0) {
+                ok = srt_cell_at<kForced, false>(a, i, j, k);
+            } else if constexpr (!kTwo) {
                 const long long base = L.idx(i, j, k);
                 double f[kQ];
                 pull(a, i, j, k, base, f);
-                ok = psm_cell_one<kForced>(f, a.inv_tau, a.F, a.btot[c], a.b0[c], a.v0[3 * (size_t)c],
-                                           a.v0[3 * (size_t)c + 1], a.v0[3 * (size_t)c + 2], a.dst, L.plane,
-                                           base, m);
-                if constexpr (kFused) {
-                    cc[0] = (double)(a.blk_lo[0] + i) + 0.5;
-                    cc[1] = (double)(a.blk_lo[1] + j) + 0.5;
-                    cc[2] = (double)(a.blk_lo[2] + k) + 0.5;
-                    p0 = snapshot_of(a, a.id0[c]);
-                    if (p0 < 0) atomicAdd(&a.err->unknown, 1ull);
-                } else {
-                    for (int d = 0; d < 3; ++d) a.m0[3 * (size_t)c + d] = m[d];
-                }
-            }
-        }
-        count_bad(a.err, !ok);
-        if constexpr (kFused) fused_accumulate(a, p0, m, cc);
-    }
-}
-
-// K2b: two-entry covered cells (back of the list), general operator (psm_cell_opt)
-template <bool kForced, bool kFused>
-__global__ void __launch_bounds__(128) psm_list_kernel(const SweepArgs a) {
-    const int n = a.cov_n[1];
-    const int stride = gridDim.x * blockDim.x;
-    const Layout& L = a.L;
-    for (int base = blockIdx.x * blockDim.x; base < n; base += stride) {
-        const int t = base + threadIdx.x;
-        bool ok = true;
-        int cnt = 0;
-        double m[2][3];
-        double cc[3] = {0, 0, 0};
-        int p0 = -1, p1 = -1;
-        if (t < n) {
-            const unsigned c = a.cov_list[a.cov_cap - 1 - t];
-            const int i = (int)(c % (unsigned)L.nx);
-            const int j = (int)((c / (unsigned)L.nx) % (unsigned)L.ny);
-            const int k = (int)(c / ((unsigned)L.nx * (unsigned)L.ny));
-            if (in_boxes(a, i, j, k)) {
+                ok = psm_cell_one<kForced>(f, a.inv_tau, a.F, a.btot[fc], a.b0[fc], a.v0[3 * fc], a.v0[3 * fc + 1],
+                                           a.v0[3 * fc + 2], a.dst, L.plane, base, m[0]);
+                if constexpr (!kFused)
+                    for (int d = 0; d < 3; ++d) a.m0[3 * fc + d] = m[0][d];
+            } else {
                 ok = psm_cell_at<kForced, kFused>(a, i, j, k, cnt, m);
-                if constexpr (kFused) {
+            }
+            if constexpr (kFused) {
+                if (cnt > 0) {
                     cc[0] = (double)(a.blk_lo[0] + i) + 0.5;
                     cc[1] = (double)(a.blk_lo[1] + j) + 0.5;
                     cc[2] = (double)(a.blk_lo[2] + k) + 0.5;
-                    p0 = snapshot_of(a, a.id0[c]);
-                    if (cnt > 1) p1 = snapshot_of(a, a.id1[c]);
+                    p0 = snapshot_of(a, a.id0[fc]);
+                    if (cnt > 1) p1 = snapshot_of(a, a.id1[fc]);
                     if (p0 < 0 || (cnt > 1 && p1 < 0)) atomicAdd(&a.err->unknown, 1ull);
                 }
             }
@@ -378,6 +367,9 @@ static SweepArgs make_args(lbg_block b, const lbg_fluid* fl) {
         a.cov_list = b->cov_list;
         a.cov_n = b->cov_n;
         a.cov_cap = (long long)b->L.nx * b->L.ny * b->L.nz;
+        a.seg_list = b->seg_list;
+        a.seg_n = b->seg_n;
+        a.seg_cap = b->seg_cap;
         a.id0 = b->id0;
         a.id1 = b->id1;
         a.snaps = b->snaps_d;
@@ -427,21 +419,21 @@ static void launch_psm_list(lbg_block b, const SweepArgs& a, bool forced) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, b->device);
     const bool fused = b->force_mode == LBG_FORCE_FUSED;
-    // one-entry cells (the bulk): lean pair-scheduled kernel, more CTAs per SM
+    // segments with one-entry cells only (the bulk): lean pair-scheduled operator
     if (forced)
-        fused ? psm_one_kernel<true, true><<<sms * 8, 128, 0, b->stream>>>(a)
-              : psm_one_kernel<true, false><<<sms * 8, 128, 0, b->stream>>>(a);
+        fused ? psm_seg_kernel<true, true, false><<<sms * 8, 128, 0, b->stream>>>(a)
+              : psm_seg_kernel<true, false, false><<<sms * 8, 128, 0, b->stream>>>(a);
     else
-        fused ? psm_one_kernel<false, true><<<sms * 8, 128, 0, b->stream>>>(a)
-              : psm_one_kernel<false, false><<<sms * 8, 128, 0, b->stream>>>(a);
+        fused ? psm_seg_kernel<false, true, false><<<sms * 8, 128, 0, b->stream>>>(a)
+              : psm_seg_kernel<false, false, false><<<sms * 8, 128, 0, b->stream>>>(a);
     count_launch();
-    // two-entry cells (particle contacts)
+    // segments holding a two-entry cell (particle contacts): general operator
     if (forced)
-        fused ? psm_list_kernel<true, true><<<sms * 4, 128, 0, b->stream>>>(a)
-              : psm_list_kernel<true, false><<<sms * 4, 128, 0, b->stream>>>(a);
+        fused ? psm_seg_kernel<true, true, true><<<sms * 4, 128, 0, b->stream>>>(a)
+              : psm_seg_kernel<true, false, true><<<sms * 4, 128, 0, b->stream>>>(a);
     else
-        fused ? psm_list_kernel<false, true><<<sms * 4, 128, 0, b->stream>>>(a)
-              : psm_list_kernel<false, false><<<sms * 4, 128, 0, b->stream>>>(a);
+        fused ? psm_seg_kernel<false, true, true><<<sms * 4, 128, 0, b->stream>>>(a)
+              : psm_seg_kernel<false, false, true><<<sms * 4, 128, 0, b->stream>>>(a);
 }
 
 }  // namespace lbg
