@@ -93,6 +93,14 @@ public:
                                     f.b1.data(), f.btot.data()));
     }
 
+    /// Per-cell {rho, mx, my, mz, btot} (lbg_moments), the input of the observers below.
+    void moments(std::vector<double>& out) const {
+        int dims[3];
+        check(lbg_block_info(b_, dims, nullptr, nullptr, nullptr));
+        out.resize(static_cast<std::size_t>(dims[0]) * dims[1] * dims[2] * 5);
+        check(lbg_moments(b_, 1, out.data()));
+    }
+
     void pack_slab(const Vec3i& off, std::vector<double>& values) const {
         long long n = 0;
         const int o[3] = {off.x, off.y, off.z};

@@ -220,6 +220,16 @@ lbg_status lbg_total_momentum(lbg_block b, double out[3]);
  * sum 0.5 rho |u|^2 and max |u| with the observable u = m + f_ext/2 (lbm.hpp:55-63)}.
  * Compensated, deterministic for a given device; not bitwise equal to the serial order. */
 lbg_status lbg_observe(lbg_block b, const double f_ext[3], double out[6]);
+/* Per-cell moments of the src interior for observers and grid dumps, replacing the host
+ * walks over the PDF field in lbm::cell_macroscopic / total_mass / total_momentum
+ * (lbm.cpp:61-93) and io::sample_scalars / write_grid_dump (output.cpp:22-107).
+ * out[c*S + 0..3] = {rho, mx, my, mz}: rho = sum f_q and m = sum f_q c_q in q order, bitwise
+ * the reference's sums; the observable velocity is m / 1.0 + 0.5 * f_ext (lbm.hpp:62), done
+ * by the caller. With with_frac, S = 5 and out[c*S + 4] = btot (0 for an uncoupled block,
+ * as write_grid_dump prints). Cells c = (k*ny + j)*nx + i. `out`: host memory of
+ * nx*ny*nz*S doubles (pinned is faster). Blocking; 32-40 B per cell cross PCIe instead of
+ * the 152 B of the populations. */
+lbg_status lbg_moments(lbg_block b, int with_frac, double* out);
 
 /* ------------------------------------------------------------------ halo exchange */
 /* Simulation::begin/complete_halo_exchange (sim.cpp:156-201) for a slab decomposition

@@ -45,6 +45,8 @@ def load(path: str = SO):
         L.dropin_sim_shear_wave.argtypes = [vp]
         L.dropin_sim_reset_timers.argtypes = [vp]
         L.dropin_sim_timings.argtypes = [vp, dp]
+        L.dropin_sim_observe.argtypes = [vp, dp]
+        L.dropin_sim_grid_dump.argtypes = [vp, C.c_char_p]
         _lib = L
     return _lib
 
@@ -90,6 +92,15 @@ class DropinSim:
 
     def mass(self):
         return self.L.dropin_sim_mass(self.h)
+
+    def observe(self):
+        """io::sample_scalars: [step, mass, px, py, pz, fluid_ke, particle_ke, min_gap, max_u]."""
+        out = np.zeros(9)
+        self._check(self.L.dropin_sim_observe(self.h, out))
+        return out
+
+    def grid_dump(self, path):
+        self._check(self.L.dropin_sim_grid_dump(self.h, str(path).encode()))
 
     def reset_timers(self):
         self.L.dropin_sim_reset_timers(self.h)

@@ -12,6 +12,7 @@
 
 #include "lbdem/config.hpp"
 #include "lbdem/errors.hpp"
+#include "lbdem/output.hpp"
 #include "lbdem/perf.hpp"
 #include "lbdem/scenario.hpp"
 #include "lbdem/sim.hpp"
@@ -134,8 +135,25 @@ int dropin_sim_shear_wave(void* h) {
                         for (int q = 0; q < lbm::kQ; ++q) blk.field.src(q)[base] = feq[q];
                     }
             blk.dev->upload_src(blk.field);
+            blk.moments_stale = true;
         }
     });
+}
+
+/// io::sample_scalars (output.cpp:22-61): step, mass, momentum xyz, fluid KE, particle KE,
+/// min gap, max |u| — through the drop-in observers (device moments).
+int dropin_sim_observe(void* h, double out[9]) {
+    return guarded([&] {
+        const io::ScalarSample s = io::sample_scalars(*R(h)->sim);
+        const double v[9] = {static_cast<double>(s.step), s.mass, s.momentum.x, s.momentum.y,
+                             s.momentum.z, s.fluid_ke, s.particle_ke, s.min_gap, s.max_u};
+        for (int a = 0; a < 9; ++a) out[a] = v[a];
+    });
+}
+
+/// io::write_grid_dump (output.cpp:76-107) of the current state to `path`.
+int dropin_sim_grid_dump(void* h, const char* path) {
+    return guarded([&] { io::write_grid_dump(*R(h)->sim, path); });
 }
 
 void dropin_sim_reset_timers(void* h) { R(h)->sim->reset_timers(); }

@@ -4,8 +4,8 @@ This is what a maintainer of the reference does: the host progr
 Simulation's phase structure, DEM, particle messaging, partial routing, config, scenarios —
 stays the reference's own code, and the call sites of the fluid/coupling operators in
 sim.cpp / the fields in sim.hpp's BlockState are pointed at lbdem::gpu::DeviceBlock
-(include/lbdem_gpu.hpp). The edits are applied to copies of the two files in
-integration/_build/ (git-ignored; no reference source enters the repository); every other
+(include/lbdem_gpu.hpp). The edits are applied to copies of those files (and of output.cpp, whose observers read
+device moments) in integration/_build/ (git-ignored; no reference source enters the repository); every other
 reference source compiles unmodified from /root/reference.
 
     python integration/make_dropin.py      # -> integration/_build/liblbdem_dropin.so
@@ -28,13 +28,15 @@ SIM_HPP_EDITS = [
     ("    bool halo_pending = false;\n",
      "    bool halo_pending = false;\n"
      "    std::shared_ptr<gpu::DeviceBlock> dev;  ///< liblbg block (drop-in)\n"
-     "    mutable bool host_stale = false;        ///< host field copy behind the device\n"),
+     "    mutable bool host_stale = false;        ///< host field copy behind the device\n"
+     "    mutable std::vector<double> moments;    ///< device moments cache (observers)\n"
+     "    mutable bool moments_stale = true;\n"),
 ]
 
 SIM_CPP_EDITS = [
     # includes + host-copy refresh used by the observers
     ("#include <set>\n",
-     "#include <set>\n#include <cstdlib>\n\n#include \"lbdem_gpu.hpp\"\n"),
+     "#include <set>\n#include <cstdlib>\n\n#include \"lbdem_gpu.hpp\"\n#include \"dropin_observe.hpp\"\n"),
     ("namespace lbdem {\n\nusing partition::MsgKind;",
      "namespace lbdem {\n\n"
      "namespace {\n"
@@ -84,6 +86,7 @@ SIM_CPP_EDITS = [
      "    for (auto& blk : blocks_) {\n"
      "        if (host_mirror()) blk->field.fill_src(feq);\n"
      "        blk->dev->initialize_fluid(rho, u);\n"
+     "        blk->moments_stale = true;\n"
      "    }\n"),
     # sim.cpp:156-158 — halo begin: stage the source slabs on the device (no host copy); the
     # message-bus path below stays available with LBDEM_GPU_HALO=host
@@ -173,30 +176,47 @@ SIM_CPP_EDITS = [
      "        blk.dev->sync();\n"
      "    }\n"
      "    blk.dev->swap();\n"
-     "    blk.host_stale = true;\n"),
+     "    blk.host_stale = true;\n"
+     "    blk.moments_stale = true;\n"),
     # sim.cpp:321 — finalize_hydro_forces on the device (PARITY: bitwise partials)
     ("    auto partials = psm::finalize_hydro_forces(blk.frac, blk.scratch, blk.box, blk.snapshots);\n",
      "    auto partials = blk.dev->finalize_hydro_forces();\n"),
-    # sim.cpp:740-772 — observers read refreshed host copies
-    ("double Simulation::total_fluid_mass() const {\n",
-     "double Simulation::total_fluid_mass() const {\n    refresh_host(blocks_, params_.coupling);\n"),
-    ("Vec3 Simulation::total_fluid_momentum() const {\n",
-     "Vec3 Simulation::total_fluid_momentum() const {\n    refresh_host(blocks_, params_.coupling);\n"),
-    ("void Simulation::macroscopic_at(const Vec3i& cell, double& rho, Vec3& u) const {\n",
-     "void Simulation::macroscopic_at(const Vec3i& cell, double& rho, Vec3& u) const {\n"
-     "    refresh_host(blocks_, params_.coupling);\n"),
+    # sim.cpp:740-772 — observers: mass, momentum, macroscopic_at and fraction_at from the
+    # device moments (dropin_observe.hpp, bitwise the reference's sums, no host mirror);
+    # pdf_at still reads the refreshed host copy of the populations
+    ("    for (const auto& blk : blocks_) m.add(lbm::total_mass(blk->field));\n",
+     "    for (const auto& blk : blocks_) m.add(gpu::total_mass(*blk));\n"),
+    ("    for (const auto& blk : blocks_) mom.add(lbm::total_momentum(blk->field));\n",
+     "    for (const auto& blk : blocks_) mom.add(gpu::total_momentum(*blk));\n"),
+    ("    lbm::cell_macroscopic(blk.field, params_.fluid.f_ext, cell.x - blk.box.lo.x,\n",
+     "    gpu::cell_macroscopic(blk, params_.fluid.f_ext, cell.x - blk.box.lo.x,\n"),
     ("double Simulation::pdf_at(const Vec3i& cell, int q) const {\n",
      "double Simulation::pdf_at(const Vec3i& cell, int q) const {\n    refresh_host(blocks_, params_.coupling);\n"),
-    ("double Simulation::fraction_at(const Vec3i& cell) const {\n",
-     "double Simulation::fraction_at(const Vec3i& cell) const {\n    refresh_host(blocks_, params_.coupling);\n"),
+    ("    return blk.frac.btot[blk.frac.idx(cell.x - blk.box.lo.x, cell.y - blk.box.lo.y,\n"
+     "                                      cell.z - blk.box.lo.z)];\n",
+     "    return gpu::cell_fraction(blk, cell.x - blk.box.lo.x, cell.y - blk.box.lo.y,\n"
+     "                              cell.z - blk.box.lo.z);\n"),
+]
+
+
+# output.cpp:22-107 — sample_scalars and write_grid_dump read the device moments (the two
+# per-cell macroscopic calls are the same line; (anchor, replacement, occurrences))
+OUTPUT_CPP_EDITS = [
+    ('#include "lbdem/output.hpp"\n',
+     '#include "lbdem/output.hpp"\n#include "dropin_observe.hpp"\n', 1),
+    ("lbm::cell_macroscopic(blk.field, sim.params().fluid.f_ext, i, j, k, rho, u);\n",
+     "gpu::cell_macroscopic(blk, sim.params().fluid.f_ext, i, j, k, rho, u);\n", 2),
+    ("sim.params().coupling ? blk.frac.btot[blk.frac.idx(i, j, k)] : 0.0;\n",
+     "sim.params().coupling ? gpu::cell_fraction(blk, i, j, k) : 0.0;\n", 1),
 ]
 
 
 def patch(src, edits, name):
     text = open(src).read()
-    for anchor, repl in edits:
-        if text.count(anchor) != 1:
-            sys.exit(f"{name}: anchor not found exactly once:\n{anchor}")
+    for e in edits:
+        anchor, repl, n = e if len(e) == 3 else (*e, 1)
+        if text.count(anchor) != n:
+            sys.exit(f"{name}: anchor not found exactly {n}x:\n{anchor}")
         text = text.replace(anchor, repl)
     return text
 
@@ -210,7 +230,9 @@ def main():
     os.makedirs(os.path.join(BUILD, "src"), exist_ok=True)
     hpp = patch(os.path.join(REF, "include/lbdem/sim.hpp"), SIM_HPP_EDITS, "sim.hpp")
     cpp = patch(os.path.join(REF, "src/sim.cpp"), SIM_CPP_EDITS, "sim.cpp")
-    for path, text in ((os.path.join(BUILD, "include/lbdem/sim.hpp"), hpp), (os.path.join(BUILD, "src/sim.cpp"), cpp)):
+    out = patch(os.path.join(REF, "src/output.cpp"), OUTPUT_CPP_EDITS, "output.cpp")
+    for path, text in ((os.path.join(BUILD, "include/lbdem/sim.hpp"), hpp), (os.path.join(BUILD, "src/sim.cpp"), cpp),
+                       (os.path.join(BUILD, "src/output.cpp"), out)):
         if not os.path.exists(path) or open(path).read() != text:
             open(path, "w").write(text)
     subprocess.check_call(["make", "-s", "-j8", "-C", HERE, f"REF={REF}"])

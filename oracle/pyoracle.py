@@ -23,6 +23,11 @@ _u8 = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
 _i3 = C.c_int * 3
 _d3 = C.c_double * 3
 
+# D3Q19 velocity set in the reference's order (lattice.hpp:18-29: rest, then opposite pairs)
+LATTICE_C = [(0, 0, 0), (1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1),
+             (1, 1, 0), (-1, -1, 0), (1, -1, 0), (-1, 1, 0), (1, 0, 1), (-1, 0, -1),
+             (1, 0, -1), (-1, 0, 1), (0, 1, 1), (0, -1, -1), (0, 1, -1), (0, -1, 1)]
+
 # status codes shared with include/lbg.h and oracle/ref_shim.cpp
 CONFIG_ERROR, NUMERIC_ERROR, SYNC_ERROR, IO_ERROR = 1, 2, 3, 4
 
@@ -118,6 +123,25 @@ class Oracle:
     def total_momentum(self, dims, src):
         out = np.zeros(3)
         self.L.orc_total_momentum(*dims, src, out)
+        return out
+
+    @staticmethod
+    def moments(dims, src):
+        """Per-cell {rho, mx, my, mz}, shape (nz, ny, nx, 4), in the reference's sum order:
+        rho = 0 + f_0 + ... + f_18, m = 0 + f_q * c_q for q = 0..18 (lbm.hpp:55-60,
+        lbm.cpp:61-67 / 82-91). Elementwise numpy, so each cell's arithmetic is exactly that."""
+        nx, ny, nz = dims
+        f = src[:, 1:nz + 1, 1:ny + 1, 1:nx + 1]
+        out = np.zeros((nz, ny, nx, 4))
+        rho = np.zeros((nz, ny, nx))
+        m = [np.zeros((nz, ny, nx)) for _ in range(3)]
+        for q in range(19):
+            rho = rho + f[q]
+            for a in range(3):
+                m[a] = m[a] + f[q] * float(LATTICE_C[q][a])
+        out[..., 0] = rho
+        for a in range(3):
+            out[..., 1 + a] = m[a]
         return out
 
     # -- coupling ------------------------------------------------------------
@@ -261,6 +285,8 @@ class RefLib:
         L.ref_sim_particles.argtypes = [vp, _dp]
         L.ref_sim_mass.restype = C.c_double
         L.ref_sim_mass.argtypes = [vp]
+        L.ref_sim_observe.argtypes = [vp, _dp]
+        L.ref_sim_grid_dump.argtypes = [vp, C.c_char_p]
         L.ref_sim_reset_timers.argtypes = [vp]
         L.ref_sim_timings.argtypes = [vp, _dp]
         L.ref_set_threads.argtypes = [C.c_int]
@@ -420,6 +446,15 @@ class RefSim:
 
     def mass(self):
         return self.L.ref_sim_mass(self.h)
+
+    def observe(self):
+        """io::sample_scalars: [step, mass, px, py, pz, fluid_ke, particle_ke, min_gap, max_u]."""
+        out = np.zeros(9)
+        self.lib.check(self.L.ref_sim_observe(self.h, out))
+        return out
+
+    def grid_dump(self, path):
+        self.lib.check(self.L.ref_sim_grid_dump(self.h, str(path).encode()))
 
     def reset_timers(self):
         self.L.ref_sim_reset_timers(self.h)

@@ -28,6 +28,7 @@
 #include "lbdem/errors.hpp"
 #include "lbdem/field.hpp"
 #include "lbdem/lbm.hpp"
+#include "lbdem/output.hpp"
 #include "lbdem/perf.hpp"
 #include "lbdem/psm.hpp"
 #include "lbdem/scenario.hpp"
@@ -385,6 +386,22 @@ void ref_sim_particles(void* h, double* rows) {
 }
 
 double ref_sim_mass(void* h) { return static_cast<RefSim*>(h)->sim->total_fluid_mass(); }
+
+/// io::sample_scalars (output.cpp:22-61): step, mass, momentum xyz, fluid KE, particle KE,
+/// min gap, max |u|.
+int ref_sim_observe(void* h, double out[9]) {
+    return guarded([&] {
+        const io::ScalarSample s = io::sample_scalars(*static_cast<RefSim*>(h)->sim);
+        const double v[9] = {static_cast<double>(s.step), s.mass, s.momentum.x, s.momentum.y,
+                             s.momentum.z, s.fluid_ke, s.particle_ke, s.min_gap, s.max_u};
+        for (int a = 0; a < 9; ++a) out[a] = v[a];
+    });
+}
+
+/// io::write_grid_dump (output.cpp:76-107).
+int ref_sim_grid_dump(void* h, const char* path) {
+    return guarded([&] { io::write_grid_dump(*static_cast<RefSim*>(h)->sim, path); });
+}
 
 void ref_sim_reset_timers(void* h) { static_cast<RefSim*>(h)->sim->reset_timers(); }
 

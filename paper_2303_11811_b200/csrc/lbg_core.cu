@@ -234,6 +234,36 @@ __global__ void __launch_bounds__(kObsThreads) observe_kernel(const double* __re
     }
 }
 
+// ---- per-cell moments for observers and grid dumps (lbm.hpp:55-63 macroscopic before the
+// f_ext shift, lbm.cpp:61-93): rho = 0 + f_0 + ... + f_18 and m = 0 + f_q c_q in q order,
+// i.e. the reference's own sums (the c_q = 0 terms add a signed zero to a partial sum that
+// starts at +0, which never changes it). One thread per cell of a z-chunk, AoS output in the
+// reference's lexicographic cell order; btot appended when the block is coupled.
+__global__ void moments_kernel(const double* __restrict__ src, Layout L, int k0, int nk,
+                               const double* __restrict__ btot, int with_frac, double* __restrict__ out) {
+    const long long slice = (long long)L.nx * L.ny;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= slice * nk) return;
+    const int i = (int)(t % L.nx), j = (int)((t / L.nx) % L.ny), k = k0 + (int)(t / slice);
+    const long long base = L.idx(i, j, k);
+    double rho = 0.0, mx = 0.0, my = 0.0, mz = 0.0;
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+        const double f = src[q * L.plane + base];
+        rho += f;
+        if (cx(q) == 1) mx += f; else if (cx(q) == -1) mx -= f;
+        if (cy(q) == 1) my += f; else if (cy(q) == -1) my -= f;
+        if (cz(q) == 1) mz += f; else if (cz(q) == -1) mz -= f;
+    }
+    const int stride = with_frac ? 5 : 4;
+    double* o = out + t * stride;
+    o[0] = rho;
+    o[1] = mx;
+    o[2] = my;
+    o[3] = mz;
+    if (with_frac) o[4] = btot ? btot[k * slice + (long long)j * L.nx + i] : 0.0;
+}
+
 }  // namespace lbg
 
 using namespace lbg;
@@ -276,6 +306,35 @@ lbg_status lbg_observe(lbg_block b, const double f_ext[3], double out[6]) {
     }
     for (int a = 0; a < kObsVals; ++a) out[a] = s[a] + c[a];
     out[5] = std::sqrt(mx);
+    return LBG_OK;
+}
+
+lbg_status lbg_moments(lbg_block b, int with_frac, double* out) {
+    if (!b || !out) return set_error(LBG_INVALID, "null argument");
+    LBG_CUDA(cudaSetDevice(b->device));
+    const Layout& L = b->L;
+    const int stride = with_frac ? 5 : 4;
+    const long long slice = (long long)L.nx * L.ny;
+    // z-chunks of at most ~64 MB staged on the device, copied out on the compute stream
+    const long long kz = std::max(1LL, std::min<long long>(L.nz, (8LL << 20) / (slice * stride)));
+    const size_t bytes = sizeof(double) * (size_t)(kz * slice * stride);
+    if (b->mom_cap < bytes) {
+        if (b->mom_d) LBG_CUDA(cudaFree(b->mom_d));
+        b->mom_d = nullptr;
+        LBG_CUDA(cudaMalloc(&b->mom_d, bytes));
+        b->mom_cap = bytes;
+    }
+    Span span(b, LBG_CAT_OTHER);
+    for (long long k0 = 0; k0 < L.nz; k0 += kz) {
+        const int nk = (int)std::min<long long>(kz, L.nz - k0);
+        const long long n = slice * nk;
+        moments_kernel<<<(unsigned)((n + 255) / 256), 256, 0, b->stream>>>(
+            b->src(), L, (int)k0, nk, with_frac ? b->btot : nullptr, with_frac, b->mom_d);
+        LBG_LAUNCH_CHECK();
+        LBG_CUDA(cudaMemcpyAsync(out + k0 * slice * stride, b->mom_d, sizeof(double) * n * stride,
+                                 cudaMemcpyDeviceToHost, b->stream));
+    }
+    LBG_CUDA(cudaStreamSynchronize(b->stream));
     return LBG_OK;
 }
 
@@ -391,7 +450,7 @@ lbg_status lbg_block_destroy(lbg_block b) {
     if (b->p2p) lbg_p2p_destroy(b);
     void* dev[] = {b->buf[0], b->buf[1], b->count, b->id0, b->id1, b->b0, b->b1, b->btot,
                    b->v0, b->v1, b->m0, b->m1, b->snaps_d, b->bin_count, b->bin_start,
-                   b->bin_items, b->red_rows, b->red_used, b->err_d, b->cov_list, b->cov_n, b->facc, b->fused_used, b->scan_tmp, b->obs_d,
+                   b->bin_items, b->red_rows, b->red_used, b->err_d, b->cov_list, b->cov_n, b->facc, b->fused_used, b->scan_tmp, b->obs_d, b->mom_d,
                    b->seg_list, b->seg_n};
     for (void* p : dev)
         if (p) cudaFree(p);

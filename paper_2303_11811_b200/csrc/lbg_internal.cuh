@@ -168,6 +168,8 @@ struct lbg_block_s {
     long long device_bytes = 0;
     double* obs_d = nullptr;  // observer partials (lbg_observe)
     double* obs_h = nullptr;
+    double* mom_d = nullptr;  // per-cell moments staging (lbg_moments)
+    size_t mom_cap = 0;
 
     // device-side generic halo (lbg_halo_stage / lbg_halo_fetch): staged source slabs per
     // neighbour offset (index (ox+1)*9+(oy+1)*3+(oz+1)), a receive buffer, a staging event

@@ -416,6 +416,15 @@ class Block:
         v = list(out)
         return {"mass": v[0], "momentum": np.array(v[1:4]), "fluid_ke": v[4], "max_u": v[5]}
 
+    def moments(self, with_frac=False) -> np.ndarray:
+        """Per-cell {rho, mx, my, mz[, btot]} of the src interior, shape (nz, ny, nx, 4|5):
+        the reference's own per-cell sums (lbm.cpp:61-93), for observers and grid dumps."""
+        nx, ny, nz = self.dims
+        S = 5 if with_frac else 4
+        out = np.empty((nz, ny, nx, S), dtype=np.float64)
+        check(_lib().lbg_moments(self.h, 1 if with_frac else 0, out.ctypes.data))
+        return out
+
     # halo
     def comm_init(self, nranks, rank, uid: bytes, axis=2, periodic=(1, 1, 1)):
         check(_lib().lbg_comm_init(self.h, nranks, rank, uid, axis,

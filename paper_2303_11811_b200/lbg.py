@@ -100,6 +100,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "lbg_total_mass": (st, [blk, d3]),
         "lbg_total_momentum": (st, [blk, d3]),
         "lbg_observe": (st, [blk, d3, d3]),
+        "lbg_moments": (st, [blk, C.c_int, vp]),
         "lbg_comm_unique_id": (st, [C.c_char_p]),
         "lbg_comm_init": (st, [blk, C.c_int, C.c_int, C.c_char_p, C.c_int, i3]),
         "lbg_comm_destroy": (st, [blk]),

@@ -64,6 +64,26 @@ def test_particle_bed_matches_reference(dropin, ref, blocks, workers):
     assert equal_bits(a.pdfs(), b.pdfs())
 
 
+@pytest.mark.parametrize("mirror", ["1", "0"])
+def test_observers_and_grid_dump_match_reference(dropin, ref, tmp_path, monkeypatch, mirror):
+    """§8(f) row 1: io::sample_scalars and io::write_grid_dump through the drop-in read the
+    device moments (lbg_moments, 40 B per cell) instead of the host PDF field — the scalar
+    series and the grid dump file are identical to the reference's, with or without a host
+    mirror of the populations."""
+    monkeypatch.setenv("LBDEM_GPU_HOST_MIRROR", mirror)
+    cfg = BED.format(nx=24, ny=20, nz=32, blocks=[2, 1, 2], workers=2, count=8, d=8)
+    a = dropin.DropinSim(cfg, (24, 20, 32))
+    b = ref.sim(cfg)
+    for steps in (1, 3):
+        a.run(steps)
+        b.run(steps)
+        assert equal_bits(a.observe(), b.observe())
+    a.grid_dump(tmp_path / "gpu.dat")
+    b.grid_dump(tmp_path / "ref.dat")
+    ga, gb = (tmp_path / "gpu.dat").read_bytes(), (tmp_path / "ref.dat").read_bytes()
+    assert len(ga) > 24 * 20 * 32 * 40 and ga == gb
+
+
 @pytest.mark.parametrize("halo", ["device", "host"])
 def test_decomposition_invariance_2x2x2(dropin, halo, monkeypatch):
     """Acceptance criterion 11 on the GPU: 2x2x2 device blocks (26-neighbour halo, device to

@@ -133,6 +133,45 @@ def test_in_kernel_periodic_wrap_bitwise(gpu, oracle, wrap, coupled):
         assert equal_bits(m0[c > 0], scr["m0"][c > 0])
 
 
+@pytest.mark.parametrize("dims", [(64, 4, 3), (66, 5, 3), (127, 3, 4), (130, 6, 3)])
+@pytest.mark.parametrize("wrap", [(0, 0, 0), (1, 1, 1), (1, 0, 0), (0, 1, 1)])
+def test_sweep_warp_edges_bitwise(gpu, oracle, dims, wrap):
+    """K1 at row lengths that end mid-warp / mid-pair, odd box origins and x-wrap on even and
+    odd nx (with LBG_SWEEP_PAIR=1 — test_pair_kernel_variant — the 128-bit pair kernel:
+    two cells per lane, x-neighbours by shuffle)."""
+    src0 = random_pdf(dims, seed=dims[0])
+    tau, fext = 0.81, (2e-6, -1e-6, 0.0)
+    boxes = [((0, 0, 0), dims), ((1, 1, 1), tuple(d - 1 for d in dims)),
+             ((3, 0, 1), (min(dims[0], 61), dims[1], dims[2]))]
+    for lo, hi in boxes:
+        src_o = src0.copy()
+        oracle.fill_periodic(dims, src_o, ALL_P)
+        dst_o = np.zeros_like(src_o)
+        oracle.collide_stream(dims, src_o, dst_o, tau, fext, lo, hi)
+        blk = gpu.Block(dims)
+        blk.upload_src(src0)
+        blk.set_periodic_wrap(wrap)
+        blk.fill_periodic(tuple(1 - w for w in wrap), full=False)
+        blk.sweep(gpu.FluidParams(tau, fext), gpu.CellBox(lo, hi))
+        blk.sync()
+        got = blk.download_dst()
+        assert n_bit_mismatch(interior(got), interior(dst_o)) == 0, (lo, hi)
+
+
+def test_pair_kernel_variant():
+    """The same edge cases through the 128-bit pair kernel (selected per process)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, LBG_SWEEP_PAIR="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        "test_gpu_parity.py::test_sweep_warp_edges_bitwise",
+                        "test_gpu_parity.py::test_fused_sweep_bitwise"], env=env,
+                       cwd=os.path.dirname(os.path.abspath(__file__)), capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
 def bed_spec(gpu, zm_vel=(0.0, 0.0, 2.2472e-3), rho_out=1.0):
     spec = gpu.BcSpec()
     for f in range(4):
@@ -199,6 +238,26 @@ def test_device_observers_match_sample_scalars(gpu, oracle):
     assert abs(obs["fluid_ke"] - ke) <= 1e-12 * ke
     assert abs(obs["max_u"] - np.sqrt(u2.max())) <= 1e-15
     assert abs(blk.total_mass() - mass) <= 1e-14 * mass
+
+
+@pytest.mark.parametrize("coupled", [False, True])
+def test_device_moments_bitwise(gpu, oracle, coupled):
+    """lbg_moments: per-cell {rho, mx, my, mz[, btot]} equal to the reference's per-cell sums
+    (lbm.cpp:61-93) bit for bit, so observers and grid dumps built on the host from 32-40 B
+    per cell reproduce total_mass / total_momentum / write_grid_dump exactly."""
+    dims = (37, 21, 19)
+    src = random_pdf(dims, seed=77)
+    blk = gpu.Block(dims, coupling=coupled)
+    blk.upload_src(src)
+    want = oracle.moments(dims, src)
+    if coupled:
+        frac, _ = random_fraction(dims, seed=8)
+        blk.upload_fraction(frac)
+    got = blk.moments(with_frac=True)
+    assert n_bit_mismatch(got[..., :4], want) == 0
+    btot = frac["btot"].reshape(dims[::-1]) if coupled else np.zeros(dims[::-1])
+    assert equal_bits(got[..., 4], btot)
+    assert n_bit_mismatch(blk.moments(with_frac=False), want) == 0
 
 
 def test_pinned_chunked_transfers_roundtrip(gpu):

@@ -196,3 +196,44 @@ def test_survey_known_answers_config1(ref):
     assert p[3] == ka["steps"]["10"]["x_z"]
     assert p[6] == ka["steps"]["10"]["u_z"]
     assert p[12] == ka["steps"]["10"]["f_hydro_z"]
+
+
+def _neumaier(values):
+    """CompensatedSum (vec3.hpp:71-95) in iteration order: Neumaier add, value = sum + comp."""
+    s = c = 0.0
+    for v in values:
+        t = s + v
+        c += (s - t) + v if abs(s) >= abs(v) else (v - t) + s
+        s = t
+    return s + c
+
+
+def test_moments_restatement_pinned_to_total_mass_momentum(oracle):
+    """Oracle.moments (per-cell rho and bare momentum, the sums of lbm.cpp:61-93) summed in the
+    reference's serial order reproduces total_mass / total_momentum of the C restatement
+    bitwise, which test_fused_sweep_matches_reference pins to the reference."""
+    dims = (7, 5, 6)
+    src = random_pdf(dims, seed=12)
+    mom = oracle.moments(dims, src).reshape(-1, 4)
+    assert equal_bits(np.float64(_neumaier(mom[:, 0])), np.float64(oracle.total_mass(dims, src)))
+    tm = oracle.total_momentum(dims, src)
+    for a in range(3):
+        assert equal_bits(np.float64(_neumaier(mom[:, 1 + a])), np.float64(tm[a]))
+
+
+def test_reference_observers_shim(ref):
+    """oracle/_ref exposes io::sample_scalars / write_grid_dump (the drop-in observer checks):
+    the sampled mass is the simulation's total_fluid_mass, the dump has one line per cell."""
+    import tempfile
+    ka = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "config1_known_answers.json")))
+    cfg = json.loads(ka["config"])
+    cfg["domain"] = [16, 16, 16]
+    cfg["particles"] = {"count": 0}
+    sim = ref.sim(json.dumps(cfg))
+    sim.run(1)
+    obs = sim.observe()
+    assert obs[0] == 1 and equal_bits(np.float64(obs[1]), np.float64(sim.mass()))
+    with tempfile.TemporaryDirectory() as d:
+        sim.grid_dump(os.path.join(d, "g.dat"))
+        lines = open(os.path.join(d, "g.dat")).read().splitlines()
+    assert lines[1] == "# columns: x y z rho ux uy uz B" and len(lines) == 2 + 16 ** 3
