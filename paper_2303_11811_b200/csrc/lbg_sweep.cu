@@ -345,7 +345,22 @@ __global__ void __launch_bounds__(128) psm_seg_kernel(const SweepArgs a) {
         if (i < L.nx && in_boxes(a, i, j, k)) {
             const long long fc = L.frac(i, j, k);
             cnt = a.count[fc];
-            if (cnt == 0) {
+            if (!kTwo && !kForced) {
+                // unforced one-entry segments: fluid lanes run the same operator with
+                // B = b = 0 and v = 0, which is collide_cell exactly (fluid weight 1 - 0 = 1,
+                // f + 1 * coll == f + coll, and the solid term adds 0 * C = +-0 to a nonzero
+                // value), so a mixed warp issues one operator instead of SRT and PSM in turn
+                const bool cov = cnt > 0;
+                const long long base = L.idx(i, j, k);
+                double f[kQ];
+                pull(a, i, j, k, base, f);
+                ok = psm_cell_one<kForced>(f, a.inv_tau, a.F, cov ? a.btot[fc] : 0.0, cov ? a.b0[fc] : 0.0,
+                                           cov ? a.v0[3 * fc] : 0.0, cov ? a.v0[3 * fc + 1] : 0.0,
+                                           cov ? a.v0[3 * fc + 2] : 0.0, a.dst, L.plane, base, m[0]);
+                if constexpr (!kFused)
+                    if (cov)
+                        for (int d = 0; d < 3; ++d) a.m0[3 * fc + d] = m[0][d];
+            } else if (cnt == 0) {
                 ok = srt_cell_at<kForced, false>(a, i, j, k);
             } else if constexpr (!kTwo) {
                 const long long base = L.idx(i, j, k);

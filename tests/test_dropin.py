@@ -71,8 +71,8 @@ def test_observers_and_grid_dump_match_reference(dropin, ref, tmp_path, monkeypa
     series and the grid dump file are identical to the reference's, with or without a host
     mirror of the populations."""
     monkeypatch.setenv("LBDEM_GPU_HOST_MIRROR", mirror)
-    cfg = BED.format(nx=24, ny=20, nz=32, blocks=[2, 1, 2], workers=2, count=8, d=8)
-    a = dropin.DropinSim(cfg, (24, 20, 32))
+    cfg = BED.format(nx=32, ny=24, nz=48, blocks=[2, 1, 2], workers=2, count=8, d=8)
+    a = dropin.DropinSim(cfg, (32, 24, 48))
     b = ref.sim(cfg)
     for steps in (1, 3):
         a.run(steps)
@@ -81,7 +81,7 @@ def test_observers_and_grid_dump_match_reference(dropin, ref, tmp_path, monkeypa
     a.grid_dump(tmp_path / "gpu.dat")
     b.grid_dump(tmp_path / "ref.dat")
     ga, gb = (tmp_path / "gpu.dat").read_bytes(), (tmp_path / "ref.dat").read_bytes()
-    assert len(ga) > 24 * 20 * 32 * 40 and ga == gb
+    assert len(ga) > 32 * 24 * 48 * 40 and ga == gb
 
 
 @pytest.mark.parametrize("halo", ["device", "host"])
