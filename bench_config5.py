@@ -1,15 +1,18 @@
 #!/usr/bin/env python
-"""Config 5 (BASELINE.json): fluidized-bed four-way coupled PSM + DEM, weak scaling over
-the GPUs of one box, through the drop-in build (the reference Simulation with its GPU-side
-operators on liblbg; host DEM = the reference's code).
+"""Config 5 (BASELINE.json): fluidized-bed four-way coupled PSM + DEM, weak and strong
+scaling over the GPUs of one box, through the drop-in build (the reference Simulation with
+its GPU-side operators on liblbg; host DEM = the reference's code).
 
     python bench_config5.py --gpus N [--steps K] [--edge 512] [--per-gpu 12500]
+    python bench_config5.py --gpus N --mode strong [--steps K]
 
 Weak scaling as SURVEY §8(d): domain (edge*N) x edge x edge, block grid {N,1,1} (x-slabs, so
-the bottom-settled bed splits evenly), edge^3 cells and `per_gpu` spheres (d = 10) per GPU,
-one block per GPU (LBDEM_GPU_SPREAD=1), one reference worker thread per block, no host PDF
-mirror (LBDEM_GPU_HOST_MIRROR=0). Prints one JSON line with the reference's own
-per-category TimingReport (perf.hpp:17-51) and MLUPS = cells * steps / wall time.
+the bottom-settled bed splits evenly), edge^3 cells and `per_gpu` spheres (d = 10) per GPU.
+Strong scaling: the fixed 1024 x 512 x 512 bed (2.7e8 cells, 10^5 spheres; about 120 GB on a
+single GPU) split into {N,1,1} x-slabs. Either way one block per GPU (LBDEM_GPU_SPREAD=1), one
+reference worker thread per block, no host PDF mirror (LBDEM_GPU_HOST_MIRROR=0). Prints one
+JSON line with the reference's own per-category TimingReport (perf.hpp:17-51) and
+MLUPS = cells * steps / wall time.
 """
 import argparse
 import json
@@ -37,6 +40,7 @@ def main():
     ap.add_argument("--per-gpu", type=int, default=12500)
     ap.add_argument("--settle", type=int, default=100)
     ap.add_argument("--force", choices=["scratch", "fused"], default="fused")
+    ap.add_argument("--mode", choices=["weak", "strong"], default="weak")
     args = ap.parse_args()
     os.environ["LBDEM_GPU_SPREAD"] = "1"
     os.environ["LBDEM_GPU_HOST_MIRROR"] = "0"
@@ -44,9 +48,13 @@ def main():
     import torch  # noqa: F401  (CUDA plumbing)
     import dropin
     g, n = args.gpus, args.edge
-    cfg = CFG.format(nx=n * g, n=n, g=g, p=args.per_gpu * g, settle=args.settle)
+    if args.mode == "strong":
+        nx, particles = 2 * n, 100000
+    else:
+        nx, particles = n * g, args.per_gpu * g
+    cfg = CFG.format(nx=nx, n=n, g=g, p=particles, settle=args.settle)
     t0 = time.perf_counter()
-    sim = dropin.DropinSim(cfg, (n * g, n, n))
+    sim = dropin.DropinSim(cfg, (nx, n, n))
     setup = time.perf_counter() - t0
     sim.run(1)
     sim.reset_timers()
@@ -54,15 +62,16 @@ def main():
     sim.run(args.steps)
     dt = time.perf_counter() - t0
     cat = sim.timings()
-    cells = n * n * n * g
+    cells = nx * n * n
     print(json.dumps({
-        "workload": f"config 5 weak: {n * g}x{n}x{n} fluidized bed, {args.per_gpu * g} spheres d=10, "
+        "workload": f"config 5 {args.mode}: {nx}x{n}x{n} fluidized bed, {particles} spheres d=10, "
                     f"blocks {{{g},1,1}}, one per GPU, host DEM (reference), force mode {args.force}",
+        "scaling": args.mode,
         "n_gpus": g, "steps": args.steps, "ms_per_step": round(dt * 1e3 / args.steps, 2),
         "mlups": round(cells * args.steps / dt / 1e6, 1),
         "mlups_per_gpu": round(cells * args.steps / dt / 1e6 / g, 1),
         "categories_ms_per_step": {c: round(v * 1e3 / args.steps, 3) for c, v in zip(CATS, cat)},
-        "particles": args.per_gpu * g, "setup_s": round(setup, 1)}))
+        "particles": particles, "setup_s": round(setup, 1)}))
     sim.close()
 
 

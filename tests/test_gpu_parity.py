@@ -386,6 +386,36 @@ def test_psm_sweep_bitwise(gpu, oracle, fext):
     assert equal_bits(m1[c > 1], scr["m1"][c > 1])
 
 
+@pytest.mark.parametrize("fext", [(0.0, 0.0, 0.0), (0.0, 2e-6, 0.0)])
+@pytest.mark.parametrize("cover", [0.05, 0.4, 0.9])
+def test_psm_one_entry_segments_bitwise(gpu, oracle, fext, cover):
+    """K2's one-entry segments (no two-entry cell): fluid and covered lanes of one warp share
+    the one-entry operator when unforced (B = b = 0, v = 0 is collide_cell exactly) and take
+    SRT / PSM in turn when forced — bitwise either way, sparse to dense cover, long rows."""
+    dims = (70, 6, 5)
+    src0 = random_pdf(dims, seed=91)
+    frac, sv = random_fraction(dims, seed=13, cover=cover)
+    frac["count"][:] = np.minimum(frac["count"], 1)
+    frac["btot"][:] = np.minimum(1.0, frac["b0"])
+    tau = 0.6
+    src_o = src0.copy()
+    oracle.fill_periodic(dims, src_o, ALL_P)
+    dst_o = np.zeros_like(src_o)
+    scr = new_scratch(dims)
+    assert oracle.psm_collide_stream(dims, src_o, dst_o, tau, fext, (0, 0, 0), dims, frac, sv, scr) == 0
+    blk = gpu.Block(dims, coupling=True)
+    blk.upload_src(src0)
+    blk.upload_fraction(frac)
+    blk.upload_solid_velocity(sv["v0"], sv["v1"])
+    blk.fill_periodic(ALL_P, full=True)
+    blk.sweep(gpu.FluidParams(tau, fext), gpu.CellBox((0, 0, 0), dims))
+    blk.sync()
+    assert n_bit_mismatch(interior(blk.download_dst()), interior(dst_o)) == 0
+    m0, _ = blk.download_scratch()
+    c = frac["count"]
+    assert equal_bits(m0[c > 0], scr["m0"][c > 0])
+
+
 def test_psm_with_zero_fraction_is_plain_srt(gpu, oracle):
     """test_psm.cpp:269-304 — B = 0 PSM == SRT, bitwise."""
     dims = (12, 12, 12)
