@@ -321,22 +321,38 @@ __global__ void __launch_bounds__(192) chain_kernel(const unsigned long long* __
     const int i0 = start[p], i1 = end[p];
     double sum = 0.0, comp = 0.0;
     const double x0 = s[p].x[0], x1 = s[p].x[1], x2 = s[p].x[2];
-    for (int i = i0; i < i1; ++i) {
-        const unsigned long long key = keys[i];
+    // this lane's term of entry `key` (force component d, or torque component d-3:
+    // cross(c - x, m), psm.cpp:296)
+    auto term = [&](unsigned long long key) {
         const long long c = (long long)((key >> 1) & 0x7fffffffull);
         const double* mp = ((key & 1ull) ? m1 : m0) + 3 * c;
-        double v;
-        if (d < 3) {
-            v = mp[d];
-        } else {
-            const int ci = (int)(c % g.dims[0]), cj = (int)((c / g.dims[0]) % g.dims[1]),
-                      ck = (int)(c / ((long long)g.dims[0] * g.dims[1]));
-            const double r0 = ((double)(g.lo[0] + ci) + 0.5) - x0;
-            const double r1 = ((double)(g.lo[1] + cj) + 0.5) - x1;
-            const double r2 = ((double)(g.lo[2] + ck) + 0.5) - x2;
-            const double a0 = mp[0], a1 = mp[1], a2 = mp[2];
-            v = d == 3 ? r1 * a2 - r2 * a1 : (d == 4 ? r2 * a0 - r0 * a2 : r0 * a1 - r1 * a0);
+        if (d < 3) return mp[d];
+        const int ci = (int)(c % g.dims[0]), cj = (int)((c / g.dims[0]) % g.dims[1]),
+                  ck = (int)(c / ((long long)g.dims[0] * g.dims[1]));
+        const double r0 = ((double)(g.lo[0] + ci) + 0.5) - x0;
+        const double r1 = ((double)(g.lo[1] + cj) + 0.5) - x1;
+        const double r2 = ((double)(g.lo[2] + ck) + 0.5) - x2;
+        const double a0 = mp[0], a1 = mp[1], a2 = mp[2];
+        return d == 3 ? r1 * a2 - r2 * a1 : (d == 4 ? r2 * a0 - r0 * a2 : r0 * a1 - r1 * a0);
+    };
+    // the terms are independent of the chain: gather kBatch of them (loads in flight
+    // together), then add them in entry order
+    constexpr int kBatch = 8;
+    int i = i0;
+    for (; i + kBatch <= i1; i += kBatch) {
+        double v[kBatch];
+#pragma unroll
+        for (int t = 0; t < kBatch; ++t) v[t] = term(keys[i + t]);
+#pragma unroll
+        for (int t = 0; t < kBatch; ++t) {
+            if (fast)
+                sum += v[t];
+            else
+                nm_add(sum, comp, v[t]);
         }
+    }
+    for (; i < i1; ++i) {
+        const double v = term(keys[i]);
         if (fast)
             sum += v;
         else
@@ -553,15 +569,36 @@ lbg_status lbg_set_solid_velocities(lbg_block b, const lbg_snapshot* snaps, int 
 }
 
 // LBG_FORCE_FUSED: the sweep already summed; copy the accumulators out
+// per-particle output rows (device + pinned host), grown geometrically, kept across steps
+static lbg_status reserve_rows(lbg_block b, int n) {
+    if (n > b->red_cap) {
+        if (b->red_rows) cudaFree(b->red_rows);
+        if (b->red_used) cudaFree(b->red_used);
+        if (b->red_rows_h) cudaFreeHost(b->red_rows_h);
+        if (b->red_used_h) cudaFreeHost(b->red_used_h);
+        b->red_cap = std::max(n, 2 * b->red_cap);
+        LBG_CUDA(cudaMalloc(&b->red_rows, sizeof(double) * 12 * b->red_cap + 16));
+        LBG_CUDA(cudaMalloc(&b->red_used, sizeof(int) * b->red_cap));
+        LBG_CUDA(cudaMallocHost(&b->red_rows_h, sizeof(double) * 12 * b->red_cap + 16));
+        LBG_CUDA(cudaMallocHost(&b->red_used_h, sizeof(int) * b->red_cap));
+    }
+    if (!b->red_rows) {
+        LBG_CUDA(cudaMalloc(&b->red_rows, 16 + sizeof(double) * 12));
+        LBG_CUDA(cudaMallocHost(&b->red_rows_h, 16 + sizeof(double) * 12));
+    }
+    return LBG_OK;
+}
+
 static lbg_status reduce_fused(lbg_block b, lbg_hydro_partial* out, int capacity, int* n_out) {
     const int n = b->n_snaps;
-    std::vector<double> acc((size_t)6 * std::max(n, 1));
-    std::vector<int> used((size_t)std::max(n, 1));
+    if (lbg_status s = reserve_rows(b, n)) return s;
+    double* acc = b->red_rows_h;  // pinned: 6 per particle
+    int* used = b->red_used_h;
     {
         Span span(b, LBG_CAT_REDF);
         if (n > 0) {
-            LBG_CUDA(cudaMemcpyAsync(acc.data(), b->facc, sizeof(double) * 6 * n, cudaMemcpyDeviceToHost, b->stream));
-            LBG_CUDA(cudaMemcpyAsync(used.data(), b->fused_used, sizeof(int) * n, cudaMemcpyDeviceToHost, b->stream));
+            LBG_CUDA(cudaMemcpyAsync(acc, b->facc, sizeof(double) * 6 * n, cudaMemcpyDeviceToHost, b->stream));
+            LBG_CUDA(cudaMemcpyAsync(used, b->fused_used, sizeof(int) * n, cudaMemcpyDeviceToHost, b->stream));
         }
     }
     if (lbg_status s = lbg_sync(b, nullptr)) {
@@ -597,21 +634,7 @@ lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int c
     }
     LBG_CUDA(cudaSetDevice(b->device));
     const int n = b->n_snaps;
-    if (n > b->red_cap) {
-        if (b->red_rows) cudaFree(b->red_rows);
-        if (b->red_used) cudaFree(b->red_used);
-        if (b->red_rows_h) cudaFreeHost(b->red_rows_h);
-        if (b->red_used_h) cudaFreeHost(b->red_used_h);
-        b->red_cap = std::max(n, 2 * b->red_cap);
-        LBG_CUDA(cudaMalloc(&b->red_rows, sizeof(double) * 12 * b->red_cap + 16));
-        LBG_CUDA(cudaMalloc(&b->red_used, sizeof(int) * b->red_cap));
-        LBG_CUDA(cudaMallocHost(&b->red_rows_h, sizeof(double) * 12 * b->red_cap + 16));
-        LBG_CUDA(cudaMallocHost(&b->red_used_h, sizeof(int) * b->red_cap));
-    }
-    if (!b->red_rows) {
-        LBG_CUDA(cudaMalloc(&b->red_rows, 16 + sizeof(double) * 12));
-        LBG_CUDA(cudaMallocHost(&b->red_rows_h, 16 + sizeof(double) * 12));
-    }
+    if (lbg_status s = reserve_rows(b, n)) return s;
     const BinGeom g = geom(b);
     const long long cells = (long long)g.dims[0] * g.dims[1] * g.dims[2];
     if (b->cov_dirty)
