@@ -321,42 +321,51 @@ __global__ void __launch_bounds__(192) chain_kernel(const unsigned long long* __
     const int i0 = start[p], i1 = end[p];
     double sum = 0.0, comp = 0.0;
     const double x0 = s[p].x[0], x1 = s[p].x[1], x2 = s[p].x[2];
-    // this lane's term of entry `key` (force component d, or torque component d-3:
-    // cross(c - x, m), psm.cpp:296)
-    auto term = [&](unsigned long long key) {
-        const long long c = (long long)((key >> 1) & 0x7fffffffull);
-        const double* mp = ((key & 1ull) ? m1 : m0) + 3 * c;
-        if (d < 3) return mp[d];
+    // this lane's term of an entry (force component d, or torque component d-3:
+    // cross(c - x, m), psm.cpp:296), from the entry's cell and its momentum m
+    auto term = [&](long long c, double a0, double a1, double a2) {
+        if (d < 3) return d == 0 ? a0 : (d == 1 ? a1 : a2);
         const int ci = (int)(c % g.dims[0]), cj = (int)((c / g.dims[0]) % g.dims[1]),
                   ck = (int)(c / ((long long)g.dims[0] * g.dims[1]));
         const double r0 = ((double)(g.lo[0] + ci) + 0.5) - x0;
         const double r1 = ((double)(g.lo[1] + cj) + 0.5) - x1;
         const double r2 = ((double)(g.lo[2] + ck) + 0.5) - x2;
-        const double a0 = mp[0], a1 = mp[1], a2 = mp[2];
         return d == 3 ? r1 * a2 - r2 * a1 : (d == 4 ? r2 * a0 - r0 * a2 : r0 * a1 - r1 * a0);
     };
-    // the terms are independent of the chain: gather kBatch of them (loads in flight
-    // together), then add them in entry order
+    auto add = [&](double v) {
+        if (fast) {
+            sum += v;
+        } else {
+            nm_add(sum, comp, v);
+        }
+    };
+    // The terms are independent of the chain: a batch of keys, then the batch's momenta, are
+    // loaded back to back (branch-free, so they are in flight together), then the terms are
+    // added in entry order.
     constexpr int kBatch = 8;
     int i = i0;
     for (; i + kBatch <= i1; i += kBatch) {
-        double v[kBatch];
+        unsigned long long kk[kBatch];
 #pragma unroll
-        for (int t = 0; t < kBatch; ++t) v[t] = term(keys[i + t]);
+        for (int t = 0; t < kBatch; ++t) kk[t] = keys[i + t];
+        long long c[kBatch];
+        double a0[kBatch], a1[kBatch], a2[kBatch];
 #pragma unroll
         for (int t = 0; t < kBatch; ++t) {
-            if (fast)
-                sum += v[t];
-            else
-                nm_add(sum, comp, v[t]);
+            c[t] = (long long)((kk[t] >> 1) & 0x7fffffffull);
+            const double* mp = ((kk[t] & 1ull) ? m1 : m0) + 3 * c[t];
+            a0[t] = mp[0];
+            a1[t] = mp[1];
+            a2[t] = mp[2];
         }
+#pragma unroll
+        for (int t = 0; t < kBatch; ++t) add(term(c[t], a0[t], a1[t], a2[t]));
     }
     for (; i < i1; ++i) {
-        const double v = term(keys[i]);
-        if (fast)
-            sum += v;
-        else
-            nm_add(sum, comp, v);
+        const unsigned long long key = keys[i];
+        const long long c = (long long)((key >> 1) & 0x7fffffffull);
+        const double* mp = ((key & 1ull) ? m1 : m0) + 3 * c;
+        add(term(c, mp[0], mp[1], mp[2]));
     }
     const int slot = d < 3 ? d : 6 + (d - 3);
     rows[12 * (size_t)p + slot] = sum;

@@ -455,6 +455,17 @@ class Block:
         check(_lib().lbg_halo_complete(self.h))
 
     # instrumentation
+    def halo_stage(self, offsets):
+        """begin_halo_exchange (sim.cpp:156-179) without the host: stage source_slab(o) of every
+        neighbour offset on the device."""
+        flat = [int(v) for o in offsets for v in o]
+        check(_lib().lbg_halo_stage(self.h, (C.c_int * max(1, len(flat)))(*flat), len(offsets)))
+
+    def halo_fetch(self, direction, src: "Block"):
+        """complete_halo_exchange for one neighbour entry: src's staged source_slab(-dir) into
+        this block's ghost_region(dir), device to device."""
+        check(_lib().lbg_halo_fetch(self.h, (C.c_int * 3)(*direction), src.h))
+
     def set_timing(self, on=True):
         check(_lib().lbg_set_timing(self.h, int(on)))
 

@@ -643,3 +643,47 @@ def test_single_rank_halo_equals_periodic_fill(gpu, oracle):
                          gpu.CellBox((0, 0, dims[2] - 1), dims)])
     blk2.sync()
     assert equal_bits(interior(blk2.download_dst()), interior(dst_o))
+
+
+@pytest.mark.parametrize("grid", [(1, 1, 1), (2, 2, 1)])
+def test_poisoned_halos_never_leak(gpu, oracle, grid):
+    """test_partition.cpp:130-151 on the device path: every block's ghosts are NaN, the
+    26-neighbour halo runs device to device (lbg_halo_stage / lbg_halo_fetch, periodic
+    self-messages included), then a full sweep. Every interior population is finite and the
+    decomposed step equals the single-domain oracle step bitwise (test_partition.cpp:95-128)."""
+    import itertools
+    D = (12, 12, 12)
+    tau, fext = 0.8, (1e-6, 0.0, 0.0)
+    bd = tuple(D[a] // grid[a] for a in range(3))
+    offs = [o for o in itertools.product((-1, 0, 1), repeat=3) if any(o)]
+    src_g = random_pdf(D, seed=101)
+    blocks = {}
+    for g in itertools.product(*(range(n) for n in grid)):
+        lo = tuple(g[a] * bd[a] for a in range(3))
+        b = gpu.Block(bd, lo=lo)
+        sub = np.full((19, bd[2] + 2, bd[1] + 2, bd[0] + 2), np.nan)
+        sub[:, 1:-1, 1:-1, 1:-1] = interior(src_g)[:, lo[2]:lo[2] + bd[2], lo[1]:lo[1] + bd[1],
+                                                    lo[0]:lo[0] + bd[0]]
+        b.upload_src(sub)
+        b.fill_ghosts_src(np.nan)
+        blocks[g] = b
+    for b in blocks.values():
+        b.halo_stage(offs)
+    for g, b in blocks.items():
+        for o in offs:
+            nb = tuple((g[a] + o[a]) % grid[a] for a in range(3))
+            b.halo_fetch(o, blocks[nb])
+    p = gpu.FluidParams(tau, fext)
+    for b in blocks.values():
+        b.sweep(p, gpu.CellBox((0, 0, 0), bd))
+        b.sync()
+    src_o = src_g.copy()
+    oracle.fill_periodic(D, src_o, ALL_P)
+    dst_o = np.zeros_like(src_o)
+    oracle.collide_stream(D, src_o, dst_o, tau, fext, (0, 0, 0), D)
+    want = interior(dst_o)
+    for g, b in blocks.items():
+        lo = tuple(g[a] * bd[a] for a in range(3))
+        got = interior(b.download_dst())
+        assert np.isfinite(got).all()
+        assert n_bit_mismatch(got, want[:, lo[2]:lo[2] + bd[2], lo[1]:lo[1] + bd[1], lo[0]:lo[0] + bd[0]]) == 0
