@@ -412,7 +412,6 @@ lbg_status lbg_block_create(int device, const int box_lo[3], const int dims[3], 
         // FractionField::resize fills id0/id1 with -1 (field.cpp:37-46)
         cudaMemset(b->id0, 0xff, n * 4);
         cudaMemset(b->id1, 0xff, n * 4);
-        if ((e = cudaMalloc(&b->cov_list, sizeof(unsigned) * n)) != cudaSuccess) return fail(e, "cudaMalloc(cov)");
         if ((e = cudaMalloc(&b->cov_n, 2 * sizeof(int))) != cudaSuccess) return fail(e, "cudaMalloc(cov_n)");
         cudaMemset(b->cov_n, 0, 2 * sizeof(int));
         b->seg_cap = (long long)((L.nx + 31) / 32) * L.ny * L.nz;
@@ -450,8 +449,8 @@ lbg_status lbg_block_destroy(lbg_block b) {
     if (b->p2p) lbg_p2p_destroy(b);
     void* dev[] = {b->buf[0], b->buf[1], b->count, b->id0, b->id1, b->b0, b->b1, b->btot,
                    b->v0, b->v1, b->m0, b->m1, b->snaps_d, b->bin_count, b->bin_start,
-                   b->bin_items, b->red_rows, b->red_used, b->err_d, b->cov_list, b->cov_n, b->facc, b->fused_used, b->scan_tmp, b->obs_d, b->mom_d,
-                   b->seg_list, b->seg_n};
+                   b->bin_items, b->red_rows, b->red_used, b->err_d, b->cov_n, b->facc, b->fused_used, b->scan_tmp, b->obs_d, b->mom_d,
+                   b->seg_list, b->seg_n, b->tile_buf, b->snap_tab};
     for (void* p : dev)
         if (p) cudaFree(p);
     void* host[] = {b->snaps_h, b->err_h, b->red_rows_h, b->red_used_h, b->obs_h, b->cn_h};

@@ -76,6 +76,33 @@ struct TimedSpan {
     cudaEvent_t a, b;
 };
 
+// snapshot_index (psm.cpp:46-51): id -> index in the id-sorted snapshot list. A dense table
+// over [id_min, id_min + range) is built at every snapshot upload when the ids are dense
+// enough (the usual case: particle ids 0..N-1); otherwise a binary search. Either way an
+// absent id gives -1.
+struct SnapIndex {
+    const lbg_snapshot* s;
+    int n;
+    const int* tab;  // nullptr: binary search
+    int id_min;
+    int range;
+    __device__ __forceinline__ int operator()(int id) const {
+        if (tab) {
+            const long long o = (long long)id - id_min;
+            return (o >= 0 && o < range) ? tab[o] : -1;
+        }
+        int lo = 0, hi = n;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (s[mid].id < id)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        return (lo < n && s[lo].id == id) ? lo : -1;
+    }
+};
+
 struct Comm;  // lbg_halo.cu
 struct P2P;   // lbg_p2p.cu
 
@@ -100,9 +127,8 @@ struct lbg_block_s {
     double* v1 = nullptr;
     double* m0 = nullptr;
     double* m1 = nullptr;
-    // covered cells (count > 0), compacted by the mapping kernel / after a fraction upload;
-    // the PSM operator runs over this list so the SRT sweep keeps its low register count
-    unsigned* cov_list = nullptr;
+    // covered-cell counts (one-entry, two-entry), from the mapping kernel / after a fraction
+    // upload; they size the PARITY reduction's entry list
     int* cov_n = nullptr;  // device counters [2]
     bool cov_dirty = true;
     // aligned 32-cell row segments holding covered cells (first cell index): segments with
@@ -127,6 +153,10 @@ struct lbg_block_s {
     lbg_snapshot* snaps_d = nullptr;
     int snaps_cap = 0;
     int n_snaps = 0;
+    int* snap_tab = nullptr;  // dense id -> index table (SnapIndex)
+    long long snap_tab_cap = 0;
+    int snap_id_min = 0;
+    int snap_range = 0;  // 0: no table (sparse ids)
     // device binning for the mapping kernel (lbg_psm.cu)
     int* bin_count = nullptr;
     int* bin_start = nullptr;
@@ -149,6 +179,8 @@ struct lbg_block_s {
     int* red_seg = nullptr;  // start[n], end[n]
     int red_seg_cap = 0;
     int* cn_h = nullptr;  // pinned copy of cov_n
+    int* tile_buf = nullptr;  // per-tile entry totals and offsets (ordered entry emission)
+    long long tile_cap = 0;
 
     lbg::DeviceErrors* err_d = nullptr;
     lbg::DeviceErrors* err_h = nullptr;  // pinned
@@ -190,8 +222,13 @@ struct lbg_block_s {
 
 namespace lbg {
 
-// covered-cell list rebuild from `count` (lbg_psm.cu)
+// covered-cell counts and segment lists rebuilt from `count` (lbg_psm.cu)
 lbg_status rebuild_covered(lbg_block b);
+// the block's current snapshot index
+inline SnapIndex snap_index(const lbg_block_s* b) {
+    return SnapIndex{b->snaps_d, b->n_snaps, b->snap_range > 0 ? b->snap_tab : nullptr, b->snap_id_min,
+                     b->snap_range};
+}
 
 // warp-aggregated append of `pred` lanes' values to list[*n ...]
 __device__ __forceinline__ void warp_append(bool pred, unsigned v, unsigned* list, int* n) {
@@ -205,18 +242,14 @@ __device__ __forceinline__ void warp_append(bool pred, unsigned v, unsigned* lis
     if (pred) list[base + __popc(m & ((1u << lane) - 1))] = v;
 }
 
-// covered cells split by entry count: one-entry cells fill the list from the front
-// (counter n[0]), two-entry cells from the back (counter n[1], slot cap-1-i)
-__device__ __forceinline__ void covered_append(int cnt, unsigned v, unsigned* list, long long cap, int* n) {
-    warp_append(cnt == 1, v, list, n);
-    const unsigned m = __ballot_sync(0xffffffffu, cnt == 2);
-    if (!m) return;
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(m) - 1;
-    int base = 0;
-    if (lane == leader) base = atomicAdd(n + 1, __popc(m));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (cnt == 2) list[cap - 1 - (base + __popc(m & ((1u << lane) - 1)))] = v;
+// covered cells counted by entry count (n[0]: one-entry, n[1]: two-entry), warp-aggregated
+__device__ __forceinline__ void covered_count(int cnt, int* n) {
+    const unsigned m1 = __ballot_sync(0xffffffffu, cnt == 1);
+    const unsigned m2 = __ballot_sync(0xffffffffu, cnt == 2);
+    if ((threadIdx.x & 31) == 0) {
+        if (m1) atomicAdd(n, __popc(m1));
+        if (m2) atomicAdd(n + 1, __popc(m2));
+    }
 }
 
 // error plumbing (lbg_core.cu)

@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "lbg_internal.cuh"
@@ -116,85 +117,121 @@ struct MapArgs {
     double* __restrict__ v1;
     DeviceErrors* err;
     int with_velocity;
-    unsigned* cov_list;
     int* cov_n;
-    unsigned* seg_list;
-    int* seg_n;
-    long long seg_cap;
 };
 
-// psm.cpp:28-32 overlap_fraction, psm.cpp:93-136 per-cell entry rule, psm.cpp:157-163 setU
-__global__ void __launch_bounds__(256) map_kernel(const MapArgs a) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int j = blockIdx.y;
-    const int k = blockIdx.z;
+// K3 mapping (psm.cpp:28-32 overlap_fraction, psm.cpp:93-136 per-cell entry rule, psm.cpp:157-163
+// setU fused): one CTA per 8^3 bin, two cells per thread. The bin's candidate
+// snapshots are staged in shared memory in list (= id) order, 64 at a time, so every lane reads
+// the same candidate (broadcast) and the loop has no per-lane trip count. The overlap test is
+// overlap_fraction (psm.cpp:28-32) with two exact shortcuts on the squared distance d2 =
+// (dx*dx + dy*dy) + dz*dz (the radicand the reference takes the root of):
+//   d2 > (r + f_r)^2 (1 + 1e-9)      => eps <= 0 (skip), the rounding of the root and of
+//                                       -(dist - r) + f_r is ~1e-16 relative, far inside the
+//                                       margin;
+//   d2 < (r + f_r - 1)^2 (1 - 1e-9)  => eps >= 1, which the clamp makes exactly 1.0.
+// Every other candidate takes the reference's sqrt path, so count/ids/fractions/velocities are
+// bitwise those of build_fraction_field + set_solid_velocities. Segment lists are registered
+// by a separate pass (segments_kernel), since a warp here is not a row segment.
+constexpr int kMapCand = 64;
+
+__global__ void __launch_bounds__(256) map_bin_kernel(const MapArgs a) {
     const BinGeom& g = a.g;
-    bool over = false;
-    int covered = 0;  // entry count for the covered-cell lists
-    unsigned cell = 0;
-    if (i < g.dims[0]) {
-        const long long c = ((long long)k * g.dims[1] + j) * g.dims[0] + i;
-        const int b = ((k / kBin) * g.nb[1] + (j / kBin)) * g.nb[0] + (i / kBin);
-        const double cc0 = (double)(g.lo[0] + i) + 0.5;
-        const double cc1 = (double)(g.lo[1] + j) + 0.5;
-        const double cc2 = (double)(g.lo[2] + k) + 0.5;
-        const int* list = a.items + a.start[b];
-        const int n = a.cnt[b];
-        int cnt = 0;
-        double sum = 0.0;
-        for (int t = 0; t < n; ++t) {
-            const lbg_snapshot& p = a.s[list[t]];
-            const double d0 = cc0 - p.x[0], d1 = cc1 - p.x[1], d2 = cc2 - p.x[2];
-            const double dist = sqrt((d0 * d0 + d1 * d1) + d2 * d2);
-            double eps = -(dist - p.r) + p.f_r;
-            eps = eps < 0.0 ? 0.0 : (1.0 < eps ? 1.0 : eps);  // std::clamp
-            if (eps <= 0.0) continue;
-            if (cnt >= 2) {
-                over = true;
-                break;
+    const int b = blockIdx.x;
+    const int bx = b % g.nb[0], by = (b / g.nb[0]) % g.nb[1], bz = b / (g.nb[0] * g.nb[1]);
+    __shared__ double sx0[kMapCand], sx1[kMapCand], sx2[kMapCand], sr[kMapCand], sfr[kMapCand];
+    __shared__ double sout2[kMapCand], sin2[kMapCand];
+    __shared__ double su[3][kMapCand], sw[3][kMapCand];
+    __shared__ int sid[kMapCand];
+    const int t = threadIdx.x;
+    const int i = bx * kBin + (t & 7), j = by * kBin + ((t >> 3) & 7);
+    int k[2] = {bz * kBin + (t >> 6), bz * kBin + (t >> 6) + 4};
+    bool valid[2];
+    long long c[2];
+    double cc0 = (double)(g.lo[0] + i) + 0.5, cc1 = (double)(g.lo[1] + j) + 0.5, cc2[2];
+    int cnt[2] = {0, 0};
+    double sum[2] = {0.0, 0.0};
+    bool over[2] = {false, false};
+    for (int h = 0; h < 2; ++h) {
+        valid[h] = i < g.dims[0] && j < g.dims[1] && k[h] < g.dims[2];
+        c[h] = ((long long)k[h] * g.dims[1] + j) * g.dims[0] + i;
+        cc2[h] = (double)(g.lo[2] + k[h]) + 0.5;
+    }
+    const int* list = a.items + a.start[b];
+    const int n = a.cnt[b];
+    for (int base = 0; base < n; base += kMapCand) {
+        const int m = min(kMapCand, n - base);
+        __syncthreads();
+        if (t < m) {
+            const lbg_snapshot& p = a.s[list[base + t]];
+            sx0[t] = p.x[0];
+            sx1[t] = p.x[1];
+            sx2[t] = p.x[2];
+            sr[t] = p.r;
+            sfr[t] = p.f_r;
+            const double ro = p.r + p.f_r, ri = ro - 1.0;
+            sout2[t] = (ro * ro) * (1.0 + 1e-9);
+            sin2[t] = ri > 0.0 ? (ri * ri) * (1.0 - 1e-9) : -1.0;
+            for (int d = 0; d < 3; ++d) {
+                su[d][t] = p.u[d];
+                sw[d][t] = p.omega[d];
             }
-            if (a.with_velocity) {
-                // v = u + cross(omega, c - x)  (vec3.hpp:92-94)
-                const double r0 = cc0 - p.x[0], r1 = cc1 - p.x[1], r2 = cc2 - p.x[2];
-                const double w0 = p.omega[0], w1 = p.omega[1], w2 = p.omega[2];
-                double* v = (cnt == 0 ? a.v0 : a.v1) + 3 * c;
-                v[0] = p.u[0] + (w1 * r2 - w2 * r1);
-                v[1] = p.u[1] + (w2 * r0 - w0 * r2);
-                v[2] = p.u[2] + (w0 * r1 - w1 * r0);
-            }
-            if (cnt == 0) {
-                a.id0[c] = p.id;
-                a.b0[c] = eps;
-            } else {
-                a.id1[c] = p.id;
-                a.b1[c] = eps;
-            }
-            ++cnt;
-            sum += eps;
+            sid[t] = p.id;
         }
-        a.count[c] = (uint8_t)cnt;
-        a.btot[c] = sum < 1.0 ? sum : 1.0;  // std::min(1.0, sum)
-        covered = cnt;
-        cell = (unsigned)c;
+        __syncthreads();
+        for (int h = 0; h < 2; ++h) {
+            if (!valid[h] || over[h]) continue;
+            for (int q = 0; q < m; ++q) {
+                const double d0 = cc0 - sx0[q], d1 = cc1 - sx1[q], d2 = cc2[h] - sx2[q];
+                const double rad = (d0 * d0 + d1 * d1) + d2 * d2;
+                if (rad > sout2[q]) continue;
+                double eps;
+                if (rad < sin2[q]) {
+                    eps = 1.0;
+                } else {
+                    eps = -(sqrt(rad) - sr[q]) + sfr[q];
+                    eps = eps < 0.0 ? 0.0 : (1.0 < eps ? 1.0 : eps);  // std::clamp
+                    if (eps <= 0.0) continue;
+                }
+                if (cnt[h] >= 2) {
+                    over[h] = true;
+                    break;
+                }
+                if (a.with_velocity) {
+                    // v = u + cross(omega, c - x)  (vec3.hpp:92-94)
+                    double* v = (cnt[h] == 0 ? a.v0 : a.v1) + 3 * c[h];
+                    v[0] = su[0][q] + (sw[1][q] * d2 - sw[2][q] * d1);
+                    v[1] = su[1][q] + (sw[2][q] * d0 - sw[0][q] * d2);
+                    v[2] = su[2][q] + (sw[0][q] * d1 - sw[1][q] * d0);
+                }
+                if (cnt[h] == 0) {
+                    a.id0[c[h]] = sid[q];
+                    a.b0[c[h]] = eps;
+                } else {
+                    a.id1[c[h]] = sid[q];
+                    a.b1[c[h]] = eps;
+                }
+                ++cnt[h];
+                sum[h] += eps;
+            }
+        }
     }
-    covered_append(covered, cell, a.cov_list, (long long)g.dims[0] * g.dims[1] * g.dims[2], a.cov_n);
-    // this warp is one aligned 32-cell row segment: register it for the PSM sweep (K2)
-    const int segmax = __reduce_max_sync(0xffffffffu, covered);
-    if ((threadIdx.x & 31) == 0 && segmax > 0) {
-        if (segmax == 1)
-            a.seg_list[atomicAdd(&a.seg_n[0], 1)] = cell;
-        else
-            a.seg_list[a.seg_cap - 1 - atomicAdd(&a.seg_n[1], 1)] = cell;
+    for (int h = 0; h < 2; ++h) {
+        if (valid[h]) {
+            a.count[c[h]] = (uint8_t)cnt[h];
+            a.btot[c[h]] = sum[h] < 1.0 ? sum[h] : 1.0;  // std::min(1.0, sum)
+        }
+        covered_count(valid[h] ? cnt[h] : 0, a.cov_n);
+        const unsigned mo = __ballot_sync(0xffffffffu, over[h]);
+        if (mo && (t & 31) == 0) atomicAdd(&a.err->overfull, (unsigned long long)__popc(mo));
     }
-    const unsigned m = __ballot_sync(0xffffffffu, over);
-    if (m && (threadIdx.x & 31) == 0) atomicAdd(&a.err->overfull, (unsigned long long)__popc(m));
 }
 
 // covered-cell list from an externally set fraction field
 __global__ void __launch_bounds__(256) covered_kernel(const uint8_t* __restrict__ count, long long cells,
-                                                      unsigned* __restrict__ list, int* __restrict__ n) {
+                                                      int* __restrict__ n) {
     const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    covered_append(c < cells ? count[c] : 0, (unsigned)c, list, cells, n);
+    covered_count(c < cells ? count[c] : 0, n);
 }
 
 // segment lists from an externally set fraction field (one thread per 32-cell row segment)
@@ -215,20 +252,8 @@ __global__ void __launch_bounds__(256) segments_kernel(const uint8_t* __restrict
         seg_list[seg_cap - 1 - atomicAdd(&seg_n[1], 1)] = (unsigned)c0;
 }
 
-__device__ __forceinline__ int find_snapshot(const lbg_snapshot* s, int n, int id) {
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (s[mid].id < id)
-            lo = mid + 1;
-        else
-            hi = mid;
-    }
-    return (lo < n && s[lo].id == id) ? lo : -1;
-}
-
 // psm.cpp:138-169 — standalone setU over an existing fraction field
-__global__ void __launch_bounds__(256) setu_kernel(const lbg_snapshot* __restrict__ s, int n, BinGeom g,
+__global__ void __launch_bounds__(256) setu_kernel(const lbg_snapshot* __restrict__ s, SnapIndex sidx, BinGeom g,
                                                    const uint8_t* __restrict__ count,
                                                    const int* __restrict__ id0, const int* __restrict__ id1,
                                                    double* __restrict__ v0, double* __restrict__ v1,
@@ -243,7 +268,7 @@ __global__ void __launch_bounds__(256) setu_kernel(const lbg_snapshot* __restric
         const double cc[3] = {(double)(g.lo[0] + i) + 0.5, (double)(g.lo[1] + j) + 0.5,
                               (double)(g.lo[2] + k) + 0.5};
         for (int e = 0; e < cnt; ++e) {
-            const int p = find_snapshot(s, n, e == 0 ? id0[c] : id1[c]);
+            const int p = sidx(e == 0 ? id0[c] : id1[c]);
             if (p < 0) {
                 ++unknown;
                 continue;
@@ -272,30 +297,57 @@ __device__ __forceinline__ void nm_add(double& sum, double& comp, double v) {  /
 }
 
 // ---- sorted-entry PARITY reduction -------------------------------------------------------
-// Every fraction entry (cell c, slot e) of the covered-cell lists becomes a 64-bit key
-// (particle index << 32 | c << 1 | e); a radix sort orders the entries by particle, then
-// lexicographic cell — exactly finalize_hydro_forces' visiting order per particle
-// (psm.cpp:288-308) — and six threads per particle (f.x f.y f.z t.x t.y t.z) run the
-// Neumaier chains over the particle's segment. No walk over empty cells, any fraction field.
-__global__ void __launch_bounds__(256) entry_keys_kernel(const unsigned* __restrict__ cov_list,
-                                                         const int* __restrict__ cov_n, long long cap,
-                                                         const int* __restrict__ id0, const int* __restrict__ id1,
-                                                         const lbg_snapshot* __restrict__ s, int n_snaps,
-                                                         unsigned long long* __restrict__ keys,
-                                                         DeviceErrors* err) {
-    const long long n1 = cov_n[0], n2 = cov_n[1];
-    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n1 + n2) return;
-    const bool one = t < n1;
-    const unsigned c = one ? cov_list[t] : cov_list[cap - 1 - (t - n1)];
-    unsigned long long* out = one ? keys + t : keys + n1 + 2 * (t - n1);
-    for (int e = 0; e < (one ? 1 : 2); ++e) {
-        const int p = find_snapshot(s, n_snaps, e == 0 ? id0[c] : id1[c]);
-        if (p < 0) {
-            atomicAdd(&err->unknown, 1ull);
-            out[e] = ((unsigned long long)n_snaps << 32) | ((unsigned long long)c << 1) | (unsigned long long)e;
-        } else {
-            out[e] = ((unsigned long long)p << 32) | ((unsigned long long)c << 1) | (unsigned long long)e;
+// Every fraction entry (cell c, slot e) becomes a 64-bit key (particle index << 32 | c << 1 |
+// e). The entries are emitted in lexicographic cell order (a tiled scan over the count field:
+// per-tile entry totals, a scan over tiles, then each tile writes its entries in order), so a
+// STABLE radix sort on the particle bits alone — two 8-bit passes for up to 65k particles —
+// leaves each particle's entries in finalize_hydro_forces' visiting order (cells
+// lexicographic, entry 0 before 1, psm.cpp:288-308). Six threads per particle (f.x f.y f.z
+// t.x t.y t.z) then run the Neumaier chains over the particle's segment. No walk over empty
+// cells, any fraction field.
+constexpr int kEntryThreads = 256;
+constexpr int kEntryPerThread = 16;
+constexpr int kEntryTile = kEntryThreads * kEntryPerThread;
+
+__global__ void __launch_bounds__(kEntryThreads) entry_tile_sums_kernel(const uint8_t* __restrict__ count,
+                                                                        long long cells, int* __restrict__ sums) {
+    using Reduce = cub::BlockReduce<int, kEntryThreads>;
+    __shared__ typename Reduce::TempStorage tmp;
+    const long long c0 = (long long)blockIdx.x * kEntryTile + (long long)threadIdx.x * kEntryPerThread;
+    int n = 0;
+#pragma unroll
+    for (int t = 0; t < kEntryPerThread; ++t)
+        if (c0 + t < cells) n += count[c0 + t];
+    const int total = Reduce(tmp).Sum(n);
+    if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kEntryThreads) entry_emit_kernel(
+    const uint8_t* __restrict__ count, long long cells, const int* __restrict__ tile_off,
+    const int* __restrict__ id0, const int* __restrict__ id1, SnapIndex sidx, int n_snaps,
+    unsigned long long* __restrict__ keys, DeviceErrors* err) {
+    using Scan = cub::BlockScan<int, kEntryThreads>;
+    __shared__ typename Scan::TempStorage tmp;
+    const long long c0 = (long long)blockIdx.x * kEntryTile + (long long)threadIdx.x * kEntryPerThread;
+    int cnt[kEntryPerThread];
+    int n = 0;
+#pragma unroll
+    for (int t = 0; t < kEntryPerThread; ++t) {
+        cnt[t] = c0 + t < cells ? count[c0 + t] : 0;
+        n += cnt[t];
+    }
+    int off = 0;
+    Scan(tmp).ExclusiveSum(n, off);
+    unsigned long long* out = keys + tile_off[blockIdx.x] + off;
+    for (int t = 0; t < kEntryPerThread; ++t) {
+        const long long c = c0 + t;
+        for (int e = 0; e < cnt[t]; ++e) {
+            int p = sidx(e == 0 ? id0[c] : id1[c]);
+            if (p < 0) {
+                atomicAdd(&err->unknown, 1ull);
+                p = n_snaps;  // sorts last, outside every particle's segment
+            }
+            *out++ = ((unsigned long long)p << 32) | ((unsigned long long)c << 1) | (unsigned long long)e;
         }
     }
 }
@@ -394,6 +446,11 @@ static BinGeom geom(lbg_block b) {
     return g;
 }
 
+__global__ void snap_table_kernel(const lbg_snapshot* __restrict__ s, int n, int id_min, int* __restrict__ tab) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < n) tab[s[p].id - id_min] = p;
+}
+
 static lbg_status upload_snapshots(lbg_block b, const lbg_snapshot* snaps, int n) {
     for (int t = 1; t < n; ++t)
         if (snaps[t].id <= snaps[t - 1].id)
@@ -422,6 +479,24 @@ static lbg_status upload_snapshots(lbg_block b, const lbg_snapshot* snaps, int n
     LBG_CUDA(cudaEventRecord(b->ev_side, b->side));
     LBG_CUDA(cudaStreamWaitEvent(b->stream, b->ev_side, 0));
     b->n_snaps = n;
+    // dense id -> index table when the ids are dense (SnapIndex), on the compute stream
+    b->snap_range = 0;
+    if (n > 0) {
+        const long long range = (long long)snaps[n - 1].id - snaps[0].id + 1;
+        if (range <= 4LL * n + 4096) {
+            if (range > b->snap_tab_cap) {
+                if (b->snap_tab) LBG_CUDA(cudaFree(b->snap_tab));
+                b->snap_tab = nullptr;
+                b->snap_tab_cap = std::max(range, 2 * b->snap_tab_cap);
+                LBG_CUDA(cudaMalloc(&b->snap_tab, sizeof(int) * b->snap_tab_cap));
+            }
+            b->snap_id_min = snaps[0].id;
+            b->snap_range = (int)range;
+            LBG_CUDA(cudaMemsetAsync(b->snap_tab, 0xff, sizeof(int) * range, b->stream));
+            snap_table_kernel<<<(n + 255) / 256, 256, 0, b->stream>>>(b->snaps_d, n, b->snap_id_min, b->snap_tab);
+            LBG_LAUNCH_CHECK();
+        }
+    }
     return LBG_OK;
 }
 
@@ -438,7 +513,7 @@ static lbg_status ensure_bins(lbg_block b, long long nbins) {
 lbg_status rebuild_covered(lbg_block b) {
     const long long cells = (long long)b->L.nx * b->L.ny * b->L.nz;
     LBG_CUDA(cudaMemsetAsync(b->cov_n, 0, 2 * sizeof(int), b->stream));
-    covered_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, b->stream>>>(b->count, cells, b->cov_list, b->cov_n);
+    covered_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, b->stream>>>(b->count, cells, b->cov_n);
     LBG_LAUNCH_CHECK();
     const long long rows = (long long)b->L.ny * b->L.nz;
     const long long nseg = rows * ((b->L.nx + 31) / 32);
@@ -550,15 +625,15 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
     a.v1 = b->v1;
     a.err = b->err_d;
     a.with_velocity = 1;
-    a.cov_list = b->cov_list;
     a.cov_n = b->cov_n;
-    a.seg_list = b->seg_list;
-    a.seg_n = b->seg_n;
-    a.seg_cap = b->seg_cap;
     LBG_CUDA(cudaMemsetAsync(b->cov_n, 0, 2 * sizeof(int), b->stream));
     LBG_CUDA(cudaMemsetAsync(b->seg_n, 0, 2 * sizeof(int), b->stream));
-    dim3 grid((g.dims[0] + 127) / 128, g.dims[1], g.dims[2]);
-    map_kernel<<<grid, 128, 0, b->stream>>>(a);
+    map_bin_kernel<<<(unsigned)nbins, 256, 0, b->stream>>>(a);
+    LBG_LAUNCH_CHECK();
+    const long long rows = (long long)b->L.ny * b->L.nz;
+    const long long nseg = rows * ((b->L.nx + 31) / 32);
+    segments_kernel<<<(unsigned)((nseg + 255) / 256), 256, 0, b->stream>>>(b->count, b->L.nx, rows, b->seg_list,
+                                                                           b->seg_n, b->seg_cap);
     LBG_LAUNCH_CHECK();
     b->cov_dirty = false;
     return LBG_OK;
@@ -571,7 +646,7 @@ lbg_status lbg_set_solid_velocities(lbg_block b, const lbg_snapshot* snaps, int 
     if (lbg_status s = upload_snapshots(b, snaps, n)) return s;
     const BinGeom g = geom(b);
     dim3 grid((g.dims[0] + 127) / 128, g.dims[1], g.dims[2]);
-    setu_kernel<<<grid, 128, 0, b->stream>>>(b->snaps_d, n, g, b->count, b->id0, b->id1, b->v0, b->v1,
+    setu_kernel<<<grid, 128, 0, b->stream>>>(b->snaps_d, snap_index(b), g, b->count, b->id0, b->id1, b->v0, b->v1,
                                             b->err_d);
     LBG_LAUNCH_CHECK();
     return LBG_OK;
@@ -673,20 +748,39 @@ lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int c
             LBG_CUDA(cudaMalloc(&b->red_seg, sizeof(int) * 2 * b->red_seg_cap));
         }
         if (ne > 0) {
-            entry_keys_kernel<<<(unsigned)((cn[0] + cn[1] + 255) / 256), 256, 0, b->stream>>>(
-                b->cov_list, b->cov_n, cells, b->id0, b->id1, b->snaps_d, n, b->ekeys[0], b->err_d);
+            const long long tiles = (cells + kEntryTile - 1) / kEntryTile;
+            if (tiles > b->tile_cap) {
+                if (b->tile_buf) cudaFree(b->tile_buf);
+                b->tile_cap = tiles;
+                LBG_CUDA(cudaMalloc(&b->tile_buf, sizeof(int) * 2 * tiles));
+            }
+            int* sums = b->tile_buf;
+            int* offs = b->tile_buf + b->tile_cap;
+            entry_tile_sums_kernel<<<(unsigned)tiles, kEntryThreads, 0, b->stream>>>(b->count, cells, sums);
             LBG_LAUNCH_CHECK();
+            size_t tmp = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, tmp, sums, offs, (int)tiles, b->stream);
+            if (tmp > b->scan_tmp_bytes) {
+                if (b->scan_tmp) cudaFree(b->scan_tmp);
+                LBG_CUDA(cudaMalloc(&b->scan_tmp, tmp));
+                b->scan_tmp_bytes = tmp;
+            }
+            cub::DeviceScan::ExclusiveSum(b->scan_tmp, tmp, sums, offs, (int)tiles, b->stream);
+            entry_emit_kernel<<<(unsigned)tiles, kEntryThreads, 0, b->stream>>>(
+                b->count, cells, offs, b->id0, b->id1, snap_index(b), n, b->ekeys[0], b->err_d);
+            LBG_LAUNCH_CHECK();
+            // stable LSD sort on the particle-index bits only (unknown ids carry index n)
             int bits = 1;
             while ((1ll << bits) < n + 1) ++bits;
-            size_t tmp = 0;
-            cub::DeviceRadixSort::SortKeys(nullptr, tmp, b->ekeys[0], b->ekeys[1], (int)ne, 0, 32 + bits,
-                                           b->stream);  // unknown ids carry index n: still < 2^bits
+            tmp = 0;
+            cub::DeviceRadixSort::SortKeys(nullptr, tmp, b->ekeys[0], b->ekeys[1], (int)ne, 32, 32 + bits,
+                                           b->stream);
             if (tmp > b->sort_tmp_bytes) {
                 if (b->sort_tmp) cudaFree(b->sort_tmp);
                 LBG_CUDA(cudaMalloc(&b->sort_tmp, tmp));
                 b->sort_tmp_bytes = tmp;
             }
-            cub::DeviceRadixSort::SortKeys(b->sort_tmp, tmp, b->ekeys[0], b->ekeys[1], (int)ne, 0, 32 + bits,
+            cub::DeviceRadixSort::SortKeys(b->sort_tmp, tmp, b->ekeys[0], b->ekeys[1], (int)ne, 32, 32 + bits,
                                            b->stream);
             LBG_LAUNCH_CHECK();
         }

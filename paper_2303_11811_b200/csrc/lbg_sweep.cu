@@ -47,9 +47,6 @@ struct SweepArgs {
     const double* __restrict__ v1;
     double* __restrict__ m0;
     double* __restrict__ m1;
-    const unsigned* __restrict__ cov_list;  // one-entry cells from the front, two-entry from the back
-    const int* __restrict__ cov_n;          // [0] one-entry count, [1] two-entry count
-    long long cov_cap;
     const unsigned* __restrict__ seg_list;  // covered 32-cell row segments: max count 1 front, 2 back
     const int* __restrict__ seg_n;
     long long seg_cap;
@@ -58,6 +55,7 @@ struct SweepArgs {
     // fused force reduction (LBG_FORCE_FUSED)
     const lbg_snapshot* __restrict__ snaps;
     int n_snaps;
+    SnapIndex sidx;
     int blk_lo[3];
     double* __restrict__ facc;
     int* __restrict__ fused_used;
@@ -274,18 +272,6 @@ __device__ __forceinline__ bool in_boxes(const SweepArgs& a, int i, int j, int k
     return false;
 }
 
-__device__ __forceinline__ int snapshot_of(const SweepArgs& a, int id) {
-    int lo = 0, hi = a.n_snaps;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (a.snaps[mid].id < id)
-            lo = mid + 1;
-        else
-            hi = mid;
-    }
-    return (lo < a.n_snaps && a.snaps[lo].id == id) ? lo : -1;
-}
-
 // LBG_FORCE_FUSED: lanes holding an entry of the same particle form a group (match_any);
 // the group leader sums the group's force and torque (cross(c - x_p, m), psm.cpp:296) by
 // shuffles in lane order and issues one atomicAdd per component.
@@ -378,8 +364,8 @@ __global__ void __launch_bounds__(128) psm_seg_kernel(const SweepArgs a) {
                     cc[0] = (double)(a.blk_lo[0] + i) + 0.5;
                     cc[1] = (double)(a.blk_lo[1] + j) + 0.5;
                     cc[2] = (double)(a.blk_lo[2] + k) + 0.5;
-                    p0 = snapshot_of(a, a.id0[fc]);
-                    if (cnt > 1) p1 = snapshot_of(a, a.id1[fc]);
+                    p0 = a.sidx(a.id0[fc]);
+                    if (cnt > 1) p1 = a.sidx(a.id1[fc]);
                     if (p0 < 0 || (cnt > 1 && p1 < 0)) atomicAdd(&a.err->unknown, 1ull);
                 }
             }
@@ -414,8 +400,8 @@ __global__ void __launch_bounds__(128) sweep_flat_coupled_kernel(const SweepArgs
                 cc[0] = (double)(a.blk_lo[0] + i) + 0.5;
                 cc[1] = (double)(a.blk_lo[1] + j) + 0.5;
                 cc[2] = (double)(a.blk_lo[2] + k) + 0.5;
-                p0 = snapshot_of(a, a.id0[fc]);
-                if (cnt > 1) p1 = snapshot_of(a, a.id1[fc]);
+                p0 = a.sidx(a.id0[fc]);
+                if (cnt > 1) p1 = a.sidx(a.id1[fc]);
                 if (p0 < 0 || (cnt > 1 && p1 < 0)) atomicAdd(&a.err->unknown, 1ull);
             }
         }
@@ -468,9 +454,6 @@ static SweepArgs make_args(lbg_block b, const lbg_fluid* fl) {
         a.v1 = b->v1;
         a.m0 = b->m0;
         a.m1 = b->m1;
-        a.cov_list = b->cov_list;
-        a.cov_n = b->cov_n;
-        a.cov_cap = (long long)b->L.nx * b->L.ny * b->L.nz;
         a.seg_list = b->seg_list;
         a.seg_n = b->seg_n;
         a.seg_cap = b->seg_cap;
@@ -478,6 +461,7 @@ static SweepArgs make_args(lbg_block b, const lbg_fluid* fl) {
         a.id1 = b->id1;
         a.snaps = b->snaps_d;
         a.n_snaps = b->n_snaps;
+        a.sidx = snap_index(b);
         for (int c = 0; c < 3; ++c) a.blk_lo[c] = b->lo[c];
         a.facc = b->facc;
         a.fused_used = b->fused_used;

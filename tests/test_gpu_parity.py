@@ -469,6 +469,51 @@ def test_mapping_and_solid_velocity_bitwise(gpu, oracle, lo):
     assert equal_bits(v1[c > 1], sv_o["v1"][c > 1])
 
 
+@pytest.mark.parametrize("id_step", [1, 1000])
+def test_mapping_dense_bins_bitwise(gpu, oracle, id_step):
+    """2197 small spheres (r = 0.75) on a jittered 1.8-cell lattice: ~125 candidates per 8^3
+    bin, so the bin-major mapping kernel stages them in several shared-memory chunks; 1662
+    two-entry cells. Fraction field, ids and solid velocities bitwise vs build_fraction_field /
+    set_solid_velocities. Dense ids use the id -> index table, sparse ids (step 1000) the
+    binary search."""
+    dims = (24, 24, 24)
+    rng = np.random.default_rng(3)
+    g = np.arange(1.2, 24, 1.8)
+    centers = np.array([(x, y, z) for z in g for y in g for x in g]) + (rng.random((len(g) ** 3, 3)) - 0.5) * 0.2
+    n = len(centers)
+    s = spheres(oracle, centers, [0.75] * n, ids=[id_step * i for i in range(n)],
+                u=0.01 * (rng.random((n, 3)) - 0.5), w=0.002 * (rng.random((n, 3)) - 0.5))
+    f_o, over = oracle.build_fraction_field((0, 0, 0), dims, s)
+    assert over == 0
+    sv_o, _ = oracle.set_solid_velocities((0, 0, 0), dims, s, f_o)
+    blk = gpu.Block(dims, coupling=True)
+    gpu.build_fraction_field(blk, s)
+    gpu.set_solid_velocities(blk, s)
+    f = blk.download_fraction()
+    c = f["count"]
+    assert np.array_equal(c, f_o["count"]) and (c == 2).sum() > 1000
+    assert equal_bits(f["btot"], f_o["btot"])
+    for e, (idk, bk, vk) in enumerate((("id0", "b0", "v0"), ("id1", "b1", "v1"))):
+        sel = c > e
+        assert np.array_equal(f[idk][sel], f_o[idk][sel])
+        assert equal_bits(f[bk][sel], f_o[bk][sel])
+    v0, v1 = blk.download_solid_velocity()
+    assert equal_bits(v0[c > 0], sv_o["v0"][c > 0])
+    assert equal_bits(v1[c > 1], sv_o["v1"][c > 1])
+
+
+def test_mapping_dense_bins_overfull_raises(gpu, oracle):
+    """The same lattice at 1.6-cell spacing has cells inside three spheres (77 of them)."""
+    g = np.arange(1.2, 24, 1.6)
+    centers = np.array([(x, y, z) for z in g for y in g for x in g]) + \
+        (np.random.default_rng(3).random((len(g) ** 3, 3)) - 0.5) * 0.2
+    s = spheres(oracle, centers, [0.75] * len(centers))
+    assert oracle.build_fraction_field((0, 0, 0), (24, 24, 24), s)[1] == 77
+    blk = gpu.Block((24, 24, 24), coupling=True)
+    with pytest.raises(gpu.NumericError, match="more than two particles"):
+        gpu.build_fraction_field(blk, s)
+
+
 def test_mapping_overfull_raises(gpu, oracle):
     """test_psm.cpp:166-176 — three particles through one cell."""
     dims = (40, 40, 40)
