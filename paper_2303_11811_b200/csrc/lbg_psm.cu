@@ -362,67 +362,74 @@ __global__ void __launch_bounds__(256) segment_kernel(const unsigned long long* 
     if (i == n - 1 || (unsigned)(keys[i + 1] >> 32) != p) end[p] = (int)(i + 1);
 }
 
-__global__ void __launch_bounds__(192) chain_kernel(const unsigned long long* __restrict__ keys,
-                                                    const int* __restrict__ start, const int* __restrict__ end,
-                                                    const lbg_snapshot* __restrict__ s, int n_snaps, BinGeom g,
-                                                    const double* __restrict__ m0, const double* __restrict__ m1,
-                                                    double* __restrict__ rows, int* __restrict__ used, int fast) {
-    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int p = tid / 6, d = tid % 6;
-    if (p >= n_snaps) return;
+// One warp per particle. The warp loads 32 consecutive entries of the particle's segment at a
+// time (coalesced keys, then the 32 momenta, all in flight together), each lane computes its
+// entry's six terms (f = m, t = cross(c - x, m), psm.cpp:294-296) into shared memory, and lanes
+// 0..5 — one per component — add the 32 terms in entry order with Neumaier steps (vec3.hpp:75-82),
+// so each component's (sum, comp) is the reference's serial walk exactly. The next batch's
+// loads are issued before the current batch is replayed. (Clearing the scratch from here, by
+// the loading lane, measured 10x slower than the separate clear_entries_kernel pass.)
+constexpr int kChainWarps = 8;
+
+__global__ void __launch_bounds__(32 * kChainWarps) chain_kernel(
+    const unsigned long long* __restrict__ keys, const int* __restrict__ start, const int* __restrict__ end,
+    const lbg_snapshot* __restrict__ s, int n_snaps, BinGeom g, const double* __restrict__ m0,
+    const double* __restrict__ m1, double* __restrict__ rows, int* __restrict__ used, int fast) {
+    __shared__ double terms[kChainWarps][32][7];  // padded row: lanes 0..5 read a column
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int p = blockIdx.x * kChainWarps + w;
+    if (p >= n_snaps) return;  // warp-uniform
     const int i0 = start[p], i1 = end[p];
-    double sum = 0.0, comp = 0.0;
     const double x0 = s[p].x[0], x1 = s[p].x[1], x2 = s[p].x[2];
-    // this lane's term of an entry (force component d, or torque component d-3:
-    // cross(c - x, m), psm.cpp:296), from the entry's cell and its momentum m
-    auto term = [&](long long c, double a0, double a1, double a2) {
-        if (d < 3) return d == 0 ? a0 : (d == 1 ? a1 : a2);
-        const int ci = (int)(c % g.dims[0]), cj = (int)((c / g.dims[0]) % g.dims[1]),
-                  ck = (int)(c / ((long long)g.dims[0] * g.dims[1]));
-        const double r0 = ((double)(g.lo[0] + ci) + 0.5) - x0;
-        const double r1 = ((double)(g.lo[1] + cj) + 0.5) - x1;
-        const double r2 = ((double)(g.lo[2] + ck) + 0.5) - x2;
-        return d == 3 ? r1 * a2 - r2 * a1 : (d == 4 ? r2 * a0 - r0 * a2 : r0 * a1 - r1 * a0);
-    };
-    auto add = [&](double v) {
-        if (fast) {
-            sum += v;
-        } else {
-            nm_add(sum, comp, v);
+    double (*tw)[7] = terms[w];
+    auto load = [&](int base, long long& c, double& a0, double& a1, double& a2) {
+        if (base + lane < i1) {
+            const unsigned long long key = keys[base + lane];
+            c = (long long)((key >> 1) & 0x7fffffffull);
+            const double* mp = ((key & 1ull) ? m1 : m0) + 3 * c;
+            a0 = mp[0];
+            a1 = mp[1];
+            a2 = mp[2];
         }
     };
-    // The terms are independent of the chain: a batch of keys, then the batch's momenta, are
-    // loaded back to back (branch-free, so they are in flight together), then the terms are
-    // added in entry order.
-    constexpr int kBatch = 8;
-    int i = i0;
-    for (; i + kBatch <= i1; i += kBatch) {
-        unsigned long long kk[kBatch];
-#pragma unroll
-        for (int t = 0; t < kBatch; ++t) kk[t] = keys[i + t];
-        long long c[kBatch];
-        double a0[kBatch], a1[kBatch], a2[kBatch];
-#pragma unroll
-        for (int t = 0; t < kBatch; ++t) {
-            c[t] = (long long)((kk[t] >> 1) & 0x7fffffffull);
-            const double* mp = ((kk[t] & 1ull) ? m1 : m0) + 3 * c[t];
-            a0[t] = mp[0];
-            a1[t] = mp[1];
-            a2[t] = mp[2];
+    long long c = 0;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    load(i0, c, a0, a1, a2);
+    double sum = 0.0, comp = 0.0;
+    for (int base = i0; base < i1; base += 32) {
+        const int n = min(32, i1 - base);
+        if (lane < n) {
+            const int ci = (int)(c % g.dims[0]), cj = (int)((c / g.dims[0]) % g.dims[1]),
+                      ck = (int)(c / ((long long)g.dims[0] * g.dims[1]));
+            const double r0 = ((double)(g.lo[0] + ci) + 0.5) - x0;
+            const double r1 = ((double)(g.lo[1] + cj) + 0.5) - x1;
+            const double r2 = ((double)(g.lo[2] + ck) + 0.5) - x2;
+            tw[lane][0] = a0;
+            tw[lane][1] = a1;
+            tw[lane][2] = a2;
+            tw[lane][3] = r1 * a2 - r2 * a1;
+            tw[lane][4] = r2 * a0 - r0 * a2;
+            tw[lane][5] = r0 * a1 - r1 * a0;
         }
-#pragma unroll
-        for (int t = 0; t < kBatch; ++t) add(term(c[t], a0[t], a1[t], a2[t]));
+        __syncwarp();
+        load(base + 32, c, a0, a1, a2);  // next batch in flight during the replay
+        if (lane < 6) {
+            for (int e = 0; e < n; ++e) {
+                const double v = tw[e][lane];
+                if (fast)
+                    sum += v;
+                else
+                    nm_add(sum, comp, v);
+            }
+        }
+        __syncwarp();
     }
-    for (; i < i1; ++i) {
-        const unsigned long long key = keys[i];
-        const long long c = (long long)((key >> 1) & 0x7fffffffull);
-        const double* mp = ((key & 1ull) ? m1 : m0) + 3 * c;
-        add(term(c, mp[0], mp[1], mp[2]));
+    if (lane < 6) {
+        const int slot = lane < 3 ? lane : 6 + (lane - 3);
+        rows[12 * (size_t)p + slot] = sum;
+        rows[12 * (size_t)p + slot + 3] = comp;
     }
-    const int slot = d < 3 ? d : 6 + (d - 3);
-    rows[12 * (size_t)p + slot] = sum;
-    rows[12 * (size_t)p + slot + 3] = comp;
-    if (d == 0) used[p] = i1 > i0;
+    if (lane == 0) used[p] = i1 > i0;
 }
 
 // the reference clears the scratch of every visited entry (psm.cpp:305)
@@ -793,7 +800,7 @@ lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int c
                 segment_kernel<<<(unsigned)((ne + 255) / 256), 256, 0, b->stream>>>(b->ekeys[1], ne, n, start, end);
                 LBG_LAUNCH_CHECK();
             }
-            chain_kernel<<<(unsigned)((6LL * n + 191) / 192), 192, 0, b->stream>>>(
+            chain_kernel<<<(unsigned)((n + kChainWarps - 1) / kChainWarps), 32 * kChainWarps, 0, b->stream>>>(
                 b->ekeys[1], start, end, b->snaps_d, n, g, b->m0, b->m1, b->red_rows, b->red_used,
                 mode == LBG_REDUCE_FAST);
             LBG_LAUNCH_CHECK();
