@@ -277,9 +277,12 @@ lbg_status lbg_observe(lbg_block b, const double f_ext[3], double out[6]) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, b->device);
     const int blocks = sms * 4;
     const size_t per = 2 * kObsVals + 1;
-    if (!b->obs_d) {
-        LBG_CUDA(cudaMalloc(&b->obs_d, sizeof(double) * per * blocks));
-        LBG_CUDA(cudaMallocHost(&b->obs_h, sizeof(double) * per * blocks));
+    if (!b->obs_d || !b->obs_h) {
+        size_t cap = 0;
+        if (lbg_status s = grow_device(b->obs_d, cap, (long long)(per * blocks), (long long)(per * blocks),
+                                       "cudaMalloc(observers)"))
+            return s;
+        if (!b->obs_h) LBG_CUDA(cudaMallocHost(&b->obs_h, sizeof(double) * per * blocks));
     }
     const double fx = f_ext ? f_ext[0] : 0.0, fy = f_ext ? f_ext[1] : 0.0, fz = f_ext ? f_ext[2] : 0.0;
     {
@@ -318,12 +321,9 @@ lbg_status lbg_moments(lbg_block b, int with_frac, double* out) {
     // z-chunks of at most ~64 MB staged on the device, copied out on the compute stream
     const long long kz = std::max(1LL, std::min<long long>(L.nz, (8LL << 20) / (slice * stride)));
     const size_t bytes = sizeof(double) * (size_t)(kz * slice * stride);
-    if (b->mom_cap < bytes) {
-        if (b->mom_d) LBG_CUDA(cudaFree(b->mom_d));
-        b->mom_d = nullptr;
-        LBG_CUDA(cudaMalloc(&b->mom_d, bytes));
-        b->mom_cap = bytes;
-    }
+    if (lbg_status s = grow_device(b->mom_d, b->mom_cap, (long long)(bytes / sizeof(double)),
+                                   (long long)(bytes / sizeof(double)), "cudaMalloc(moments)"))
+        return s;
     Span span(b, LBG_CAT_OTHER);
     for (long long k0 = 0; k0 < L.nz; k0 += kz) {
         const int nk = (int)std::min<long long>(kz, L.nz - k0);
@@ -449,13 +449,12 @@ lbg_status lbg_block_destroy(lbg_block b) {
     if (b->p2p) lbg_p2p_destroy(b);
     void* dev[] = {b->buf[0], b->buf[1], b->count, b->id0, b->id1, b->b0, b->b1, b->btot,
                    b->v0, b->v1, b->m0, b->m1, b->snaps_d, b->bin_count, b->bin_start,
-                   b->bin_items, b->red_rows, b->red_used, b->err_d, b->cov_n, b->facc, b->fused_used, b->scan_tmp, b->obs_d, b->mom_d,
-                   b->seg_list, b->seg_n, b->tile_buf, b->snap_tab};
+                   b->bin_items, b->red_rows, b->red_used, b->err_d, b->cov_n, b->facc, b->fused_used,
+                   b->scan_tmp, b->obs_d, b->mom_d, b->seg_list, b->seg_n, b->tile_buf, b->snap_tab,
+                   b->ekeys[0], b->ekeys[1], b->sort_tmp, b->red_seg};
     for (void* p : dev)
         if (p) cudaFree(p);
     void* host[] = {b->snaps_h, b->err_h, b->red_rows_h, b->red_used_h, b->obs_h, b->cn_h};
-    for (void* p : {(void*)b->ekeys[0], (void*)b->ekeys[1], b->sort_tmp, (void*)b->red_seg})
-        if (p) cudaFree(p);
     for (void* p : host)
         if (p) cudaFreeHost(p);
     for (auto& s : b->spans) {
@@ -520,11 +519,14 @@ static lbg_status copy_pdf_pinned(lbg_block b, double* dev, const double* host_i
     const long long rows = (long long)kQ * L.py * L.pz;
     const long long chunk_rows = std::max<long long>(1, (256ll << 20) / (8ll * w));
     const size_t chunk_bytes = sizeof(double) * (size_t)chunk_rows * w;
-    if (!b->xfer[0]) {
+    if (!b->xfer[0] || !b->xfer[1]) {
         for (int s = 0; s < 2; ++s) {
-            LBG_CUDA(cudaMalloc(&b->xfer[s], chunk_bytes));
-            LBG_CUDA(cudaEventCreateWithFlags(&b->ev_copy[s], cudaEventDisableTiming));
-            LBG_CUDA(cudaEventCreateWithFlags(&b->ev_done[s], cudaEventDisableTiming));
+            size_t cap = 0;
+            if (lbg_status st = grow_device(b->xfer[s], cap, (long long)(chunk_bytes / sizeof(double)),
+                                            (long long)(chunk_bytes / sizeof(double)), "cudaMalloc(transfer staging)"))
+                return st;
+            if (!b->ev_copy[s]) LBG_CUDA(cudaEventCreateWithFlags(&b->ev_copy[s], cudaEventDisableTiming));
+            if (!b->ev_done[s]) LBG_CUDA(cudaEventCreateWithFlags(&b->ev_done[s], cudaEventDisableTiming));
             LBG_CUDA(cudaEventRecord(b->ev_done[s], b->stream));
         }
     }

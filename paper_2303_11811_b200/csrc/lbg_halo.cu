@@ -356,11 +356,9 @@ lbg_status lbg_halo_stage(lbg_block b, const int (*offs)[3], int n) {
         slab_box(b->L, offs[t], false, lo, ext);
         const size_t cnt = (size_t)kQ * ext[0] * ext[1] * ext[2];
         const int key = (offs[t][0] + 1) * 9 + (offs[t][1] + 1) * 3 + (offs[t][2] + 1);
-        if (b->stage_cap[key] < cnt) {
-            if (b->stage[key]) cudaFree(b->stage[key]);
-            LBG_CUDA(cudaMalloc(&b->stage[key], sizeof(double) * cnt));
-            b->stage_cap[key] = cnt;
-        }
+        if (lbg_status s = grow_device(b->stage[key], b->stage_cap[key], (long long)cnt, (long long)cnt,
+                                       "cudaMalloc(halo staging)"))
+            return s;
         slab_copy_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, b->stream>>>(
             b->src(), b->L, lo[0], lo[1], lo[2], ext[0], ext[1], ext[2], b->stage[key], 1);
         LBG_LAUNCH_CHECK();
@@ -384,11 +382,9 @@ lbg_status lbg_halo_fetch(lbg_block dst, const int dir[3], lbg_block src) {
     LBG_CUDA(cudaStreamWaitEvent(dst->stream, src->ev_stage, 0));
     const double* from = src->stage[key];
     if (src->device != dst->device) {
-        if (dst->recv_cap < cnt) {
-            if (dst->recv_buf) cudaFree(dst->recv_buf);
-            LBG_CUDA(cudaMalloc(&dst->recv_buf, sizeof(double) * cnt));
-            dst->recv_cap = cnt;
-        }
+        if (lbg_status s = grow_device(dst->recv_buf, dst->recv_cap, (long long)cnt, (long long)cnt,
+                                       "cudaMalloc(halo receive)"))
+            return s;
         LBG_CUDA(cudaMemcpyPeerAsync(dst->recv_buf, dst->device, from, src->device, sizeof(double) * cnt,
                                      dst->stream));
         from = dst->recv_buf;

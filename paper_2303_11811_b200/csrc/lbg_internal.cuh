@@ -163,7 +163,7 @@ struct lbg_block_s {
     int* bin_items = nullptr;
     long long bin_items_cap = 0;
     long long n_bins_cap = 0;
-    void* scan_tmp = nullptr;
+    unsigned char* scan_tmp = nullptr;  // CUB workspace
     size_t scan_tmp_bytes = 0;
     // hydro reduction scratch
     double* red_rows = nullptr;  // n_snaps x 12
@@ -174,7 +174,7 @@ struct lbg_block_s {
     // sorted-entry PARITY reduction: entry keys (in/out), radix-sort workspace, segments
     unsigned long long* ekeys[2] = {nullptr, nullptr};
     long long ekeys_cap = 0;
-    void* sort_tmp = nullptr;
+    unsigned char* sort_tmp = nullptr;
     size_t sort_tmp_bytes = 0;
     int* red_seg = nullptr;  // start[n], end[n]
     int red_seg_cap = 0;
@@ -256,6 +256,25 @@ __device__ __forceinline__ void covered_count(int cnt, int* n) {
 lbg_status set_error(lbg_status s, const std::string& msg);
 lbg_status cuda_check(cudaError_t e, const char* what);
 void count_launch();
+
+// Grow-only device buffer: holds at least `need` elements afterwards (`want` when it has to
+// grow, for geometric growth). The old buffer is freed first; on failure the pointer is null
+// and the capacity 0, so no later call sees a stale capacity over a freed buffer. Callers
+// order the free after pending work (the buffers are per block and used on its streams).
+template <class T, class C>
+inline lbg_status grow_device(T*& p, C& cap, long long need, long long want, const char* what) {
+    if (p && (long long)cap >= need) return LBG_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    const long long n = need > want ? need : want;
+    void* q = nullptr;
+    const cudaError_t e = cudaMalloc(&q, sizeof(T) * (size_t)n);
+    if (e != cudaSuccess) return cuda_check(e, what);
+    p = static_cast<T*>(q);
+    cap = static_cast<C>(n);
+    return LBG_OK;
+}
 
 // timing spans around a launch (no-ops unless timing is on)
 struct Span {

@@ -466,12 +466,12 @@ static lbg_status upload_snapshots(lbg_block b, const lbg_snapshot* snaps, int n
         LBG_CUDA(cudaStreamSynchronize(b->side));
         LBG_CUDA(cudaStreamSynchronize(b->stream));
         if (b->snaps_h) cudaFreeHost(b->snaps_h);
-        if (b->snaps_d) cudaFree(b->snaps_d);
         b->snaps_h = nullptr;
-        b->snaps_d = nullptr;
         const int cap = std::max(n, 2 * b->snaps_cap);
+        b->snaps_cap = 0;
         LBG_CUDA(cudaMallocHost(&b->snaps_h, sizeof(lbg_snapshot) * cap));
-        LBG_CUDA(cudaMalloc(&b->snaps_d, sizeof(lbg_snapshot) * cap));
+        int dcap = 0;
+        if (lbg_status s = grow_device(b->snaps_d, dcap, cap, cap, "cudaMalloc(snapshots)")) return s;
         b->snaps_cap = cap;
     }
     // staging buffer may still feed the previous copy
@@ -491,12 +491,9 @@ static lbg_status upload_snapshots(lbg_block b, const lbg_snapshot* snaps, int n
     if (n > 0) {
         const long long range = (long long)snaps[n - 1].id - snaps[0].id + 1;
         if (range <= 4LL * n + 4096) {
-            if (range > b->snap_tab_cap) {
-                if (b->snap_tab) LBG_CUDA(cudaFree(b->snap_tab));
-                b->snap_tab = nullptr;
-                b->snap_tab_cap = std::max(range, 2 * b->snap_tab_cap);
-                LBG_CUDA(cudaMalloc(&b->snap_tab, sizeof(int) * b->snap_tab_cap));
-            }
+            if (lbg_status s = grow_device(b->snap_tab, b->snap_tab_cap, range, 2 * b->snap_tab_cap,
+                                           "cudaMalloc(snapshot index)"))
+                return s;
             b->snap_id_min = snaps[0].id;
             b->snap_range = (int)range;
             LBG_CUDA(cudaMemsetAsync(b->snap_tab, 0xff, sizeof(int) * range, b->stream));
@@ -508,11 +505,11 @@ static lbg_status upload_snapshots(lbg_block b, const lbg_snapshot* snaps, int n
 }
 
 static lbg_status ensure_bins(lbg_block b, long long nbins) {
-    if (nbins <= b->n_bins_cap) return LBG_OK;
-    if (b->bin_count) cudaFree(b->bin_count);
-    if (b->bin_start) cudaFree(b->bin_start);
-    LBG_CUDA(cudaMalloc(&b->bin_count, sizeof(int) * 2 * nbins));  // count + cursor
-    LBG_CUDA(cudaMalloc(&b->bin_start, sizeof(int) * (nbins + 1)));
+    if (nbins <= b->n_bins_cap && b->bin_count && b->bin_start) return LBG_OK;
+    b->n_bins_cap = 0;
+    long long c1 = 0, c2 = 0;
+    if (lbg_status s = grow_device(b->bin_count, c1, 2 * nbins, 2 * nbins, "cudaMalloc(bins)")) return s;  // count + cursor
+    if (lbg_status s = grow_device(b->bin_start, c2, nbins + 1, nbins + 1, "cudaMalloc(bins)")) return s;
     b->n_bins_cap = nbins;
     return LBG_OK;
 }
@@ -545,12 +542,13 @@ static lbg_status need_coupling(lbg_block b) {
 // per-particle accumulators of LBG_FORCE_FUSED, zeroed once per step (at the mapping)
 static lbg_status prepare_fused(lbg_block b, int n) {
     if (b->force_mode != LBG_FORCE_FUSED) return LBG_OK;
-    if (n > b->facc_cap || !b->facc) {
-        if (b->facc) cudaFree(b->facc);
-        if (b->fused_used) cudaFree(b->fused_used);
-        b->facc_cap = std::max(n, std::max(1, 2 * b->facc_cap));
-        LBG_CUDA(cudaMalloc(&b->facc, sizeof(double) * 6 * b->facc_cap));
-        LBG_CUDA(cudaMalloc(&b->fused_used, sizeof(int) * b->facc_cap));
+    if (n > b->facc_cap || !b->facc || !b->fused_used) {
+        const int cap = std::max(n, std::max(1, 2 * b->facc_cap));
+        b->facc_cap = 0;
+        long long c1 = 0, c2 = 0;
+        if (lbg_status s = grow_device(b->facc, c1, 6LL * cap, 6LL * cap, "cudaMalloc(fused)")) return s;
+        if (lbg_status s = grow_device(b->fused_used, c2, cap, cap, "cudaMalloc(fused)")) return s;
+        b->facc_cap = cap;
     }
     LBG_CUDA(cudaMemsetAsync(b->facc, 0, sizeof(double) * 6 * b->facc_cap, b->stream));
     LBG_CUDA(cudaMemsetAsync(b->fused_used, 0, sizeof(int) * b->facc_cap, b->stream));
@@ -586,11 +584,9 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
     // persistent scan workspace (no per-call allocation)
     size_t tmp_bytes = 0;
     cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, cnt, b->bin_start + 1, (int)nbins, b->stream);
-    if (tmp_bytes > b->scan_tmp_bytes) {
-        if (b->scan_tmp) cudaFree(b->scan_tmp);
-        LBG_CUDA(cudaMalloc(&b->scan_tmp, tmp_bytes));
-        b->scan_tmp_bytes = tmp_bytes;
-    }
+    if (lbg_status s = grow_device(b->scan_tmp, b->scan_tmp_bytes, (long long)tmp_bytes, (long long)tmp_bytes,
+                                   "cudaMalloc(scan_tmp)"))
+        return s;
     LBG_CUDA(cudaMemsetAsync(b->bin_start, 0, sizeof(int), b->stream));
     cub::DeviceScan::InclusiveSum(b->scan_tmp, tmp_bytes, cnt, b->bin_start + 1, (int)nbins, b->stream);
     LBG_LAUNCH_CHECK();
@@ -603,11 +599,9 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
             nb *= std::min<long long>(g.nb[d], (long long)((2.0 * (snaps[p].r + 0.5) + 4.0) / kBin) + 2);
         bound += nb;
     }
-    if (bound > b->bin_items_cap) {
-        if (b->bin_items) cudaFree(b->bin_items);
-        b->bin_items_cap = std::max<long long>(bound, 2 * b->bin_items_cap);
-        LBG_CUDA(cudaMalloc(&b->bin_items, sizeof(int) * b->bin_items_cap));
-    }
+    if (lbg_status s = grow_device(b->bin_items, b->bin_items_cap, bound, 2 * b->bin_items_cap,
+                                   "cudaMalloc(bin items)"))
+        return s;
     if (n > 0) {
         bin_fill_kernel<<<(n + 127) / 128, 128, 0, b->stream>>>(b->snaps_d, n, g, b->bin_start, cursor,
                                                                 b->bin_items);
@@ -662,21 +656,20 @@ lbg_status lbg_set_solid_velocities(lbg_block b, const lbg_snapshot* snaps, int 
 // LBG_FORCE_FUSED: the sweep already summed; copy the accumulators out
 // per-particle output rows (device + pinned host), grown geometrically, kept across steps
 static lbg_status reserve_rows(lbg_block b, int n) {
-    if (n > b->red_cap) {
-        if (b->red_rows) cudaFree(b->red_rows);
-        if (b->red_used) cudaFree(b->red_used);
-        if (b->red_rows_h) cudaFreeHost(b->red_rows_h);
-        if (b->red_used_h) cudaFreeHost(b->red_used_h);
-        b->red_cap = std::max(n, 2 * b->red_cap);
-        LBG_CUDA(cudaMalloc(&b->red_rows, sizeof(double) * 12 * b->red_cap + 16));
-        LBG_CUDA(cudaMalloc(&b->red_used, sizeof(int) * b->red_cap));
-        LBG_CUDA(cudaMallocHost(&b->red_rows_h, sizeof(double) * 12 * b->red_cap + 16));
-        LBG_CUDA(cudaMallocHost(&b->red_used_h, sizeof(int) * b->red_cap));
-    }
-    if (!b->red_rows) {
-        LBG_CUDA(cudaMalloc(&b->red_rows, 16 + sizeof(double) * 12));
-        LBG_CUDA(cudaMallocHost(&b->red_rows_h, 16 + sizeof(double) * 12));
-    }
+    const int need = std::max(n, 1);
+    if (need <= b->red_cap) return LBG_OK;
+    const int cap = std::max(need, 2 * b->red_cap);
+    b->red_cap = 0;  // set again only when all four buffers exist
+    long long c1 = 0, c2 = 0;
+    if (lbg_status s = grow_device(b->red_rows, c1, 12LL * cap, 12LL * cap, "cudaMalloc(partials)")) return s;
+    if (lbg_status s = grow_device(b->red_used, c2, cap, cap, "cudaMalloc(partials)")) return s;
+    if (b->red_rows_h) cudaFreeHost(b->red_rows_h);
+    if (b->red_used_h) cudaFreeHost(b->red_used_h);
+    b->red_rows_h = nullptr;
+    b->red_used_h = nullptr;
+    LBG_CUDA(cudaMallocHost(&b->red_rows_h, sizeof(double) * 12 * cap));
+    LBG_CUDA(cudaMallocHost(&b->red_used_h, sizeof(int) * cap));
+    b->red_cap = cap;
     return LBG_OK;
 }
 
@@ -737,29 +730,35 @@ lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int c
         LBG_CUDA(cudaStreamSynchronize(b->stream));
         const int cn[2] = {b->cn_h[0], b->cn_h[1]};
         const long long ne = (long long)cn[0] + 2LL * cn[1];
-        if (!b->ekeys[0]) {
+        if (!b->ekeys[0] || !b->ekeys[1] || !b->sort_tmp) {
             // sized once for the worst case (two entries per cell): steady-state steps never
             // allocate (cudaFree/cudaMalloc serialise all block-worker threads of a process)
-            b->ekeys_cap = std::max(2 * cells, 1LL);
-            LBG_CUDA(cudaMalloc(&b->ekeys[0], sizeof(unsigned long long) * b->ekeys_cap));
-            LBG_CUDA(cudaMalloc(&b->ekeys[1], sizeof(unsigned long long) * b->ekeys_cap));
+            const long long cap = std::max(2 * cells, 1LL);
+            long long c1 = 0, c2 = 0;
+            if (lbg_status s = grow_device(b->ekeys[0], c1, cap, cap, "cudaMalloc(entry keys)")) return s;
+            if (lbg_status s = grow_device(b->ekeys[1], c2, cap, cap, "cudaMalloc(entry keys)")) return s;
+            b->ekeys_cap = cap;
             size_t tmp = 0;
-            cub::DeviceRadixSort::SortKeys(nullptr, tmp, b->ekeys[0], b->ekeys[1], (int)b->ekeys_cap, 0, 64,
-                                           b->stream);
-            LBG_CUDA(cudaMalloc(&b->sort_tmp, tmp));
-            b->sort_tmp_bytes = tmp;
+            cub::DeviceRadixSort::SortKeys(nullptr, tmp, b->ekeys[0], b->ekeys[1], (int)cap, 0, 64, b->stream);
+            if (lbg_status s = grow_device(b->sort_tmp, b->sort_tmp_bytes, (long long)tmp, (long long)tmp,
+                                           "cudaMalloc(sort workspace)"))
+                return s;
         }
-        if (std::max(n, 1) > b->red_seg_cap) {
-            if (b->red_seg) cudaFree(b->red_seg);
-            b->red_seg_cap = std::max(std::max(n, 1), 2 * b->red_seg_cap);
-            LBG_CUDA(cudaMalloc(&b->red_seg, sizeof(int) * 2 * b->red_seg_cap));
+        if (std::max(n, 1) > b->red_seg_cap || !b->red_seg) {
+            const int cap = std::max(std::max(n, 1), 2 * b->red_seg_cap);
+            int c1 = 0;
+            b->red_seg_cap = 0;
+            if (lbg_status s = grow_device(b->red_seg, c1, 2LL * cap, 2LL * cap, "cudaMalloc(segments)")) return s;
+            b->red_seg_cap = cap;
         }
         if (ne > 0) {
             const long long tiles = (cells + kEntryTile - 1) / kEntryTile;
-            if (tiles > b->tile_cap) {
-                if (b->tile_buf) cudaFree(b->tile_buf);
+            if (tiles > b->tile_cap || !b->tile_buf) {
+                long long c1 = 0;
+                b->tile_cap = 0;
+                if (lbg_status s = grow_device(b->tile_buf, c1, 2 * tiles, 2 * tiles, "cudaMalloc(entry tiles)"))
+                    return s;
                 b->tile_cap = tiles;
-                LBG_CUDA(cudaMalloc(&b->tile_buf, sizeof(int) * 2 * tiles));
             }
             int* sums = b->tile_buf;
             int* offs = b->tile_buf + b->tile_cap;
@@ -767,11 +766,9 @@ lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int c
             LBG_LAUNCH_CHECK();
             size_t tmp = 0;
             cub::DeviceScan::ExclusiveSum(nullptr, tmp, sums, offs, (int)tiles, b->stream);
-            if (tmp > b->scan_tmp_bytes) {
-                if (b->scan_tmp) cudaFree(b->scan_tmp);
-                LBG_CUDA(cudaMalloc(&b->scan_tmp, tmp));
-                b->scan_tmp_bytes = tmp;
-            }
+            if (lbg_status s = grow_device(b->scan_tmp, b->scan_tmp_bytes, (long long)tmp, (long long)tmp,
+                                           "cudaMalloc(scan_tmp)"))
+                return s;
             cub::DeviceScan::ExclusiveSum(b->scan_tmp, tmp, sums, offs, (int)tiles, b->stream);
             entry_emit_kernel<<<(unsigned)tiles, kEntryThreads, 0, b->stream>>>(
                 b->count, cells, offs, b->id0, b->id1, snap_index(b), n, b->ekeys[0], b->err_d);
@@ -782,11 +779,9 @@ lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int c
             tmp = 0;
             cub::DeviceRadixSort::SortKeys(nullptr, tmp, b->ekeys[0], b->ekeys[1], (int)ne, 32, 32 + bits,
                                            b->stream);
-            if (tmp > b->sort_tmp_bytes) {
-                if (b->sort_tmp) cudaFree(b->sort_tmp);
-                LBG_CUDA(cudaMalloc(&b->sort_tmp, tmp));
-                b->sort_tmp_bytes = tmp;
-            }
+            if (lbg_status s = grow_device(b->sort_tmp, b->sort_tmp_bytes, (long long)tmp, (long long)tmp,
+                                           "cudaMalloc(sort_tmp)"))
+                return s;
             cub::DeviceRadixSort::SortKeys(b->sort_tmp, tmp, b->ekeys[0], b->ekeys[1], (int)ne, 32, 32 + bits,
                                            b->stream);
             LBG_LAUNCH_CHECK();

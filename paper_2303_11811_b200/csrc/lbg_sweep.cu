@@ -11,12 +11,15 @@
 //   K1 sweep_box   — one CellBox, 3-D grid; thread x maps to global i with the chunk origin
 //                    aligned to 32 cells, so a warp's loads/stores of a q-plane are two 128-B
 //                    lines (the pulled x-neighbour costs one extra sector per warp, from L2).
+//   K1 sweep_pair  — the same sweep with 128-bit accesses (two cells per lane), selected by
+//                    LBG_SWEEP_PAIR=1; measured 2 % slower than sweep_box at 512^3.
 //   K1 sweep_flat  — up to 8 boxes in one launch (the boundary_shell boxes, field.cpp:55-72).
 //   K2 psm_seg     — the aligned 32-cell row segments that hold covered cells (count > 0),
-//                    from the segment lists the mapping kernel writes; K1 skips exactly those
+//                    from the segment lists the mapping pass writes; K1 skips exactly those
 //                    segments, so each DRAM sector is swept by one kernel. Segments with only
-//                    one-entry cells use the pair-scheduled operator (~80 registers), segments
-//                    with a two-entry cell the general one (~170); the fluid majority keeps the
+//                    one-entry cells run the pair-scheduled one-entry operator on every lane
+//                    (~90 registers; fluid lanes with B = 0 when unforced), segments with a
+//                    two-entry cell the general operator (~220); the fluid majority keeps the
 //                    70-register SRT kernel (the paper's fused A100 kernel ran at 196 registers,
 //                    12.5 % occupancy).
 // Periodic wrap: for axes in b->wrap the pull reads the wrapped interior cell directly
@@ -524,7 +527,7 @@ static void launch_flat(const SweepArgs& a, cudaStream_t s) {
     sweep_flat_kernel<kForced, kSkip><<<(unsigned)((n + T - 1) / T), T, 0, s>>>(a);
 }
 
-static void launch_psm_list(lbg_block b, const SweepArgs& a, bool forced) {
+static void launch_psm_segments(lbg_block b, const SweepArgs& a, bool forced) {
     // persistent grid: 4 CTAs of 128 per SM, the list length is read on the device
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, b->device);
@@ -584,7 +587,7 @@ lbg_status lbg_sweep(lbg_block b, const lbg_fluid* fl, const lbg_box* range) {
     if (b->coupling) {
         fo ? launch_box<true, true>(a, b->stream) : launch_box<false, true>(a, b->stream);
         LBG_LAUNCH_CHECK();
-        launch_psm_list(b, a, fo);
+        launch_psm_segments(b, a, fo);
     } else if (pair_sweep()) {
         fo ? launch_pair<true>(a, b->stream) : launch_pair<false>(a, b->stream);
     } else {
