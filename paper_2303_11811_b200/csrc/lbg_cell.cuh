@@ -132,9 +132,11 @@ __device__ __forceinline__ bool psm_cell(double (&f)[kQ], double inv_tau, Force 
             const int qb = opposite(q);
             const double c_solid = (f[qb] - feq_f[qb]) - (f[q] - feq_p[q]);
             fout[q] += be[e] * c_solid;
-            mx -= c_solid * (double)cx(q);
-            my -= c_solid * (double)cy(q);
-            mz -= c_solid * (double)cz(q);
+            // c_q = 0 terms subtract a signed zero from a sum that starts at +0 and
+            // can never become -0 (x - x is +0), so they are skipped exactly
+            if (cx(q) != 0) mx -= c_solid * (double)cx(q);
+            if (cy(q) != 0) my -= c_solid * (double)cy(q);
+            if (cz(q) != 0) mz -= c_solid * (double)cz(q);
         }
         m_out[e][0] = be[e] * mx;
         m_out[e][1] = be[e] * my;
@@ -227,9 +229,11 @@ __device__ __forceinline__ bool psm_cell_opt(double (&f)[kQ], double inv_tau, Fo
         for (int q = 0; q < kQ; ++q) {
             const double c_solid = d[opposite(q)] - (f[q] - fp[q]);
             fout[q] += be[e] * c_solid;
-            mx -= c_solid * (double)cx(q);
-            my -= c_solid * (double)cy(q);
-            mz -= c_solid * (double)cz(q);
+            // c_q = 0 terms subtract a signed zero from a sum that starts at +0 and
+            // can never become -0 (x - x is +0), so they are skipped exactly
+            if (cx(q) != 0) mx -= c_solid * (double)cx(q);
+            if (cy(q) != 0) my -= c_solid * (double)cy(q);
+            if (cz(q) != 0) mz -= c_solid * (double)cz(q);
         }
         m_out[e][0] = be[e] * mx;
         m_out[e][1] = be[e] * my;
@@ -263,9 +267,9 @@ __device__ __forceinline__ bool psm_cell_one(const double (&f)[kQ], double inv_t
         const double coll = inv_tau * (feq_q - fq);
         const double base_out = fq + fluid_w * (kForced ? coll + force : coll);
         const double c_solid = (fqb - feq_qb) - (fq - fp_q);
-        mx -= c_solid * (double)cx(q);
-        my -= c_solid * (double)cy(q);
-        mz -= c_solid * (double)cz(q);
+        if (cx(q) != 0) mx -= c_solid * (double)cx(q);  // c_q = 0 terms are exact no-ops
+        if (cy(q) != 0) my -= c_solid * (double)cy(q);
+        if (cz(q) != 0) mz -= c_solid * (double)cz(q);
         dst[q * plane + base] = base_out + be * c_solid;
     };
     {
