@@ -166,7 +166,8 @@ def test_pair_kernel_variant():
     env = dict(os.environ, LBG_SWEEP_PAIR="1")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
                         "test_gpu_parity.py::test_sweep_warp_edges_bitwise",
-                        "test_gpu_parity.py::test_fused_sweep_bitwise"], env=env,
+                        "test_gpu_parity.py::test_fused_sweep_bitwise",
+                        "test_gpu_parity.py::test_unstable_cell_count_matches_reference"], env=env,
                        cwd=os.path.dirname(os.path.abspath(__file__)), capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
@@ -295,6 +296,41 @@ def test_stability_guard_raises(gpu):
     gpu.fill_periodic_ghosts(blk, ALL_P)
     with pytest.raises(gpu.NumericError, match="fluid instability"):
         gpu.collide_stream(blk, gpu.FluidParams(0.51), gpu.CellBox((0, 0, 0), dims))
+
+
+@pytest.mark.parametrize("coupled", [False, True])
+def test_unstable_cell_count_matches_reference(gpu, oracle, coupled):
+    """lbm.cpp:47-48 / psm.cpp:260-261: the NumericError message carries the number of unstable
+    cells; the device ballot count (K1 fluid warps, K2 fluid and covered lanes, the shell)
+    equals the oracle's count, cells scattered over row segments of both kinds."""
+    import re
+    dims = (70, 9, 6)
+    src0 = random_pdf(dims, seed=123)
+    rng = np.random.default_rng(5)
+    inner = interior(src0)
+    for _ in range(37):  # push |u|^2 past 0.57^2 in scattered cells
+        i, j, k = rng.integers(0, dims[0]), rng.integers(0, dims[1]), rng.integers(0, dims[2])
+        inner[1, k, j, i] = 2.0
+    src_o = src0.copy()
+    oracle.fill_periodic(dims, src_o, ALL_P)
+    dst_o = np.zeros_like(src_o)
+    tau, fext = 0.7, (0.0, 0.0, 0.0)
+    blk = gpu.Block(dims, coupling=coupled)
+    if coupled:
+        frac, sv = random_fraction(dims, seed=6, cover=0.3)
+        scr = new_scratch(dims)
+        bad = oracle.psm_collide_stream(dims, src_o, dst_o, tau, fext, (0, 0, 0), dims, frac, sv, scr)
+        blk.upload_fraction(frac)
+        blk.upload_solid_velocity(sv["v0"], sv["v1"])
+    else:
+        bad = oracle.collide_stream(dims, src_o, dst_o, tau, fext, (0, 0, 0), dims)
+    assert 10 < bad <= 37
+    blk.upload_src(src0)
+    blk.fill_periodic(ALL_P, full=True)
+    blk.sweep(gpu.FluidParams(tau, fext), gpu.CellBox((0, 0, 0), dims))
+    with pytest.raises(gpu.NumericError) as e:
+        blk.sync()
+    assert int(re.search(r"instability[^:]*: (\d+)", str(e.value)).group(1)) == bad
 
 
 def test_config_validation_errors(gpu):
