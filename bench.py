@@ -244,6 +244,18 @@ def coupled_step(steps, with_reference, ref_steps=1, blocks=(1, 1, 1), workers=1
     return out
 
 
+def host_mem_available():
+    """MemAvailable of this host in bytes (None if unknown)."""
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return None
+
+
 # --------------------------------------------------------------------------- GPU path
 def run_lbg(args):
     import torch
@@ -273,7 +285,26 @@ def run_lbg(args):
 
     # x, y (and z on one GPU) are periodic and spanned by the block: wrapped in-kernel;
     # z between GPUs: NCCL halo behind the inner sweep, or the outer sweep's P2P stores
-    st = FluidStepper(dec, rank, p, device=local, uid=uid[0], halo=args.halo, allgather=allgather)
+    halo = args.halo
+    st = None
+    if N > 1 and halo == "p2p":
+        # the P2P mapping is opened per rank after the handle exchange; if any rank cannot
+        # map its neighbours, every rank falls back to the NCCL halo (decided collectively)
+        err = None
+        try:
+            st = FluidStepper(dec, rank, p, device=local, uid=uid[0], halo="p2p", allgather=allgather)
+        except Exception as e:  # noqa: BLE001 — reported, then the NCCL path is used
+            err = f"{type(e).__name__}: {e}"
+        errs = [x for x in allgather(err) if x]
+        if errs:
+            if rank == 0:
+                print(f"P2P halo unavailable ({errs[0]}); using the NCCL halo", file=sys.stderr)
+            if st is not None:
+                st.block.close()
+                st = None
+            halo = "nccl"
+    if st is None:
+        st = FluidStepper(dec, rank, p, device=local, uid=uid[0], halo=halo, allgather=allgather)
     blk = st.block
     blk.init_shear_wave(domain)
     if N > 1:
@@ -346,28 +377,37 @@ def run_lbg(args):
     import numpy as np
     from paper_2303_11811_b200 import lbg as abi
     pdf_bytes = 8 * 19 * (n + 2) ** 3
-    hp = C.c_void_p()
-    lbdem.check(abi.load().lbg_host_alloc(pdf_bytes, C.byref(hp)))
-    host = np.ctypeslib.as_array(C.cast(hp, C.POINTER(C.c_double)), shape=(19, n + 2, n + 2, n + 2))
-    lbdem.check(abi.load().lbg_download_src(blk.h, hp))  # the current state as the job's input
-    barrier()
-    t0 = time.perf_counter()
-    lbdem.check(abi.load().lbg_upload_src(blk.h, hp))
-    tl0 = time.perf_counter()
-    for _ in range(args.steps):
-        step()
-        blk.sync()  # lbg_sync: D2H of the 3 error counters, raises NumericError/SyncError
-    tl1 = time.perf_counter()
-    lbdem.check(abi.load().lbg_download_src(blk.h, hp))
-    t1 = time.perf_counter()
-    barrier()
-    e2e_s = max_over_ranks(t1 - t0)
-    loop_s = max_over_ranks(tl1 - tl0)
-    e2e_mlups = cells * N * args.steps / e2e_s / 1e6
-    loop_mlups = cells * N * args.steps / loop_s / 1e6
-    finite = bool(np.isfinite(host[:, n // 2, n // 2, 1:5]).all())
-    del host
-    abi.load().lbg_host_free(hp)
+    # every rank of this host pins its own full host PdfField: run the job only if they all fit
+    # comfortably in the host's available memory (an 8-GPU box must not be driven out of RAM)
+    local_ranks = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+    avail = host_mem_available()
+    fits = avail is None or local_ranks * pdf_bytes <= 0.6 * avail
+    fits = all(allgather(fits)) if N > 1 else fits
+    e2e_mlups = loop_mlups = None
+    finite = None
+    if fits:
+        hp = C.c_void_p()
+        lbdem.check(abi.load().lbg_host_alloc(pdf_bytes, C.byref(hp)))
+        host = np.ctypeslib.as_array(C.cast(hp, C.POINTER(C.c_double)), shape=(19, n + 2, n + 2, n + 2))
+        lbdem.check(abi.load().lbg_download_src(blk.h, hp))  # the current state as the job's input
+        barrier()
+        t0 = time.perf_counter()
+        lbdem.check(abi.load().lbg_upload_src(blk.h, hp))
+        tl0 = time.perf_counter()
+        for _ in range(args.steps):
+            step()
+            blk.sync()  # lbg_sync: D2H of the 3 error counters, raises NumericError/SyncError
+        tl1 = time.perf_counter()
+        lbdem.check(abi.load().lbg_download_src(blk.h, hp))
+        t1 = time.perf_counter()
+        barrier()
+        e2e_s = max_over_ranks(t1 - t0)
+        loop_s = max_over_ranks(tl1 - tl0)
+        e2e_mlups = cells * N * args.steps / e2e_s / 1e6
+        loop_mlups = cells * N * args.steps / loop_s / 1e6
+        finite = bool(np.isfinite(host[:, n // 2, n // 2, 1:5]).all())
+        del host
+        abi.load().lbg_host_free(hp)
 
     out = None
     if rank == 0:
@@ -388,10 +428,10 @@ def run_lbg(args):
             "config": {"workload": (f"config 2: pure-fluid D3Q19 SRT {n}^3 periodic, 1 GPU" if N == 1 else
                                     f"config 4: pure-fluid D3Q19 SRT weak scaling {n}^3 per GPU, "
                                     f"{n}x{n}x{n * N} periodic z-slabs, halo "
-                                    + ("fused into the outer sweep (NVLink P2P stores)" if args.halo == "p2p"
+                                    + ("fused into the outer sweep (NVLink P2P stores)" if halo == "p2p"
                                        else "over NCCL hidden behind the inner sweep")),
                        "tau": args.tau, "cells_per_gpu": cells, "parallelism": f"z-slab x{N}",
-                       "halo": args.halo if N > 1 else None,
+                       "halo": halo if N > 1 else None,
                        "l2": f"inputs larger than L2 ({2 * 19 * 8 * cells / 1e9:.1f} GB PDF working set)"},
             "mlups_per_gpu": round(mlups / N, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -402,14 +442,18 @@ def run_lbg(args):
                          "sweep_launches": sweep_n},
             "hbm_roofline_frac_of_step": round(BYTES_PER_LUP * cells / (ms_step / 1e3) / 1e9 / peak, 4),
             "timings_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in tm.items() if v[1]},
-            "e2e": {"value": round(e2e_mlups, 1), "unit": "MLUPS",
-                    "h2d_bytes_per_step": round(pdf_bytes / args.steps),
-                    "d2h_bytes_per_step": round(pdf_bytes / args.steps) + 24,
-                    "how": (f"job of {args.steps} steps through the C-ABI with host buffers: lbg_upload_src "
-                            "from pinned host memory (reference layout), per step sweep [+ halo] + swap + "
-                            "lbg_sync (error-counter D2H, NumericError check), lbg_download_src; wall clock, "
-                            "max over ranks"),
-                    "steady_state_loop_mlups": round(loop_mlups, 1), "result_finite": finite},
+            "e2e": ({"value": round(e2e_mlups, 1), "unit": "MLUPS",
+                     "h2d_bytes_per_step": round(pdf_bytes / args.steps),
+                     "d2h_bytes_per_step": round(pdf_bytes / args.steps) + 24,
+                     "how": (f"job of {args.steps} steps through the C-ABI with host buffers: lbg_upload_src "
+                             "from pinned host memory (reference layout), per step sweep [+ halo] + swap + "
+                             "lbg_sync (error-counter D2H, NumericError check), lbg_download_src; wall clock, "
+                             "max over ranks"),
+                     "steady_state_loop_mlups": round(loop_mlups, 1), "result_finite": finite}
+                    if e2e_mlups is not None else
+                    {"value": None, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                     "skipped": (f"{local_ranks} host PdfFields of {pdf_bytes / 1e9:.1f} GB exceed 60 % of the "
+                                 f"host's available memory ({(avail or 0) / 1e9:.0f} GB)")}),
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
