@@ -430,6 +430,11 @@ lbg_status lbg_block_create(int device, const int box_lo[3], const int dims[3], 
         return fail(e, "cudaStreamCreate");
     if ((e = cudaStreamCreateWithPriority(&b->side, cudaStreamNonBlocking, hi_prio)) != cudaSuccess)
         return fail(e, "cudaStreamCreate(side)");
+    if ((e = cudaStreamCreateWithPriority(&b->aux, cudaStreamNonBlocking, lo_prio)) != cudaSuccess)
+        return fail(e, "cudaStreamCreate(aux)");
+    if ((e = cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&b->ev_join, cudaEventDisableTiming)) != cudaSuccess)
+        return fail(e, "cudaEventCreate(fork/join)");
     if ((e = cudaEventCreateWithFlags(&b->ev_side, cudaEventDisableTiming)) != cudaSuccess)
         return fail(e, "cudaEventCreate");
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) return fail(e, "block create");
@@ -445,6 +450,7 @@ lbg_status lbg_block_destroy(lbg_block b) {
     cudaSetDevice(b->device);
     if (b->stream) cudaStreamSynchronize(b->stream);
     if (b->side) cudaStreamSynchronize(b->side);
+    if (b->aux) cudaStreamSynchronize(b->aux);
     if (b->comm) lbg_comm_destroy(b);
     if (b->p2p) lbg_p2p_destroy(b);
     void* dev[] = {b->buf[0], b->buf[1], b->count, b->id0, b->id1, b->b0, b->b1, b->btot,
@@ -463,6 +469,8 @@ lbg_status lbg_block_destroy(lbg_block b) {
     }
     for (auto e : b->event_pool) cudaEventDestroy(e);
     if (b->ev_side) cudaEventDestroy(b->ev_side);
+    if (b->ev_fork) cudaEventDestroy(b->ev_fork);
+    if (b->ev_join) cudaEventDestroy(b->ev_join);
     if (b->ev_stage) cudaEventDestroy(b->ev_stage);
     for (int s = 0; s < 2; ++s) {
         if (b->xfer[s]) cudaFree(b->xfer[s]);
@@ -474,6 +482,7 @@ lbg_status lbg_block_destroy(lbg_block b) {
     if (b->recv_buf) cudaFree(b->recv_buf);
     if (b->stream) cudaStreamDestroy(b->stream);
     if (b->side) cudaStreamDestroy(b->side);
+    if (b->aux) cudaStreamDestroy(b->aux);
     delete b;
     return LBG_OK;
 }

@@ -188,6 +188,10 @@ struct lbg_block_s {
     cudaStream_t stream = nullptr;  // compute
     cudaStream_t side = nullptr;    // H2D/D2H of particle data
     cudaEvent_t ev_side = nullptr;
+    // coupled sweeps: K2 (covered segments) runs on `aux` concurrently with K1 on `stream`
+    // (disjoint cells); fork/join by events
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
     bool timing = false;
     std::vector<lbg::TimedSpan> spans;

@@ -527,26 +527,36 @@ static void launch_flat(const SweepArgs& a, cudaStream_t s) {
     sweep_flat_kernel<kForced, kSkip><<<(unsigned)((n + T - 1) / T), T, 0, s>>>(a);
 }
 
-static void launch_psm_segments(lbg_block b, const SweepArgs& a, bool forced) {
-    // persistent grid: 4 CTAs of 128 per SM, the list length is read on the device
+// K2 on stream `st`, `per_sm` persistent CTAs of 128 per SM for the one-entry segments
+static void launch_psm_segments(lbg_block b, const SweepArgs& a, bool forced, cudaStream_t st, int per_sm) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, b->device);
     const bool fused = b->force_mode == LBG_FORCE_FUSED;
+    const unsigned g1 = (unsigned)(sms * per_sm), g2 = (unsigned)(sms * 4);
     // segments with one-entry cells only (the bulk): lean pair-scheduled operator
     if (forced)
-        fused ? psm_seg_kernel<true, true, false><<<sms * 8, 128, 0, b->stream>>>(a)
-              : psm_seg_kernel<true, false, false><<<sms * 8, 128, 0, b->stream>>>(a);
+        fused ? psm_seg_kernel<true, true, false><<<g1, 128, 0, st>>>(a)
+              : psm_seg_kernel<true, false, false><<<g1, 128, 0, st>>>(a);
     else
-        fused ? psm_seg_kernel<false, true, false><<<sms * 8, 128, 0, b->stream>>>(a)
-              : psm_seg_kernel<false, false, false><<<sms * 8, 128, 0, b->stream>>>(a);
+        fused ? psm_seg_kernel<false, true, false><<<g1, 128, 0, st>>>(a)
+              : psm_seg_kernel<false, false, false><<<g1, 128, 0, st>>>(a);
     count_launch();
     // segments holding a two-entry cell (particle contacts): general operator
     if (forced)
-        fused ? psm_seg_kernel<true, true, true><<<sms * 4, 128, 0, b->stream>>>(a)
-              : psm_seg_kernel<true, false, true><<<sms * 4, 128, 0, b->stream>>>(a);
+        fused ? psm_seg_kernel<true, true, true><<<g2, 128, 0, st>>>(a)
+              : psm_seg_kernel<true, false, true><<<g2, 128, 0, st>>>(a);
     else
-        fused ? psm_seg_kernel<false, true, true><<<sms * 4, 128, 0, b->stream>>>(a)
-              : psm_seg_kernel<false, false, true><<<sms * 4, 128, 0, b->stream>>>(a);
+        fused ? psm_seg_kernel<false, true, true><<<g2, 128, 0, st>>>(a)
+              : psm_seg_kernel<false, false, true><<<g2, 128, 0, st>>>(a);
+}
+
+// LBG_K2_CONCURRENT=0 runs K2 after K1 on the compute stream (A/B measurement)
+static bool k2_concurrent() {
+    static const bool v = [] {
+        const char* e = std::getenv("LBG_K2_CONCURRENT");
+        return !(e && e[0] == '0');
+    }();
+    return v;
 }
 
 }  // namespace lbg
@@ -585,9 +595,22 @@ lbg_status lbg_sweep(lbg_block b, const lbg_fluid* fl, const lbg_box* range) {
     Span span(b, LBG_CAT_PSM);
     const bool fo = forced(fl);
     if (b->coupling) {
+        if (k2_concurrent()) {
+            // K1 and K2 touch disjoint cells (K1 skips K2's segments): K2 runs on the aux stream
+            // beside K1, with fewer persistent CTAs so K1's blocks find room on every SM
+            LBG_CUDA(cudaEventRecord(b->ev_fork, b->stream));
+            LBG_CUDA(cudaStreamWaitEvent(b->aux, b->ev_fork, 0));
+            launch_psm_segments(b, a, fo, b->aux, 4);
+            LBG_LAUNCH_CHECK();
+            fo ? launch_box<true, true>(a, b->stream) : launch_box<false, true>(a, b->stream);
+            LBG_LAUNCH_CHECK();
+            LBG_CUDA(cudaEventRecord(b->ev_join, b->aux));
+            LBG_CUDA(cudaStreamWaitEvent(b->stream, b->ev_join, 0));
+            return LBG_OK;
+        }
         fo ? launch_box<true, true>(a, b->stream) : launch_box<false, true>(a, b->stream);
         LBG_LAUNCH_CHECK();
-        launch_psm_segments(b, a, fo);
+        launch_psm_segments(b, a, fo, b->stream, 8);
     } else if (pair_sweep()) {
         fo ? launch_pair<true>(a, b->stream) : launch_pair<false>(a, b->stream);
     } else {
