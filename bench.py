@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--tau", type=float, default=0.8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-coupled", action="store_true", help="skip the config-3 coupled-step timing")
-    ap.add_argument("--coupled-steps", type=int, default=3)
+    ap.add_argument("--coupled-steps", type=int, default=8)
     ap.add_argument("--halo", choices=["p2p", "nccl"], default="p2p",
                     help="N > 1: outer sweep stores into the neighbours over NVLink (p2p) or NCCL halo")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
@@ -465,7 +465,7 @@ def run_lbg(args):
                 # the reference's own parallelism lever: 2x2x2 blocks, one worker thread each
                 # (host DEM per block in parallel), same blocks/workers for the reference run
                 workers = min(8, os.cpu_count() or 8)
-                out["coupled_step"] = coupled_step(args.coupled_steps, not args.no_cpu_baseline,
+                out["coupled_step"] = coupled_step(args.coupled_steps, not args.no_cpu_baseline, ref_steps=3,
                                                    blocks=(2, 2, 2), workers=workers)
                 single = coupled_step(args.coupled_steps, False)
                 out["coupled_step"]["single_block"] = {k: single[k] for k in (

@@ -135,7 +135,7 @@ struct MapArgs {
 // by a separate pass (segments_kernel), since a warp here is not a row segment.
 constexpr int kMapCand = 64;
 
-__global__ void __launch_bounds__(256) map_bin_kernel(const MapArgs a) {
+__global__ void __launch_bounds__(256, 4) map_bin_kernel(const MapArgs a) {
     const BinGeom& g = a.g;
     const int b = blockIdx.x;
     const int bx = b % g.nb[0], by = (b / g.nb[0]) % g.nb[1], bz = b / (g.nb[0] * g.nb[1]);
