@@ -256,6 +256,28 @@ def host_mem_available():
     return None
 
 
+NVLINK_GBS = 900.0  # NVLink 5 per direction per GPU (B200_PROFILING.md)
+
+
+def halo_record(halo, n, ms_step, tm, steps):
+    """PDF halo per GPU and step: 5 inbound q per face cell, from each of the
+    two slab neighbours, 8 B each — and the NVLink fraction it needs. With the NCCL halo the
+    comm-stream time (pack, ncclSend/Recv, unpack; CUDA events) is measured and overlapped
+    with the inner sweep; with P2P the stores are issued by the outer sweep kernel itself, so
+    the transfer has no separate phase."""
+    nbytes = 2 * 5 * n * n * 8
+    rec = {"mode": halo, "bytes_per_gpu_per_step": nbytes,
+           "nvlink_gbs_needed_at_step_rate": round(nbytes / (ms_step / 1e3) / 1e9, 2),
+           "frac_of_nvlink_needed": round(nbytes / (ms_step / 1e3) / 1e9 / NVLINK_GBS, 5)}
+    comm = tm.get("PSM-comm")
+    if comm and comm[1]:
+        ms = comm[0] / steps
+        rec["comm_stream_ms_per_step"] = round(ms, 4)
+        rec["achieved_gbs_during_comm"] = round(nbytes / (ms / 1e3) / 1e9, 1)
+        rec["frac_of_nvlink_during_comm"] = round(nbytes / (ms / 1e3) / 1e9 / NVLINK_GBS, 4)
+    return rec
+
+
 # --------------------------------------------------------------------------- GPU path
 def run_lbg(args):
     import torch
@@ -442,6 +464,7 @@ def run_lbg(args):
                          "sweep_launches": sweep_n},
             "hbm_roofline_frac_of_step": round(BYTES_PER_LUP * cells / (ms_step / 1e3) / 1e9 / peak, 4),
             "timings_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in tm.items() if v[1]},
+            "halo": (None if N == 1 else halo_record(halo, n, ms_step, tm, args.steps)),
             "e2e": ({"value": round(e2e_mlups, 1), "unit": "MLUPS",
                      "h2d_bytes_per_step": round(pdf_bytes / args.steps),
                      "d2h_bytes_per_step": round(pdf_bytes / args.steps) + 24,
