@@ -21,6 +21,10 @@ psm::build_fraction_field (+registry)  build_fraction_field(block, snapshots)
 psm::set_solid_velocities              set_solid_velocities(block, snapshots)
 psm::finalize_hydro_forces             finalize_hydro_forces(block)
 psm::f_of_r                            f_of_r(r)   (host, like the reference)
+lbm::total_mass / total_momentum       Block.total_mass / total_momentum
+lbm::cell_macroscopic (observers)      Block.moments (per-cell rho, bare momentum, B)
+io::sample_scalars (fluid part)        Block.observe (one device reduction)
+begin/complete_halo_exchange           Block.halo_stage / halo_fetch (device to device)
 ====================================  =============================================
 
 Like the reference operators, the free functions complete the operation and raise at the
