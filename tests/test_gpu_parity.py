@@ -241,12 +241,13 @@ def test_device_observers_match_sample_scalars(gpu, oracle):
     assert abs(blk.total_mass() - mass) <= 1e-14 * mass
 
 
-@pytest.mark.parametrize("coupled", [False, True])
-def test_device_moments_bitwise(gpu, oracle, coupled):
+@pytest.mark.parametrize("coupled,dims", [(False, (37, 21, 19)), (True, (37, 21, 19)),
+                                          (True, (150, 131, 120))])
+def test_device_moments_bitwise(gpu, oracle, coupled, dims):
     """lbg_moments: per-cell {rho, mx, my, mz[, btot]} equal to the reference's per-cell sums
     (lbm.cpp:61-93) bit for bit, so observers and grid dumps built on the host from 32-40 B
-    per cell reproduce total_mass / total_momentum / write_grid_dump exactly."""
-    dims = (37, 21, 19)
+    per cell reproduce total_mass / total_momentum / write_grid_dump exactly. The large case
+    crosses the 64 MB z-chunk staging (two chunks)."""
     src = random_pdf(dims, seed=77)
     blk = gpu.Block(dims, coupling=coupled)
     blk.upload_src(src)
