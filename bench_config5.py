@@ -41,10 +41,13 @@ def main():
     ap.add_argument("--settle", type=int, default=100)
     ap.add_argument("--force", choices=["scratch", "fused"], default="fused")
     ap.add_argument("--mode", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--blocks-per-gpu", type=int, default=1,
+                    help="x-slab blocks per GPU (consecutive ids), one host worker each: spreads the host DEM")
     args = ap.parse_args()
     os.environ["LBDEM_GPU_SPREAD"] = "1"
     os.environ["LBDEM_GPU_HOST_MIRROR"] = "0"
     os.environ["LBDEM_GPU_FORCE"] = args.force
+    os.environ["LBDEM_GPU_BLOCKS_PER_DEVICE"] = str(args.blocks_per_gpu)
     import torch  # noqa: F401  (CUDA plumbing)
     import dropin
     g, n = args.gpus, args.edge
@@ -52,7 +55,8 @@ def main():
         nx, particles = 2 * n, 100000
     else:
         nx, particles = n * g, args.per_gpu * g
-    cfg = CFG.format(nx=nx, n=n, g=g, p=particles, settle=args.settle)
+    nb = g * args.blocks_per_gpu
+    cfg = CFG.format(nx=nx, n=n, g=nb, p=particles, settle=args.settle)
     t0 = time.perf_counter()
     sim = dropin.DropinSim(cfg, (nx, n, n))
     setup = time.perf_counter() - t0
@@ -65,7 +69,9 @@ def main():
     cells = nx * n * n
     print(json.dumps({
         "workload": f"config 5 {args.mode}: {nx}x{n}x{n} fluidized bed, {particles} spheres d=10, "
-                    f"blocks {{{g},1,1}}, one per GPU, host DEM (reference), force mode {args.force}",
+                    f"blocks {{{nb},1,1}}, {args.blocks_per_gpu} per GPU (one host worker each), "
+                    f"host DEM (reference), force mode {args.force}",
+        "blocks_per_gpu": args.blocks_per_gpu,
         "scaling": args.mode,
         "n_gpus": g, "steps": args.steps, "ms_per_step": round(dt * 1e3 / args.steps, 2),
         "mlups": round(cells * args.steps / dt / 1e6, 1),

@@ -41,10 +41,16 @@ SIM_CPP_EDITS = [
      "namespace lbdem {\n\n"
      "namespace {\n"
      "/// Device of block `id`: LBDEM_GPU_DEVICE (default 0), or with LBDEM_GPU_SPREAD=1 the\n"
-     "/// blocks are dealt round-robin over all visible GPUs (one worker thread per block).\n"
+     "/// blocks are dealt over all visible GPUs (one worker thread per block): consecutive runs\n"
+     "/// of LBDEM_GPU_BLOCKS_PER_DEVICE (default 1) block ids per GPU, so neighbouring slabs of\n"
+     "/// one GPU exchange their halo on the device and the host DEM has more workers.\n"
      "int gpu_device(int id) {\n"
      "    const char* s = std::getenv(\"LBDEM_GPU_SPREAD\");\n"
-     "    if (s && std::atoi(s) != 0) return id % std::max(1, lbg_device_count());\n"
+     "    if (s && std::atoi(s) != 0) {\n"
+     "        const char* bp = std::getenv(\"LBDEM_GPU_BLOCKS_PER_DEVICE\");\n"
+     "        const int per = bp ? std::max(1, std::atoi(bp)) : 1;\n"
+     "        return (id / per) % std::max(1, lbg_device_count());\n"
+     "    }\n"
      "    const char* e = std::getenv(\"LBDEM_GPU_DEVICE\");\n"
      "    return e ? std::atoi(e) : 0;\n"
      "}\n"

@@ -29,12 +29,13 @@ def test_slab_halo_bitwise(axis, halo):
     assert r.returncode == 0
 
 
-@pytest.mark.parametrize("halo", ["device", "host"])
-def test_dropin_bed_spread_over_gpus_bitwise(halo, monkeypatch):
-    """The drop-in with its blocks dealt over the GPUs (LBDEM_GPU_SPREAD=1: block b on GPU
-    b mod N, one worker thread per block): a config-3-shaped bed on {N,1,1} x-slabs (N = 2..4)
-    with host DEM, the PDF halo peer-to-peer between GPUs (or through host slabs), PARITY
-    force partials — every PDF and particle state bitwise equal to the CPU reference."""
+@pytest.mark.parametrize("halo,per", [("device", 1), ("host", 1), ("device", 2)])
+def test_dropin_bed_spread_over_gpus_bitwise(halo, per, monkeypatch):
+    """The drop-in with its blocks dealt over the GPUs (LBDEM_GPU_SPREAD=1: `per` consecutive
+    blocks per GPU, one worker thread per block): a config-3-shaped bed on {N*per,1,1} x-slabs
+    (N = 2..4) with host DEM, the PDF halo peer-to-peer between GPUs and on-device between
+    slabs of one GPU (or through host slabs), PARITY force partials — every PDF and particle
+    state bitwise equal to the CPU reference."""
     n = _ngpus()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -48,13 +49,15 @@ def test_dropin_bed_spread_over_gpus_bitwise(halo, monkeypatch):
     g = min(n, 4)
     monkeypatch.setenv("LBDEM_GPU_SPREAD", "1")
     monkeypatch.setenv("LBDEM_GPU_HALO", halo)
+    monkeypatch.setenv("LBDEM_GPU_BLOCKS_PER_DEVICE", str(per))  # consecutive slabs per GPU
+    nb = g * per
     cfg = ('{"scenario":"fluidized_bed_dense","domain":[%d,32,48],"blocks":[%d,1,1],"workers":%d,'
            '"particles":{"count":24},"physical":{"diameter_cells":8},'
            '"fluid":{"bc":{"xm":"no_slip","xp":"no_slip","ym":"no_slip","yp":"no_slip",'
            '"zm":"velocity","zp":"pressure"}},'
            '"dem":{"k_n":230,"d_n":520,"k_t":65,"d_t":260,"subcycles":10,"settle_subcycles":20}}'
-           % (20 * g, g, g))
-    a = dropin.DropinSim(cfg, (20 * g, 32, 48))
+           % (20 * nb, nb, nb))
+    a = dropin.DropinSim(cfg, (20 * nb, 32, 48))
     ref = RefLib()
     ref.set_threads(2)
     b = ref.sim(cfg)
