@@ -127,12 +127,16 @@ __global__ void __launch_bounds__(256) bc_fill_kernel(const BcArgs a) {
     const Layout& L = a.L;
     const int n[3] = {L.nx, L.ny, L.nz};
     const int axis = face / 2, side = face % 2;
-    const int ab = (axis + 1) % 3, ac = (axis + 2) % 3;
+    // in-plane axes: the lower one varies fastest across threads (x for the y and z faces),
+    // so a warp's ghost writes and interior reads walk along rows. The reference's visiting
+    // order (jb outer, jc inner, boundary.cpp:94-95) is immaterial: each ghost slot of a face
+    // is written once, and slots shared with another face go to the lower face (below).
+    const int au = axis == 0 ? 1 : 0, av = axis == 2 ? 1 : 2;
     const long long r = t - a.fstart[fi];
     int g[3];
     g[axis] = side == 0 ? -1 : n[axis];
-    g[ab] = (int)(r / (n[ac] + 2)) - 1;  // jb outer, jc inner (boundary.cpp:94-95)
-    g[ac] = (int)(r % (n[ac] + 2)) - 1;
+    g[au] = (int)(r % (n[au] + 2)) - 1;
+    g[av] = (int)(r / (n[au] + 2)) - 1;
 
     // multi-wall flags per other axis, and edge ownership by the lower processed face
     bool multi_lo[3] = {false, false, false}, multi_hi[3] = {false, false, false};

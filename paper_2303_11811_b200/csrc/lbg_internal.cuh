@@ -125,6 +125,15 @@ struct lbg_block_s {
     double* btot = nullptr;
     double* v0 = nullptr;  // xyz per cell
     double* v1 = nullptr;
+    // v_snap: the solid velocities are those set_solid_velocities would compute from the
+    // current snapshots over the current fraction field; the PSM kernels evaluate
+    // u + omega x (c - x) inline instead of reading v0/v1 (which are then stale until
+    // materialised by setu_kernel on download or before a fraction upload)
+    bool v_snap = false;
+    // ids of the snapshot list the fraction field was mapped from (valid after lbg_map):
+    // a later set_solid_velocities list holding all of them cannot meet an unknown id
+    std::vector<int> map_ids;
+    bool map_ids_valid = false;
     double* m0 = nullptr;
     double* m1 = nullptr;
     // covered-cell counts (one-entry, two-entry), from the mapping kernel / after a fraction

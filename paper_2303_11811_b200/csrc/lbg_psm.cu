@@ -1,8 +1,8 @@
 // SPDX-License-Identifier: Apache-2.0
 //
-// K3 — particle -> cell mapping fused with the solid velocity
-//      (SubBlockRegistry::build + build_fraction_field + set_solid_velocities,
-//       psm.cpp:55-169)
+// K3 — particle -> cell mapping (SubBlockRegistry::build + build_fraction_field,
+//      psm.cpp:55-136); set_solid_velocities (psm.cpp:138-169) is evaluated inside the PSM
+//      kernels from the snapshots (v_snap), setu_kernel only materialises the field
 // K4 — hydrodynamic force/torque reduction (finalize_hydro_forces, psm.cpp:278-322)
 //
 // Mapping design (B200): the reference tests every particle against k^3 = 512 host
@@ -12,9 +12,10 @@
 // superset of the reference's eps > 0 candidates in the same order and the first-two /
 // third-is-overfull rule (psm.cpp:103-130) gives identical entries. One thread per cell
 // writes count/btot for every cell (coalesced, as the reference does) and, per entry, the
-// id, B and the solid velocity u + omega x (c - x) straight from the snapshot it just
-// tested (no id -> index search). Velocities must be the post-sync ones (sim.cpp:249-267),
-// which is why lbg_map is called after the host velocity sync.
+// id and B. The solid velocity u + omega x (c - x) of an entry is not stored: the PSM
+// kernels compute it from the snapshot list current at sweep time (set_solid_velocities'
+// post-sync list, sim.cpp:249-267 and 296-297), with the same operations as setu_kernel, so
+// the 24 B per entry write (here) and read (K2) of v0/v1 are gone.
 //
 // Reduction design: PARITY mode reproduces the reference's per-particle Neumaier sums in
 // lexicographic cell order bitwise: every fraction entry of the covered-cell lists becomes a
@@ -116,12 +117,11 @@ struct MapArgs {
     double* __restrict__ v0;
     double* __restrict__ v1;
     DeviceErrors* err;
-    int with_velocity;
     int* cov_n;
 };
 
-// K3 mapping (psm.cpp:28-32 overlap_fraction, psm.cpp:93-136 per-cell entry rule, psm.cpp:157-163
-// setU fused): one CTA per 8^3 bin, two cells per thread. The bin's candidate
+// K3 mapping (psm.cpp:28-32 overlap_fraction, psm.cpp:93-136 per-cell entry rule): one CTA
+// per 8^3 bin, two cells per thread. The bin's candidate
 // snapshots are staged in shared memory in list (= id) order, 64 at a time, so every lane reads
 // the same candidate (broadcast) and the loop has no per-lane trip count. The overlap test is
 // overlap_fraction (psm.cpp:28-32) with two exact shortcuts on the squared distance d2 =
@@ -130,10 +130,16 @@ struct MapArgs {
 //                                       -(dist - r) + f_r is ~1e-16 relative, far inside the
 //                                       margin;
 //   d2 < (r + f_r - 1)^2 (1 - 1e-9)  => eps >= 1, which the clamp makes exactly 1.0.
-// Every other candidate takes the reference's sqrt path, so count/ids/fractions/velocities are
-// bitwise those of build_fraction_field + set_solid_velocities. Segment lists are registered
+// Every other candidate takes the reference's sqrt path, so count/ids/fractions are bitwise
+// those of build_fraction_field. Segment lists are registered
 // by a separate pass (segments_kernel), since a warp here is not a row segment.
 constexpr int kMapCand = 64;
+
+// distance from x to the interval [lo, hi] of cell-centre coordinates, as |c - x| of its
+// nearest member c is computed (c - x rounded; for x > hi, x - hi = -(hi - x) exactly)
+__device__ __forceinline__ double axis_gap(double lo, double hi, double x) {
+    return x < lo ? lo - x : (x > hi ? x - hi : 0.0);
+}
 
 __global__ void __launch_bounds__(256, 4) map_bin_kernel(const MapArgs a) {
     const BinGeom& g = a.g;
@@ -141,7 +147,6 @@ __global__ void __launch_bounds__(256, 4) map_bin_kernel(const MapArgs a) {
     const int bx = b % g.nb[0], by = (b / g.nb[0]) % g.nb[1], bz = b / (g.nb[0] * g.nb[1]);
     __shared__ double sx0[kMapCand], sx1[kMapCand], sx2[kMapCand], sr[kMapCand], sfr[kMapCand];
     __shared__ double sout2[kMapCand], sin2[kMapCand];
-    __shared__ double su[3][kMapCand], sw[3][kMapCand];
     __shared__ int sid[kMapCand];
     const int t = threadIdx.x;
     const int i = bx * kBin + (t & 7), j = by * kBin + ((t >> 3) & 7);
@@ -157,8 +162,14 @@ __global__ void __launch_bounds__(256, 4) map_bin_kernel(const MapArgs a) {
         c[h] = ((long long)k[h] * g.dims[1] + j) * g.dims[0] + i;
         cc2[h] = (double)(g.lo[2] + k[h]) + 0.5;
     }
-    const int* list = a.items + a.start[b];
+    // cell-centre box of this warp's cells: x 8, y 4 (z per h)
+    const int lane = t & 31;
+    const int wj = by * kBin + (((t & ~31) >> 3) & 7);
+    const double wx0 = (double)(g.lo[0] + bx * kBin) + 0.5, wx1 = (double)(g.lo[0] + bx * kBin + 7) + 0.5;
+    const double wy0 = (double)(g.lo[1] + wj) + 0.5, wy1 = (double)(g.lo[1] + wj + 3) + 0.5;
     const int n = a.cnt[b];
+    if (n == 0) return;  // count and btot of the whole field were zeroed before the launch
+    const int* list = a.items + a.start[b];
     for (int base = 0; base < n; base += kMapCand) {
         const int m = min(kMapCand, n - base);
         __syncthreads();
@@ -172,52 +183,60 @@ __global__ void __launch_bounds__(256, 4) map_bin_kernel(const MapArgs a) {
             const double ro = p.r + p.f_r, ri = ro - 1.0;
             sout2[t] = (ro * ro) * (1.0 + 1e-9);
             sin2[t] = ri > 0.0 ? (ri * ri) * (1.0 - 1e-9) : -1.0;
-            for (int d = 0; d < 3; ++d) {
-                su[d][t] = p.u[d];
-                sw[d][t] = p.omega[d];
-            }
             sid[t] = p.id;
         }
         __syncthreads();
         for (int h = 0; h < 2; ++h) {
+            // warp-level cull: a candidate enters the cell loop only if it can reach a cell
+            // centre of this warp's 8 x 4 x 1 row block. The squared gap between the candidate
+            // and the box of cell centres bounds every cell's radicand from below in floating
+            // point too (each per-axis gap is the smallest |c - x| over the box, and rounding
+            // is monotonic), so the box rejects only candidates every cell rejects (rad > sout2)
+            unsigned rel[2];
+            for (int half = 0; half < 2; ++half) {
+                const int q = lane + 32 * half;
+                bool r = false;
+                if (q < m) {
+                    const double g0 = axis_gap(wx0, wx1, sx0[q]), g1 = axis_gap(wy0, wy1, sx1[q]);
+                    const double g2 = axis_gap(cc2[h], cc2[h], sx2[q]);
+                    r = !((g0 * g0 + g1 * g1) + g2 * g2 > sout2[q]);
+                }
+                rel[half] = __ballot_sync(0xffffffffu, r);
+            }
             if (!valid[h] || over[h]) continue;
-            for (int q = 0; q < m; ++q) {
-                const double d0 = cc0 - sx0[q], d1 = cc1 - sx1[q], d2 = cc2[h] - sx2[q];
-                const double rad = (d0 * d0 + d1 * d1) + d2 * d2;
-                if (rad > sout2[q]) continue;
-                double eps;
-                if (rad < sin2[q]) {
-                    eps = 1.0;
-                } else {
-                    eps = -(sqrt(rad) - sr[q]) + sfr[q];
-                    eps = eps < 0.0 ? 0.0 : (1.0 < eps ? 1.0 : eps);  // std::clamp
-                    if (eps <= 0.0) continue;
+            for (int half = 0; half < 2 && !over[h]; ++half) {
+                for (unsigned mask = rel[half]; mask; mask &= mask - 1) {  // ascending = id order
+                    const int q = 32 * half + __ffs(mask) - 1;
+                    const double d0 = cc0 - sx0[q], d1 = cc1 - sx1[q], d2 = cc2[h] - sx2[q];
+                    const double rad = (d0 * d0 + d1 * d1) + d2 * d2;
+                    if (rad > sout2[q]) continue;
+                    double eps;
+                    if (rad < sin2[q]) {
+                        eps = 1.0;
+                    } else {
+                        eps = -(sqrt(rad) - sr[q]) + sfr[q];
+                        eps = eps < 0.0 ? 0.0 : (1.0 < eps ? 1.0 : eps);  // std::clamp
+                        if (eps <= 0.0) continue;
+                    }
+                    if (cnt[h] >= 2) {
+                        over[h] = true;
+                        break;
+                    }
+                    if (cnt[h] == 0) {
+                        a.id0[c[h]] = sid[q];
+                        a.b0[c[h]] = eps;
+                    } else {
+                        a.id1[c[h]] = sid[q];
+                        a.b1[c[h]] = eps;
+                    }
+                    ++cnt[h];
+                    sum[h] += eps;
                 }
-                if (cnt[h] >= 2) {
-                    over[h] = true;
-                    break;
-                }
-                if (a.with_velocity) {
-                    // v = u + cross(omega, c - x)  (vec3.hpp:92-94)
-                    double* v = (cnt[h] == 0 ? a.v0 : a.v1) + 3 * c[h];
-                    v[0] = su[0][q] + (sw[1][q] * d2 - sw[2][q] * d1);
-                    v[1] = su[1][q] + (sw[2][q] * d0 - sw[0][q] * d2);
-                    v[2] = su[2][q] + (sw[0][q] * d1 - sw[1][q] * d0);
-                }
-                if (cnt[h] == 0) {
-                    a.id0[c[h]] = sid[q];
-                    a.b0[c[h]] = eps;
-                } else {
-                    a.id1[c[h]] = sid[q];
-                    a.b1[c[h]] = eps;
-                }
-                ++cnt[h];
-                sum[h] += eps;
             }
         }
     }
     for (int h = 0; h < 2; ++h) {
-        if (valid[h]) {
+        if (valid[h] && cnt[h] > 0) {  // uncovered cells keep the zeroed count and btot (+0.0)
             a.count[c[h]] = (uint8_t)cnt[h];
             a.btot[c[h]] = sum[h] < 1.0 ? sum[h] : 1.0;  // std::min(1.0, sum)
         }
@@ -625,10 +644,15 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
     a.v0 = b->v0;
     a.v1 = b->v1;
     a.err = b->err_d;
-    a.with_velocity = 1;
     a.cov_n = b->cov_n;
     LBG_CUDA(cudaMemsetAsync(b->cov_n, 0, 2 * sizeof(int), b->stream));
     LBG_CUDA(cudaMemsetAsync(b->seg_n, 0, 2 * sizeof(int), b->stream));
+    // build_fraction_field writes count and btot for every cell (psm.cpp:128-129):
+    // zero them at copy bandwidth, so the mapping kernel skips bins without candidates and
+    // writes only covered cells
+    const size_t cells = (size_t)b->L.nx * b->L.ny * b->L.nz;
+    LBG_CUDA(cudaMemsetAsync(b->count, 0, cells, b->stream));
+    LBG_CUDA(cudaMemsetAsync(b->btot, 0, sizeof(double) * cells, b->stream));
     map_bin_kernel<<<(unsigned)nbins, 256, 0, b->stream>>>(a);
     LBG_LAUNCH_CHECK();
     const long long rows = (long long)b->L.ny * b->L.nz;
@@ -637,7 +661,27 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
                                                                            b->seg_n, b->seg_cap);
     LBG_LAUNCH_CHECK();
     b->cov_dirty = false;
+    b->v_snap = true;
+    b->map_ids.resize(n);
+    for (int p = 0; p < n; ++p) b->map_ids[p] = snaps[p].id;
+    b->map_ids_valid = true;
     return LBG_OK;
+}
+
+// setu_kernel over the current fraction field with the current snapshots (psm.cpp:138-169)
+static lbg_status run_setu(lbg_block b) {
+    const BinGeom g = geom(b);
+    dim3 grid((g.dims[0] + 127) / 128, g.dims[1], g.dims[2]);
+    setu_kernel<<<grid, 128, 0, b->stream>>>(b->snaps_d, snap_index(b), g, b->count, b->id0, b->id1, b->v0, b->v1,
+                                            b->err_d);
+    LBG_LAUNCH_CHECK();
+    return LBG_OK;
+}
+
+// write the v_snap velocities into v0/v1 (before they are read or partly overwritten)
+static lbg_status materialize_velocity(lbg_block b) {
+    if (!b->v_snap) return LBG_OK;
+    return run_setu(b);
 }
 
 lbg_status lbg_set_solid_velocities(lbg_block b, const lbg_snapshot* snaps, int n) {
@@ -645,12 +689,21 @@ lbg_status lbg_set_solid_velocities(lbg_block b, const lbg_snapshot* snaps, int 
     LBG_CUDA(cudaSetDevice(b->device));
     Span span(b, LBG_CAT_SETU);
     if (lbg_status s = upload_snapshots(b, snaps, n)) return s;
-    const BinGeom g = geom(b);
-    dim3 grid((g.dims[0] + 127) / 128, g.dims[1], g.dims[2]);
-    setu_kernel<<<grid, 128, 0, b->stream>>>(b->snaps_d, snap_index(b), g, b->count, b->id0, b->id1, b->v0, b->v1,
-                                            b->err_d);
-    LBG_LAUNCH_CHECK();
-    return LBG_OK;
+    // every entry of a mapped field names a snapshot of the mapping list; if the new list
+    // (id-sorted, like it) holds all of those ids, no entry can be unknown (psm.cpp:165-168)
+    // and the PSM kernels evaluate u + omega x (c - x) from these snapshots inline. Otherwise
+    // the field is filled here, counting unknown ids for lbg_sync's SyncError.
+    bool superset = b->map_ids_valid;
+    for (size_t p = 0, q = 0; superset && p < b->map_ids.size(); ++p) {
+        while (q < (size_t)n && snaps[q].id < b->map_ids[p]) ++q;
+        superset = q < (size_t)n && snaps[q].id == b->map_ids[p];
+    }
+    if (superset) {
+        b->v_snap = true;
+        return LBG_OK;
+    }
+    b->v_snap = false;
+    return run_setu(b);
 }
 
 // LBG_FORCE_FUSED: the sweep already summed; copy the accumulators out
@@ -856,7 +909,13 @@ static lbg_status copy_frac(lbg_block b, bool up, uint8_t* count, int* id0, int*
 
 lbg_status lbg_upload_fraction(lbg_block b, const uint8_t* count, const int* id0, const int* id1,
                                const double* b0, const double* b1, const double* btot) {
-    if (b) b->cov_dirty = true;
+    if (lbg_status s = need_coupling(b)) return s;
+    LBG_CUDA(cudaSetDevice(b->device));
+    // the stored velocities belong to the old field: materialise them, then they are plain data
+    if (lbg_status s = materialize_velocity(b)) return s;
+    b->v_snap = false;
+    b->map_ids_valid = false;
+    b->cov_dirty = true;
     return copy_frac(b, true, (uint8_t*)count, (int*)id0, (int*)id1, (double*)b0, (double*)b1, (double*)btot);
 }
 
@@ -877,9 +936,16 @@ static lbg_status copy_vec_pair(lbg_block b, bool up, double* d0, double* d1, do
 }
 
 lbg_status lbg_upload_solid_velocity(lbg_block b, const double* v0, const double* v1) {
+    if (lbg_status s = need_coupling(b)) return s;
+    LBG_CUDA(cudaSetDevice(b->device));
+    if (lbg_status s = materialize_velocity(b)) return s;  // a null side keeps its values
+    b->v_snap = false;
     return copy_vec_pair(b, true, b ? b->v0 : nullptr, b ? b->v1 : nullptr, (double*)v0, (double*)v1);
 }
 lbg_status lbg_download_solid_velocity(lbg_block b, double* v0, double* v1) {
+    if (lbg_status s = need_coupling(b)) return s;
+    LBG_CUDA(cudaSetDevice(b->device));
+    if (lbg_status s = materialize_velocity(b)) return s;
     return copy_vec_pair(b, false, b ? b->v0 : nullptr, b ? b->v1 : nullptr, v0, v1);
 }
 lbg_status lbg_upload_scratch(lbg_block b, const double* m0, const double* m1) {

@@ -30,6 +30,7 @@
 #include "lbg_cell.cuh"
 #include "lbg_internal.cuh"
 #include <cstdlib>
+#include <type_traits>
 
 namespace lbg {
 
@@ -107,9 +108,72 @@ __device__ __forceinline__ bool srt_cell_at(const SweepArgs& a, int i, int j, in
     return ok;
 }
 
+// solid velocity of entry e of cell (i, j, k): with kVsnap, set_solid_velocities' value
+// u + cross(omega, c - x) (psm.cpp:157-163, vec3.hpp:39-41; the operations of setu_kernel)
+// from the current snapshot list, else the stored field v0/v1
+template <bool kVsnap>
+__device__ __forceinline__ void solid_velocity(const SweepArgs& a, int e, long long fc, int i, int j, int k,
+                                               double (&v)[3]) {
+    if constexpr (kVsnap) {
+        const int p = a.sidx(e == 0 ? a.id0[fc] : a.id1[fc]);
+        if (p < 0) {  // cannot happen for a v_snap field (checked on the host); never read wild
+            atomicAdd(&a.err->unknown, 1ull);
+            v[0] = v[1] = v[2] = 0.0;
+            return;
+        }
+        const lbg_snapshot& s = a.snaps[p];
+        const double r0 = ((double)(a.blk_lo[0] + i) + 0.5) - s.x[0];
+        const double r1 = ((double)(a.blk_lo[1] + j) + 0.5) - s.x[1];
+        const double r2 = ((double)(a.blk_lo[2] + k) + 0.5) - s.x[2];
+        v[0] = s.u[0] + (s.omega[1] * r2 - s.omega[2] * r1);
+        v[1] = s.u[1] + (s.omega[2] * r0 - s.omega[0] * r2);
+        v[2] = s.u[2] + (s.omega[0] * r1 - s.omega[1] * r0);
+    } else {
+        const double* w = (e == 0 ? a.v0 : a.v1) + 3 * fc;
+        v[0] = w[0];
+        v[1] = w[1];
+        v[2] = w[2];
+    }
+}
+
+// solid velocity of the first entry of a one-entry-segment lane, selected to 0 where the cell
+// is not covered. Every index load (id0, the id -> index table, the snapshot) is issued
+// without waiting for the cell's count, so the chain seg_list -> cell fields -> table ->
+// snapshot overlaps the 19 population loads instead of following them.
+template <bool kVsnap>
+__device__ __forceinline__ void solid_velocity_sel(const SweepArgs& a, bool cov, long long fc, int i, int j,
+                                                   int k, double (&v)[3]) {
+    if constexpr (kVsnap) {
+        const int p = a.sidx(a.id0[fc]);  // id0 of an uncovered cell is stale: selected away
+        if (cov && p < 0) atomicAdd(&a.err->unknown, 1ull);
+        double x[3] = {0.0, 0.0, 0.0}, u[3] = {0.0, 0.0, 0.0}, w[3] = {0.0, 0.0, 0.0};
+        if (p >= 0) {
+            const lbg_snapshot& s = a.snaps[p];
+            for (int d = 0; d < 3; ++d) {
+                x[d] = s.x[d];
+                u[d] = s.u[d];
+                w[d] = s.omega[d];
+            }
+        }
+        const double r0 = ((double)(a.blk_lo[0] + i) + 0.5) - x[0];
+        const double r1 = ((double)(a.blk_lo[1] + j) + 0.5) - x[1];
+        const double r2 = ((double)(a.blk_lo[2] + k) + 0.5) - x[2];
+        const bool use = cov && p >= 0;
+        v[0] = use ? u[0] + (w[1] * r2 - w[2] * r1) : 0.0;
+        v[1] = use ? u[1] + (w[2] * r0 - w[0] * r2) : 0.0;
+        v[2] = use ? u[2] + (w[0] * r1 - w[1] * r0) : 0.0;
+    } else {
+        const double* w = a.v0 + 3 * fc;
+        const double w0 = w[0], w1 = w[1], w2 = w[2];
+        v[0] = cov ? w0 : 0.0;
+        v[1] = cov ? w1 : 0.0;
+        v[2] = cov ? w2 : 0.0;
+    }
+}
+
 // covered cell, psm.cpp:236-258; with kFused the per-entry momentum goes to m_out instead of
 // the scratch
-template <bool kForced, bool kFused>
+template <bool kForced, bool kFused, bool kVsnap>
 __device__ __forceinline__ bool psm_cell_at(const SweepArgs& a, int i, int j, int k, int& cnt,
                                             double (&m)[2][3]) {
     const Layout& L = a.L;
@@ -119,11 +183,9 @@ __device__ __forceinline__ bool psm_cell_at(const SweepArgs& a, int i, int j, in
     double f[kQ];
     pull(a, i, j, k, base, f);
     const double be[2] = {a.b0[fc], cnt > 1 ? a.b1[fc] : 0.0};
-    double ue[2][3];
-    for (int c = 0; c < 3; ++c) {
-        ue[0][c] = a.v0[3 * fc + c];
-        ue[1][c] = cnt > 1 ? a.v1[3 * fc + c] : 0.0;
-    }
+    double ue[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+    solid_velocity<kVsnap>(a, 0, fc, i, j, k, ue[0]);
+    if (cnt > 1) solid_velocity<kVsnap>(a, 1, fc, i, j, k, ue[1]);
     const bool ok = psm_cell_opt<kForced>(f, a.inv_tau, a.F, cnt, a.btot[fc], be, ue, m);
     if constexpr (!kFused) {
         for (int c = 0; c < 3; ++c) a.m0[3 * fc + c] = m[0][c];
@@ -310,68 +372,88 @@ __device__ __forceinline__ void fused_accumulate(const SweepArgs& a, int p, cons
     }
 }
 
+// One lane of the coupled sweep at interior cell (i, j, k) with fraction count cnt: SRT
+// (count 0), the pair-scheduled one-entry operator (count 1) or, with kGeneral, the general
+// operator (count 2). For the fused force mode it also names the entries' particles (p0, p1)
+// and the cell centre for fused_accumulate.
+template <bool kForced, bool kFused, bool kGeneral, bool kVsnap>
+__device__ __forceinline__ bool coupled_lane(const SweepArgs& a, int i, int j, int k, long long fc, int cnt,
+                                             double (&m)[2][3], int& p0, int& p1, double (&cc)[3]) {
+    const Layout& L = a.L;
+    bool ok;
+    if (!kGeneral && !kForced) {
+        // unforced one-entry lanes: fluid lanes run the same operator with B = b = 0 and
+        // v = 0, which is collide_cell exactly (fluid weight 1 - 0 = 1, f + 1 * coll ==
+        // f + coll, and the solid term adds 0 * C = +-0 to a nonzero value), so a mixed warp
+        // issues one operator instead of SRT and PSM in turn
+        const bool cov = cnt > 0;
+        const long long base = L.idx(i, j, k);
+        // cell fields loaded unconditionally (fc is an interior cell), selected by cov
+        const double bt = a.btot[fc], b0 = a.b0[fc];
+        double v[3];
+        solid_velocity_sel<kVsnap>(a, cov, fc, i, j, k, v);
+        double f[kQ];
+        pull(a, i, j, k, base, f);
+        ok = psm_cell_one<kForced>(f, a.inv_tau, a.F, cov ? bt : 0.0, cov ? b0 : 0.0, v[0], v[1], v[2], a.dst,
+                                   L.plane, base, m[0]);
+        if constexpr (!kFused)
+            if (cov)
+                for (int d = 0; d < 3; ++d) a.m0[3 * fc + d] = m[0][d];
+    } else if (cnt == 0) {
+        ok = srt_cell_at<kForced, false>(a, i, j, k);
+    } else if constexpr (!kGeneral) {
+        const long long base = L.idx(i, j, k);
+        double f[kQ];
+        pull(a, i, j, k, base, f);
+        double v[3];
+        solid_velocity<kVsnap>(a, 0, fc, i, j, k, v);
+        ok = psm_cell_one<kForced>(f, a.inv_tau, a.F, a.btot[fc], a.b0[fc], v[0], v[1], v[2], a.dst, L.plane,
+                                   base, m[0]);
+        if constexpr (!kFused)
+            for (int d = 0; d < 3; ++d) a.m0[3 * fc + d] = m[0][d];
+    } else {
+        int c2 = 0;
+        ok = psm_cell_at<kForced, kFused, kVsnap>(a, i, j, k, c2, m);
+    }
+    if constexpr (kFused) {
+        if (cnt > 0) {
+            cc[0] = (double)(a.blk_lo[0] + i) + 0.5;
+            cc[1] = (double)(a.blk_lo[1] + j) + 0.5;
+            cc[2] = (double)(a.blk_lo[2] + k) + 0.5;
+            p0 = a.sidx(a.id0[fc]);
+            if (cnt > 1) p1 = a.sidx(a.id1[fc]);
+            if (p0 < 0 || (cnt > 1 && p1 < 0)) atomicAdd(&a.err->unknown, 1ull);
+        }
+    }
+    return ok;
+}
+
 // K2: one warp per covered 32-cell row segment (segment lists written by the mapping kernel).
 // Each lane takes its cell through SRT (count 0), the pair-scheduled one-entry operator
 // (count 1) or — in segments holding a two-entry cell (kTwo) — the general operator. K1 skips
 // exactly these segments, so every DRAM sector of the PDF planes is read and written once.
-template <bool kForced, bool kFused, bool kTwo>
+template <bool kForced, bool kFused, bool kTwo, bool kVsnap>
 __global__ void __launch_bounds__(128) psm_seg_kernel(const SweepArgs a) {
     const int nseg = kTwo ? a.seg_n[1] : a.seg_n[0];
     const int lane = threadIdx.x & 31;
     const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
     const Layout& L = a.L;
+    auto seg_at = [&](int s) { return kTwo ? a.seg_list[a.seg_cap - 1 - s] : a.seg_list[s]; };
+    unsigned c_next = warp < nseg ? seg_at(warp) : 0u;
     for (int s = warp; s < nseg; s += nwarps) {
-        const unsigned c0 = kTwo ? a.seg_list[a.seg_cap - 1 - s] : a.seg_list[s];
+        const unsigned c0 = c_next;
+        if (s + nwarps < nseg) c_next = seg_at(s + nwarps);  // the next segment's origin in flight
         const int i = (int)(c0 % (unsigned)L.nx) + lane;
         const int j = (int)((c0 / (unsigned)L.nx) % (unsigned)L.ny);
         const int k = (int)(c0 / ((unsigned)L.nx * (unsigned)L.ny));
         bool ok = true;
-        int cnt = 0;
         double m[2][3] = {{0, 0, 0}, {0, 0, 0}};
         double cc[3] = {0, 0, 0};
         int p0 = -1, p1 = -1;
         if (i < L.nx && in_boxes(a, i, j, k)) {
             const long long fc = L.frac(i, j, k);
-            cnt = a.count[fc];
-            if (!kTwo && !kForced) {
-                // unforced one-entry segments: fluid lanes run the same operator with
-                // B = b = 0 and v = 0, which is collide_cell exactly (fluid weight 1 - 0 = 1,
-                // f + 1 * coll == f + coll, and the solid term adds 0 * C = +-0 to a nonzero
-                // value), so a mixed warp issues one operator instead of SRT and PSM in turn
-                const bool cov = cnt > 0;
-                const long long base = L.idx(i, j, k);
-                double f[kQ];
-                pull(a, i, j, k, base, f);
-                ok = psm_cell_one<kForced>(f, a.inv_tau, a.F, cov ? a.btot[fc] : 0.0, cov ? a.b0[fc] : 0.0,
-                                           cov ? a.v0[3 * fc] : 0.0, cov ? a.v0[3 * fc + 1] : 0.0,
-                                           cov ? a.v0[3 * fc + 2] : 0.0, a.dst, L.plane, base, m[0]);
-                if constexpr (!kFused)
-                    if (cov)
-                        for (int d = 0; d < 3; ++d) a.m0[3 * fc + d] = m[0][d];
-            } else if (cnt == 0) {
-                ok = srt_cell_at<kForced, false>(a, i, j, k);
-            } else if constexpr (!kTwo) {
-                const long long base = L.idx(i, j, k);
-                double f[kQ];
-                pull(a, i, j, k, base, f);
-                ok = psm_cell_one<kForced>(f, a.inv_tau, a.F, a.btot[fc], a.b0[fc], a.v0[3 * fc], a.v0[3 * fc + 1],
-                                           a.v0[3 * fc + 2], a.dst, L.plane, base, m[0]);
-                if constexpr (!kFused)
-                    for (int d = 0; d < 3; ++d) a.m0[3 * fc + d] = m[0][d];
-            } else {
-                ok = psm_cell_at<kForced, kFused>(a, i, j, k, cnt, m);
-            }
-            if constexpr (kFused) {
-                if (cnt > 0) {
-                    cc[0] = (double)(a.blk_lo[0] + i) + 0.5;
-                    cc[1] = (double)(a.blk_lo[1] + j) + 0.5;
-                    cc[2] = (double)(a.blk_lo[2] + k) + 0.5;
-                    p0 = a.sidx(a.id0[fc]);
-                    if (cnt > 1) p1 = a.sidx(a.id1[fc]);
-                    if (p0 < 0 || (cnt > 1 && p1 < 0)) atomicAdd(&a.err->unknown, 1ull);
-                }
-            }
+            ok = coupled_lane<kForced, kFused, kTwo, kVsnap>(a, i, j, k, fc, a.count[fc], m, p0, p1, cc);
         }
         count_bad(a.err, !ok);
         if constexpr (kFused) {
@@ -381,33 +463,24 @@ __global__ void __launch_bounds__(128) psm_seg_kernel(const SweepArgs a) {
     }
 }
 
-// Thin boxes of a coupled block (the boundary shell): covered cells are handled inline
-// instead of re-scanning the whole covered list for the few shell cells.
-template <bool kForced, bool kFused>
+// Thin boxes of a coupled block (the boundary shell), split like K1/K2 by the operator a cell
+// needs rather than by segment: kTwo = false sweeps every shell cell with count <= 1 (the
+// ~94-register one-entry path), kTwo = true only the two-entry cells (general operator), so
+// the heavy operator's registers never limit the bulk of the shell.
+template <bool kForced, bool kFused, bool kTwo, bool kVsnap>
 __global__ void __launch_bounds__(128) sweep_flat_coupled_kernel(const SweepArgs a) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     bool ok = true;
-    int cnt = 0;
-    double m[2][3];
+    double m[2][3] = {{0, 0, 0}, {0, 0, 0}};
     double cc[3] = {0, 0, 0};
     int p0 = -1, p1 = -1;
     if (t < a.bstart[a.nbox]) {
         int i, j, k;
         flat_cell(a, t, i, j, k);
         const long long fc = a.L.frac(i, j, k);
-        if (a.count[fc] == 0) {
-            ok = srt_cell_at<kForced, false>(a, i, j, k);
-        } else {
-            ok = psm_cell_at<kForced, kFused>(a, i, j, k, cnt, m);
-            if constexpr (kFused) {
-                cc[0] = (double)(a.blk_lo[0] + i) + 0.5;
-                cc[1] = (double)(a.blk_lo[1] + j) + 0.5;
-                cc[2] = (double)(a.blk_lo[2] + k) + 0.5;
-                p0 = a.sidx(a.id0[fc]);
-                if (cnt > 1) p1 = a.sidx(a.id1[fc]);
-                if (p0 < 0 || (cnt > 1 && p1 < 0)) atomicAdd(&a.err->unknown, 1ull);
-            }
-        }
+        const int cnt = a.count[fc];
+        if (kTwo ? cnt > 1 : cnt <= 1)
+            ok = coupled_lane<kForced, kFused, kTwo, kVsnap>(a, i, j, k, fc, cnt, m, p0, p1, cc);
     }
     count_bad(a.err, !ok);
     if constexpr (kFused) {
@@ -527,27 +600,28 @@ static void launch_flat(const SweepArgs& a, cudaStream_t s) {
     sweep_flat_kernel<kForced, kSkip><<<(unsigned)((n + T - 1) / T), T, 0, s>>>(a);
 }
 
+// calls fn(std::bool_constant<x>, std::bool_constant<y>, std::bool_constant<z>): runtime
+// flags to kernel template arguments
+template <class Fn>
+static void with_flags(bool x, bool y, bool z, Fn&& fn) {
+    auto zf = [&](auto X, auto Y) { z ? fn(X, Y, std::true_type{}) : fn(X, Y, std::false_type{}); };
+    auto yf = [&](auto X) { y ? zf(X, std::true_type{}) : zf(X, std::false_type{}); };
+    x ? yf(std::true_type{}) : yf(std::false_type{});
+}
+
 // K2 on stream `st`, `per_sm` persistent CTAs of 128 per SM for the one-entry segments
 static void launch_psm_segments(lbg_block b, const SweepArgs& a, bool forced, cudaStream_t st, int per_sm) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, b->device);
     const bool fused = b->force_mode == LBG_FORCE_FUSED;
     const unsigned g1 = (unsigned)(sms * per_sm), g2 = (unsigned)(sms * 4);
-    // segments with one-entry cells only (the bulk): lean pair-scheduled operator
-    if (forced)
-        fused ? psm_seg_kernel<true, true, false><<<g1, 128, 0, st>>>(a)
-              : psm_seg_kernel<true, false, false><<<g1, 128, 0, st>>>(a);
-    else
-        fused ? psm_seg_kernel<false, true, false><<<g1, 128, 0, st>>>(a)
-              : psm_seg_kernel<false, false, false><<<g1, 128, 0, st>>>(a);
-    count_launch();
-    // segments holding a two-entry cell (particle contacts): general operator
-    if (forced)
-        fused ? psm_seg_kernel<true, true, true><<<g2, 128, 0, st>>>(a)
-              : psm_seg_kernel<true, false, true><<<g2, 128, 0, st>>>(a);
-    else
-        fused ? psm_seg_kernel<false, true, true><<<g2, 128, 0, st>>>(a)
-              : psm_seg_kernel<false, false, true><<<g2, 128, 0, st>>>(a);
+    with_flags(forced, fused, b->v_snap, [&](auto F, auto U, auto V) {
+        // segments with one-entry cells only (the bulk): lean pair-scheduled operator
+        psm_seg_kernel<decltype(F)::value, decltype(U)::value, false, decltype(V)::value><<<g1, 128, 0, st>>>(a);
+        count_launch();
+        // segments holding a two-entry cell (particle contacts): general operator
+        psm_seg_kernel<decltype(F)::value, decltype(U)::value, true, decltype(V)::value><<<g2, 128, 0, st>>>(a);
+    });
 }
 
 // LBG_K2_CONCURRENT=0 runs K2 after K1 on the compute stream (A/B measurement)
@@ -636,12 +710,12 @@ lbg_status lbg_sweep_boxes(lbg_block b, const lbg_fluid* fl, const lbg_box* boxe
         const long long n_cells = a.bstart[a.nbox];
         const unsigned grid = (unsigned)((n_cells + 127) / 128);
         const bool fu = b->force_mode == LBG_FORCE_FUSED;
-        if (fo)
-            fu ? sweep_flat_coupled_kernel<true, true><<<grid, 128, 0, b->stream>>>(a)
-               : sweep_flat_coupled_kernel<true, false><<<grid, 128, 0, b->stream>>>(a);
-        else
-            fu ? sweep_flat_coupled_kernel<false, true><<<grid, 128, 0, b->stream>>>(a)
-               : sweep_flat_coupled_kernel<false, false><<<grid, 128, 0, b->stream>>>(a);
+        with_flags(fo, fu, b->v_snap, [&](auto F, auto U, auto V) {
+            constexpr bool kF = decltype(F)::value, kU = decltype(U)::value, kV = decltype(V)::value;
+            sweep_flat_coupled_kernel<kF, kU, false, kV><<<grid, 128, 0, b->stream>>>(a);
+            count_launch();
+            sweep_flat_coupled_kernel<kF, kU, true, kV><<<grid, 128, 0, b->stream>>>(a);
+        });
     } else {
         fo ? launch_flat<true, false>(a, b->stream) : launch_flat<false, false>(a, b->stream);
     }

@@ -376,23 +376,25 @@ class Block:
         arrs = [np.ascontiguousarray(f[k]) for k in ("count", "id0", "id1", "b0", "b1", "btot")]
         check(_lib().lbg_upload_fraction(self.h, *[_ptr(a) for a in arrs]))
 
-    def _vec_pair(self, fn, a=None, b=None):
+    def _vec_pair(self, fn, a=None, b=None, download=False):
         nx, ny, nz = self.dims
-        if a is None:
+        if download:
             a, b = np.zeros((nz, ny, nx, 3)), np.zeros((nz, ny, nx, 3))
             check(fn(self.h, _ptr(a), _ptr(b)))
             return a, b
-        a, b = np.ascontiguousarray(a, dtype=np.float64), np.ascontiguousarray(b, dtype=np.float64)
-        check(fn(self.h, _ptr(a), _ptr(b)))
+        # None leaves that side untouched (a null pointer at the C ABI)
+        a = None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+        b = None if b is None else np.ascontiguousarray(b, dtype=np.float64)
+        check(fn(self.h, None if a is None else _ptr(a), None if b is None else _ptr(b)))
 
     def download_solid_velocity(self):
-        return self._vec_pair(_lib().lbg_download_solid_velocity)
+        return self._vec_pair(_lib().lbg_download_solid_velocity, download=True)
 
     def upload_solid_velocity(self, v0, v1):
         self._vec_pair(_lib().lbg_upload_solid_velocity, v0, v1)
 
     def download_scratch(self):
-        return self._vec_pair(_lib().lbg_download_scratch)
+        return self._vec_pair(_lib().lbg_download_scratch, download=True)
 
     def upload_scratch(self, m0, m1):
         self._vec_pair(_lib().lbg_upload_scratch, m0, m1)
@@ -515,9 +517,10 @@ def apply_boundaries(block: Block, spec: BcSpec, touches) -> None:
 
 
 def build_fraction_field(block: Block, snapshots, subdivisions: int = 8) -> None:
-    """SubBlockRegistry::build + psm::build_fraction_field (psm.cpp:55-136), fused with
-    set_solid_velocities (psm.cpp:138-169) on the same snapshots. NumericError if a cell
-    sees more than two particles."""
+    """SubBlockRegistry::build + psm::build_fraction_field (psm.cpp:55-136). The solid
+    velocities (psm.cpp:138-169) follow from these snapshots until set_solid_velocities
+    registers a new list; the PSM kernels evaluate them inline. NumericError if a cell sees
+    more than two particles."""
     block.map(snapshots, subdivisions)
     block.sync()
 

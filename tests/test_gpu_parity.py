@@ -573,6 +573,89 @@ def test_set_solid_velocities_unknown_id(gpu, oracle):
         gpu.set_solid_velocities(blk, make_snapshots([], np.zeros((0, 3)), [], []))
 
 
+def _moved(oracle, s, rng):
+    """The post-sync snapshot list: same particles, new velocities, plus a ghost id the
+    mapping never saw (sim.cpp:249-267 refreshes u and omega between mapping and setU)."""
+    n = len(s["id"])
+    return make_snapshots(list(s["id"]) + [int(max(s["id"])) + 7], list(s["x"]) + [(500.0, 500.0, 500.0)],
+                          list(s["r"]) + [3.0], list(s["f_r"]) + [oracle.f_of_r(3.0)],
+                          list(0.01 * (rng.random((n, 3)) - 0.5)) + [(0.0, 0.0, 0.0)],
+                          list(0.002 * (rng.random((n, 3)) - 0.5)) + [(0.0, 0.0, 0.0)])
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_setu_after_velocity_sync_inline_bitwise(gpu, oracle, fused):
+    """map(A) -> set_solid_velocities(B: new u/omega, one extra id) -> PSM sweep: the PSM
+    kernels evaluate u + omega x (c - x) from B inline (no v0/v1 traffic); PDFs, scratch and
+    the downloaded (materialised) solid velocities are bitwise the reference's setU(B)."""
+    dims = (32, 30, 34)
+    src0 = random_pdf(dims, seed=93)
+    rng = np.random.default_rng(21)
+    centers = [(9.2, 10.1, 11.7), (17.5, 10.4, 12.2), (22.0, 21.0, 23.3), (8.0, 24.0, 26.0)]
+    a = spheres(oracle, centers, [5.0, 4.5, 6.0, 3.5], ids=[1, 3, 4, 8],
+                u=0.01 * (rng.random((4, 3)) - 0.5), w=0.001 * (rng.random((4, 3)) - 0.5))
+    b = _moved(oracle, a, rng)
+    tau, fext = 0.7, (0.0, 0.0, -1e-5)
+    f_o, _ = oracle.build_fraction_field((0, 0, 0), dims, a)
+    sv_o, unk = oracle.set_solid_velocities((0, 0, 0), dims, b, f_o)
+    assert unk == 0 and (f_o["count"] == 2).any()
+    src_o = src0.copy()
+    oracle.fill_periodic(dims, src_o, ALL_P)
+    dst_o = np.zeros_like(src_o)
+    scr = new_scratch(dims)
+    oracle.psm_collide_stream(dims, src_o, dst_o, tau, fext, (0, 0, 0), dims, f_o, sv_o, scr)
+    blk = gpu.Block(dims, coupling=True)
+    if fused:
+        blk.set_force_mode(1)
+    blk.upload_src(src0)
+    gpu.build_fraction_field(blk, a)
+    gpu.set_solid_velocities(blk, b)
+    blk.fill_periodic(ALL_P)
+    p = gpu.FluidParams(tau, fext)
+    blk.sweep(p, gpu.CellBox((1, 1, 1), (dims[0] - 1, dims[1] - 1, dims[2] - 1)))
+    blk.sweep_boxes(p, gpu.boundary_shell(dims))  # shell cells: the flat coupled kernel
+    blk.sync()
+    assert equal_bits(interior(blk.download_dst()), interior(dst_o))
+    c = f_o["count"]
+    if not fused:
+        m0, m1 = blk.download_scratch()
+        assert equal_bits(m0[c > 0], scr["m0"][c > 0]) and equal_bits(m1[c > 1], scr["m1"][c > 1])
+    v0, v1 = blk.download_solid_velocity()
+    assert equal_bits(v0[c > 0], sv_o["v0"][c > 0])
+    assert equal_bits(v1[c > 1], sv_o["v1"][c > 1])
+
+
+def test_setu_missing_mapped_id_raises(gpu, oracle):
+    """A post-sync list that lost a particle the field still names: SyncError from
+    set_solid_velocities, as psm.cpp:165-168 (the exact per-entry walk runs then)."""
+    dims = (24, 24, 24)
+    a = spheres(oracle, [(8.0, 8.0, 8.0), (16.0, 16.0, 16.0)], [4.0, 4.0], ids=[3, 9])
+    blk = gpu.Block(dims, coupling=True)
+    gpu.build_fraction_field(blk, a)
+    b = spheres(oracle, [(8.0, 8.0, 8.0)], [4.0], ids=[3])
+    with pytest.raises(gpu.SyncError, match="unknown particle ids"):
+        gpu.set_solid_velocities(blk, b)
+
+
+def test_partial_velocity_upload_keeps_mapped_side(gpu, oracle):
+    """Uploading v0 only keeps v1 = the mapped snapshots' setU values (materialised first)."""
+    dims = (24, 24, 24)
+    rng = np.random.default_rng(5)
+    a = spheres(oracle, [(10.0, 12.0, 12.0), (15.5, 12.0, 12.0)], [4.5, 4.5], ids=[0, 1],
+                u=0.01 * (rng.random((2, 3)) - 0.5), w=0.002 * (rng.random((2, 3)) - 0.5))
+    f_o, _ = oracle.build_fraction_field((0, 0, 0), dims, a)
+    sv_o, _ = oracle.set_solid_velocities((0, 0, 0), dims, a, f_o)
+    c = f_o["count"]
+    assert (c == 2).any()
+    blk = gpu.Block(dims, coupling=True)
+    gpu.build_fraction_field(blk, a)
+    mine = rng.random((24, 24, 24, 3))
+    blk.upload_solid_velocity(mine, None)
+    v0, v1 = blk.download_solid_velocity()
+    assert equal_bits(v0, mine)
+    assert equal_bits(v1[c > 1], sv_o["v1"][c > 1])
+
+
 @pytest.mark.parametrize("mode", [0, 1])
 def test_full_coupled_pass_and_reduction(gpu, oracle, mode):
     """map -> setU -> PSM sweep -> finalize: PARITY mode bitwise, FAST within L1 tolerance."""
