@@ -244,6 +244,75 @@ def coupled_step(steps, with_reference, ref_steps=1, blocks=(1, 1, 1), workers=1
     return out
 
 
+def coupled_sweep_roofline(steps=10, warmup=3):
+    """Device-side roofline of the coupled fluid step on config 3's bed (one 256^3 block):
+    the particle list is the reference scenario's own (drop-in construction, 10^4 spheres
+    d = 10 after settling), mapped once (K3); each step is the bed BCs (K5) followed by the
+    coupled sweep of the whole block — K1 over the fluid segments || K2 over the covered
+    segments — and a swap. With one block and no halo, BCs-then-sweep equals the reference's
+    inner / BC / outer order (the BCs read and write only src; the sweep writes only dst).
+    Algorithmic bytes per step: 305 B per cell + 44 B per one-entry cell + 80 B per two-entry
+    cell (btot 8; per entry b 8 + id 4 read, m 24 written; v evaluated from the snapshots),
+    SURVEY §8(d). CUDA events on the block's stream; inputs (5.4 GB) exceed L2."""
+    import numpy as np
+    import torch
+
+    from paper_2303_11811_b200 import lbdem
+    sys.path.insert(0, os.path.join(ROOT, "integration"))
+    import dropin
+    n = 256
+    sim = dropin.DropinSim(config3(), (n, n, n))
+    rows = sim.particles()
+    sim.close()
+    r = 5.0  # physical.diameter_cells / 2
+    snaps = {"id": rows[:, 0].astype(np.int32), "x": rows[:, 1:4].copy(), "r": np.full(len(rows), r),
+             "f_r": np.full(len(rows), lbdem.f_of_r(r)), "u": rows[:, 4:7].copy(), "w": rows[:, 7:10].copy()}
+    tau, u_in = 0.567416, 2.2472e-3
+    blk = lbdem.Block((n, n, n), coupling=True)
+    try:
+        blk.fill_equilibrium(1.0, (0.0, 0.0, u_in))
+        blk.map(snaps)
+        blk.sync()
+        cnt = blk.download_fraction()["count"]
+        n1, n2 = int((cnt == 1).sum()), int((cnt == 2).sum())
+        del cnt
+        F = lbdem.FaceBc
+        spec = lbdem.BcSpec([F(lbdem.BcKind.no_slip)] * 4 +
+                            [F(lbdem.BcKind.velocity, (0.0, 0.0, u_in)), F(lbdem.BcKind.pressure, rho=1.0)])
+        p = lbdem.FluidParams(tau)
+        box = lbdem.CellBox((0, 0, 0), (n, n, n))
+        stream = torch.cuda.ExternalStream(blk.stream)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        bc_ms = sweep_ms = 0.0
+        for it in range(warmup + steps):
+            ev[0].record(stream)
+            blk.apply_boundaries(spec, [1] * 6)
+            ev[1].record(stream)
+            blk.sweep(p, box)
+            ev[2].record(stream)
+            blk.swap()
+            if it >= warmup:
+                ev[2].synchronize()
+                bc_ms += ev[0].elapsed_time(ev[1])
+                sweep_ms += ev[1].elapsed_time(ev[2])
+        blk.sync()
+    finally:
+        blk.close()
+    cells = n ** 3
+    algo = 305 * cells + 44 * n1 + 80 * n2
+    sweep_ms /= steps
+    pk = peaks()
+    peak = pk["hbm_gbs"] if pk and pk.get("hbm_gbs") else 6650.0
+    achieved = algo / (sweep_ms / 1e3) / 1e9
+    return {"workload": "config 3 bed (reference scenario particles), one 256^3 block, tau 0.567416",
+            "kernels": "K1 sweep_box_kernel<skip> || K2 psm_seg_kernel (one-entry, two-entry segments)",
+            "cells": cells, "one_entry_cells": n1, "two_entry_cells": n2,
+            "algorithmic_bytes_per_step": algo, "sweep_ms": round(sweep_ms, 4), "bc_ms": round(bc_ms / steps, 4),
+            "mlups": round(cells / (sweep_ms / 1e3) / 1e6, 1),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4)}}
+
+
 def host_mem_available():
     """MemAvailable of this host in bytes (None if unknown)."""
     try:
@@ -493,6 +562,7 @@ def run_lbg(args):
                 single = coupled_step(args.coupled_steps, False)
                 out["coupled_step"]["single_block"] = {k: single[k] for k in (
                     "ms_per_step", "categories_ms_per_step", "gpu_side_ms_per_step", "fused_force_mode")}
+                out["coupled_step"]["psm_sweep"] = coupled_sweep_roofline()
             except Exception as e:  # noqa: BLE001
                 out["coupled_step"] = {"unavailable": f"{type(e).__name__}: {e}"}
         print(json.dumps(out))

@@ -29,6 +29,7 @@
 // counter; lbg_sync() raises NumericError like the reference does after the sweep.
 #include "lbg_cell.cuh"
 #include "lbg_internal.cuh"
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -142,9 +143,9 @@ __device__ __forceinline__ void solid_velocity(const SweepArgs& a, int e, long l
 // snapshot overlaps the 19 population loads instead of following them.
 template <bool kVsnap>
 __device__ __forceinline__ void solid_velocity_sel(const SweepArgs& a, bool cov, long long fc, int i, int j,
-                                                   int k, double (&v)[3]) {
+                                                   int k, double (&v)[3], int id0 = 0) {
     if constexpr (kVsnap) {
-        const int p = a.sidx(a.id0[fc]);  // id0 of an uncovered cell is stale: selected away
+        const int p = a.sidx(id0);  // id0 of an uncovered cell is stale: selected away
         if (cov && p < 0) atomicAdd(&a.err->unknown, 1ull);
         double x[3] = {0.0, 0.0, 0.0}, u[3] = {0.0, 0.0, 0.0}, w[3] = {0.0, 0.0, 0.0};
         if (p >= 0) {
@@ -169,32 +170,6 @@ __device__ __forceinline__ void solid_velocity_sel(const SweepArgs& a, bool cov,
         v[1] = cov ? w1 : 0.0;
         v[2] = cov ? w2 : 0.0;
     }
-}
-
-// covered cell, psm.cpp:236-258; with kFused the per-entry momentum goes to m_out instead of
-// the scratch
-template <bool kForced, bool kFused, bool kVsnap>
-__device__ __forceinline__ bool psm_cell_at(const SweepArgs& a, int i, int j, int k, int& cnt,
-                                            double (&m)[2][3]) {
-    const Layout& L = a.L;
-    const long long base = L.idx(i, j, k);
-    const long long fc = L.frac(i, j, k);
-    cnt = a.count[fc];
-    double f[kQ];
-    pull(a, i, j, k, base, f);
-    const double be[2] = {a.b0[fc], cnt > 1 ? a.b1[fc] : 0.0};
-    double ue[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
-    solid_velocity<kVsnap>(a, 0, fc, i, j, k, ue[0]);
-    if (cnt > 1) solid_velocity<kVsnap>(a, 1, fc, i, j, k, ue[1]);
-    const bool ok = psm_cell_opt<kForced>(f, a.inv_tau, a.F, cnt, a.btot[fc], be, ue, m);
-    if constexpr (!kFused) {
-        for (int c = 0; c < 3; ++c) a.m0[3 * fc + c] = m[0][c];
-        if (cnt > 1)
-            for (int c = 0; c < 3; ++c) a.m1[3 * fc + c] = m[1][c];
-    }
-#pragma unroll
-    for (int q = 0; q < kQ; ++q) a.dst[q * L.plane + base] = f[q];
-    return ok;
 }
 
 __device__ __forceinline__ void count_bad(DeviceErrors* err, bool bad) {
@@ -391,7 +366,7 @@ __device__ __forceinline__ bool coupled_lane(const SweepArgs& a, int i, int j, i
         // cell fields loaded unconditionally (fc is an interior cell), selected by cov
         const double bt = a.btot[fc], b0 = a.b0[fc];
         double v[3];
-        solid_velocity_sel<kVsnap>(a, cov, fc, i, j, k, v);
+        solid_velocity_sel<kVsnap>(a, cov, fc, i, j, k, v, kVsnap ? a.id0[fc] : 0);
         double f[kQ];
         pull(a, i, j, k, base, f);
         ok = psm_cell_one<kForced>(f, a.inv_tau, a.F, cov ? bt : 0.0, cov ? b0 : 0.0, v[0], v[1], v[2], a.dst,
@@ -399,7 +374,7 @@ __device__ __forceinline__ bool coupled_lane(const SweepArgs& a, int i, int j, i
         if constexpr (!kFused)
             if (cov)
                 for (int d = 0; d < 3; ++d) a.m0[3 * fc + d] = m[0][d];
-    } else if (cnt == 0) {
+    } else if (!kGeneral && cnt == 0) {
         ok = srt_cell_at<kForced, false>(a, i, j, k);
     } else if constexpr (!kGeneral) {
         const long long base = L.idx(i, j, k);
@@ -411,9 +386,27 @@ __device__ __forceinline__ bool coupled_lane(const SweepArgs& a, int i, int j, i
                                    base, m[0]);
         if constexpr (!kFused)
             for (int d = 0; d < 3; ++d) a.m0[3 * fc + d] = m[0][d];
+    } else if (!kForced || cnt > 0) {
+        // two-entry segments: the pair-scheduled operator with entry 1 where cnt > 1 (unforced
+        // fluid lanes as in the one-entry case: B = b = 0, v = 0)
+        const bool cov = cnt > 0, two = cnt > 1;
+        const long long base = L.idx(i, j, k);
+        const double bt = a.btot[fc], b0 = a.b0[fc], b1 = a.b1[fc];
+        double v0[3], v1[3] = {0.0, 0.0, 0.0};
+        solid_velocity_sel<kVsnap>(a, cov, fc, i, j, k, v0, kVsnap ? a.id0[fc] : 0);
+        if (two) solid_velocity<kVsnap>(a, 1, fc, i, j, k, v1);
+        double f[kQ];
+        pull(a, i, j, k, base, f);
+        ok = psm_cell_two<kForced>(f, a.inv_tau, a.F, cov ? bt : 0.0, cov ? b0 : 0.0, v0, two ? b1 : 0.0, v1, two,
+                                   a.dst, L.plane, base, m);
+        if constexpr (!kFused) {
+            if (cov)
+                for (int d = 0; d < 3; ++d) a.m0[3 * fc + d] = m[0][d];
+            if (two)
+                for (int d = 0; d < 3; ++d) a.m1[3 * fc + d] = m[1][d];
+        }
     } else {
-        int c2 = 0;
-        ok = psm_cell_at<kForced, kFused, kVsnap>(a, i, j, k, c2, m);
+        ok = srt_cell_at<kForced, false>(a, i, j, k);
     }
     if constexpr (kFused) {
         if (cnt > 0) {
@@ -460,6 +453,89 @@ __global__ void __launch_bounds__(128) psm_seg_kernel(const SweepArgs a) {
             fused_accumulate(a, p0, m[0], cc);
             fused_accumulate(a, p1, m[1], cc);
         }
+    }
+}
+
+// K2 for unforced one-entry segments with software pipelining across the grid-stride loop:
+// the next segment's populations and cell fields are loaded (SegIn) before the current
+// segment's arithmetic, so a warp's DRAM latency hides behind its own fp64 work instead of
+// only behind other warps'. Same per-lane operator as psm_seg_kernel<false, *, false, *>.
+struct SegIn {
+    double f[kQ];
+    double bt, b0;
+    long long fc, base;
+    int i, j, k, cnt, id0;
+    bool act;
+};
+
+template <bool kVsnap>
+__device__ __forceinline__ void seg_load(const SweepArgs& a, unsigned c0, int lane, SegIn& in) {
+    const Layout& L = a.L;
+    in.i = (int)(c0 % (unsigned)L.nx) + lane;
+    in.j = (int)((c0 / (unsigned)L.nx) % (unsigned)L.ny);
+    in.k = (int)(c0 / ((unsigned)L.nx * (unsigned)L.ny));
+    in.act = in.i < L.nx && in_boxes(a, in.i, in.j, in.k);
+    in.cnt = 0;
+    if (in.act) {
+        in.fc = L.frac(in.i, in.j, in.k);
+        in.base = L.idx(in.i, in.j, in.k);
+        in.cnt = a.count[in.fc];
+        in.bt = a.btot[in.fc];
+        in.b0 = a.b0[in.fc];
+        if constexpr (kVsnap) in.id0 = a.id0[in.fc];
+        pull(a, in.i, in.j, in.k, in.base, in.f);
+    }
+}
+
+template <bool kFused, bool kVsnap>
+__device__ __forceinline__ void seg_compute(const SweepArgs& a, const SegIn& in) {
+    bool ok = true;
+    double m[2][3] = {{0, 0, 0}, {0, 0, 0}};
+    double cc[3] = {0, 0, 0};
+    int p0 = -1;
+    if (in.act) {
+        const bool cov = in.cnt > 0;
+        double v[3];
+        solid_velocity_sel<kVsnap>(a, cov, in.fc, in.i, in.j, in.k, v, in.id0);
+        ok = psm_cell_one<false>(in.f, a.inv_tau, a.F, cov ? in.bt : 0.0, cov ? in.b0 : 0.0, v[0], v[1], v[2],
+                                 a.dst, a.L.plane, in.base, m[0]);
+        if constexpr (!kFused) {
+            if (cov)
+                for (int d = 0; d < 3; ++d) a.m0[3 * in.fc + d] = m[0][d];
+        } else if (cov) {
+            cc[0] = (double)(a.blk_lo[0] + in.i) + 0.5;
+            cc[1] = (double)(a.blk_lo[1] + in.j) + 0.5;
+            cc[2] = (double)(a.blk_lo[2] + in.k) + 0.5;
+            p0 = a.sidx(kVsnap ? in.id0 : a.id0[in.fc]);
+            if (p0 < 0) atomicAdd(&a.err->unknown, 1ull);
+        }
+    }
+    count_bad(a.err, !ok);
+    if constexpr (kFused) fused_accumulate(a, p0, m[0], cc);
+}
+
+template <bool kFused, bool kVsnap>
+__global__ void __launch_bounds__(128) psm_seg_pipe_kernel(const SweepArgs a) {
+    const int nseg = a.seg_n[0];
+    const int lane = threadIdx.x & 31;
+    const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
+    if (warp >= nseg) return;  // warp-uniform
+    SegIn cur, nxt;
+    seg_load<kVsnap>(a, a.seg_list[warp], lane, cur);
+    int s = warp;
+    for (;;) {
+        const bool more = s + nwarps < nseg;
+        if (more) seg_load<kVsnap>(a, a.seg_list[s + nwarps], lane, nxt);
+        seg_compute<kFused, kVsnap>(a, cur);
+        if (!more) break;
+        s += nwarps;
+        // second half of the unrolled pair: roles swapped, no register copy
+        const bool more2 = s + nwarps < nseg;
+        if (more2) seg_load<kVsnap>(a, a.seg_list[s + nwarps], lane, cur);
+        seg_compute<kFused, kVsnap>(a, nxt);
+        if (!more2) break;
+        s += nwarps;
     }
 }
 
@@ -609,6 +685,24 @@ static void with_flags(bool x, bool y, bool z, Fn&& fn) {
     x ? yf(std::true_type{}) : yf(std::false_type{});
 }
 
+// unforced one-entry K2: the software-pipelined kernel (default; config 3 coupled sweep
+// 1.17 -> 1.13 ms, profiles/r01_ab_k2.txt), LBG_K2_PIPE=0 the plain segment loop
+static bool k2_pipe() {
+    static const bool v = [] {
+        const char* e = std::getenv("LBG_K2_PIPE");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
+static int k2_pipe_per_sm() {
+    static const int v = [] {
+        const char* e = std::getenv("LBG_K2_PIPE_SM");
+        return e ? std::max(1, std::atoi(e)) : 3;
+    }();
+    return v;
+}
+
 // K2 on stream `st`, `per_sm` persistent CTAs of 128 per SM for the one-entry segments
 static void launch_psm_segments(lbg_block b, const SweepArgs& a, bool forced, cudaStream_t st, int per_sm) {
     int sms = 148;
@@ -617,7 +711,11 @@ static void launch_psm_segments(lbg_block b, const SweepArgs& a, bool forced, cu
     const unsigned g1 = (unsigned)(sms * per_sm), g2 = (unsigned)(sms * 4);
     with_flags(forced, fused, b->v_snap, [&](auto F, auto U, auto V) {
         // segments with one-entry cells only (the bulk): lean pair-scheduled operator
-        psm_seg_kernel<decltype(F)::value, decltype(U)::value, false, decltype(V)::value><<<g1, 128, 0, st>>>(a);
+        if (!decltype(F)::value && k2_pipe())
+            psm_seg_pipe_kernel<decltype(U)::value, decltype(V)::value>
+                <<<(unsigned)(sms * k2_pipe_per_sm()), 128, 0, st>>>(a);
+        else
+            psm_seg_kernel<decltype(F)::value, decltype(U)::value, false, decltype(V)::value><<<g1, 128, 0, st>>>(a);
         count_launch();
         // segments holding a two-entry cell (particle contacts): general operator
         psm_seg_kernel<decltype(F)::value, decltype(U)::value, true, decltype(V)::value><<<g2, 128, 0, st>>>(a);
