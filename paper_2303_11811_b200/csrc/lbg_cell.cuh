@@ -102,6 +102,13 @@ __device__ __forceinline__ void moments(const double (&f)[kQ], double& rho, doub
 // d = f - feq (feq - f == -d exactly); the momentum sum keeps the q
 // order because pairs are visited in q order. Returns ok; m_out = B * sum C c_qbar.
 template <bool kForced>
+__device__ __forceinline__ void psm_cell_one_pairs(const double (&f)[kQ], double rho, double ux, double uy,
+                                                   double uz, double usq, double inv_tau, Force F, double b_tot,
+                                                   double be, double vx, double vy, double vz,
+                                                   double* __restrict__ dst, long long plane, long long base,
+                                                   double (&m_out)[3]);
+
+template <bool kForced>
 __device__ __forceinline__ bool psm_cell_one(const double (&f)[kQ], double inv_tau, Force F,
                                              double b_tot, double be, double vx, double vy, double vz,
                                              double* __restrict__ dst, long long plane, long long base,
@@ -110,6 +117,18 @@ __device__ __forceinline__ bool psm_cell_one(const double (&f)[kQ], double inv_t
     moments(f, rho, ux, uy, uz);
     const double usq = (ux * ux + uy * uy) + uz * uz;
     const bool ok = rho > 0.0 && usq <= kMaxVelocity * kMaxVelocity && isfinite(rho);
+    psm_cell_one_pairs<kForced>(f, rho, ux, uy, uz, usq, inv_tau, F, b_tot, be, vx, vy, vz, dst, plane, base,
+                                m_out);
+    return ok;
+}
+
+// psm_cell_one after the moments: the pair-by-pair outputs and the entry's momentum
+template <bool kForced>
+__device__ __forceinline__ void psm_cell_one_pairs(const double (&f)[kQ], double rho, double ux, double uy,
+                                                   double uz, double usq, double inv_tau, Force F, double b_tot,
+                                                   double be, double vx, double vy, double vz,
+                                                   double* __restrict__ dst, long long plane, long long base,
+                                                   double (&m_out)[3]) {
     const double T = (0.5 * usq) * 3.0;
     const double Tp = (0.5 * ((vx * vx + vy * vy) + vz * vz)) * 3.0;
     const double fluid_w = 1.0 - b_tot;
@@ -151,7 +170,6 @@ __device__ __forceinline__ bool psm_cell_one(const double (&f)[kQ], double inv_t
     m_out[0] = be * mx;
     m_out[1] = be * my;
     m_out[2] = be * mz;
-    return ok;
 }
 
 // psm_cell for a cell with one or two entries, scheduled pair by pair like psm_cell_one

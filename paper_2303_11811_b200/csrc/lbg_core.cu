@@ -382,7 +382,8 @@ lbg_status lbg_block_create(int device, const int box_lo[3], const int dims[3], 
         lbg_block_destroy(b);
         return cuda_check(e, what);
     };
-    const size_t pdf_bytes = sizeof(double) * kQ * (size_t)L.plane;
+    // + slack: the TMA-fed K2 copies 40-double row windows that may run past the last row
+    const size_t pdf_bytes = sizeof(double) * (kQ * (size_t)L.plane + 128);
     cudaError_t e;
     for (int s = 0; s < 2; ++s) {
         if ((e = cudaMalloc(&b->buf[s], pdf_bytes)) != cudaSuccess) return fail(e, "cudaMalloc(pdf)");
@@ -390,7 +391,8 @@ lbg_status lbg_block_create(int device, const int box_lo[3], const int dims[3], 
         b->device_bytes += pdf_bytes;
     }
     if (b->coupling) {
-        const size_t n = (size_t)L.nx * L.ny * L.nz;
+        // + 64 cells of slack: the TMA-fed K2 copies 34/36/48-element field windows per segment
+        const size_t n = (size_t)L.nx * L.ny * L.nz + 64;
         struct A {
             void** p;
             size_t bytes;

@@ -487,21 +487,40 @@ __device__ __forceinline__ void seg_load(const SweepArgs& a, unsigned c0, int la
     }
 }
 
+// first half of a segment's update: everything that consumes the segment's loaded registers
+// (solid velocity from its id, the moments). The pipelined loop issues the next segment's
+// loads only after this, so no wait on this segment's data can also wait on those loads
+// (loads share the warp's few scoreboard counters).
+struct SegPre {
+    double v[3];
+    double rho, ux, uy, uz, usq;
+    bool ok;
+};
+
+template <bool kVsnap>
+__device__ __forceinline__ void seg_pre(const SweepArgs& a, const SegIn& in, SegPre& pre) {
+    if (!in.act) return;
+    solid_velocity_sel<kVsnap>(a, in.cnt > 0, in.fc, in.i, in.j, in.k, pre.v, in.id0);
+    moments(in.f, pre.rho, pre.ux, pre.uy, pre.uz);
+    pre.usq = (pre.ux * pre.ux + pre.uy * pre.uy) + pre.uz * pre.uz;
+    pre.ok = pre.rho > 0.0 && pre.usq <= kMaxVelocity * kMaxVelocity && isfinite(pre.rho);
+}
+
 template <bool kFused, bool kVsnap>
-__device__ __forceinline__ void seg_compute(const SweepArgs& a, const SegIn& in) {
+__device__ __forceinline__ void seg_finish(const SweepArgs& a, const SegIn& in, const SegPre& pre) {
     bool ok = true;
-    double m[2][3] = {{0, 0, 0}, {0, 0, 0}};
+    double m[3] = {0, 0, 0};
     double cc[3] = {0, 0, 0};
     int p0 = -1;
     if (in.act) {
         const bool cov = in.cnt > 0;
-        double v[3];
-        solid_velocity_sel<kVsnap>(a, cov, in.fc, in.i, in.j, in.k, v, in.id0);
-        ok = psm_cell_one<false>(in.f, a.inv_tau, a.F, cov ? in.bt : 0.0, cov ? in.b0 : 0.0, v[0], v[1], v[2],
-                                 a.dst, a.L.plane, in.base, m[0]);
+        psm_cell_one_pairs<false>(in.f, pre.rho, pre.ux, pre.uy, pre.uz, pre.usq, a.inv_tau, a.F,
+                                  cov ? in.bt : 0.0, cov ? in.b0 : 0.0, pre.v[0], pre.v[1], pre.v[2], a.dst,
+                                  a.L.plane, in.base, m);
+        ok = pre.ok;
         if constexpr (!kFused) {
             if (cov)
-                for (int d = 0; d < 3; ++d) a.m0[3 * in.fc + d] = m[0][d];
+                for (int d = 0; d < 3; ++d) a.m0[3 * in.fc + d] = m[d];
         } else if (cov) {
             cc[0] = (double)(a.blk_lo[0] + in.i) + 0.5;
             cc[1] = (double)(a.blk_lo[1] + in.j) + 0.5;
@@ -511,7 +530,7 @@ __device__ __forceinline__ void seg_compute(const SweepArgs& a, const SegIn& in)
         }
     }
     count_bad(a.err, !ok);
-    if constexpr (kFused) fused_accumulate(a, p0, m[0], cc);
+    if constexpr (kFused) fused_accumulate(a, p0, m, cc);
 }
 
 template <bool kFused, bool kVsnap>
@@ -522,20 +541,175 @@ __global__ void __launch_bounds__(128) psm_seg_pipe_kernel(const SweepArgs a) {
     const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
     if (warp >= nseg) return;  // warp-uniform
     SegIn cur, nxt;
+    SegPre pre;
     seg_load<kVsnap>(a, a.seg_list[warp], lane, cur);
     int s = warp;
     for (;;) {
         const bool more = s + nwarps < nseg;
+        seg_pre<kVsnap>(a, cur, pre);
         if (more) seg_load<kVsnap>(a, a.seg_list[s + nwarps], lane, nxt);
-        seg_compute<kFused, kVsnap>(a, cur);
+        seg_finish<kFused, kVsnap>(a, cur, pre);
         if (!more) break;
         s += nwarps;
         // second half of the unrolled pair: roles swapped, no register copy
         const bool more2 = s + nwarps < nseg;
+        seg_pre<kVsnap>(a, nxt, pre);
         if (more2) seg_load<kVsnap>(a, a.seg_list[s + nwarps], lane, cur);
-        seg_compute<kFused, kVsnap>(a, nxt);
+        seg_finish<kFused, kVsnap>(a, nxt, pre);
         if (!more2) break;
         s += nwarps;
+    }
+}
+
+// K2 for unforced one-entry segments fed by the Tensor Memory Accelerator: per warp, lane 0
+// issues one 1-D bulk copy (cp.async.bulk, completion counted on an mbarrier) per pulled
+// q-row — the 40 doubles [i0 - 4, i0 + 36) of the row the direction pulls from, with the
+// periodic y/z wrap applied to the row — plus the segment's btot, b0, id0 and count
+// windows, into one of two shared-memory stages, while the warp computes the previous
+// segment from the other stage. A lane's population q is stage.f[q][4 + lane - c_x(q)].
+// 23 copy instructions per segment instead of 23 loads per lane, and nothing in flight
+// occupies registers or the warp's scoreboards (the register-pipelined variant stalled on
+// them; per-lane cp.async saturated the LSU queue: profiles/r01_ab_k2.txt). Lanes at an
+// x-wrapped block face re-pull from global (pull()).
+struct SegStage {
+    double f[kQ][40];
+    double bt[34];
+    double b0[34];
+    int id0[36];
+    unsigned char cnt[48];
+};
+static_assert(sizeof(SegStage) % 16 == 0, "stage must keep 16-byte alignment");
+constexpr int kTmaWarps = 4;  // warps per CTA (128 threads), two stages each
+constexpr unsigned kRowBytes = 40 * 8;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void tma_bulk(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+    unsigned done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+    } while (!done);
+}
+
+// lane 0: the copies of segment c0 into `st`, completing on `bar`
+template <bool kVsnap>
+__device__ __forceinline__ void seg_tma_issue(const SweepArgs& a, unsigned c0, SegStage& st,
+                                              unsigned long long* bar) {
+    const Layout& L = a.L;
+    const int i0 = (int)(c0 % (unsigned)L.nx);
+    const int j = (int)((c0 / (unsigned)L.nx) % (unsigned)L.ny);
+    const int k = (int)(c0 / ((unsigned)L.nx * (unsigned)L.ny));
+    const unsigned tx = kQ * kRowBytes + 2 * 272 + (kVsnap ? 144 : 0) + 48;
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // prior generic reads of st
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(tx)
+                 : "memory");
+    const long long sy = L.px, sz = (long long)L.px * L.py;
+    const long long yl = (a.wrap[1] && j == 0) ? L.ny * sy : 0;
+    const long long yh = (a.wrap[1] && j == L.ny - 1) ? -L.ny * sy : 0;
+    const long long zl = (a.wrap[2] && k == 0) ? L.nz * sz : 0;
+    const long long zh = (a.wrap[2] && k == L.nz - 1) ? -L.nz * sz : 0;
+    const long long row0 = L.idx(i0, j, k) - 4;
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+        const long long r = q * L.plane + row0 - cy(q) * sy - cz(q) * sz + (cy(q) == 1 ? yl : (cy(q) == -1 ? yh : 0)) +
+                            (cz(q) == 1 ? zl : (cz(q) == -1 ? zh : 0));
+        tma_bulk(st.f[q], a.src + r, kRowBytes, bar);
+    }
+    const long long c = (long long)c0;
+    tma_bulk(st.bt, a.btot + (c & ~1LL), 272, bar);
+    tma_bulk(st.b0, a.b0 + (c & ~1LL), 272, bar);
+    if constexpr (kVsnap) tma_bulk(st.id0, a.id0 + (c & ~3LL), 144, bar);
+    tma_bulk(st.cnt, a.count + (c & ~15LL), 48, bar);
+}
+
+template <bool kFused, bool kVsnap>
+__device__ __forceinline__ void seg_from_tma(const SweepArgs& a, unsigned c0, int lane, const SegStage& st) {
+    const Layout& L = a.L;
+    const int i = (int)(c0 % (unsigned)L.nx) + lane;
+    const int j = (int)((c0 / (unsigned)L.nx) % (unsigned)L.ny);
+    const int k = (int)(c0 / ((unsigned)L.nx * (unsigned)L.ny));
+    const bool act = i < L.nx && in_boxes(a, i, j, k);
+    bool ok = true;
+    double m[3] = {0, 0, 0};
+    double cc[3] = {0, 0, 0};
+    int p0 = -1;
+    if (act) {
+        const long long base = L.idx(i, j, k), fc = L.frac(i, j, k);
+        const int cnt = st.cnt[lane + (int)(c0 & 15u)];
+        const bool cov = cnt > 0;
+        const int id0 = kVsnap ? st.id0[lane + (int)(c0 & 3u)] : 0;
+        const double bt = st.bt[lane + (int)(c0 & 1u)], b0 = st.b0[lane + (int)(c0 & 1u)];
+        double f[kQ];
+        if (a.wrap[0] && (i == 0 || i == L.nx - 1)) {
+            pull(a, i, j, k, base, f);
+        } else {
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) f[q] = st.f[q][4 + lane - cx(q)];
+        }
+        double v[3];
+        solid_velocity_sel<kVsnap>(a, cov, fc, i, j, k, v, id0);
+        ok = psm_cell_one<false>(f, a.inv_tau, a.F, cov ? bt : 0.0, cov ? b0 : 0.0, v[0], v[1], v[2], a.dst,
+                                 L.plane, base, m);
+        if constexpr (!kFused) {
+            if (cov)
+                for (int d = 0; d < 3; ++d) a.m0[3 * fc + d] = m[d];
+        } else if (cov) {
+            cc[0] = (double)(a.blk_lo[0] + i) + 0.5;
+            cc[1] = (double)(a.blk_lo[1] + j) + 0.5;
+            cc[2] = (double)(a.blk_lo[2] + k) + 0.5;
+            p0 = a.sidx(kVsnap ? id0 : a.id0[fc]);
+            if (p0 < 0) atomicAdd(&a.err->unknown, 1ull);
+        }
+    }
+    count_bad(a.err, !ok);
+    if constexpr (kFused) fused_accumulate(a, p0, m, cc);
+}
+
+template <bool kFused, bool kVsnap>
+__global__ void __launch_bounds__(32 * kTmaWarps) psm_seg_tma_kernel(const SweepArgs a) {
+    extern __shared__ __align__(128) unsigned char seg_smem[];
+    const int nseg = a.seg_n[0];
+    const int lane = threadIdx.x & 31;
+    const int wl = threadIdx.x >> 5;
+    const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
+    SegStage* stage = reinterpret_cast<SegStage*>(seg_smem) + 2 * wl;
+    unsigned long long* bar =
+        reinterpret_cast<unsigned long long*>(seg_smem + sizeof(SegStage) * 2 * kTmaWarps) + 2 * wl;
+    if (warp >= nseg) return;  // warp-uniform
+    if (lane == 0) {
+        for (int t = 0; t < 2; ++t)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bar[t])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    unsigned c_cur = a.seg_list[warp];
+    if (lane == 0) seg_tma_issue<kVsnap>(a, c_cur, stage[0], &bar[0]);
+    unsigned phase[2] = {0u, 0u};
+    int b = 0;
+    for (int s = warp; s < nseg; s += nwarps) {
+        const bool more = s + nwarps < nseg;
+        const unsigned c_next = more ? a.seg_list[s + nwarps] : 0u;
+        if (more && lane == 0) seg_tma_issue<kVsnap>(a, c_next, stage[b ^ 1], &bar[b ^ 1]);
+        mbar_wait(&bar[b], phase[b]);
+        phase[b] ^= 1u;
+        seg_from_tma<kFused, kVsnap>(a, c_cur, lane, stage[b]);
+        __syncwarp();  // every lane is done with stage b before lane 0 refills it
+        c_cur = c_next;
+        b ^= 1;
     }
 }
 
@@ -685,12 +859,20 @@ static void with_flags(bool x, bool y, bool z, Fn&& fn) {
     x ? yf(std::true_type{}) : yf(std::false_type{});
 }
 
-// unforced one-entry K2: the software-pipelined kernel (default; config 3 coupled sweep
-// 1.17 -> 1.13 ms, profiles/r01_ab_k2.txt), LBG_K2_PIPE=0 the plain segment loop
-static bool k2_pipe() {
-    static const bool v = [] {
-        const char* e = std::getenv("LBG_K2_PIPE");
-        return !(e && e[0] == '0');
+// unforced one-entry K2 variant, LBG_K2_MODE: 0 plain segment loop, 1 register-pipelined,
+// 2 TMA-fed (profiles/r01_ab_k2.txt)
+static int k2_mode() {
+    static const int v = [] {
+        const char* e = std::getenv("LBG_K2_MODE");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
+static int k2_tma_per_sm() {
+    static const int v = [] {
+        const char* e = std::getenv("LBG_K2_TMA_SM");
+        return e ? std::max(1, std::atoi(e)) : 4;
     }();
     return v;
 }
@@ -711,7 +893,12 @@ static void launch_psm_segments(lbg_block b, const SweepArgs& a, bool forced, cu
     const unsigned g1 = (unsigned)(sms * per_sm), g2 = (unsigned)(sms * 4);
     with_flags(forced, fused, b->v_snap, [&](auto F, auto U, auto V) {
         // segments with one-entry cells only (the bulk): lean pair-scheduled operator
-        if (!decltype(F)::value && k2_pipe())
+        if (!decltype(F)::value && k2_mode() == 2) {
+            constexpr size_t smem = (sizeof(SegStage) + 8) * 2 * kTmaWarps;
+            auto kern = psm_seg_tma_kernel<decltype(U)::value, decltype(V)::value>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            kern<<<(unsigned)(sms * k2_tma_per_sm()), 32 * kTmaWarps, smem, st>>>(a);
+        } else if (!decltype(F)::value && k2_mode() == 1)
             psm_seg_pipe_kernel<decltype(U)::value, decltype(V)::value>
                 <<<(unsigned)(sms * k2_pipe_per_sm()), 128, 0, st>>>(a);
         else

@@ -1,0 +1,29 @@
+"""The coupled-sweep parity tests under every selectable kernel variant (the switches are read
+once per process, so each variant runs the tests in a subprocess):
+  LBG_K2_MODE=0 plain segment loop, 1 register-pipelined (default), 2 TMA-fed one-entry K2;
+  LBG_K2_CONCURRENT=0 K2 after K1 on one stream; LBG_SWEEP_PAIR=1 the 128-bit K1."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+SELECT = "coupled or setu or fused or mapping_and_solid or shear or sweep"
+
+
+@pytest.mark.parametrize("env", [{"LBG_K2_MODE": "0"}, {"LBG_K2_MODE": "2"}, {"LBG_K2_CONCURRENT": "0"},
+                                 {"LBG_SWEEP_PAIR": "1"}])
+def test_parity_suite_under_variant(env):
+    e = dict(os.environ, **env)
+    # the parity cases, and config 1 through the drop-in (periodic block: in-kernel x/y/z wrap)
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_parity.py"),
+                        os.path.join(ROOT, "tests", "test_dropin.py"), "-m", "gpu", "-q", "-x",
+                        "-k", f"({SELECT}) or config1_known_answers", "-p", "no:cacheprovider"],
+                       cwd=ROOT, env=e, capture_output=True, text=True, timeout=900)
+    tail = (r.stdout + r.stderr)[-2000:]
+    assert r.returncode == 0, tail
+    assert " passed" in tail and "failed" not in tail, tail
