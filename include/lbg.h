@@ -181,12 +181,17 @@ lbg_status lbg_fill_periodic(lbg_block b, const int periodic[3], int full);
 lbg_status lbg_apply_boundaries(lbg_block b, const lbg_face_bc faces[6], const int touches[6]);
 
 /* ------------------------------------------------------------------ particle coupling */
-/* SubBlockRegistry::build + build_fraction_field + set_solid_velocities
- * (psm.cpp:55-169): snapshots must be id-sorted; staged through pinned memory and
- * copied H2D on the block's side stream. `subdivisions` is accepted for API parity
- * (the device binning is finer and gives the same candidate order). */
+/* SubBlockRegistry::build + build_fraction_field (psm.cpp:55-136), with the solid
+ * velocities of set_solid_velocities (psm.cpp:138-169) following from these snapshots until
+ * lbg_set_solid_velocities registers others: snapshots must be id-sorted; staged through
+ * pinned memory and copied H2D on the block's side stream. `subdivisions` is accepted for
+ * API parity (the device binning is finer and gives the same candidate order). */
 lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisions);
-/* set_solid_velocities alone (psm.cpp:138-169) for a fraction field set by the caller. */
+/* set_solid_velocities (psm.cpp:138-169), replaces Simulation::phase_setu_inner's call
+ * (sim.cpp:296-297). Uploads the (post velocity-sync) snapshots; the PSM sweep evaluates
+ * u + omega x (c - x) per entry from them. If the list lost an id of the mapping list (or
+ * the fraction field was uploaded by the caller), the per-entry walk runs here and counts
+ * unknown ids (SyncError from lbg_sync). lbg_download_solid_velocity materialises v0/v1. */
 lbg_status lbg_set_solid_velocities(lbg_block b, const lbg_snapshot* snaps, int n);
 /* LBG_FORCE_SCRATCH (default) or LBG_FORCE_FUSED; takes effect from the next lbg_map. */
 lbg_status lbg_set_force_mode(lbg_block b, int mode);
