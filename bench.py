@@ -325,6 +325,26 @@ def host_mem_available():
     return None
 
 
+def gpu_local_cpus(device):
+    """Host CPUs NVML reports closest to CUDA device `device` (its NUMA node), matched by PCI
+    bus id; None if unknown. The e2e job pins its host PdfField from a thread bound to them,
+    so the pages and the DMA stay on the GPU's socket."""
+    try:
+        import pynvml
+        import torch
+        pr = torch.cuda.get_device_properties(device)
+        bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        words = ((os.cpu_count() or 64) + 63) // 64
+        mask = pynvml.nvmlDeviceGetCpuAffinity(h, words)
+        cpus = {64 * w + b for w, m in enumerate(mask) for b in range(64) if (m >> b) & 1}
+        cpus &= os.sched_getaffinity(0)
+        return cpus or None
+    except Exception:  # noqa: BLE001 — no NVML / no PCI info: leave the affinity alone
+        return None
+
+
 NVLINK_GBS = 900.0  # NVLink 5 per direction per GPU (B200_PROFILING.md)
 
 
@@ -476,6 +496,12 @@ def run_lbg(args):
     fits = all(allgather(fits)) if N > 1 else fits
     e2e_mlups = loop_mlups = None
     finite = None
+    numa_cpus = None
+    saved_affinity = os.sched_getaffinity(0)
+    if fits and os.environ.get("LBG_BENCH_NUMA", "1") != "0":
+        numa_cpus = gpu_local_cpus(local)
+        if numa_cpus:
+            os.sched_setaffinity(0, numa_cpus)
     if fits:
         hp = C.c_void_p()
         lbdem.check(abi.load().lbg_host_alloc(pdf_bytes, C.byref(hp)))
@@ -499,6 +525,7 @@ def run_lbg(args):
         finite = bool(np.isfinite(host[:, n // 2, n // 2, 1:5]).all())
         del host
         abi.load().lbg_host_free(hp)
+    os.sched_setaffinity(0, saved_affinity)  # the CPU baseline below uses every host core
 
     out = None
     if rank == 0:
@@ -541,7 +568,8 @@ def run_lbg(args):
                              "from pinned host memory (reference layout), per step sweep [+ halo] + swap + "
                              "lbg_sync (error-counter D2H, NumericError check), lbg_download_src; wall clock, "
                              "max over ranks"),
-                     "steady_state_loop_mlups": round(loop_mlups, 1), "result_finite": finite}
+                     "steady_state_loop_mlups": round(loop_mlups, 1), "result_finite": finite,
+                     "host_buffer_numa_cpus": len(numa_cpus) if numa_cpus else None}
                     if e2e_mlups is not None else
                     {"value": None, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                      "skipped": (f"{local_ranks} host PdfFields of {pdf_bytes / 1e9:.1f} GB exceed 60 % of the "
