@@ -191,7 +191,8 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
  * (sim.cpp:296-297). Uploads the (post velocity-sync) snapshots; the PSM sweep evaluates
  * u + omega x (c - x) per entry from them. If the list lost an id of the mapping list (or
  * the fraction field was uploaded by the caller), the per-entry walk runs here and counts
- * unknown ids (SyncError from lbg_sync). lbg_download_solid_velocity materialises v0/v1. */
+ * unknown ids, returning LBG_SYNC_ERROR itself (a synchronising call only then).
+ * lbg_download_solid_velocity materialises v0/v1. */
 lbg_status lbg_set_solid_velocities(lbg_block b, const lbg_snapshot* snaps, int n);
 /* LBG_FORCE_SCRATCH (default) or LBG_FORCE_FUSED; takes effect from the next lbg_map. */
 lbg_status lbg_set_force_mode(lbg_block b, int mode);

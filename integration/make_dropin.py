@@ -159,11 +159,12 @@ SIM_CPP_EDITS = [
      "                                  params_.kernels == KernelMode::openmp);\n",
      "        blk.dev->map(blk.snapshots, params_.subdivisions);\n"
      "        blk.dev->sync();\n"),
-    # sim.cpp:296-297 — set_solid_velocities on the device (post velocity-sync snapshots)
+    # sim.cpp:296-297 — set_solid_velocities on the device (post velocity-sync snapshots):
+    # an asynchronous snapshot upload the PSM sweep evaluates u + omega x (c - x) from; it
+    # raises SyncError itself when the exact per-entry walk finds unknown ids, so no sync here
     ("        psm::set_solid_velocities(blk.svel, blk.frac, blk.box, blk.snapshots,\n"
      "                                  params_.kernels == KernelMode::openmp);\n",
-     "        blk.dev->set_solid_velocities(blk.snapshots);\n"
-     "        blk.dev->sync();\n"),
+     "        blk.dev->set_solid_velocities(blk.snapshots);\n"),
     # sim.cpp:302 — inner kernel + end-of-operator check
     ("        run_kernel(blk, {{1, 1, 1}, {d.x - 1, d.y - 1, d.z - 1}});\n",
      "        run_kernel(blk, {{1, 1, 1}, {d.x - 1, d.y - 1, d.z - 1}});\n"

@@ -698,12 +698,15 @@ lbg_status lbg_set_solid_velocities(lbg_block b, const lbg_snapshot* snaps, int 
         while (q < (size_t)n && snaps[q].id < b->map_ids[p]) ++q;
         superset = q < (size_t)n && snaps[q].id == b->map_ids[p];
     }
-    if (superset) {
+    if (superset) {  // nothing on the device can fail: the caller need not synchronise
         b->v_snap = true;
         return LBG_OK;
     }
     b->v_snap = false;
-    return run_setu(b);
+    if (lbg_status s = run_setu(b)) return s;
+    // the exact walk ran: report its unknown-id count here, as set_solid_velocities throws
+    // SyncError itself (psm.cpp:165-168)
+    return lbg_sync(b, nullptr);
 }
 
 // LBG_FORCE_FUSED: the sweep already summed; copy the accumulators out
