@@ -105,7 +105,8 @@ def _worker(rank, world, port, domain, axis, out_q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,domain,axis", [(2, (6, 5, 8), 2), (2, (8, 4, 5), 0), (3, (5, 4, 9), 2)])
+@pytest.mark.parametrize("world,domain,axis", [(2, (6, 5, 8), 2), (2, (8, 4, 5), 0), (3, (5, 4, 9), 2),
+                                               (8, (4, 3, 16), 2)])  # the 8-GPU ring of config 4
 def test_slab_halo_protocol_gloo(world, domain, axis):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
@@ -130,6 +131,9 @@ def test_decomposition_rules():
     assert [d.prev(r) for r in range(4)] == [3, 0, 1, 2]
     assert [d.next(r) for r in range(4)] == [1, 2, 3, 0]
     assert d.wrap_axes() == (1, 1, 0)
+    d8 = SlabDecomposition((512, 512, 4096), 8)  # config 4 at 8 GPUs
+    assert d8.block_dims() == (512, 512, 512) and d8.block_lo(7) == (0, 0, 3584)
+    assert [d8.prev(r) for r in range(8)] == [7, 0, 1, 2, 3, 4, 5, 6]
     assert d.domain_faces(0) == (True, True, True, True, True, False)
     nd = SlabDecomposition((64, 32, 32), 2, axis=0, periodic=(0, 1, 1))
     assert nd.prev(0) == -1 and nd.next(1) == -1
