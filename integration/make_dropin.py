@@ -30,7 +30,8 @@ SIM_HPP_EDITS = [
      "    std::shared_ptr<gpu::DeviceBlock> dev;  ///< liblbg block (drop-in)\n"
      "    mutable bool host_stale = false;        ///< host field copy behind the device\n"
      "    mutable std::vector<double> moments;    ///< device moments cache (observers)\n"
-     "    mutable bool moments_stale = true;\n"),
+     "    mutable bool moments_stale = true;\n"
+     "    bool outer_done = false;                ///< whole block swept in phase_setu_inner\n"),
 ]
 
 SIM_CPP_EDITS = [
@@ -64,6 +65,14 @@ SIM_CPP_EDITS = [
      "bool device_halo() {\n"
      "    const char* e = std::getenv(\"LBDEM_GPU_HALO\");\n"
      "    return !(e && std::string(e) == \"host\");\n"
+     "}\n"
+     "/// LBDEM_GPU_SWEEP=split: the reference's inner sweep / halo / BCs / outer-shell sweep;\n"
+     "/// default one sweep of the whole block in phase_setu_inner after the halo and BCs (the\n"
+     "/// halo messages were posted in phase_post_and_map; the inner sweep reads no ghost, so\n"
+     "/// the results are identical) - no strided x-face shell sweep.\n"
+     "bool full_sweep() {\n"
+     "    const char* e = std::getenv(\"LBDEM_GPU_SWEEP\");\n"
+     "    return !(e && std::string(e) == \"split\");\n"
      "}\n"
      "/// Observers read the host copies; refresh them from the device after a step.\n"
      "void refresh_host(const std::vector<std::unique_ptr<BlockState>>& blocks, bool coupling) {\n"
@@ -165,23 +174,52 @@ SIM_CPP_EDITS = [
     ("        psm::set_solid_velocities(blk.svel, blk.frac, blk.box, blk.snapshots,\n"
      "                                  params_.kernels == KernelMode::openmp);\n",
      "        blk.dev->set_solid_velocities(blk.snapshots);\n"),
-    # sim.cpp:302 — inner kernel + end-of-operator check
-    ("        run_kernel(blk, {{1, 1, 1}, {d.x - 1, d.y - 1, d.z - 1}});\n",
+    # sim.cpp:299-303 — inner kernel + end-of-operator check; by default the whole block
+    # (halo completion and BCs of sim.cpp:307-312 moved ahead of it, see full_sweep())
+    ("    {\n"
+     "        ScopedTimer t(blk.timings, Category::kPsm);\n"
+     "        const Vec3i d = blk.dims();\n"
      "        run_kernel(blk, {{1, 1, 1}, {d.x - 1, d.y - 1, d.z - 1}});\n"
-     "        blk.dev->sync();\n"),
-    # sim.cpp:312-317 — BCs, outer shell in one launch, swap
-    ("    lbm::apply_boundaries(blk.field, params_.bc, blk.domain_faces);\n"
+     "    }\n",
+     "    const Vec3i d = blk.dims();\n"
+     "    if (full_sweep()) {\n"
+     "        {\n"
+     "            ScopedTimer t(blk.timings, Category::kPsmComm);\n"
+     "            complete_halo_exchange(b);\n"
+     "        }\n"
+     "        blk.dev->apply_boundaries(params_.bc, blk.domain_faces);\n"
+     "        ScopedTimer t(blk.timings, Category::kPsm);\n"
+     "        run_kernel(blk, {{0, 0, 0}, {d.x, d.y, d.z}});\n"
+     "        blk.dev->sync();\n"
+     "        blk.outer_done = true;\n"
+     "    } else {\n"
+     "        ScopedTimer t(blk.timings, Category::kPsm);\n"
+     "        run_kernel(blk, {{1, 1, 1}, {d.x - 1, d.y - 1, d.z - 1}});\n"
+     "        blk.dev->sync();\n"
+     "    }\n"),
+    # sim.cpp:307-317 — halo completion, BCs, outer shell in one launch, swap (skipped
+    # when phase_setu_inner swept the whole block)
+    ("    {\n"
+     "        ScopedTimer t(blk.timings, Category::kPsmComm);\n"
+     "        complete_halo_exchange(b);\n"
+     "    }\n"
+     "    lbm::apply_boundaries(blk.field, params_.bc, blk.domain_faces);\n"
      "    {\n"
      "        ScopedTimer t(blk.timings, Category::kPsm);\n"
      "        for (const CellBox& box : boundary_shell(blk.dims())) run_kernel(blk, box);\n"
      "    }\n"
      "    blk.field.swap();\n",
-     "    blk.dev->apply_boundaries(params_.bc, blk.domain_faces);\n"
-     "    {\n"
+     "    if (!blk.outer_done) {\n"
+     "        {\n"
+     "            ScopedTimer t(blk.timings, Category::kPsmComm);\n"
+     "            complete_halo_exchange(b);\n"
+     "        }\n"
+     "        blk.dev->apply_boundaries(params_.bc, blk.domain_faces);\n"
      "        ScopedTimer t(blk.timings, Category::kPsm);\n"
      "        blk.dev->sweep_boxes(params_.fluid, boundary_shell(blk.dims()));\n"
      "        blk.dev->sync();\n"
      "    }\n"
+     "    blk.outer_done = false;\n"
      "    blk.dev->swap();\n"
      "    blk.host_stale = true;\n"
      "    blk.moments_stale = true;\n"),
