@@ -1,7 +1,8 @@
 """The coupled-sweep parity tests under every selectable kernel variant (the switches are read
 once per process, so each variant runs the tests in a subprocess):
   LBG_K2_MODE=0 plain segment loop, 1 register-pipelined (default), 2 TMA-fed one-entry K2;
-  LBG_K2_CONCURRENT=0 K2 after K1 on one stream; LBG_SWEEP_PAIR=1 the 128-bit K1."""
+  LBG_K2_CONCURRENT=0 K2 after K1 on one stream; LBG_SWEEP_PAIR=1 the 128-bit K1;
+  LBDEM_GPU_SWEEP=split the drop-in in the reference's inner / halo / BC / outer-shell order."""
 import os
 import subprocess
 import sys
@@ -13,16 +14,18 @@ from conftest import ROOT
 pytestmark = pytest.mark.gpu
 
 SELECT = "coupled or setu or fused or mapping_and_solid or shear or sweep"
+DROPIN = "config1_known_answers or particle_bed or decomposition_invariance"
 
 
 @pytest.mark.parametrize("env", [{"LBG_K2_MODE": "0"}, {"LBG_K2_MODE": "2"}, {"LBG_K2_CONCURRENT": "0"},
-                                 {"LBG_SWEEP_PAIR": "1"}])
+                                 {"LBG_SWEEP_PAIR": "1"}, {"LBDEM_GPU_SWEEP": "split"}])
 def test_parity_suite_under_variant(env):
     e = dict(os.environ, **env)
-    # the parity cases, and config 1 through the drop-in (periodic block: in-kernel x/y/z wrap)
+    # the parity cases, and drop-in runs vs the reference (config 1: periodic block, in-kernel
+    # wrap; the bed: walls, inflow, outflow; 2x2x2 decomposition)
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(ROOT, "tests", "test_gpu_parity.py"),
                         os.path.join(ROOT, "tests", "test_dropin.py"), "-m", "gpu", "-q", "-x",
-                        "-k", f"({SELECT}) or config1_known_answers", "-p", "no:cacheprovider"],
+                        "-k", f"({SELECT}) or {DROPIN}", "-p", "no:cacheprovider"],
                        cwd=ROOT, env=e, capture_output=True, text=True, timeout=900)
     tail = (r.stdout + r.stderr)[-2000:]
     assert r.returncode == 0, tail
