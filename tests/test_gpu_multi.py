@@ -29,6 +29,23 @@ def test_slab_halo_bitwise(axis, halo):
     assert r.returncode == 0
 
 
+@pytest.mark.parametrize("halo", ["p2p", "nccl"])
+def test_config4_full_size_two_gpus_vs_one_block(halo):
+    """Config 4 at 512^3 per GPU on 2 GPUs against the same 512 x 512 x 1024 domain as one
+    block: per-plane hashes of the per-cell moments equal over all 2.7e8 cells (tests/
+    mp_fullsize_gpu.py). Needs 131 GB on GPU 0."""
+    n = _ngpus()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    env = dict(os.environ, SLAB_HALO=halo, SLAB_STEPS="3")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(HERE, "mp_fullsize_gpu.py")],
+                       env=env, capture_output=True, text=True, timeout=900)
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0
+    assert "rank 1: 0 of 512 z-planes differ" in r.stdout
+
+
 @pytest.mark.parametrize("halo,per", [("device", 1), ("host", 1), ("device", 2)])
 def test_dropin_bed_spread_over_gpus_bitwise(halo, per, monkeypatch):
     """The drop-in with its blocks dealt over the GPUs (LBDEM_GPU_SPREAD=1: `per` consecutive
