@@ -43,7 +43,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["lbg", "reference"], default="lbg")
-    ap.add_argument("--n", type=int, default=512, help="cells per axis of each GPU's block")
+    ap.add_argument("--n", "--edge", dest="n", type=int, default=512,
+                    help="cells per axis of each GPU's block (--edge under torchrun, whose parser takes --n)")
     ap.add_argument("--tau", type=float, default=0.8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-coupled", action="store_true", help="skip the config-3 coupled-step timing")
@@ -376,9 +377,18 @@ def run_lbg(args):
 
     rank, world, local = dist_env()
     N = world
+    share = os.environ.get("LBG_BENCH_SHARE_GPUS") == "1"
+    if share:
+        # functional check of an N-rank ring on fewer GPUs (ranks share devices, so the
+        # plumbing runs on gloo — NCCL refuses two ranks per GPU — and the timings are not
+        # per-GPU numbers)
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2303_11811_b200.driver import FluidStepper, SlabDecomposition
     n = args.n
     dims = (n, n, n)
@@ -433,7 +443,7 @@ def run_lbg(args):
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if share else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
