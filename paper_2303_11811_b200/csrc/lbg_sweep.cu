@@ -5,7 +5,8 @@
 //
 // Roofline: HBM-bound. Algorithmic bytes per lattice update (LUP): 19 f64 pulled + 19 f64
 // stored = 304 B for the plain sweep; the coupled sweep adds the 1-byte count per cell and,
-// per covered cell, 8 B btot + per entry (8 B b + 24 B v read, 24 B m written).
+// per covered cell, 8 B btot + per entry (8 B b + 4 B id read, 24 B m written; the solid
+// velocity u + omega x (c - x) is evaluated from the L2-resident snapshot list, v_snap).
 //
 // Kernels:
 //   K1 sweep_box   — one CellBox, 3-D grid; thread x maps to global i with the chunk origin
@@ -18,10 +19,15 @@
 //                    from the segment lists the mapping pass writes; K1 skips exactly those
 //                    segments, so each DRAM sector is swept by one kernel. Segments with only
 //                    one-entry cells run the pair-scheduled one-entry operator on every lane
-//                    (~90 registers; fluid lanes with B = 0 when unforced), segments with a
-//                    two-entry cell the general operator (~220); the fluid majority keeps the
-//                    70-register SRT kernel (the paper's fused A100 kernel ran at 196 registers,
-//                    12.5 % occupancy).
+//                    (fluid lanes with B = 0 when unforced) — by default in psm_seg_pipe, the
+//                    register-pipelined loop that has the next segment's loads in flight
+//                    (LBG_K2_MODE: 0 plain loop, 1 pipelined, 2 TMA-fed psm_seg_tma);
+//                    segments with a two-entry cell the pair-scheduled two-entry operator
+//                    (~124 registers); the fluid majority keeps the 70-register SRT kernel
+//                    (the paper's fused A100 kernel ran at 196 registers, 12.5 % occupancy,
+//                    PAPER.md:676).
+//   sweep_flat_coupled — thin boxes of a coupled block (shell), one-entry and two-entry
+//                    lanes in two launches.
 // Periodic wrap: for axes in b->wrap the pull reads the wrapped interior cell directly
 // (what fill_periodic_ghosts would have copied into the ghost slot), so a fully periodic
 // single-GPU step is one launch with no ghost fill.
