@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--tau", type=float, default=0.8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-coupled", action="store_true", help="skip the config-3 coupled-step timing")
-    ap.add_argument("--coupled-steps", type=int, default=8)
+    ap.add_argument("--coupled-steps", type=int, default=4, help="coupled steps per repetition (best of 3)")
     ap.add_argument("--halo", choices=["p2p", "nccl"], default="p2p",
                     help="N > 1: outer sweep stores into the neighbours over NVLink (p2p) or NCCL halo")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
@@ -191,30 +191,46 @@ def config3(blocks=(1, 1, 1), workers=1):
     return json.dumps(c)
 
 
+REPS = 3  # best of >= 3 repetitions, the reference's own perf protocol (perf.cpp:104)
+
+
+def _best_of(sim, steps, reps=REPS):
+    """Run `reps` repetitions of `steps` coupled steps; (seconds, categories) of the fastest
+    and the median wall time. Host-side phases (the reference's DEM and messaging on 8
+    worker threads with nested OpenMP teams) see transient scheduling noise of up to +40 %
+    on a shared host; the best repetition is the reference's reporting rule."""
+    runs = []
+    for _ in range(reps):
+        sim.reset_timers()
+        t0 = time.perf_counter()
+        sim.run(steps)
+        runs.append((time.perf_counter() - t0, sim.timings()))
+    runs.sort(key=lambda r: r[0])
+    return runs[0][0], runs[0][1], runs[len(runs) // 2][0]
+
+
 def coupled_step(steps, with_reference, ref_steps=1, blocks=(1, 1, 1), workers=1):
     """Config 3: ~10^4 spheres d = 10 in 256^3, bed BCs, four-way coupled
     with the reference's host DEM. GPU side through the drop-in build (the reference
     Simulation with its fluid/coupling operators on liblbg); the same config on the
     unmodified reference (oracle/_ref, OpenMP on all host cores) for comparison. Times are
-    the reference's own per-category wall-clock TimingReport (perf.hpp:17-51)."""
+    the reference's own per-category wall-clock TimingReport (perf.hpp:17-51), best of
+    REPS repetitions for both (perf.cpp:104)."""
     sys.path.insert(0, os.path.join(ROOT, "integration"))
     import dropin
     cfg = config3(blocks, workers)
     out = {"workload": "config 3: 10^4 spheres (d = 10) in 256^3, no-slip walls, velocity inflow, "
                        "pressure outflow, 10 DEM sub-cycles per fluid step (host DEM = reference code)",
-           "blocks": list(blocks), "workers": workers}
+           "blocks": list(blocks), "workers": workers, "repetitions": REPS}
     for mode in ("scratch", "fused"):
         # scratch: reference semantics, partials bitwise (PARITY reduction);
         # fused: force/torque summed inside the PSM kernel (FAST, tolerance-level partials)
         os.environ["LBDEM_GPU_FORCE"] = mode
         sim = dropin.DropinSim(cfg, (256, 256, 256))
         sim.run(1)  # warm-up (allocations, first mapping)
-        sim.reset_timers()
-        t0 = time.perf_counter()
-        sim.run(steps)
-        dt = time.perf_counter() - t0
-        cat = sim.timings()
-        rec = {"ms_per_step": round(dt * 1e3 / steps, 2), "steps": steps,
+        dt, cat, med = _best_of(sim, steps)
+        rec = {"ms_per_step": round(dt * 1e3 / steps, 2), "median_ms_per_step": round(med * 1e3 / steps, 2),
+               "steps": steps,
                "categories_ms_per_step": {c: round(v * 1e3 / steps, 3) for c, v in zip(CATS, cat)},
                "gpu_side_ms_per_step": round(sum(cat[i] for i in (0, 1, 2, 3, 4)) * 1e3 / steps, 3),
                "particles": len(sim.particles()),
@@ -232,13 +248,10 @@ def coupled_step(steps, with_reference, ref_steps=1, blocks=(1, 1, 1), workers=1
         threads = max(1, (os.cpu_count() or 1) // max(1, workers))
         ref.set_threads(threads)
         rs = ref.sim(cfg)
-        rs.reset_timers()
-        t0 = time.perf_counter()
-        rs.run(ref_steps)
-        rdt = time.perf_counter() - t0
-        rc = rs.timings()
-        out["reference"] = {"ms_per_step": round(rdt * 1e3 / ref_steps, 1), "steps": ref_steps,
-                            "threads": threads * max(1, workers), "workers": workers,
+        rdt, rc, rmed = _best_of(rs, ref_steps)
+        out["reference"] = {"ms_per_step": round(rdt * 1e3 / ref_steps, 1),
+                            "median_ms_per_step": round(rmed * 1e3 / ref_steps, 1), "steps": ref_steps,
+                            "repetitions": REPS, "threads": threads * max(1, workers), "workers": workers,
                             "omp_threads_per_worker": threads, "kind": "reference",
                             "categories_ms_per_step": {c: round(v * 1e3 / ref_steps, 2) for c, v in zip(CATS, rc)}}
         out["speedup_vs_reference"] = round(out["reference"]["ms_per_step"] / out["ms_per_step"], 2)
@@ -595,7 +608,7 @@ def run_lbg(args):
                 # the reference's own parallelism lever: 2x2x2 blocks, one worker thread each
                 # (host DEM per block in parallel), same blocks/workers for the reference run
                 workers = min(8, os.cpu_count() or 8)
-                out["coupled_step"] = coupled_step(args.coupled_steps, not args.no_cpu_baseline, ref_steps=3,
+                out["coupled_step"] = coupled_step(args.coupled_steps, not args.no_cpu_baseline, ref_steps=1,
                                                    blocks=(2, 2, 2), workers=workers)
                 single = coupled_step(args.coupled_steps, False)
                 out["coupled_step"]["single_block"] = {k: single[k] for k in (
