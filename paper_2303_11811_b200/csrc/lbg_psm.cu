@@ -386,7 +386,8 @@ __global__ void __launch_bounds__(256) segment_kernel(const unsigned long long* 
 // entry's six terms (f = m, t = cross(c - x, m), psm.cpp:294-296) into shared memory, and lanes
 // 0..5 — one per component — add the 32 terms in entry order with Neumaier steps (vec3.hpp:75-82),
 // so each component's (sum, comp) is the reference's serial walk exactly. The next batch's
-// loads are issued before the current batch is replayed. (Clearing the scratch from here, by
+// momenta are gathered before the current batch is replayed, with their keys loaded one
+// batch earlier still. (Clearing the scratch from here, by
 // the loading lane, measured 10x slower than the separate clear_entries_kernel pass.)
 constexpr int kChainWarps = 8;
 
@@ -401,9 +402,11 @@ __global__ void __launch_bounds__(32 * kChainWarps) chain_kernel(
     const int i0 = start[p], i1 = end[p];
     const double x0 = s[p].x[0], x1 = s[p].x[1], x2 = s[p].x[2];
     double (*tw)[7] = terms[w];
-    auto load = [&](int base, long long& c, double& a0, double& a1, double& a2) {
+    // software pipeline: the keys two batches ahead, the momenta one batch ahead, so neither
+    // the key load nor the dependent momentum gather of a batch is waited on before its replay
+    auto key_at = [&](int base) { return base + lane < i1 ? keys[base + lane] : 0ull; };
+    auto gather = [&](int base, unsigned long long key, long long& c, double& a0, double& a1, double& a2) {
         if (base + lane < i1) {
-            const unsigned long long key = keys[base + lane];
             c = (long long)((key >> 1) & 0x7fffffffull);
             const double* mp = ((key & 1ull) ? m1 : m0) + 3 * c;
             a0 = mp[0];
@@ -413,7 +416,8 @@ __global__ void __launch_bounds__(32 * kChainWarps) chain_kernel(
     };
     long long c = 0;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    load(i0, c, a0, a1, a2);
+    gather(i0, key_at(i0), c, a0, a1, a2);
+    unsigned long long knext = key_at(i0 + 32);
     double sum = 0.0, comp = 0.0;
     for (int base = i0; base < i1; base += 32) {
         const int n = min(32, i1 - base);
@@ -431,7 +435,8 @@ __global__ void __launch_bounds__(32 * kChainWarps) chain_kernel(
             tw[lane][5] = r0 * a1 - r1 * a0;
         }
         __syncwarp();
-        load(base + 32, c, a0, a1, a2);  // next batch in flight during the replay
+        gather(base + 32, knext, c, a0, a1, a2);  // next batch's momenta in flight during the replay
+        knext = key_at(base + 64);                  // and the keys of the batch after
         if (lane < 6) {
             for (int e = 0; e < n; ++e) {
                 const double v = tw[e][lane];
