@@ -129,6 +129,32 @@ __global__ void __launch_bounds__(256) slab_copy_kernel(double* __restrict__ src
         *p = buf[t];
 }
 
+// all source slabs of a block in one launch (lbg_halo_stage): slab t covers the threads
+// [begin[t], begin[t+1]) and is packed [q][k][j][i] into its own staging buffer, exactly as
+// slab_copy_kernel(to_buf = 1) packs it
+struct StageArgs {
+    int n;
+    int lo[26][3];
+    int ext[26][3];
+    long long begin[27];
+    double* out[26];
+};
+
+__global__ void __launch_bounds__(256) slab_stage_kernel(const double* __restrict__ src, Layout L, StageArgs a) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.begin[a.n]) return;
+    int s = 0;
+    while (t >= a.begin[s + 1]) ++s;
+    const long long u = t - a.begin[s];
+    const long long cells = (long long)a.ext[s][0] * a.ext[s][1] * a.ext[s][2];
+    const int q = (int)(u / cells);
+    const long long r = u - q * cells;
+    const int i = a.lo[s][0] + (int)(r % a.ext[s][0]);
+    const int j = a.lo[s][1] + (int)((r / a.ext[s][0]) % a.ext[s][1]);
+    const int k = a.lo[s][2] + (int)(r / ((long long)a.ext[s][0] * a.ext[s][1]));
+    a.out[s][u] = src[q * L.plane + L.idx(i, j, k)];
+}
+
 static lbg_status nccl_check(ncclResult_t r, const char* what) {
     if (r == ncclSuccess) return LBG_OK;
     return set_error(LBG_CUDA_ERROR, std::string(what) + ": " + ncclGetErrorString(r));
@@ -350,7 +376,11 @@ lbg_status lbg_halo_stage(lbg_block b, const int (*offs)[3], int n) {
     if (!b || (n > 0 && !offs)) return set_error(LBG_INVALID, "null argument");
     LBG_CUDA(cudaSetDevice(b->device));
     if (!b->ev_stage) LBG_CUDA(cudaEventCreateWithFlags(&b->ev_stage, cudaEventDisableTiming));
+    if (n > 26) return set_error(LBG_INVALID, "at most 26 halo neighbours");
     Span span(b, LBG_CAT_PSM_COMM);
+    StageArgs a{};
+    a.n = 0;
+    a.begin[0] = 0;
     for (int t = 0; t < n; ++t) {
         int lo[3], ext[3];
         slab_box(b->L, offs[t], false, lo, ext);
@@ -359,8 +389,16 @@ lbg_status lbg_halo_stage(lbg_block b, const int (*offs)[3], int n) {
         if (lbg_status s = grow_device(b->stage[key], b->stage_cap[key], (long long)cnt, (long long)cnt,
                                        "cudaMalloc(halo staging)"))
             return s;
-        slab_copy_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, b->stream>>>(
-            b->src(), b->L, lo[0], lo[1], lo[2], ext[0], ext[1], ext[2], b->stage[key], 1);
+        for (int c = 0; c < 3; ++c) {
+            a.lo[a.n][c] = lo[c];
+            a.ext[a.n][c] = ext[c];
+        }
+        a.out[a.n] = b->stage[key];
+        a.begin[a.n + 1] = a.begin[a.n] + (long long)cnt;
+        ++a.n;
+    }
+    if (a.n > 0) {  // every neighbour's slab in one launch
+        slab_stage_kernel<<<(unsigned)((a.begin[a.n] + 255) / 256), 256, 0, b->stream>>>(b->src(), b->L, a);
         LBG_LAUNCH_CHECK();
     }
     LBG_CUDA(cudaEventRecord(b->ev_stage, b->stream));
