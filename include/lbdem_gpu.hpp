@@ -127,6 +127,17 @@ public:
         const int d[3] = {dir.x, dir.y, dir.z};
         check(lbg_halo_fetch(b_, d, from.b_));
     }
+    /// complete_halo_exchange for all neighbour entries (dir, source block) in one launch
+    void fetch_slabs(const std::vector<std::pair<Vec3i, const DeviceBlock*>>& from) {
+        std::vector<std::array<int, 3>> d;
+        std::vector<lbg_block> s;
+        for (const auto& [v, blk] : from) {
+            d.push_back({v.x, v.y, v.z});
+            s.push_back(blk->b_);
+        }
+        check(lbg_halo_fetch_all(b_, reinterpret_cast<const int(*)[3]>(d.data()), s.data(),
+                                 static_cast<int>(s.size())));
+    }
 
     void map(const std::vector<psm::ParticleSnapshot>& snaps, int subdivisions) {
         to_c(snaps);

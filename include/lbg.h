@@ -269,6 +269,10 @@ lbg_status lbg_unpack_slab(lbg_block b, const int dir[3], const double* in, long
  * identical values to the message-bus path. */
 lbg_status lbg_halo_stage(lbg_block b, const int (*offs)[3], int n);
 lbg_status lbg_halo_fetch(lbg_block dst, const int dir[3], lbg_block src);
+/* complete_halo_exchange (sim.cpp:181-201) for all n neighbour entries of dst at once:
+ * (dirs[t], srcs[t]) as in lbg_halo_fetch, one unpack launch (the ghost regions of distinct
+ * directions are disjoint, so the order of the reference's loop does not matter). */
+lbg_status lbg_halo_fetch_all(lbg_block dst, const int (*dirs)[3], const lbg_block* srcs, int n);
 
 /* The slab halo fused into the outer sweep over NVLink peer memory (one process per GPU,
  * >= 2 ranks, plain-fluid blocks). lbg_p2p_handles exports 192 bytes of CUDA IPC handles

@@ -115,12 +115,14 @@ SIM_CPP_EDITS = [
      "        return;\n"
      "    }\n"),
     # sim.cpp:181-186 — halo complete: each neighbour entry (s, o) fills ghost_region(o) with
-    # s's staged source_slab(-o), device to device (peer copy across GPUs)
+    # s's staged source_slab(-o), device to device (peer copy across GPUs), all in one launch
     ("    if (!blk.halo_pending) throw SyncError(\"halo completion without a pending exchange\");\n",
      "    if (!blk.halo_pending) throw SyncError(\"halo completion without a pending exchange\");\n"
      "    if (device_halo()) {\n"
+     "        std::vector<std::pair<Vec3i, const gpu::DeviceBlock*>> from;\n"
      "        for (const auto& n : decomp_.blocks[b].neighbors)\n"
-     "            blk.dev->fetch_slab(n.offset, *blocks_[n.block]->dev);\n"
+     "            from.emplace_back(n.offset, blocks_[n.block]->dev.get());\n"
+     "        blk.dev->fetch_slabs(from);  // every neighbour entry in one unpack launch\n"
      "        blk.halo_pending = false;\n"
      "        return;\n"
      "    }\n"),

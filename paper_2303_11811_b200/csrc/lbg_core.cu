@@ -482,6 +482,8 @@ lbg_status lbg_block_destroy(lbg_block b) {
     for (double* p : b->stage)
         if (p) cudaFree(p);
     if (b->recv_buf) cudaFree(b->recv_buf);
+    for (double* p : b->recv_multi)
+        if (p) cudaFree(p);
     if (b->stream) cudaStreamDestroy(b->stream);
     if (b->side) cudaStreamDestroy(b->side);
     if (b->aux) cudaStreamDestroy(b->aux);

@@ -155,6 +155,23 @@ __global__ void __launch_bounds__(256) slab_stage_kernel(const double* __restric
     a.out[s][u] = src[q * L.plane + L.idx(i, j, k)];
 }
 
+// the receive side in one launch (lbg_halo_fetch_all): slab t is unpacked from out[t] into
+// dst's ghost_region, as slab_copy_kernel(to_buf = 0) unpacks it
+__global__ void __launch_bounds__(256) slab_unpack_kernel(double* __restrict__ src, Layout L, StageArgs a) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.begin[a.n]) return;
+    int s = 0;
+    while (t >= a.begin[s + 1]) ++s;
+    const long long u = t - a.begin[s];
+    const long long cells = (long long)a.ext[s][0] * a.ext[s][1] * a.ext[s][2];
+    const int q = (int)(u / cells);
+    const long long r = u - q * cells;
+    const int i = a.lo[s][0] + (int)(r % a.ext[s][0]);
+    const int j = a.lo[s][1] + (int)((r / a.ext[s][0]) % a.ext[s][1]);
+    const int k = a.lo[s][2] + (int)(r / ((long long)a.ext[s][0] * a.ext[s][1]));
+    src[q * L.plane + L.idx(i, j, k)] = a.out[s][u];
+}
+
 static lbg_status nccl_check(ncclResult_t r, const char* what) {
     if (r == ncclSuccess) return LBG_OK;
     return set_error(LBG_CUDA_ERROR, std::string(what) + ": " + ncclGetErrorString(r));
@@ -430,6 +447,50 @@ lbg_status lbg_halo_fetch(lbg_block dst, const int dir[3], lbg_block src) {
     slab_copy_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, dst->stream>>>(
         dst->src(), dst->L, lo[0], lo[1], lo[2], ext[0], ext[1], ext[2], const_cast<double*>(from), 0);
     LBG_LAUNCH_CHECK();
+    return LBG_OK;
+}
+
+lbg_status lbg_halo_fetch_all(lbg_block dst, const int (*dirs)[3], const lbg_block* srcs, int n) {
+    using namespace lbg;
+    if (!dst || (n > 0 && (!dirs || !srcs))) return set_error(LBG_INVALID, "null argument");
+    if (n > 26) return set_error(LBG_INVALID, "at most 26 halo neighbours");
+    LBG_CUDA(cudaSetDevice(dst->device));
+    Span span(dst, LBG_CAT_PSM_COMM);
+    StageArgs a{};
+    a.begin[0] = 0;
+    for (int t = 0; t < n; ++t) {
+        lbg_block src = srcs[t];
+        if (!src) return set_error(LBG_INVALID, "null source block");
+        const int back[3] = {-dirs[t][0], -dirs[t][1], -dirs[t][2]};
+        const int key = (back[0] + 1) * 9 + (back[1] + 1) * 3 + (back[2] + 1);
+        int lo[3], ext[3];
+        slab_box(dst->L, dirs[t], true, lo, ext);
+        const size_t cnt = (size_t)kQ * ext[0] * ext[1] * ext[2];
+        if (!src->stage[key] || src->stage_cap[key] < cnt)
+            return set_error(LBG_SYNC_ERROR, "halo completion without a pending exchange");
+        LBG_CUDA(cudaStreamWaitEvent(dst->stream, src->ev_stage, 0));
+        const double* from = src->stage[key];
+        if (src->device != dst->device) {  // NVLink peer copy into this block's receive slot
+            const int rkey = (dirs[t][0] + 1) * 9 + (dirs[t][1] + 1) * 3 + (dirs[t][2] + 1);
+            if (lbg_status st = grow_device(dst->recv_multi[rkey], dst->recv_multi_cap[rkey], (long long)cnt,
+                                            (long long)cnt, "cudaMalloc(halo receive)"))
+                return st;
+            LBG_CUDA(cudaMemcpyPeerAsync(dst->recv_multi[rkey], dst->device, from, src->device,
+                                         sizeof(double) * cnt, dst->stream));
+            from = dst->recv_multi[rkey];
+        }
+        for (int c = 0; c < 3; ++c) {
+            a.lo[a.n][c] = lo[c];
+            a.ext[a.n][c] = ext[c];
+        }
+        a.out[a.n] = const_cast<double*>(from);
+        a.begin[a.n + 1] = a.begin[a.n] + (long long)cnt;
+        ++a.n;
+    }
+    if (a.n > 0) {  // every neighbour's slab in one launch
+        slab_unpack_kernel<<<(unsigned)((a.begin[a.n] + 255) / 256), 256, 0, dst->stream>>>(dst->src(), dst->L, a);
+        LBG_LAUNCH_CHECK();
+    }
     return LBG_OK;
 }
 

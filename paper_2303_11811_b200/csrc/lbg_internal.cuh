@@ -222,6 +222,8 @@ struct lbg_block_s {
     size_t stage_cap[27] = {};
     double* recv_buf = nullptr;
     size_t recv_cap = 0;
+    double* recv_multi[27] = {};  // lbg_halo_fetch_all: per-direction receive slots (peer copies)
+    size_t recv_multi_cap[27] = {};
     cudaEvent_t ev_stage = nullptr;
 
     // pinned-host PDF transfers: double-buffered device staging (lbg_core.cu)

@@ -472,6 +472,13 @@ class Block:
         this block's ghost_region(dir), device to device."""
         check(_lib().lbg_halo_fetch(self.h, (C.c_int * 3)(*direction), src.h))
 
+    def halo_fetch_all(self, entries):
+        """complete_halo_exchange for all (direction, source Block) entries in one launch."""
+        n = len(entries)
+        dirs = (C.c_int * (3 * max(n, 1)))(*[v for d, _ in entries for v in d])
+        srcs = (C.c_void_p * max(n, 1))(*[s.h.value for _, s in entries])
+        check(_lib().lbg_halo_fetch_all(self.h, dirs, srcs, n))
+
     def set_timing(self, on=True):
         check(_lib().lbg_set_timing(self.h, int(on)))
 

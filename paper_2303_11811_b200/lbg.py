@@ -110,6 +110,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "lbg_unpack_slab": (st, [blk, i3, vp, C.c_longlong]),
         "lbg_halo_stage": (st, [blk, i3, C.c_int]),
         "lbg_halo_fetch": (st, [blk, i3, blk]),
+        "lbg_halo_fetch_all": (st, [blk, i3, C.POINTER(C.c_void_p), C.c_int]),
         "lbg_p2p_handles": (st, [blk, vp, C.POINTER(C.c_size_t)]),
         "lbg_p2p_connect": (st, [blk, C.c_int, C.c_int, C.c_char_p, C.c_int, i3]),
         "lbg_p2p_prime": (st, [blk]),

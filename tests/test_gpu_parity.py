@@ -810,8 +810,8 @@ def test_single_rank_halo_equals_periodic_fill(gpu, oracle):
     assert equal_bits(interior(blk2.download_dst()), interior(dst_o))
 
 
-@pytest.mark.parametrize("grid", [(1, 1, 1), (2, 2, 1)])
-def test_poisoned_halos_never_leak(gpu, oracle, grid):
+@pytest.mark.parametrize("grid,batched", [((1, 1, 1), False), ((2, 2, 1), False), ((2, 2, 1), True)])
+def test_poisoned_halos_never_leak(gpu, oracle, grid, batched):
     """test_partition.cpp:130-151 on the device path: every block's ghosts are NaN, the
     26-neighbour halo runs device to device (lbg_halo_stage / lbg_halo_fetch, periodic
     self-messages included), then a full sweep. Every interior population is finite and the
@@ -835,9 +835,12 @@ def test_poisoned_halos_never_leak(gpu, oracle, grid):
     for b in blocks.values():
         b.halo_stage(offs)
     for g, b in blocks.items():
-        for o in offs:
-            nb = tuple((g[a] + o[a]) % grid[a] for a in range(3))
-            b.halo_fetch(o, blocks[nb])
+        entries = [(o, blocks[tuple((g[a] + o[a]) % grid[a] for a in range(3))]) for o in offs]
+        if batched:  # lbg_halo_fetch_all: every neighbour entry in one unpack launch
+            b.halo_fetch_all(entries)
+        else:
+            for o, nb in entries:
+                b.halo_fetch(o, nb)
     p = gpu.FluidParams(tau, fext)
     for b in blocks.values():
         b.sweep(p, gpu.CellBox((0, 0, 0), bd))
