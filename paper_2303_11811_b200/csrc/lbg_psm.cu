@@ -246,6 +246,36 @@ __global__ void __launch_bounds__(256, 4) map_bin_kernel(const MapArgs a) {
     }
 }
 
+// the zero fills of one mapping in one launch (instead of six memsets, each an API call that
+// the block-worker threads sharing a GPU serialise on): the bin counters and cursors, the
+// scan's leading zero, the covered/segment counters, and count (u8) + btot (+0.0) of every
+// cell — what build_fraction_field stores for an uncovered cell (psm.cpp:128-129). A thread
+// clears 16 cells (one 16-byte count chunk, 128 bytes of btot).
+__global__ void __launch_bounds__(256) map_zero_kernel(int* __restrict__ bins2, long long nbins2,
+                                                       int* __restrict__ start0, int* __restrict__ cov_n,
+                                                       int* __restrict__ seg_n, uint8_t* __restrict__ count,
+                                                       double* __restrict__ btot, long long cells) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < nbins2) bins2[t] = 0;
+    if (t < 2) {
+        cov_n[t] = 0;
+        seg_n[t] = 0;
+    }
+    if (t == 0) *start0 = 0;
+    const long long c0 = 16 * t;
+    if (c0 + 16 <= cells) {
+        reinterpret_cast<uint4*>(count)[t] = make_uint4(0u, 0u, 0u, 0u);
+        double2* bt = reinterpret_cast<double2*>(btot + c0);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) bt[u] = make_double2(0.0, 0.0);
+    } else {
+        for (long long c = c0; c < cells; ++c) {
+            count[c] = 0;
+            btot[c] = 0.0;
+        }
+    }
+}
+
 // covered-cell list from an externally set fraction field
 __global__ void __launch_bounds__(256) covered_kernel(const uint8_t* __restrict__ count, long long cells,
                                                       int* __restrict__ n) {
@@ -600,7 +630,13 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
     if (lbg_status s = ensure_bins(b, nbins)) return s;
     int* cnt = b->bin_count;
     int* cursor = b->bin_count + nbins;
-    LBG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * 2 * nbins, b->stream));
+    const long long cells = (long long)b->L.nx * b->L.ny * b->L.nz;
+    {
+        const long long threads = std::max(2 * nbins, (cells + 15) / 16);
+        map_zero_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, b->stream>>>(
+            cnt, 2 * nbins, b->bin_start, b->cov_n, b->seg_n, b->count, b->btot, cells);
+        LBG_LAUNCH_CHECK();
+    }
     if (n > 0) {
         bin_count_kernel<<<(n + 127) / 128, 128, 0, b->stream>>>(b->snaps_d, n, g, cnt);
         LBG_LAUNCH_CHECK();
@@ -611,7 +647,6 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
     if (lbg_status s = grow_device(b->scan_tmp, b->scan_tmp_bytes, (long long)tmp_bytes, (long long)tmp_bytes,
                                    "cudaMalloc(scan_tmp)"))
         return s;
-    LBG_CUDA(cudaMemsetAsync(b->bin_start, 0, sizeof(int), b->stream));
     cub::DeviceScan::InclusiveSum(b->scan_tmp, tmp_bytes, cnt, b->bin_start + 1, (int)nbins, b->stream);
     LBG_LAUNCH_CHECK();
     // host upper bound of the registrations (bins a particle's reach box can touch), so the
@@ -650,14 +685,8 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
     a.v1 = b->v1;
     a.err = b->err_d;
     a.cov_n = b->cov_n;
-    LBG_CUDA(cudaMemsetAsync(b->cov_n, 0, 2 * sizeof(int), b->stream));
-    LBG_CUDA(cudaMemsetAsync(b->seg_n, 0, 2 * sizeof(int), b->stream));
-    // build_fraction_field writes count and btot for every cell (psm.cpp:128-129):
-    // zero them at copy bandwidth, so the mapping kernel skips bins without candidates and
-    // writes only covered cells
-    const size_t cells = (size_t)b->L.nx * b->L.ny * b->L.nz;
-    LBG_CUDA(cudaMemsetAsync(b->count, 0, cells, b->stream));
-    LBG_CUDA(cudaMemsetAsync(b->btot, 0, sizeof(double) * cells, b->stream));
+    // count and btot of every cell were zeroed by map_zero_kernel, so the mapping kernel skips
+    // bins without candidates and writes only covered cells
     map_bin_kernel<<<(unsigned)nbins, 256, 0, b->stream>>>(a);
     LBG_LAUNCH_CHECK();
     const long long rows = (long long)b->L.ny * b->L.nz;
