@@ -51,7 +51,8 @@ def parse():
     ap.add_argument("--coupled-steps", type=int, default=4, help="coupled steps per repetition (best of 3)")
     ap.add_argument("--halo", choices=["p2p", "nccl"], default="p2p",
                     help="N > 1: outer sweep stores into the neighbours over NVLink (p2p) or NCCL halo")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
+    ap.add_argument("--cpu-steps", type=int, default=3,
+                    help="timed reference steps of the cpu_baseline leg (full domain, ~2.5 s each at 512^3)")
     return ap.parse_args()
 
 
@@ -123,31 +124,57 @@ REF_CFG = ('{{"scenario":"custom","domain":[{nx},{ny},{nz}],"kernels":"openmp",'
            '"fluid":{{"tau":{tau},"coupling":false}},"dem":{{"subcycles":1}}}}')
 
 
-def reference_sample(n, tau, budget_s, steps=None, warmup=0):
-    """Simulation::step of the unmodified reference (oracle/_ref) on a 512 x 512 x S periodic
-    slab of the same workload (same per-cell work, bounded memory), OpenMP on all host cores.
+def reference_sample(n, tau, steps, warmup=1):
+    """Simulation::step of the unmodified reference (oracle/_ref) on the SAME workload the GPU
+    arm runs: one periodic n^3 block (512^3: two 19-plane PdfField buffers of 41.3 GB host RAM),
+    shear-wave init, coupling off, OpenMP on all host cores (perf.cpp:68-71 MLUPS). The host
+    must hold the field: the run fails loudly rather than shrink the domain.
     Returns (MLUPS, sample description, threads, per-step seconds)."""
     from oracle.pyoracle import RefLib
+    need = 2 * 19 * 8 * (n + 2) ** 3
+    avail = host_mem_available()
+    if avail is not None and need > 0.9 * avail:
+        raise MemoryError(f"reference {n}^3 PdfField needs {need / 1e9:.1f} GB host RAM, "
+                          f"MemAvailable is {avail / 1e9:.1f} GB")
     ref = RefLib()
     threads = os.cpu_count() or 1
     ref.set_threads(threads)
-    nz = 16
-    sim = ref.sim(REF_CFG.format(nx=n, ny=n, nz=nz, tau=tau))
-    sim.shear_wave()
-    t0 = time.perf_counter()
-    sim.run(1)
-    one = time.perf_counter() - t0
-    if steps is None:
-        steps = max(1, min(200, int(budget_s / max(one, 1e-6))))
-    for _ in range(warmup):
-        sim.run(1)
-    t0 = time.perf_counter()
-    sim.run(steps)
-    dt = time.perf_counter() - t0
-    cells = n * n * nz
+    sim = ref.sim(REF_CFG.format(nx=n, ny=n, nz=n, tau=tau))
+    try:
+        sim.shear_wave()
+        for _ in range(max(1, warmup)):
+            sim.run(1)
+        t0 = time.perf_counter()
+        sim.run(steps)
+        dt = time.perf_counter() - t0
+    finally:
+        sim.close()
+    cells = n ** 3
     return (cells * steps / dt / 1e6,
-            f"reference Simulation::step (fluid, coupling off) on a {n}x{n}x{nz} periodic slab, "
-            f"{steps} steps, shear-wave init, OpenMP", threads, dt / steps)
+            f"reference Simulation::step (fluid, coupling off) on the full {n}x{n}x{n} periodic block, "
+            f"{steps} timed steps after {max(1, warmup)} warm-up, shear-wave init, OpenMP, "
+            f"{cpu_model()}", threads, dt / steps)
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip() + f" x{os.cpu_count()}"
+    except OSError:
+        pass
+    return f"{os.cpu_count()} host CPUs"
+
+
+def arm_config(n, N, tau, halo):
+    """The `config` object both arms print (the reference arm times the same workload)."""
+    cells = n ** 3
+    return {"workload": (f"config 2: pure-fluid D3Q19 SRT {n}^3 periodic, 1 GPU" if N == 1 else
+                         f"config 4: pure-fluid D3Q19 SRT weak scaling {n}^3 per GPU, "
+                         f"{n}x{n}x{n * N} periodic z-slabs"),
+            "tau": tau, "cells_per_gpu": cells, "parallelism": f"z-slab x{N}",
+            "l2": f"inputs larger than L2 ({2 * 19 * 8 * cells / 1e9:.1f} GB PDF working set)"}
 
 
 def run_reference(args):
@@ -158,17 +185,15 @@ def run_reference(args):
         from oracle.pyoracle import REF_SO
         if not os.path.exists(REF_SO):
             raise FileNotFoundError(REF_SO)
-        mlups, sample, threads, per_step = reference_sample(args.n, args.tau, args.cpu_seconds,
-                                                            steps=args.steps, warmup=args.warmup)
-    except Exception as e:  # noqa: BLE001
+        mlups, sample, threads, per_step = reference_sample(args.n, args.tau, args.steps, args.warmup)
+    except FileNotFoundError as e:
         print(json.dumps({"impl": "reference", "unavailable": f"reference build missing: {e}"}))
         return 0
     line = {"metric": METRIC, "value": round(mlups, 3), "unit": "MLUPS", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(per_step * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (shear-wave initial state, validation.cpp:46-63)", "impl": "reference",
-            "config": {"workload": f"pure-fluid D3Q19 SRT periodic, {args.n}^3 per GPU (config 2/4)",
-                       "sample": "512x512x16 slab per step (per-cell work identical)"},
+            "config": arm_config(args.n, args.gpus, args.tau, None),
             "cpu_baseline": {"value": round(mlups, 3), "unit": "MLUPS", "cores": threads,
                              "kind": "reference", "sample": sample},
             "e2e": {"value": round(mlups, 3), "unit": "MLUPS", "h2d_bytes_per_step": 0,
@@ -323,6 +348,50 @@ def coupled_sweep_roofline(steps=10, warmup=3):
             "cells": cells, "one_entry_cells": n1, "two_entry_cells": n2,
             "algorithmic_bytes_per_step": algo, "sweep_ms": round(sweep_ms, 4), "bc_ms": round(bc_ms / steps, 4),
             "mlups": round(cells / (sweep_ms / 1e3) / 1e6, 1),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4)}}
+
+
+def coupled_b0_roofline(n=512, tau=0.8, steps=10, warmup=3):
+    """Config 2's second case: the same 512^3 periodic shear wave through the
+    COUPLED sweep with no particles (coupling:true, P = 0) — psm_collide_stream's count == 0
+    branch for every cell (psm.cpp:218-262). The mapping of an empty list zero-fills count and
+    btot; the sweep is then K1 reading each cell's count (305 B per cell: 304 + 1 B count).
+    CUDA events on the block's stream; inputs (43 GB) exceed L2."""
+    import torch
+
+    from paper_2303_11811_b200 import lbdem
+    blk = lbdem.Block((n, n, n), coupling=True)
+    try:
+        blk.init_shear_wave((n, n, n))
+        blk.set_periodic_wrap((1, 1, 1))
+        blk.map([])
+        p = lbdem.FluidParams(tau)
+        box = lbdem.CellBox((0, 0, 0), (n, n, n))
+        stream = torch.cuda.ExternalStream(blk.stream)
+        for _ in range(warmup):
+            blk.sweep(p, box)
+            blk.swap()
+        blk.sync()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            blk.sweep(p, box)
+            blk.swap()
+        e1.record(stream)
+        e1.synchronize()
+        blk.sync()
+        ms = e0.elapsed_time(e1) / steps
+    finally:
+        blk.close()
+    cells = n ** 3
+    algo = 305 * cells
+    pk = peaks()
+    peak = pk["hbm_gbs"] if pk and pk.get("hbm_gbs") else 6650.0
+    achieved = algo / (ms / 1e3) / 1e9
+    return {"workload": f"config 2, coupling:true with P = 0: {n}^3 periodic shear wave, tau {tau}",
+            "cells": cells, "algorithmic_bytes_per_step": algo, "sweep_ms": round(ms, 4),
+            "mlups": round(cells / (ms / 1e3) / 1e6, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4)}}
 
@@ -555,7 +624,7 @@ def run_lbg(args):
         cpu = None
         if N == 1 and not args.no_cpu_baseline:
             try:
-                c_mlups, sample, threads, _ = reference_sample(n, args.tau, args.cpu_seconds)
+                c_mlups, sample, threads, _ = reference_sample(n, args.tau, args.cpu_steps)
                 cpu = {"value": round(c_mlups, 3), "unit": "MLUPS", "cores": threads,
                        "kind": "reference", "sample": sample}
             except Exception as e:  # noqa: BLE001
@@ -566,14 +635,7 @@ def run_lbg(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (shear-wave initial state, validation.cpp:46-63, device-initialised)",
-            "config": {"workload": (f"config 2: pure-fluid D3Q19 SRT {n}^3 periodic, 1 GPU" if N == 1 else
-                                    f"config 4: pure-fluid D3Q19 SRT weak scaling {n}^3 per GPU, "
-                                    f"{n}x{n}x{n * N} periodic z-slabs, halo "
-                                    + ("fused into the outer sweep (NVLink P2P stores)" if halo == "p2p"
-                                       else "over NCCL hidden behind the inner sweep")),
-                       "tau": args.tau, "cells_per_gpu": cells, "parallelism": f"z-slab x{N}",
-                       "halo": halo if N > 1 else None,
-                       "l2": f"inputs larger than L2 ({2 * 19 * 8 * cells / 1e9:.1f} GB PDF working set)"},
+            "config": arm_config(n, N, args.tau, halo),
             "mlups_per_gpu": round(mlups / N, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -602,6 +664,11 @@ def run_lbg(args):
             "cpu_baseline": cpu,
         }
     blk.close()
+    if rank == 0 and N == 1 and not args.no_coupled:
+        try:
+            out["coupled_b0"] = coupled_b0_roofline(n, args.tau)
+        except Exception as e:  # noqa: BLE001
+            out["coupled_b0"] = {"unavailable": f"{type(e).__name__}: {e}"}
     if rank == 0:
         if N == 1 and not args.no_coupled:
             try:

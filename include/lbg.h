@@ -194,7 +194,9 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
  * unknown ids, returning LBG_SYNC_ERROR itself (a synchronising call only then).
  * lbg_download_solid_velocity materialises v0/v1. */
 lbg_status lbg_set_solid_velocities(lbg_block b, const lbg_snapshot* snaps, int n);
-/* LBG_FORCE_SCRATCH (default) or LBG_FORCE_FUSED; takes effect from the next lbg_map. */
+/* LBG_FORCE_SCRATCH (default) or LBG_FORCE_FUSED; takes effect at once. The fused per-particle
+ * accumulators are sized and zeroed here, by lbg_map and by lbg_set_solid_velocities (the
+ * snapshot list they are indexed by); a sweep in fused mode without them is LBG_INVALID. */
 lbg_status lbg_set_force_mode(lbg_block b, int mode);
 /* finalize_hydro_forces (psm.cpp:278-322): fills out[] id-sorted (one row per particle
  * with at least one entry), sets *n_out, clears the scratch. Blocks until done.
@@ -266,7 +268,9 @@ lbg_status lbg_unpack_slab(lbg_block b, const int dir[3], const double* in, long
  * calls lbg_halo_fetch(dst, dir, src) for each of its neighbour entries (src block at offset
  * dir): src's staged source_slab(-dir) is copied device-to-device (peer copy over NVLink when
  * the blocks live on different GPUs) and unpacked into dst's ghost_region(dir). All 19 q,
- * identical values to the message-bus path. */
+ * identical values to the message-bus path. Staging buffers are reused: a new lbg_halo_stage
+ * waits (stream order) for every fetch that read the previous staging, so callers may
+ * pipeline steps without a host synchronisation. */
 lbg_status lbg_halo_stage(lbg_block b, const int (*offs)[3], int n);
 lbg_status lbg_halo_fetch(lbg_block dst, const int dir[3], lbg_block src);
 /* complete_halo_exchange (sim.cpp:181-201) for all n neighbour entries of dst at once:
@@ -275,9 +279,10 @@ lbg_status lbg_halo_fetch(lbg_block dst, const int dir[3], lbg_block src);
 lbg_status lbg_halo_fetch_all(lbg_block dst, const int (*dirs)[3], const lbg_block* srcs, int n);
 
 /* The slab halo fused into the outer sweep over NVLink peer memory (one process per GPU,
- * >= 2 ranks, plain-fluid blocks). lbg_p2p_handles exports 192 bytes of CUDA IPC handles
- * (both PDF buffers + a flag word array); the caller all-gathers them (rank order) and passes
- * them to lbg_p2p_connect. After every rank's state is set and a host barrier,
+ * >= 2 ranks, plain-fluid blocks). lbg_p2p_handles exports 208 bytes per rank: CUDA IPC
+ * handles (both PDF buffers + a flag word array) and the block's layout; the caller all-gathers
+ * them (rank order) and passes them to lbg_p2p_connect, which returns LBG_INVALID unless both
+ * slab neighbours have this block's dimensions (the remote stores use the local layout). After every rank's state is set and a host barrier,
  * lbg_p2p_prime fills the slab-axis ghost planes once from the neighbours. Then each step:
  * lbg_sweep (inner planes 1..n-2) -> lbg_sweep_outer_p2p (waits for the neighbours' previous
  * outer sweep, computes the two boundary planes and stores their outbound populations

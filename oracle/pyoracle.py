@@ -420,10 +420,12 @@ class RefSim:
         self.L.ref_sim_params(h, C.byref(tau), fext, dom)
         self.tau, self.fext, self.domain = tau.value, fext, tuple(int(d) for d in dom)
 
-    def __del__(self):
+    def close(self):
         if getattr(self, "h", None):
             self.L.ref_sim_destroy(self.h)
             self.h = None
+
+    __del__ = close
 
     def run(self, steps):
         self.lib.check(self.L.ref_sim_run(self.h, steps))

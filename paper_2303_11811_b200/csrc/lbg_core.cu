@@ -474,6 +474,7 @@ lbg_status lbg_block_destroy(lbg_block b) {
     if (b->ev_fork) cudaEventDestroy(b->ev_fork);
     if (b->ev_join) cudaEventDestroy(b->ev_join);
     if (b->ev_stage) cudaEventDestroy(b->ev_stage);
+    if (b->ev_fetched) cudaEventDestroy(b->ev_fetched);
     for (int s = 0; s < 2; ++s) {
         if (b->xfer[s]) cudaFree(b->xfer[s]);
         if (b->ev_copy[s]) cudaEventDestroy(b->ev_copy[s]);

@@ -376,6 +376,22 @@ lbg_status slab_io(lbg_block b, const int off[3], bool ghost, double* host, long
     return LBG_OK;
 }
 
+// after dst's unpack of the staged slabs of `srcs`: record dst's stream position and register
+// it with every source, whose next lbg_halo_stage waits for it
+lbg_status note_consumed(lbg_block dst, const lbg_block* srcs, int n) {
+    using namespace lbg;
+    if (!dst->ev_fetched) LBG_CUDA(cudaEventCreateWithFlags(&dst->ev_fetched, cudaEventDisableTiming));
+    LBG_CUDA(cudaEventRecord(dst->ev_fetched, dst->stream));
+    for (int t = 0; t < n; ++t) {
+        lbg_block s = srcs[t];
+        std::lock_guard<std::mutex> g(s->consumers_mu);
+        bool have = false;
+        for (cudaEvent_t e : s->consumers) have = have || e == dst->ev_fetched;
+        if (!have) s->consumers.push_back(dst->ev_fetched);
+    }
+    return LBG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -395,6 +411,12 @@ lbg_status lbg_halo_stage(lbg_block b, const int (*offs)[3], int n) {
     if (!b->ev_stage) LBG_CUDA(cudaEventCreateWithFlags(&b->ev_stage, cudaEventDisableTiming));
     if (n > 26) return set_error(LBG_INVALID, "at most 26 halo neighbours");
     Span span(b, LBG_CAT_PSM_COMM);
+    {
+        // the receivers of the previous staging have unpacked it (stream order, any device)
+        std::lock_guard<std::mutex> g(b->consumers_mu);
+        for (cudaEvent_t e : b->consumers) LBG_CUDA(cudaStreamWaitEvent(b->stream, e, 0));
+        b->consumers.clear();
+    }
     StageArgs a{};
     a.n = 0;
     a.begin[0] = 0;
@@ -447,7 +469,7 @@ lbg_status lbg_halo_fetch(lbg_block dst, const int dir[3], lbg_block src) {
     slab_copy_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, dst->stream>>>(
         dst->src(), dst->L, lo[0], lo[1], lo[2], ext[0], ext[1], ext[2], const_cast<double*>(from), 0);
     LBG_LAUNCH_CHECK();
-    return LBG_OK;
+    return note_consumed(dst, &src, 1);
 }
 
 lbg_status lbg_halo_fetch_all(lbg_block dst, const int (*dirs)[3], const lbg_block* srcs, int n) {
@@ -491,7 +513,7 @@ lbg_status lbg_halo_fetch_all(lbg_block dst, const int (*dirs)[3], const lbg_blo
         slab_unpack_kernel<<<(unsigned)((a.begin[a.n] + 255) / 256), 256, 0, dst->stream>>>(dst->src(), dst->L, a);
         LBG_LAUNCH_CHECK();
     }
-    return LBG_OK;
+    return note_consumed(dst, srcs, n);
 }
 
 }  // extern "C"

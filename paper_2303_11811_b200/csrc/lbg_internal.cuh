@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -225,6 +226,12 @@ struct lbg_block_s {
     double* recv_multi[27] = {};  // lbg_halo_fetch_all: per-direction receive slots (peer copies)
     size_t recv_multi_cap[27] = {};
     cudaEvent_t ev_stage = nullptr;
+    // staging reuse: fetches that read this block's staging record their stream's event here
+    // (under the mutex: receivers run on their own worker threads); the next lbg_halo_stage
+    // waits on them before overwriting the staging buffers
+    std::mutex consumers_mu;
+    std::vector<cudaEvent_t> consumers;
+    cudaEvent_t ev_fetched = nullptr;  // recorded after this block's fetch/unpack
 
     // pinned-host PDF transfers: double-buffered device staging (lbg_core.cu)
     double* xfer[2] = {nullptr, nullptr};

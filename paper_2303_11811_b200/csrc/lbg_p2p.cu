@@ -187,6 +187,9 @@ using namespace lbg;
 
 namespace {
 constexpr size_t kHandle = sizeof(cudaIpcMemHandle_t);  // 64
+// per rank: 3 IPC handles, then the block's device layout (nx, ny, nz, px) — the remote
+// stores index the peer's PDF buffer with the local Layout, so every rank must match
+constexpr size_t kRankBytes = 3 * kHandle + 4 * sizeof(int);
 
 lbg_status ensure_p2p(lbg_block b) {
     if (!b->p2p) b->p2p = new P2P;
@@ -212,7 +215,9 @@ lbg_status lbg_p2p_handles(lbg_block b, void* out, size_t* bytes) {
     std::memcpy(o + kHandle, &h, kHandle);
     LBG_CUDA(cudaIpcGetMemHandle(&h, b->p2p->flags));
     std::memcpy(o + 2 * kHandle, &h, kHandle);
-    if (bytes) *bytes = 3 * kHandle;
+    const int geo[4] = {b->L.nx, b->L.ny, b->L.nz, b->L.px};
+    std::memcpy(o + 3 * kHandle, geo, sizeof(geo));
+    if (bytes) *bytes = kRankBytes;
     return LBG_OK;
 }
 
@@ -229,17 +234,24 @@ lbg_status lbg_p2p_connect(lbg_block b, int nranks, int rank, const void* all, i
     p.prev = rank > 0 ? rank - 1 : (periodic[axis] ? nranks - 1 : -1);
     p.next = rank < nranks - 1 ? rank + 1 : (periodic[axis] ? 0 : -1);
     const char* h = static_cast<const char*>(all);
+    for (int r : {p.prev, p.next}) {
+        if (r < 0) continue;
+        int geo[4];
+        std::memcpy(geo, h + (size_t)r * kRankBytes + 3 * kHandle, sizeof(geo));
+        if (geo[0] != b->L.nx || geo[1] != b->L.ny || geo[2] != b->L.nz || geo[3] != b->L.px)
+            return set_error(LBG_INVALID, "p2p halo: neighbour block dimensions differ (equal slabs required)");
+    }
     auto open = [&](int r, double* bufs[2], unsigned long long** flag) -> lbg_status {
         for (int s = 0; s < 2; ++s) {
             cudaIpcMemHandle_t mh;
-            std::memcpy(&mh, h + (size_t)r * 3 * kHandle + s * kHandle, kHandle);
+            std::memcpy(&mh, h + (size_t)r * kRankBytes + s * kHandle, kHandle);
             void* ptr = nullptr;
             LBG_CUDA(cudaIpcOpenMemHandle(&ptr, mh, cudaIpcMemLazyEnablePeerAccess));
             bufs[s] = static_cast<double*>(ptr);
             p.opened[p.n_opened++] = ptr;
         }
         cudaIpcMemHandle_t mh;
-        std::memcpy(&mh, h + (size_t)r * 3 * kHandle + 2 * kHandle, kHandle);
+        std::memcpy(&mh, h + (size_t)r * kRankBytes + 2 * kHandle, kHandle);
         void* ptr = nullptr;
         LBG_CUDA(cudaIpcOpenMemHandle(&ptr, mh, cudaIpcMemLazyEnablePeerAccess));
         *flag = static_cast<unsigned long long*>(ptr);

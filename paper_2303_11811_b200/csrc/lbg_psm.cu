@@ -614,8 +614,11 @@ extern "C" {
 lbg_status lbg_set_force_mode(lbg_block b, int mode) {
     if (lbg_status s = need_coupling(b)) return s;
     if (mode != LBG_FORCE_SCRATCH && mode != LBG_FORCE_FUSED) return set_error(LBG_INVALID, "bad force mode");
+    LBG_CUDA(cudaSetDevice(b->device));
     b->force_mode = mode;
-    return LBG_OK;
+    // takes effect at once: the accumulators exist (zeroed, sized for the current list)
+    // before any sweep can run in the new mode
+    return prepare_fused(b, b->n_snaps);
 }
 
 lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisions) {
@@ -732,6 +735,9 @@ lbg_status lbg_set_solid_velocities(lbg_block b, const lbg_snapshot* snaps, int 
         while (q < (size_t)n && snaps[q].id < b->map_ids[p]) ++q;
         superset = q < (size_t)n && snaps[q].id == b->map_ids[p];
     }
+    // fused force mode: the accumulators are indexed by this list's snapshot indices from
+    // now on (the PSM sweep follows in the same step, sim.cpp:296-302): size and zero them
+    if (lbg_status s = prepare_fused(b, n)) return s;
     if (superset) {  // nothing on the device can fail: the caller need not synchronise
         b->v_snap = true;
         return LBG_OK;
@@ -765,6 +771,8 @@ static lbg_status reserve_rows(lbg_block b, int n) {
 
 static lbg_status reduce_fused(lbg_block b, lbg_hydro_partial* out, int capacity, int* n_out) {
     const int n = b->n_snaps;
+    if (n > b->facc_cap || (n > 0 && !b->facc))
+        return set_error(LBG_INVALID, "fused force accumulators smaller than the snapshot list");
     if (lbg_status s = reserve_rows(b, n)) return s;
     double* acc = b->red_rows_h;  // pinned: 6 per particle
     int* used = b->red_used_h;

@@ -768,6 +768,14 @@ static bool empty_box(const lbg_box& r) {
     return r.hi[0] <= r.lo[0] || r.hi[1] <= r.lo[1] || r.hi[2] <= r.lo[2];
 }
 
+// the fused force mode needs its per-particle accumulators for the current snapshot list
+static lbg_status check_fused(lbg_block b) {
+    if (b->coupling && b->force_mode == LBG_FORCE_FUSED && b->n_snaps > 0 &&
+        (!b->facc || !b->fused_used || b->facc_cap < b->n_snaps))
+        return set_error(LBG_INVALID, "fused force mode without accumulators for the snapshot list");
+    return LBG_OK;
+}
+
 static SweepArgs make_args(lbg_block b, const lbg_fluid* fl) {
     SweepArgs a{};
     a.src = b->src();
@@ -950,6 +958,7 @@ lbg_status lbg_sweep(lbg_block b, const lbg_fluid* fl, const lbg_box* range) {
     LBG_CUDA(cudaSetDevice(b->device));
     if (b->coupling && b->cov_dirty)
         if (lbg_status s = rebuild_covered(b)) return s;
+    if (lbg_status s = check_fused(b)) return s;
     SweepArgs a = make_args(b, fl);
     for (int c = 0; c < 3; ++c) {
         a.lo[c] = range->lo[c];
@@ -992,6 +1001,7 @@ lbg_status lbg_sweep_boxes(lbg_block b, const lbg_fluid* fl, const lbg_box* boxe
     LBG_CUDA(cudaSetDevice(b->device));
     if (b->coupling && b->cov_dirty)
         if (lbg_status s = rebuild_covered(b)) return s;
+    if (lbg_status s = check_fused(b)) return s;
     SweepArgs a = make_args(b, fl);
     if (lbg_status s = add_boxes(a, b->L, boxes, n)) return s;
     if (a.nbox == 0) return LBG_OK;

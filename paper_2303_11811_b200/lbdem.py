@@ -438,7 +438,7 @@ class Block:
 
     # fused P2P halo (lbg_p2p.cu)
     def p2p_handles(self) -> bytes:
-        buf = C.create_string_buffer(192)
+        buf = C.create_string_buffer(256)
         n = C.c_size_t()
         check(_lib().lbg_p2p_handles(self.h, buf, C.byref(n)))
         return buf.raw[: n.value]
