@@ -335,6 +335,23 @@ def coupled_sweep_roofline(steps=10, warmup=3):
                 bc_ms += ev[0].elapsed_time(ev[1])
                 sweep_ms += ev[1].elapsed_time(ev[2])
         blk.sync()
+        if os.environ.get("AB_REDUCE"):
+            # wall time of lbg_reduce_hydro (PARITY) after a sweep refilled the scratch:
+            # kernels + D2H + host unpacking of the partials, through the raw C-ABI call
+            import ctypes as C
+            from paper_2303_11811_b200 import lbg as abi
+            lib = abi.load()
+            cap = len(rows) + 16
+            out = (abi.HydroPartial * cap)()
+            nout = C.c_int()
+            red = []
+            for _ in range(5):
+                blk.sweep(p, box)
+                blk.sync()
+                t0 = time.perf_counter()
+                lbdem.check(lib.lbg_reduce_hydro(blk.h, abi.REDUCE_PARITY, out, cap, C.byref(nout)))
+                red.append((time.perf_counter() - t0) * 1e3)
+            os.environ["AB_REDUCE_MS"] = ",".join(f"{v:.3f}" for v in red)
     finally:
         blk.close()
     cells = n ** 3

@@ -101,12 +101,21 @@ __device__ __forceinline__ void moments(const double (&f)[kQ], double& rho, doub
 // psm_cell (psm.cpp:174-216 with cnt == 1) term for term, the fluid equilibrium entering as
 // d = f - feq (feq - f == -d exactly); the momentum sum keeps the q
 // order because pairs are visited in q order. Returns ok; m_out = B * sum C c_qbar.
+template <bool kForced, class Get>
+__device__ __forceinline__ void psm_one_pairs_g(Get f, double rho, double ux, double uy, double uz, double usq,
+                                                double inv_tau, Force F, double b_tot, double be, double vx,
+                                                double vy, double vz, double* __restrict__ dst, long long plane,
+                                                long long base, double (&m_out)[3]);
+
 template <bool kForced>
 __device__ __forceinline__ void psm_cell_one_pairs(const double (&f)[kQ], double rho, double ux, double uy,
                                                    double uz, double usq, double inv_tau, Force F, double b_tot,
                                                    double be, double vx, double vy, double vz,
                                                    double* __restrict__ dst, long long plane, long long base,
-                                                   double (&m_out)[3]);
+                                                   double (&m_out)[3]) {
+    psm_one_pairs_g<kForced>([&](int q) { return f[q]; }, rho, ux, uy, uz, usq, inv_tau, F, b_tot, be, vx, vy, vz,
+                             dst, plane, base, m_out);
+}
 
 template <bool kForced>
 __device__ __forceinline__ bool psm_cell_one(const double (&f)[kQ], double inv_tau, Force F,
@@ -122,13 +131,14 @@ __device__ __forceinline__ bool psm_cell_one(const double (&f)[kQ], double inv_t
     return ok;
 }
 
-// psm_cell_one after the moments: the pair-by-pair outputs and the entry's momentum
-template <bool kForced>
-__device__ __forceinline__ void psm_cell_one_pairs(const double (&f)[kQ], double rho, double ux, double uy,
-                                                   double uz, double usq, double inv_tau, Force F, double b_tot,
-                                                   double be, double vx, double vy, double vz,
-                                                   double* __restrict__ dst, long long plane, long long base,
-                                                   double (&m_out)[3]) {
+// psm_cell_one after the moments: the pair-by-pair outputs and the entry's momentum. f(q)
+// yields population q: a register of the pulled array, or (low-register kernels) a re-read of
+// the pulled value from L1.
+template <bool kForced, class Get>
+__device__ __forceinline__ void psm_one_pairs_g(Get f, double rho, double ux, double uy, double uz, double usq,
+                                                double inv_tau, Force F, double b_tot, double be, double vx,
+                                                double vy, double vz, double* __restrict__ dst, long long plane,
+                                                long long base, double (&m_out)[3]) {
     const double T = (0.5 * usq) * 3.0;
     const double Tp = (0.5 * ((vx * vx + vy * vy) + vz * vz)) * 3.0;
     const double fluid_w = 1.0 - b_tot;
@@ -144,18 +154,20 @@ __device__ __forceinline__ void psm_cell_one_pairs(const double (&f)[kQ], double
         dst[q * plane + base] = base_out + be * c_solid;
     };
     {
+        const double f0 = f(0);
         const double feq0 = wq(0) * (rho - T);
         const double fp0 = wq(0) * (rho - Tp);
-        out(0, f[0], feq0, f[0], feq0, fp0, kForced ? forcing<0>(0.0, ux, uy, uz, F.x, F.y, F.z) : 0.0);
+        out(0, f0, feq0, f0, feq0, fp0, kForced ? forcing<0>(0.0, ux, uy, uz, F.x, F.y, F.z) : 0.0);
     }
 #define LBG_PAIR(qa, qb, cuf, cup)                                                                   \
     {                                                                                                \
+        const double xa = f(qa), xb = f(qb);                                                         \
         double fa, fb, pa, pb;                                                                       \
         feq_pair(wq(qa), (cuf), rho, T, fa, fb);                                                     \
         feq_pair(wq(qa), (cup), rho, Tp, pa, pb);                                                    \
         const double cu_a = (cuf);                                                                   \
-        out(qa, f[qa], fa, f[qb], fb, pa, kForced ? forcing<qa>(cu_a, ux, uy, uz, F.x, F.y, F.z) : 0.0); \
-        out(qb, f[qb], fb, f[qa], fa, pb, kForced ? forcing<qb>(-cu_a, ux, uy, uz, F.x, F.y, F.z) : 0.0); \
+        out(qa, xa, fa, xb, fb, pa, kForced ? forcing<qa>(cu_a, ux, uy, uz, F.x, F.y, F.z) : 0.0);   \
+        out(qb, xb, fb, xa, fa, pb, kForced ? forcing<qb>(-cu_a, ux, uy, uz, F.x, F.y, F.z) : 0.0);  \
     }
     LBG_PAIR(1, 2, ux, vx)
     LBG_PAIR(3, 4, uy, vy)
@@ -170,6 +182,37 @@ __device__ __forceinline__ void psm_cell_one_pairs(const double (&f)[kQ], double
     m_out[0] = be * mx;
     m_out[1] = be * my;
     m_out[2] = be * mz;
+}
+
+// collide_cell (unforced) after the moments, pair by pair: the same operations as srt_cell
+// (out = f + inv_tau * (feq - f), feq from feq_pair), f(q) as in psm_one_pairs_g
+template <class Get>
+__device__ __forceinline__ void srt_pairs_g(Get f, double rho, double ux, double uy, double uz, double usq,
+                                            double inv_tau, double* __restrict__ dst, long long plane,
+                                            long long base) {
+    const double T = (0.5 * usq) * 3.0;
+    {
+        const double f0 = f(0);
+        dst[base] = f0 + inv_tau * (wq(0) * (rho - T) - f0);
+    }
+#define LBG_SPAIR(qa, qb, cuf)                                  \
+    {                                                           \
+        const double xa = f(qa), xb = f(qb);                    \
+        double fa, fb;                                          \
+        feq_pair(wq(qa), (cuf), rho, T, fa, fb);                \
+        dst[qa * plane + base] = xa + inv_tau * (fa - xa);      \
+        dst[qb * plane + base] = xb + inv_tau * (fb - xb);      \
+    }
+    LBG_SPAIR(1, 2, ux)
+    LBG_SPAIR(3, 4, uy)
+    LBG_SPAIR(5, 6, uz)
+    LBG_SPAIR(7, 8, ux + uy)
+    LBG_SPAIR(9, 10, ux - uy)
+    LBG_SPAIR(11, 12, ux + uz)
+    LBG_SPAIR(13, 14, ux - uz)
+    LBG_SPAIR(15, 16, uy + uz)
+    LBG_SPAIR(17, 18, uy - uz)
+#undef LBG_SPAIR
 }
 
 // psm_cell for a cell with one or two entries, scheduled pair by pair like psm_cell_one

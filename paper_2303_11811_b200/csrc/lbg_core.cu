@@ -399,6 +399,7 @@ lbg_status lbg_block_create(int device, const int box_lo[3], const int dims[3], 
         } allocs[] = {{(void**)&b->count, n},
                       {(void**)&b->id0, n * 4},
                       {(void**)&b->id1, n * 4},
+                      {(void**)&b->pidx0, n * 4},
                       {(void**)&b->b0, n * 8},
                       {(void**)&b->b1, n * 8},
                       {(void**)&b->btot, n * 8},
@@ -414,8 +415,6 @@ lbg_status lbg_block_create(int device, const int box_lo[3], const int dims[3], 
         // FractionField::resize fills id0/id1 with -1 (field.cpp:37-46)
         cudaMemset(b->id0, 0xff, n * 4);
         cudaMemset(b->id1, 0xff, n * 4);
-        if ((e = cudaMalloc(&b->cov_n, 2 * sizeof(int))) != cudaSuccess) return fail(e, "cudaMalloc(cov_n)");
-        cudaMemset(b->cov_n, 0, 2 * sizeof(int));
         b->seg_cap = (long long)((L.nx + 31) / 32) * L.ny * L.nz;
         if ((e = cudaMalloc(&b->seg_list, sizeof(unsigned) * b->seg_cap)) != cudaSuccess) return fail(e, "cudaMalloc(seg)");
         if ((e = cudaMalloc(&b->seg_n, 2 * sizeof(int))) != cudaSuccess) return fail(e, "cudaMalloc(seg_n)");
@@ -457,12 +456,11 @@ lbg_status lbg_block_destroy(lbg_block b) {
     if (b->p2p) lbg_p2p_destroy(b);
     void* dev[] = {b->buf[0], b->buf[1], b->count, b->id0, b->id1, b->b0, b->b1, b->btot,
                    b->v0, b->v1, b->m0, b->m1, b->snaps_d, b->bin_count, b->bin_start,
-                   b->bin_items, b->red_rows, b->red_used, b->err_d, b->cov_n, b->facc, b->fused_used,
-                   b->scan_tmp, b->obs_d, b->mom_d, b->seg_list, b->seg_n, b->tile_buf, b->snap_tab,
-                   b->ekeys[0], b->ekeys[1], b->sort_tmp, b->red_seg};
+                   b->bin_items, b->red_rows, b->red_used, b->err_d, b->facc, b->fused_used,
+                   b->obs_d, b->mom_d, b->seg_list, b->seg_n, b->snap_tab, b->red_box, b->pidx0};
     for (void* p : dev)
         if (p) cudaFree(p);
-    void* host[] = {b->snaps_h, b->err_h, b->red_rows_h, b->red_used_h, b->obs_h, b->cn_h};
+    void* host[] = {b->snaps_h, b->err_h, b->red_rows_h, b->red_used_h, b->obs_h};
     for (void* p : host)
         if (p) cudaFreeHost(p);
     for (auto& s : b->spans) {
@@ -475,6 +473,7 @@ lbg_status lbg_block_destroy(lbg_block b) {
     if (b->ev_join) cudaEventDestroy(b->ev_join);
     if (b->ev_stage) cudaEventDestroy(b->ev_stage);
     if (b->ev_fetched) cudaEventDestroy(b->ev_fetched);
+    if (b->ev_red) cudaEventDestroy(b->ev_red);
     for (int s = 0; s < 2; ++s) {
         if (b->xfer[s]) cudaFree(b->xfer[s]);
         if (b->ev_copy[s]) cudaEventDestroy(b->ev_copy[s]);

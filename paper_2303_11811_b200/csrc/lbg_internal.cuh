@@ -131,15 +131,17 @@ struct lbg_block_s {
     // u + omega x (c - x) inline instead of reading v0/v1 (which are then stale until
     // materialised by setu_kernel on download or before a fraction upload)
     bool v_snap = false;
+    // pidx0: entry 0's index in the mapping list, written by the mapping kernel; valid for the
+    // sweep while the current list is the mapping list (same ids in the same order)
+    int* pidx0 = nullptr;
+    bool p_direct = false;
     // ids of the snapshot list the fraction field was mapped from (valid after lbg_map):
     // a later set_solid_velocities list holding all of them cannot meet an unknown id
     std::vector<int> map_ids;
     bool map_ids_valid = false;
     double* m0 = nullptr;
     double* m1 = nullptr;
-    // covered-cell counts (one-entry, two-entry), from the mapping kernel / after a fraction
-    // upload; they size the PARITY reduction's entry list
-    int* cov_n = nullptr;  // device counters [2]
+    // segment lists stale (after a fraction upload): rebuilt before the next sweep
     bool cov_dirty = true;
     // aligned 32-cell row segments holding covered cells (first cell index): segments with
     // one-entry cells only from the front (seg_n[0]), with a two-entry cell from the back
@@ -173,24 +175,18 @@ struct lbg_block_s {
     int* bin_items = nullptr;
     long long bin_items_cap = 0;
     long long n_bins_cap = 0;
-    unsigned char* scan_tmp = nullptr;  // CUB workspace
-    size_t scan_tmp_bytes = 0;
     // hydro reduction scratch
     double* red_rows = nullptr;  // n_snaps x 12
     int* red_used = nullptr;
     int red_cap = 0;
     double* red_rows_h = nullptr;
     int* red_used_h = nullptr;
-    // sorted-entry PARITY reduction: entry keys (in/out), radix-sort workspace, segments
-    unsigned long long* ekeys[2] = {nullptr, nullptr};
-    long long ekeys_cap = 0;
-    unsigned char* sort_tmp = nullptr;
-    size_t sort_tmp_bytes = 0;
-    int* red_seg = nullptr;  // start[n], end[n]
-    int red_seg_cap = 0;
-    int* cn_h = nullptr;  // pinned copy of cov_n
-    int* tile_buf = nullptr;  // per-tile entry totals and offsets (ordered entry emission)
-    long long tile_cap = 0;
+    // box-walk reduction: per-particle cell boxes (generic source), the mapping list's
+    // snapshots (the reach boxes are valid while the list keeps their positions and radii)
+    int* red_box = nullptr;
+    int red_box_cap = 0;
+    std::vector<lbg_snapshot> map_snaps;
+    cudaEvent_t ev_red = nullptr;
 
     lbg::DeviceErrors* err_d = nullptr;
     lbg::DeviceErrors* err_h = nullptr;  // pinned
@@ -262,16 +258,6 @@ __device__ __forceinline__ void warp_append(bool pred, unsigned v, unsigned* lis
     if (lane == leader) base = atomicAdd(n, __popc(m));
     base = __shfl_sync(0xffffffffu, base, leader);
     if (pred) list[base + __popc(m & ((1u << lane) - 1))] = v;
-}
-
-// covered cells counted by entry count (n[0]: one-entry, n[1]: two-entry), warp-aggregated
-__device__ __forceinline__ void covered_count(int cnt, int* n) {
-    const unsigned m1 = __ballot_sync(0xffffffffu, cnt == 1);
-    const unsigned m2 = __ballot_sync(0xffffffffu, cnt == 2);
-    if ((threadIdx.x & 31) == 0) {
-        if (m1) atomicAdd(n, __popc(m1));
-        if (m2) atomicAdd(n + 1, __popc(m2));
-    }
 }
 
 // error plumbing (lbg_core.cu)

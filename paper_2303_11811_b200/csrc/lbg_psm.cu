@@ -23,7 +23,6 @@
 // visiting order, and six threads per particle run the compensated chains (f.x..t.z) over
 // the particle's segment. FAST sums the same segments plainly; the fused force mode
 // (lbg_sweep.cu) sums inside the PSM kernel with warp aggregation + atomics instead.
-#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -84,21 +83,64 @@ __global__ void bin_fill_kernel(const lbg_snapshot* __restrict__ s, int n, BinGe
             }
 }
 
-// per-bin ascending order (= id order) makes the candidate sequence deterministic
-__global__ void bin_sort_kernel(const int* __restrict__ start, const int* __restrict__ cnt, int nbins,
-                                int* __restrict__ items) {
+// Bin lists: each bin's registrations get one contiguous slot range. The ranges are handed
+// out by a warp-aggregated cursor (one atomic per 32 bins) instead of a prefix scan: where a
+// bin's list sits does not matter, only its content, which bin_sort_kernel then puts in
+// ascending snapshot-index (= id) order, so the candidate sequence is deterministic.
+__global__ void __launch_bounds__(256) bin_alloc_kernel(const int* __restrict__ cnt, int nbins,
+                                                        int* __restrict__ start, int* __restrict__ cursor) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= nbins) return;
-    int* a = items + start[b];
+    const int lane = threadIdx.x & 31;
+    const int n = b < nbins ? cnt[b] : 0;
+    int incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    int base = 0;
+    if (lane == 31 && incl > 0) base = atomicAdd(cursor, incl);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    if (b < nbins) start[b] = base + incl - n;
+}
+
+// one warp per bin: rank sort (each item's rank = number of smaller items; the items are
+// distinct snapshot indices), in shared memory for up to kSortSmem items, serially by lane 0
+// beyond that (only pathological overlap puts > 1024 particles in one 8^3 bin)
+constexpr int kSortWarps = 8;
+constexpr int kSortSmem = 1024;
+
+__global__ void __launch_bounds__(32 * kSortWarps) bin_sort_kernel(const int* __restrict__ start,
+                                                                   const int* __restrict__ cnt, int nbins,
+                                                                   int* __restrict__ items) {
+    __shared__ int buf[kSortWarps][kSortSmem];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.x * kSortWarps + w;
+    if (b >= nbins) return;  // warp-uniform
     const int n = cnt[b];
-    for (int i = 1; i < n; ++i) {
-        const int v = a[i];
-        int j = i - 1;
-        while (j >= 0 && a[j] > v) {
-            a[j + 1] = a[j];
-            --j;
-        }
-        a[j + 1] = v;
+    if (n < 2) return;
+    int* a = items + start[b];
+    if (n > kSortSmem) {
+        if (lane == 0)
+            for (int i = 1; i < n; ++i) {
+                const int v = a[i];
+                int j = i - 1;
+                while (j >= 0 && a[j] > v) {
+                    a[j + 1] = a[j];
+                    --j;
+                }
+                a[j + 1] = v;
+            }
+        return;
+    }
+    int* sb = buf[w];
+    for (int t = lane; t < n; t += 32) sb[t] = a[t];
+    __syncwarp();
+    for (int t = lane; t < n; t += 32) {
+        const int v = sb[t];
+        int r = 0;
+        for (int u = 0; u < n; ++u) r += sb[u] < v;
+        a[r] = v;
     }
 }
 
@@ -111,29 +153,28 @@ struct MapArgs {
     uint8_t* __restrict__ count;
     int* __restrict__ id0;
     int* __restrict__ id1;
+    int* __restrict__ pidx0;
     double* __restrict__ b0;
     double* __restrict__ b1;
     double* __restrict__ btot;
-    double* __restrict__ v0;
-    double* __restrict__ v1;
     DeviceErrors* err;
-    int* cov_n;
 };
 
-// K3 mapping (psm.cpp:28-32 overlap_fraction, psm.cpp:93-136 per-cell entry rule): one CTA
-// per 8^3 bin, two cells per thread. The bin's candidate
-// snapshots are staged in shared memory in list (= id) order, 64 at a time, so every lane reads
-// the same candidate (broadcast) and the loop has no per-lane trip count. The overlap test is
-// overlap_fraction (psm.cpp:28-32) with two exact shortcuts on the squared distance d2 =
-// (dx*dx + dy*dy) + dz*dz (the radicand the reference takes the root of):
+// K3 mapping (psm.cpp:28-32 overlap_fraction, psm.cpp:93-136 per-cell entry rule): one warp
+// per 8 x 4 x 8 column of an 8^3 bin (lane = 8 x 4 cells of a z-level, looping over the bin's
+// 8 z-levels), no CTA barrier. The warp stages the bin's candidates (32 at a time, list = id
+// order) in its own shared-memory slots — read by all lanes as broadcasts — and per z-level
+// keeps only the candidates that can reach a cell centre of its 8 x 4 slab (ballot), visited
+// in ascending order. The overlap test is overlap_fraction with two exact shortcuts on the
+// squared distance d2 = (dx*dx + dy*dy) + dz*dz (the radicand the reference takes the root of):
 //   d2 > (r + f_r)^2 (1 + 1e-9)      => eps <= 0 (skip), the rounding of the root and of
 //                                       -(dist - r) + f_r is ~1e-16 relative, far inside the
 //                                       margin;
 //   d2 < (r + f_r - 1)^2 (1 - 1e-9)  => eps >= 1, which the clamp makes exactly 1.0.
 // Every other candidate takes the reference's sqrt path, so count/ids/fractions are bitwise
-// those of build_fraction_field. Segment lists are registered
-// by a separate pass (segments_kernel), since a warp here is not a row segment.
-constexpr int kMapCand = 64;
+// those of build_fraction_field. count and btot of every cell were zeroed before the launch
+// (what the reference stores for an uncovered cell), so only covered cells are written.
+constexpr int kMapWarps = 8;
 
 // distance from x to the interval [lo, hi] of cell-centre coordinates, as |c - x| of its
 // nearest member c is computed (c - x rounded; for x > hi, x - hi = -(hi - x) exactly)
@@ -141,127 +182,128 @@ __device__ __forceinline__ double axis_gap(double lo, double hi, double x) {
     return x < lo ? lo - x : (x > hi ? x - hi : 0.0);
 }
 
-__global__ void __launch_bounds__(256, 4) map_bin_kernel(const MapArgs a) {
-    const BinGeom& g = a.g;
-    const int b = blockIdx.x;
-    const int bx = b % g.nb[0], by = (b / g.nb[0]) % g.nb[1], bz = b / (g.nb[0] * g.nb[1]);
-    __shared__ double sx0[kMapCand], sx1[kMapCand], sx2[kMapCand], sr[kMapCand], sfr[kMapCand];
-    __shared__ double sout2[kMapCand], sin2[kMapCand];
-    __shared__ int sid[kMapCand];
-    const int t = threadIdx.x;
-    const int i = bx * kBin + (t & 7), j = by * kBin + ((t >> 3) & 7);
-    int k[2] = {bz * kBin + (t >> 6), bz * kBin + (t >> 6) + 4};
-    bool valid[2];
-    long long c[2];
-    double cc0 = (double)(g.lo[0] + i) + 0.5, cc1 = (double)(g.lo[1] + j) + 0.5, cc2[2];
-    int cnt[2] = {0, 0};
-    double sum[2] = {0.0, 0.0};
-    bool over[2] = {false, false};
-    for (int h = 0; h < 2; ++h) {
-        valid[h] = i < g.dims[0] && j < g.dims[1] && k[h] < g.dims[2];
-        c[h] = ((long long)k[h] * g.dims[1] + j) * g.dims[0] + i;
-        cc2[h] = (double)(g.lo[2] + k[h]) + 0.5;
+struct MapCand {
+    double x0[32], x1[32], x2[32], r[32], fr[32], out2[32], in2[32];
+    int id[32], idx[32];
+};
+
+__device__ __forceinline__ void stage_cands(const MapArgs& a, const int* list, int base, int m, int lane,
+                                            MapCand& sc) {
+    if (lane < m) {
+        const int ix = list[base + lane];
+        const lbg_snapshot& p = a.s[ix];
+        sc.idx[lane] = ix;
+        sc.x0[lane] = p.x[0];
+        sc.x1[lane] = p.x[1];
+        sc.x2[lane] = p.x[2];
+        sc.r[lane] = p.r;
+        sc.fr[lane] = p.f_r;
+        const double ro = p.r + p.f_r, ri = ro - 1.0;
+        sc.out2[lane] = (ro * ro) * (1.0 + 1e-9);
+        sc.in2[lane] = ri > 0.0 ? (ri * ri) * (1.0 - 1e-9) : -1.0;
+        sc.id[lane] = p.id;
     }
-    // cell-centre box of this warp's cells: x 8, y 4 (z per h)
-    const int lane = t & 31;
-    const int wj = by * kBin + (((t & ~31) >> 3) & 7);
-    const double wx0 = (double)(g.lo[0] + bx * kBin) + 0.5, wx1 = (double)(g.lo[0] + bx * kBin + 7) + 0.5;
-    const double wy0 = (double)(g.lo[1] + wj) + 0.5, wy1 = (double)(g.lo[1] + wj + 3) + 0.5;
-    const int n = a.cnt[b];
-    if (n == 0) return;  // count and btot of the whole field were zeroed before the launch
-    const int* list = a.items + a.start[b];
-    for (int base = 0; base < n; base += kMapCand) {
-        const int m = min(kMapCand, n - base);
-        __syncthreads();
-        if (t < m) {
-            const lbg_snapshot& p = a.s[list[base + t]];
-            sx0[t] = p.x[0];
-            sx1[t] = p.x[1];
-            sx2[t] = p.x[2];
-            sr[t] = p.r;
-            sfr[t] = p.f_r;
-            const double ro = p.r + p.f_r, ri = ro - 1.0;
-            sout2[t] = (ro * ro) * (1.0 + 1e-9);
-            sin2[t] = ri > 0.0 ? (ri * ri) * (1.0 - 1e-9) : -1.0;
-            sid[t] = p.id;
-        }
-        __syncthreads();
-        for (int h = 0; h < 2; ++h) {
-            // warp-level cull: a candidate enters the cell loop only if it can reach a cell
-            // centre of this warp's 8 x 4 x 1 row block. The squared gap between the candidate
-            // and the box of cell centres bounds every cell's radicand from below in floating
-            // point too (each per-axis gap is the smallest |c - x| over the box, and rounding
-            // is monotonic), so the box rejects only candidates every cell rejects (rad > sout2)
-            unsigned rel[2];
-            for (int half = 0; half < 2; ++half) {
-                const int q = lane + 32 * half;
-                bool r = false;
-                if (q < m) {
-                    const double g0 = axis_gap(wx0, wx1, sx0[q]), g1 = axis_gap(wy0, wy1, sx1[q]);
-                    const double g2 = axis_gap(cc2[h], cc2[h], sx2[q]);
-                    r = !((g0 * g0 + g1 * g1) + g2 * g2 > sout2[q]);
-                }
-                rel[half] = __ballot_sync(0xffffffffu, r);
-            }
-            if (!valid[h] || over[h]) continue;
-            for (int half = 0; half < 2 && !over[h]; ++half) {
-                for (unsigned mask = rel[half]; mask; mask &= mask - 1) {  // ascending = id order
-                    const int q = 32 * half + __ffs(mask) - 1;
-                    const double d0 = cc0 - sx0[q], d1 = cc1 - sx1[q], d2 = cc2[h] - sx2[q];
-                    const double rad = (d0 * d0 + d1 * d1) + d2 * d2;
-                    if (rad > sout2[q]) continue;
-                    double eps;
-                    if (rad < sin2[q]) {
-                        eps = 1.0;
-                    } else {
-                        eps = -(sqrt(rad) - sr[q]) + sfr[q];
-                        eps = eps < 0.0 ? 0.0 : (1.0 < eps ? 1.0 : eps);  // std::clamp
-                        if (eps <= 0.0) continue;
-                    }
-                    if (cnt[h] >= 2) {
-                        over[h] = true;
-                        break;
-                    }
-                    if (cnt[h] == 0) {
-                        a.id0[c[h]] = sid[q];
-                        a.b0[c[h]] = eps;
-                    } else {
-                        a.id1[c[h]] = sid[q];
-                        a.b1[c[h]] = eps;
-                    }
-                    ++cnt[h];
-                    sum[h] += eps;
-                }
-            }
-        }
-    }
-    for (int h = 0; h < 2; ++h) {
-        if (valid[h] && cnt[h] > 0) {  // uncovered cells keep the zeroed count and btot (+0.0)
-            a.count[c[h]] = (uint8_t)cnt[h];
-            a.btot[c[h]] = sum[h] < 1.0 ? sum[h] : 1.0;  // std::min(1.0, sum)
-        }
-        covered_count(valid[h] ? cnt[h] : 0, a.cov_n);
-        const unsigned mo = __ballot_sync(0xffffffffu, over[h]);
-        if (mo && (t & 31) == 0) atomicAdd(&a.err->overfull, (unsigned long long)__popc(mo));
-    }
+    __syncwarp();
 }
 
-// the zero fills of one mapping in one launch (instead of six memsets, each an API call that
-// the block-worker threads sharing a GPU serialise on): the bin counters and cursors, the
-// scan's leading zero, the covered/segment counters, and count (u8) + btot (+0.0) of every
-// cell — what build_fraction_field stores for an uncovered cell (psm.cpp:128-129). A thread
-// clears 16 cells (one 16-byte count chunk, 128 bytes of btot).
+__global__ void __launch_bounds__(32 * kMapWarps) map_warp_kernel(const MapArgs a) {
+    __shared__ MapCand cand_all[kMapWarps];
+    const BinGeom& g = a.g;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long unit = (long long)blockIdx.x * kMapWarps + w;  // (bin, y half)
+    const long long nbins = (long long)g.nb[0] * g.nb[1] * g.nb[2];
+    if (unit >= 2 * nbins) return;  // warp-uniform
+    const int b = (int)(unit >> 1), yh = (int)(unit & 1);
+    const int n = a.cnt[b];
+    if (n == 0) return;
+    MapCand& sc = cand_all[w];
+    const int* list = a.items + a.start[b];
+    const int bx = b % g.nb[0], by = (b / g.nb[0]) % g.nb[1], bz = b / (g.nb[0] * g.nb[1]);
+    const int i = bx * kBin + (lane & 7), j = by * kBin + yh * 4 + (lane >> 3);
+    const double cc0 = (double)(g.lo[0] + i) + 0.5, cc1 = (double)(g.lo[1] + j) + 0.5;
+    // cell-centre box of the warp's slab: x 8, y 4 (z per level)
+    const double wx0 = (double)(g.lo[0] + bx * kBin) + 0.5, wx1 = wx0 + 7.0;
+    const double wy0 = (double)(g.lo[1] + by * kBin + yh * 4) + 0.5, wy1 = wy0 + 3.0;
+    const bool inxy = i < g.dims[0] && j < g.dims[1];
+    if (n <= 32) stage_cands(a, list, 0, n, lane, sc);
+    unsigned long long overfull = 0;
+    for (int zz = 0; zz < kBin; ++zz) {
+        const int k = bz * kBin + zz;
+        if (k >= g.dims[2]) break;  // warp-uniform
+        const double cc2 = (double)(g.lo[2] + k) + 0.5;
+        const long long c = ((long long)k * g.dims[1] + j) * g.dims[0] + i;
+        int cnt = 0;
+        double sum = 0.0;
+        bool over = false;
+        for (int base = 0; base < n; base += 32) {
+            const int m = min(32, n - base);
+            if (n > 32) {
+                __syncwarp();  // every lane is done with the previous chunk
+                stage_cands(a, list, base, m, lane, sc);
+            }
+            // warp-level cull: the squared gap between the candidate and the slab's box of cell
+            // centres bounds every cell's radicand from below in floating point too (each
+            // per-axis gap is the smallest |c - x| over the box, rounding is monotonic), so
+            // the box rejects only candidates every cell rejects (rad > out2)
+            bool rl = false;
+            if (lane < m) {
+                const double g0 = axis_gap(wx0, wx1, sc.x0[lane]), g1 = axis_gap(wy0, wy1, sc.x1[lane]);
+                const double g2 = axis_gap(cc2, cc2, sc.x2[lane]);
+                rl = !((g0 * g0 + g1 * g1) + g2 * g2 > sc.out2[lane]);
+            }
+            const unsigned rel = __ballot_sync(0xffffffffu, rl);
+            if (!inxy || over) continue;
+            for (unsigned mask = rel; mask; mask &= mask - 1) {  // ascending = id order
+                const int q = __ffs(mask) - 1;
+                const double d0 = cc0 - sc.x0[q], d1 = cc1 - sc.x1[q], d2 = cc2 - sc.x2[q];
+                const double rad = (d0 * d0 + d1 * d1) + d2 * d2;
+                if (rad > sc.out2[q]) continue;
+                double eps;
+                if (rad < sc.in2[q]) {
+                    eps = 1.0;
+                } else {
+                    eps = -(sqrt(rad) - sc.r[q]) + sc.fr[q];
+                    eps = eps < 0.0 ? 0.0 : (1.0 < eps ? 1.0 : eps);  // std::clamp
+                    if (eps <= 0.0) continue;
+                }
+                if (cnt >= 2) {
+                    over = true;
+                    break;
+                }
+                if (cnt == 0) {
+                    a.id0[c] = sc.id[q];
+                    a.pidx0[c] = sc.idx[q];
+                    a.b0[c] = eps;
+                } else {
+                    a.id1[c] = sc.id[q];
+                    a.b1[c] = eps;
+                }
+                ++cnt;
+                sum += eps;
+            }
+        }
+        if (inxy && cnt > 0) {  // uncovered cells keep the zeroed count and btot (+0.0)
+            a.count[c] = (uint8_t)cnt;
+            a.btot[c] = sum < 1.0 ? sum : 1.0;  // std::min(1.0, sum)
+        }
+        overfull += (unsigned long long)__popc(__ballot_sync(0xffffffffu, inxy && over));
+    }
+    if (overfull && lane == 0) atomicAdd(&a.err->overfull, overfull);
+}
+
+// the zero fills of one mapping in one launch (instead of separate memsets, each an API call
+// that the block-worker threads sharing a GPU serialise on): the bin counters and cursors, the
+// slot cursor, the segment counters, and count (u8) + btot (+0.0) of every cell — what
+// build_fraction_field stores for an uncovered cell (psm.cpp:128-129). A thread clears 16
+// cells (one 16-byte count chunk, 128 bytes of btot).
 __global__ void __launch_bounds__(256) map_zero_kernel(int* __restrict__ bins2, long long nbins2,
-                                                       int* __restrict__ start0, int* __restrict__ cov_n,
-                                                       int* __restrict__ seg_n, uint8_t* __restrict__ count,
-                                                       double* __restrict__ btot, long long cells) {
+                                                       int* __restrict__ slot_cursor, int* __restrict__ seg_n,
+                                                       uint8_t* __restrict__ count, double* __restrict__ btot,
+                                                       long long cells) {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t < nbins2) bins2[t] = 0;
-    if (t < 2) {
-        cov_n[t] = 0;
-        seg_n[t] = 0;
-    }
-    if (t == 0) *start0 = 0;
+    if (t < 2) seg_n[t] = 0;
+    if (t == 0) *slot_cursor = 0;
     const long long c0 = 16 * t;
     if (c0 + 16 <= cells) {
         reinterpret_cast<uint4*>(count)[t] = make_uint4(0u, 0u, 0u, 0u);
@@ -276,29 +318,30 @@ __global__ void __launch_bounds__(256) map_zero_kernel(int* __restrict__ bins2, 
     }
 }
 
-// covered-cell list from an externally set fraction field
-__global__ void __launch_bounds__(256) covered_kernel(const uint8_t* __restrict__ count, long long cells,
-                                                      int* __restrict__ n) {
-    const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    covered_count(c < cells ? count[c] : 0, n);
-}
-
-// segment lists from an externally set fraction field (one thread per 32-cell row segment)
+// segment lists from the count field (one thread per 32-cell row segment; warp-aggregated
+// appends): one-entry-only segments from the front, segments with a two-entry cell from the back
 __global__ void __launch_bounds__(256) segments_kernel(const uint8_t* __restrict__ count, int nx, long long rows,
                                                        unsigned* __restrict__ seg_list, int* __restrict__ seg_n,
                                                        long long seg_cap) {
     const int per_row = (nx + 31) / 32;
     const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= rows * per_row) return;
-    const long long row = s / per_row;
-    const int i0 = (int)(s % per_row) * 32;
-    const long long c0 = row * nx + i0;
     int mx = 0;
-    for (int i = 0; i < 32 && i0 + i < nx; ++i) mx = max(mx, (int)count[c0 + i]);
-    if (mx == 1)
-        seg_list[atomicAdd(&seg_n[0], 1)] = (unsigned)c0;
-    else if (mx >= 2)
-        seg_list[seg_cap - 1 - atomicAdd(&seg_n[1], 1)] = (unsigned)c0;
+    long long c0 = 0;
+    if (s < rows * per_row) {
+        const long long row = s / per_row;
+        const int i0 = (int)(s % per_row) * 32;
+        c0 = row * nx + i0;
+        for (int i = 0; i < 32 && i0 + i < nx; ++i) mx = max(mx, (int)count[c0 + i]);
+    }
+    warp_append(mx == 1, (unsigned)c0, seg_list, &seg_n[0]);
+    const unsigned m2 = __ballot_sync(0xffffffffu, mx >= 2);
+    if (m2) {
+        const int lane = threadIdx.x & 31, leader = __ffs(m2) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(&seg_n[1], __popc(m2));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (mx >= 2) seg_list[seg_cap - 1 - (base + __popc(m2 & ((1u << lane) - 1)))] = (unsigned)c0;
+    }
 }
 
 // psm.cpp:138-169 — standalone setU over an existing fraction field
@@ -345,155 +388,209 @@ __device__ __forceinline__ void nm_add(double& sum, double& comp, double v) {  /
     sum = t;
 }
 
-// ---- sorted-entry PARITY reduction -------------------------------------------------------
-// Every fraction entry (cell c, slot e) becomes a 64-bit key (particle index << 32 | c << 1 |
-// e). The entries are emitted in lexicographic cell order (a tiled scan over the count field:
-// per-tile entry totals, a scan over tiles, then each tile writes its entries in order), so a
-// STABLE radix sort on the particle bits alone — two 8-bit passes for up to 65k particles —
-// leaves each particle's entries in finalize_hydro_forces' visiting order (cells
-// lexicographic, entry 0 before 1, psm.cpp:288-308). Six threads per particle (f.x f.y f.z
-// t.x t.y t.z) then run the Neumaier chains over the particle's segment. No walk over empty
-// cells, any fraction field.
-constexpr int kEntryThreads = 256;
-constexpr int kEntryPerThread = 16;
-constexpr int kEntryTile = kEntryThreads * kEntryPerThread;
+// ---- box-walk reduction (PARITY / FAST) -------------------------------------------------
+// finalize_hydro_forces visits the cells in lexicographic order and, per entry, adds m and
+// cross(c - x, m) into the entry particle's Neumaier sums (psm.cpp:278-322). A particle's
+// entries all lie in a small cell box (its reach, or the box of its entries), and the
+// lexicographic order restricted to that box is the box's own (k, j, i) order — so one warp
+// per particle walks its box 32 cells at a time in that order, picks the cells whose entry 0 /
+// entry 1 names the particle (entry 0 before entry 1 within a cell), stages their six terms in
+// shared memory in walk order, and lanes 0..5 (f.x f.y f.z t.x t.y t.z) replay them with the
+// reference's Neumaier steps: each (sum, comp) is the serial walk's exactly. The entry's
+// scratch is zeroed once its value is consumed (the reference clears every visited entry,
+// psm.cpp:305). No sort, no scan, no host round trip; FAST sums the same sequence plainly.
+//   box source: the snapshot's reach (r + max(1/2, f_r), the mapping's candidate test) when
+//   the fraction field was mapped from these positions; otherwise entry_box_kernel takes the
+//   min/max cell of every particle's entries from the field itself (order-independent).
+constexpr int kWalkWarps = 4;
+constexpr int kWalkBuf = 128;  // staged terms per warp: flushed at >= 32, a step adds <= 128
 
-__global__ void __launch_bounds__(kEntryThreads) entry_tile_sums_kernel(const uint8_t* __restrict__ count,
-                                                                        long long cells, int* __restrict__ sums) {
-    using Reduce = cub::BlockReduce<int, kEntryThreads>;
-    __shared__ typename Reduce::TempStorage tmp;
-    const long long c0 = (long long)blockIdx.x * kEntryTile + (long long)threadIdx.x * kEntryPerThread;
-    int n = 0;
-#pragma unroll
-    for (int t = 0; t < kEntryPerThread; ++t)
-        if (c0 + t < cells) n += count[c0 + t];
-    const int total = Reduce(tmp).Sum(n);
-    if (threadIdx.x == 0) sums[blockIdx.x] = total;
-}
+struct WalkArgs {
+    const lbg_snapshot* __restrict__ s;
+    int n;
+    BinGeom g;
+    const uint8_t* __restrict__ count;
+    const int* __restrict__ id0;
+    const int* __restrict__ id1;
+    double* __restrict__ m0;
+    double* __restrict__ m1;
+    const int* __restrict__ box;  // 6 per particle (-lo xyz, hi xyz) or null: reach box
+    double* __restrict__ rows;
+    int* __restrict__ used;
+    int fast;
+};
 
-__global__ void __launch_bounds__(kEntryThreads) entry_emit_kernel(
-    const uint8_t* __restrict__ count, long long cells, const int* __restrict__ tile_off,
-    const int* __restrict__ id0, const int* __restrict__ id1, SnapIndex sidx, int n_snaps,
-    unsigned long long* __restrict__ keys, DeviceErrors* err) {
-    using Scan = cub::BlockScan<int, kEntryThreads>;
-    __shared__ typename Scan::TempStorage tmp;
-    const long long c0 = (long long)blockIdx.x * kEntryTile + (long long)threadIdx.x * kEntryPerThread;
-    int cnt[kEntryPerThread];
-    int n = 0;
-#pragma unroll
-    for (int t = 0; t < kEntryPerThread; ++t) {
-        cnt[t] = c0 + t < cells ? count[c0 + t] : 0;
-        n += cnt[t];
-    }
-    int off = 0;
-    Scan(tmp).ExclusiveSum(n, off);
-    unsigned long long* out = keys + tile_off[blockIdx.x] + off;
-    for (int t = 0; t < kEntryPerThread; ++t) {
-        const long long c = c0 + t;
-        for (int e = 0; e < cnt[t]; ++e) {
-            int p = sidx(e == 0 ? id0[c] : id1[c]);
-            if (p < 0) {
-                atomicAdd(&err->unknown, 1ull);
-                p = n_snaps;  // sorts last, outside every particle's segment
-            }
-            *out++ = ((unsigned long long)p << 32) | ((unsigned long long)c << 1) | (unsigned long long)e;
+__device__ __forceinline__ void nm_replay(double (*terms)[7], int nbuf, int lane, bool fast, double& sum,
+                                          double& comp) {
+    if (lane < 6) {
+        for (int e = 0; e < nbuf; ++e) {
+            const double v = terms[e][lane];
+            if (fast)
+                sum += v;
+            else
+                nm_add(sum, comp, v);
         }
     }
+    __syncwarp();
 }
 
-__global__ void __launch_bounds__(256) segment_kernel(const unsigned long long* __restrict__ keys, long long n,
-                                                      int n_snaps, int* __restrict__ start, int* __restrict__ end) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const unsigned p = (unsigned)(keys[i] >> 32);
-    if (p >= (unsigned)n_snaps) return;  // unknown id (SyncError is raised)
-    if (i == 0 || (unsigned)(keys[i - 1] >> 32) != p) start[p] = (int)i;
-    if (i == n - 1 || (unsigned)(keys[i + 1] >> 32) != p) end[p] = (int)(i + 1);
-}
+// the walk's per-lane state: two consecutive box cells (t, t + 1) with their cell fields
+struct WalkCells {
+    long long c[2];
+    int i[2], j[2], k[2];
+    int cnt[2], e0[2], e1[2];
+};
 
-// One warp per particle. The warp loads 32 consecutive entries of the particle's segment at a
-// time (coalesced keys, then the 32 momenta, all in flight together), each lane computes its
-// entry's six terms (f = m, t = cross(c - x, m), psm.cpp:294-296) into shared memory, and lanes
-// 0..5 — one per component — add the 32 terms in entry order with Neumaier steps (vec3.hpp:75-82),
-// so each component's (sum, comp) is the reference's serial walk exactly. The next batch's
-// momenta are gathered before the current batch is replayed, with their keys loaded one
-// batch earlier still. (Clearing the scratch from here, by
-// the loading lane, measured 10x slower than the separate clear_entries_kernel pass.)
-constexpr int kChainWarps = 8;
-
-__global__ void __launch_bounds__(32 * kChainWarps) chain_kernel(
-    const unsigned long long* __restrict__ keys, const int* __restrict__ start, const int* __restrict__ end,
-    const lbg_snapshot* __restrict__ s, int n_snaps, BinGeom g, const double* __restrict__ m0,
-    const double* __restrict__ m1, double* __restrict__ rows, int* __restrict__ used, int fast) {
-    __shared__ double terms[kChainWarps][32][7];  // padded row: lanes 0..5 read a column
+__global__ void __launch_bounds__(32 * kWalkWarps) walk_chain_kernel(const WalkArgs a) {
+    __shared__ double terms_all[kWalkWarps][kWalkBuf + 32][7];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int p = blockIdx.x * kChainWarps + w;
-    if (p >= n_snaps) return;  // warp-uniform
-    const int i0 = start[p], i1 = end[p];
-    const double x0 = s[p].x[0], x1 = s[p].x[1], x2 = s[p].x[2];
-    double (*tw)[7] = terms[w];
-    // software pipeline: the keys two batches ahead, the momenta one batch ahead, so neither
-    // the key load nor the dependent momentum gather of a batch is waited on before its replay
-    auto key_at = [&](int base) { return base + lane < i1 ? keys[base + lane] : 0ull; };
-    auto gather = [&](int base, unsigned long long key, long long& c, double& a0, double& a1, double& a2) {
-        if (base + lane < i1) {
-            c = (long long)((key >> 1) & 0x7fffffffull);
-            const double* mp = ((key & 1ull) ? m1 : m0) + 3 * c;
-            a0 = mp[0];
-            a1 = mp[1];
-            a2 = mp[2];
+    const int p = blockIdx.x * kWalkWarps + w;
+    if (p >= a.n) return;  // warp-uniform
+    double (*terms)[7] = terms_all[w];
+    const BinGeom& g = a.g;
+    const lbg_snapshot& sp = a.s[p];
+    const int id = sp.id;
+    const double x0 = sp.x[0], x1 = sp.x[1], x2 = sp.x[2];
+    int lo[3], hi[3];
+    if (a.box) {
+        for (int d = 0; d < 3; ++d) {
+            lo[d] = -a.box[6 * p + d];
+            hi[d] = a.box[6 * p + 3 + d];
         }
-    };
-    long long c = 0;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    gather(i0, key_at(i0), c, a0, a1, a2);
-    unsigned long long knext = key_at(i0 + 32);
+    } else {
+        // every cell with eps > 0 has |c - x| < r + f_r (psm.cpp:28-32), c = lo + i + 1/2: the
+        // cells within R = r + max(1/2, f_r) of x per axis, one cell of margin for rounding
+        const double R = sp.r + (sp.f_r > 0.5 ? sp.f_r : 0.5);
+        const double xs[3] = {x0, x1, x2};
+        for (int d = 0; d < 3; ++d) {
+            const double o = xs[d] - (double)g.lo[d] - 0.5;
+            lo[d] = max((int)ceil(o - R) - 1, 0);
+            hi[d] = min((int)floor(o + R) + 1, g.dims[d] - 1);
+        }
+    }
     double sum = 0.0, comp = 0.0;
-    for (int base = i0; base < i1; base += 32) {
-        const int n = min(32, i1 - base);
-        if (lane < n) {
-            const int ci = (int)(c % g.dims[0]), cj = (int)((c / g.dims[0]) % g.dims[1]),
-                      ck = (int)(c / ((long long)g.dims[0] * g.dims[1]));
-            const double r0 = ((double)(g.lo[0] + ci) + 0.5) - x0;
-            const double r1 = ((double)(g.lo[1] + cj) + 0.5) - x1;
-            const double r2 = ((double)(g.lo[2] + ck) + 0.5) - x2;
-            tw[lane][0] = a0;
-            tw[lane][1] = a1;
-            tw[lane][2] = a2;
-            tw[lane][3] = r1 * a2 - r2 * a1;
-            tw[lane][4] = r2 * a0 - r0 * a2;
-            tw[lane][5] = r0 * a1 - r1 * a0;
-        }
-        __syncwarp();
-        gather(base + 32, knext, c, a0, a1, a2);  // next batch's momenta in flight during the replay
-        knext = key_at(base + 64);                  // and the keys of the batch after
-        if (lane < 6) {
-            for (int e = 0; e < n; ++e) {
-                const double v = tw[e][lane];
-                if (fast)
-                    sum += v;
-                else
-                    nm_add(sum, comp, v);
+    bool any = false;
+    if (hi[0] >= lo[0] && hi[1] >= lo[1] && hi[2] >= lo[2]) {
+        const int ex = hi[0] - lo[0] + 1, ey = hi[1] - lo[1] + 1;
+        const long long total = (long long)ex * ey * (hi[2] - lo[2] + 1);
+        int nbuf = 0;
+        // 64 box cells per step (two per lane), the next step's cell fields in flight
+        auto fetch = [&](long long base, WalkCells& w2) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const long long t = base + 2 * lane + h;
+                w2.cnt[h] = 0;
+                w2.c[h] = 0;
+                if (t < total) {
+                    const long long r = t / ex;
+                    w2.i[h] = lo[0] + (int)(t - r * ex);
+                    w2.j[h] = lo[1] + (int)(r % ey);
+                    w2.k[h] = lo[2] + (int)(r / ey);
+                    const long long c = ((long long)w2.k[h] * g.dims[1] + w2.j[h]) * g.dims[0] + w2.i[h];
+                    w2.c[h] = c;
+                    w2.cnt[h] = a.count[c];
+                    w2.e0[h] = a.id0[c];
+                    w2.e1[h] = a.id1[c];
+                }
             }
+        };
+        WalkCells cur, nxt;
+        fetch(0, cur);
+        for (long long base = 0; base < total; base += 64) {
+            fetch(base + 64, nxt);
+            bool h0[2], h1[2];
+            int mine = 0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                h0[h] = cur.cnt[h] >= 1 && cur.e0[h] == id;
+                h1[h] = cur.cnt[h] >= 2 && cur.e1[h] == id;
+                mine += (int)h0[h] + (int)h1[h];
+            }
+            // entries before this lane's cells: exclusive warp scan (walk order = lane order)
+            int incl = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const int step_total = __shfl_sync(0xffffffffu, incl, 31);
+            if (step_total > 0) {
+                any = true;
+                double mv[2][2][3];
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        mv[h][0][d] = h0[h] ? a.m0[3 * cur.c[h] + d] : 0.0;
+                        mv[h][1][d] = h1[h] ? a.m1[3 * cur.c[h] + d] : 0.0;
+                    }
+                int slot = nbuf + incl - mine;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const double r0 = ((double)(g.lo[0] + cur.i[h]) + 0.5) - x0;
+                    const double r1 = ((double)(g.lo[1] + cur.j[h]) + 0.5) - x1;
+                    const double r2 = ((double)(g.lo[2] + cur.k[h]) + 0.5) - x2;
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        if (!(e == 0 ? h0[h] : h1[h])) continue;
+                        const double* m = mv[h][e];
+                        double* t = terms[slot++];
+                        t[0] = m[0];
+                        t[1] = m[1];
+                        t[2] = m[2];
+                        t[3] = r1 * m[2] - r2 * m[1];
+                        t[4] = r2 * m[0] - r0 * m[2];
+                        t[5] = r0 * m[1] - r1 * m[0];
+                        double* z = (e == 0 ? a.m0 : a.m1) + 3 * cur.c[h];  // psm.cpp:305
+                        z[0] = 0.0;
+                        z[1] = 0.0;
+                        z[2] = 0.0;
+                    }
+                }
+                nbuf += step_total;
+                __syncwarp();
+                if (nbuf >= 32) {
+                    nm_replay(terms, nbuf, lane, a.fast, sum, comp);
+                    nbuf = 0;
+                }
+            }
+            cur = nxt;
         }
-        __syncwarp();
+        nm_replay(terms, nbuf, lane, a.fast, sum, comp);
     }
     if (lane < 6) {
         const int slot = lane < 3 ? lane : 6 + (lane - 3);
-        rows[12 * (size_t)p + slot] = sum;
-        rows[12 * (size_t)p + slot + 3] = comp;
+        a.rows[12 * (size_t)p + slot] = sum;
+        a.rows[12 * (size_t)p + slot + 3] = comp;
     }
-    if (lane == 0) used[p] = i1 > i0;
+    if (lane == 0) a.used[p] = any ? 1 : 0;
 }
 
-// the reference clears the scratch of every visited entry (psm.cpp:305)
-__global__ void __launch_bounds__(256) clear_entries_kernel(const unsigned long long* __restrict__ keys, long long n,
-                                                            double* __restrict__ m0, double* __restrict__ m1) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const long long c = (long long)((keys[i] >> 1) & 0x7fffffffull);
-    double* mp = ((keys[i] & 1ull) ? m1 : m0) + 3 * c;
-    mp[0] = mp[1] = mp[2] = 0.0;
+// generic box source: per particle the min/max cell of its entries (atomic max on -lo / hi:
+// order-independent), warp-aggregated per particle; entries with an id missing from the
+// snapshot list are counted (finalize_hydro_forces' SyncError, psm.cpp:300-303)
+__global__ void __launch_bounds__(256) entry_box_kernel(const uint8_t* __restrict__ count, long long cells, int nx,
+                                                        int ny, const int* __restrict__ id0,
+                                                        const int* __restrict__ id1, SnapIndex sidx,
+                                                        int* __restrict__ box, DeviceErrors* err) {
+    const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int cnt = c < cells ? count[c] : 0;
+    const int i = (int)(c % nx), j = (int)((c / nx) % ny), k = (int)(c / ((long long)nx * ny));
+    const int lane = threadIdx.x & 31;
+    for (int e = 0; e < 2; ++e) {
+        int p = -1;
+        if (cnt > e) {
+            p = sidx(e == 0 ? id0[c] : id1[c]);
+            if (p < 0) atomicAdd(&err->unknown, 1ull);
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, p);
+        if (p < 0) continue;
+        const int v[6] = {-i, -j, -k, i, j, k};
+        int r[6];
+        for (int d = 0; d < 6; ++d) r[d] = __reduce_max_sync(peers, (unsigned)(v[d] + 0x40000000)) - 0x40000000;
+        if (lane == __ffs(peers) - 1)
+            for (int d = 0; d < 6; ++d) atomicMax(&box[6 * p + d], r[d]);
+    }
 }
 
 static BinGeom geom(lbg_block b) {
@@ -569,10 +666,6 @@ static lbg_status ensure_bins(lbg_block b, long long nbins) {
 }
 
 lbg_status rebuild_covered(lbg_block b) {
-    const long long cells = (long long)b->L.nx * b->L.ny * b->L.nz;
-    LBG_CUDA(cudaMemsetAsync(b->cov_n, 0, 2 * sizeof(int), b->stream));
-    covered_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, b->stream>>>(b->count, cells, b->cov_n);
-    LBG_LAUNCH_CHECK();
     const long long rows = (long long)b->L.ny * b->L.nz;
     const long long nseg = rows * ((b->L.nx + 31) / 32);
     LBG_CUDA(cudaMemsetAsync(b->seg_n, 0, 2 * sizeof(int), b->stream));
@@ -633,75 +726,70 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
     if (lbg_status s = ensure_bins(b, nbins)) return s;
     int* cnt = b->bin_count;
     int* cursor = b->bin_count + nbins;
+    int* slot_cursor = b->bin_start + nbins;
     const long long cells = (long long)b->L.nx * b->L.ny * b->L.nz;
     {
         const long long threads = std::max(2 * nbins, (cells + 15) / 16);
         map_zero_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, b->stream>>>(
-            cnt, 2 * nbins, b->bin_start, b->cov_n, b->seg_n, b->count, b->btot, cells);
+            cnt, 2 * nbins, slot_cursor, b->seg_n, b->count, b->btot, cells);
         LBG_LAUNCH_CHECK();
     }
-    if (n > 0) {
+    if (n > 0) {  // an empty list leaves the zeroed field and empty segment lists
+        // host upper bound of the registrations (bins a particle's reach box can touch), so
+        // the item list is sized without a read-back: the whole mapping stays asynchronous
+        long long bound = 1;
+        for (int p = 0; p < n; ++p) {
+            long long nb = 1;
+            for (int d = 0; d < 3; ++d)
+                nb *= std::min<long long>(g.nb[d], (long long)((2.0 * (snaps[p].r + 0.5) + 4.0) / kBin) + 2);
+            bound += nb;
+        }
+        if (lbg_status s = grow_device(b->bin_items, b->bin_items_cap, bound, 2 * b->bin_items_cap,
+                                       "cudaMalloc(bin items)"))
+            return s;
         bin_count_kernel<<<(n + 127) / 128, 128, 0, b->stream>>>(b->snaps_d, n, g, cnt);
         LBG_LAUNCH_CHECK();
-    }
-    // persistent scan workspace (no per-call allocation)
-    size_t tmp_bytes = 0;
-    cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, cnt, b->bin_start + 1, (int)nbins, b->stream);
-    if (lbg_status s = grow_device(b->scan_tmp, b->scan_tmp_bytes, (long long)tmp_bytes, (long long)tmp_bytes,
-                                   "cudaMalloc(scan_tmp)"))
-        return s;
-    cub::DeviceScan::InclusiveSum(b->scan_tmp, tmp_bytes, cnt, b->bin_start + 1, (int)nbins, b->stream);
-    LBG_LAUNCH_CHECK();
-    // host upper bound of the registrations (bins a particle's reach box can touch), so the
-    // item list is sized without reading the scan back: the whole mapping stays asynchronous
-    long long bound = 1;
-    for (int p = 0; p < n; ++p) {
-        long long nb = 1;
-        for (int d = 0; d < 3; ++d)
-            nb *= std::min<long long>(g.nb[d], (long long)((2.0 * (snaps[p].r + 0.5) + 4.0) / kBin) + 2);
-        bound += nb;
-    }
-    if (lbg_status s = grow_device(b->bin_items, b->bin_items_cap, bound, 2 * b->bin_items_cap,
-                                   "cudaMalloc(bin items)"))
-        return s;
-    if (n > 0) {
+        bin_alloc_kernel<<<(unsigned)((nbins + 255) / 256), 256, 0, b->stream>>>(cnt, (int)nbins, b->bin_start,
+                                                                                  slot_cursor);
+        LBG_LAUNCH_CHECK();
         bin_fill_kernel<<<(n + 127) / 128, 128, 0, b->stream>>>(b->snaps_d, n, g, b->bin_start, cursor,
                                                                 b->bin_items);
         LBG_LAUNCH_CHECK();
-        bin_sort_kernel<<<(unsigned)((nbins + 127) / 128), 128, 0, b->stream>>>(b->bin_start, cnt, (int)nbins,
-                                                                                b->bin_items);
+        bin_sort_kernel<<<(unsigned)((nbins + kSortWarps - 1) / kSortWarps), 32 * kSortWarps, 0, b->stream>>>(
+            b->bin_start, cnt, (int)nbins, b->bin_items);
+        LBG_LAUNCH_CHECK();
+        MapArgs a{};
+        a.s = b->snaps_d;
+        a.g = g;
+        a.start = b->bin_start;
+        a.cnt = cnt;
+        a.items = b->bin_items;
+        a.count = b->count;
+        a.id0 = b->id0;
+        a.id1 = b->id1;
+        a.pidx0 = b->pidx0;
+        a.b0 = b->b0;
+        a.b1 = b->b1;
+        a.btot = b->btot;
+        a.err = b->err_d;
+        // count and btot of every cell were zeroed by map_zero_kernel, so the mapping kernel
+        // skips bins without candidates and writes only covered cells
+        const long long units = 2 * nbins;
+        map_warp_kernel<<<(unsigned)((units + kMapWarps - 1) / kMapWarps), 32 * kMapWarps, 0, b->stream>>>(a);
+        LBG_LAUNCH_CHECK();
+        const long long rows = (long long)b->L.ny * b->L.nz;
+        const long long nseg = rows * ((b->L.nx + 31) / 32);
+        segments_kernel<<<(unsigned)((nseg + 255) / 256), 256, 0, b->stream>>>(b->count, b->L.nx, rows,
+                                                                               b->seg_list, b->seg_n, b->seg_cap);
         LBG_LAUNCH_CHECK();
     }
-    MapArgs a{};
-    a.s = b->snaps_d;
-    a.g = g;
-    a.start = b->bin_start;
-    a.cnt = cnt;
-    a.items = b->bin_items;
-    a.count = b->count;
-    a.id0 = b->id0;
-    a.id1 = b->id1;
-    a.b0 = b->b0;
-    a.b1 = b->b1;
-    a.btot = b->btot;
-    a.v0 = b->v0;
-    a.v1 = b->v1;
-    a.err = b->err_d;
-    a.cov_n = b->cov_n;
-    // count and btot of every cell were zeroed by map_zero_kernel, so the mapping kernel skips
-    // bins without candidates and writes only covered cells
-    map_bin_kernel<<<(unsigned)nbins, 256, 0, b->stream>>>(a);
-    LBG_LAUNCH_CHECK();
-    const long long rows = (long long)b->L.ny * b->L.nz;
-    const long long nseg = rows * ((b->L.nx + 31) / 32);
-    segments_kernel<<<(unsigned)((nseg + 255) / 256), 256, 0, b->stream>>>(b->count, b->L.nx, rows, b->seg_list,
-                                                                           b->seg_n, b->seg_cap);
-    LBG_LAUNCH_CHECK();
     b->cov_dirty = false;
     b->v_snap = true;
+    b->p_direct = true;
     b->map_ids.resize(n);
     for (int p = 0; p < n; ++p) b->map_ids[p] = snaps[p].id;
     b->map_ids_valid = true;
+    b->map_snaps.assign(snaps, snaps + n);
     return LBG_OK;
 }
 
@@ -730,6 +818,9 @@ lbg_status lbg_set_solid_velocities(lbg_block b, const lbg_snapshot* snaps, int 
     // (id-sorted, like it) holds all of those ids, no entry can be unknown (psm.cpp:165-168)
     // and the PSM kernels evaluate u + omega x (c - x) from these snapshots inline. Otherwise
     // the field is filled here, counting unknown ids for lbg_sync's SyncError.
+    bool same = b->map_ids_valid && (size_t)n == b->map_ids.size();
+    for (int p = 0; same && p < n; ++p) same = snaps[p].id == b->map_ids[p];
+    b->p_direct = same;
     bool superset = b->map_ids_valid;
     for (size_t p = 0, q = 0; superset && p < b->map_ids.size(); ++p) {
         while (q < (size_t)n && snaps[q].id < b->map_ids[p]) ++q;
@@ -819,96 +910,63 @@ lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int c
     if (lbg_status s = reserve_rows(b, n)) return s;
     const BinGeom g = geom(b);
     const long long cells = (long long)g.dims[0] * g.dims[1] * g.dims[2];
-    if (b->cov_dirty)
-        if (lbg_status s = rebuild_covered(b)) return s;
+    // reach boxes hold every entry when the field was mapped (lbg_map) from snapshots whose
+    // ids, positions and radii the current list keeps; otherwise boxes from the field itself
+    bool reach_ok = b->map_ids_valid && b->map_snaps.size() == b->map_ids.size();
+    for (size_t p = 0, q = 0; reach_ok && p < b->map_snaps.size(); ++p) {
+        const lbg_snapshot& ms = b->map_snaps[p];
+        while (q < (size_t)n && b->snaps_h[q].id < ms.id) ++q;
+        reach_ok = q < (size_t)n && b->snaps_h[q].id == ms.id;
+        if (!reach_ok) break;
+        const lbg_snapshot& cs = b->snaps_h[q];
+        reach_ok = std::memcmp(ms.x, cs.x, sizeof(ms.x)) == 0 && std::memcmp(&ms.r, &cs.r, sizeof(double)) == 0 &&
+                   std::memcmp(&ms.f_r, &cs.f_r, sizeof(double)) == 0;
+    }
     {
         Span span(b, LBG_CAT_REDF);
-        if (!b->cn_h) LBG_CUDA(cudaMallocHost(&b->cn_h, 2 * sizeof(int)));  // pinned: no staged copy
-        LBG_CUDA(cudaMemcpyAsync(b->cn_h, b->cov_n, 2 * sizeof(int), cudaMemcpyDeviceToHost, b->stream));
-        LBG_CUDA(cudaStreamSynchronize(b->stream));
-        const int cn[2] = {b->cn_h[0], b->cn_h[1]};
-        const long long ne = (long long)cn[0] + 2LL * cn[1];
-        if (!b->ekeys[0] || !b->ekeys[1] || !b->sort_tmp) {
-            // sized once for the worst case (two entries per cell): steady-state steps never
-            // allocate (cudaFree/cudaMalloc serialise all block-worker threads of a process)
-            const long long cap = std::max(2 * cells, 1LL);
-            long long c1 = 0, c2 = 0;
-            if (lbg_status s = grow_device(b->ekeys[0], c1, cap, cap, "cudaMalloc(entry keys)")) return s;
-            if (lbg_status s = grow_device(b->ekeys[1], c2, cap, cap, "cudaMalloc(entry keys)")) return s;
-            b->ekeys_cap = cap;
-            size_t tmp = 0;
-            cub::DeviceRadixSort::SortKeys(nullptr, tmp, b->ekeys[0], b->ekeys[1], (int)cap, 0, 64, b->stream);
-            if (lbg_status s = grow_device(b->sort_tmp, b->sort_tmp_bytes, (long long)tmp, (long long)tmp,
-                                           "cudaMalloc(sort workspace)"))
-                return s;
-        }
-        if (std::max(n, 1) > b->red_seg_cap || !b->red_seg) {
-            const int cap = std::max(std::max(n, 1), 2 * b->red_seg_cap);
-            int c1 = 0;
-            b->red_seg_cap = 0;
-            if (lbg_status s = grow_device(b->red_seg, c1, 2LL * cap, 2LL * cap, "cudaMalloc(segments)")) return s;
-            b->red_seg_cap = cap;
-        }
-        if (ne > 0) {
-            const long long tiles = (cells + kEntryTile - 1) / kEntryTile;
-            if (tiles > b->tile_cap || !b->tile_buf) {
+        if (!b->ev_red) LBG_CUDA(cudaEventCreateWithFlags(&b->ev_red, cudaEventDisableTiming));
+        WalkArgs a{};
+        a.s = b->snaps_d;
+        a.n = n;
+        a.g = g;
+        a.count = b->count;
+        a.id0 = b->id0;
+        a.id1 = b->id1;
+        a.m0 = b->m0;
+        a.m1 = b->m1;
+        a.rows = b->red_rows;
+        a.used = b->red_used;
+        a.fast = mode == LBG_REDUCE_FAST;
+        if (!reach_ok) {
+            if (std::max(n, 1) > b->red_box_cap || !b->red_box) {
+                const int cap = std::max(std::max(n, 1), 2 * b->red_box_cap);
+                b->red_box_cap = 0;
                 long long c1 = 0;
-                b->tile_cap = 0;
-                if (lbg_status s = grow_device(b->tile_buf, c1, 2 * tiles, 2 * tiles, "cudaMalloc(entry tiles)"))
+                if (lbg_status s = grow_device(b->red_box, c1, 6LL * cap, 6LL * cap, "cudaMalloc(particle boxes)"))
                     return s;
-                b->tile_cap = tiles;
+                b->red_box_cap = cap;
             }
-            int* sums = b->tile_buf;
-            int* offs = b->tile_buf + b->tile_cap;
-            entry_tile_sums_kernel<<<(unsigned)tiles, kEntryThreads, 0, b->stream>>>(b->count, cells, sums);
-            LBG_LAUNCH_CHECK();
-            size_t tmp = 0;
-            cub::DeviceScan::ExclusiveSum(nullptr, tmp, sums, offs, (int)tiles, b->stream);
-            if (lbg_status s = grow_device(b->scan_tmp, b->scan_tmp_bytes, (long long)tmp, (long long)tmp,
-                                           "cudaMalloc(scan_tmp)"))
-                return s;
-            cub::DeviceScan::ExclusiveSum(b->scan_tmp, tmp, sums, offs, (int)tiles, b->stream);
-            entry_emit_kernel<<<(unsigned)tiles, kEntryThreads, 0, b->stream>>>(
-                b->count, cells, offs, b->id0, b->id1, snap_index(b), n, b->ekeys[0], b->err_d);
-            LBG_LAUNCH_CHECK();
-            // stable LSD sort on the particle-index bits only (unknown ids carry index n)
-            int bits = 1;
-            while ((1ll << bits) < n + 1) ++bits;
-            tmp = 0;
-            cub::DeviceRadixSort::SortKeys(nullptr, tmp, b->ekeys[0], b->ekeys[1], (int)ne, 32, 32 + bits,
-                                           b->stream);
-            if (lbg_status s = grow_device(b->sort_tmp, b->sort_tmp_bytes, (long long)tmp, (long long)tmp,
-                                           "cudaMalloc(sort_tmp)"))
-                return s;
-            cub::DeviceRadixSort::SortKeys(b->sort_tmp, tmp, b->ekeys[0], b->ekeys[1], (int)ne, 32, 32 + bits,
-                                           b->stream);
-            LBG_LAUNCH_CHECK();
+            // empty boxes: -lo and hi start far below any cell index
+            LBG_CUDA(cudaMemsetAsync(b->red_box, 0x80, sizeof(int) * 6 * std::max(n, 1), b->stream));
+            if (cells > 0) {
+                entry_box_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, b->stream>>>(
+                    b->count, cells, g.dims[0], g.dims[1], b->id0, b->id1, snap_index(b), b->red_box, b->err_d);
+                LBG_LAUNCH_CHECK();
+            }
+            a.box = b->red_box;
         }
         if (n > 0) {
-            int* start = b->red_seg;
-            int* end = b->red_seg + b->red_seg_cap;
-            LBG_CUDA(cudaMemsetAsync(start, 0, sizeof(int) * n, b->stream));
-            LBG_CUDA(cudaMemsetAsync(end, 0, sizeof(int) * n, b->stream));
-            if (ne > 0) {
-                segment_kernel<<<(unsigned)((ne + 255) / 256), 256, 0, b->stream>>>(b->ekeys[1], ne, n, start, end);
-                LBG_LAUNCH_CHECK();
-            }
-            chain_kernel<<<(unsigned)((n + kChainWarps - 1) / kChainWarps), 32 * kChainWarps, 0, b->stream>>>(
-                b->ekeys[1], start, end, b->snaps_d, n, g, b->m0, b->m1, b->red_rows, b->red_used,
-                mode == LBG_REDUCE_FAST);
+            walk_chain_kernel<<<(unsigned)((n + kWalkWarps - 1) / kWalkWarps), 32 * kWalkWarps, 0, b->stream>>>(a);
             LBG_LAUNCH_CHECK();
-            if (ne > 0) {
-                clear_entries_kernel<<<(unsigned)((ne + 255) / 256), 256, 0, b->stream>>>(b->ekeys[1], ne, b->m0,
-                                                                                         b->m1);
-                LBG_LAUNCH_CHECK();
-            }
-            LBG_CUDA(cudaMemcpyAsync(b->red_rows_h, b->red_rows, sizeof(double) * 12 * n,
-                                     cudaMemcpyDeviceToHost, b->stream));
-            LBG_CUDA(cudaMemcpyAsync(b->red_used_h, b->red_used, sizeof(int) * n, cudaMemcpyDeviceToHost,
-                                     b->stream));
+            // partials D2H on the side stream (pinned), ordered after the walk by an event
+            LBG_CUDA(cudaEventRecord(b->ev_red, b->stream));
+            LBG_CUDA(cudaStreamWaitEvent(b->side, b->ev_red, 0));
+            LBG_CUDA(cudaMemcpyAsync(b->red_rows_h, b->red_rows, sizeof(double) * 12 * n, cudaMemcpyDeviceToHost,
+                                     b->side));
+            LBG_CUDA(cudaMemcpyAsync(b->red_used_h, b->red_used, sizeof(int) * n, cudaMemcpyDeviceToHost, b->side));
         }
     }
-    LBG_CUDA(cudaStreamSynchronize(b->stream));
+    // lbg_sync waits for the side stream's copies and reads the error counters
     if (lbg_status s = lbg_sync(b, nullptr)) {
         if (s == LBG_SYNC_ERROR)
             return set_error(LBG_SYNC_ERROR, "hydrodynamic force for unknown particle id");
@@ -959,7 +1017,9 @@ lbg_status lbg_upload_fraction(lbg_block b, const uint8_t* count, const int* id0
     // the stored velocities belong to the old field: materialise them, then they are plain data
     if (lbg_status s = materialize_velocity(b)) return s;
     b->v_snap = false;
+    b->p_direct = false;
     b->map_ids_valid = false;
+    b->map_snaps.clear();
     b->cov_dirty = true;
     return copy_frac(b, true, (uint8_t*)count, (int*)id0, (int*)id1, (double*)b0, (double*)b1, (double*)btot);
 }

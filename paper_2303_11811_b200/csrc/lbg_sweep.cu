@@ -63,6 +63,7 @@ struct SweepArgs {
     long long seg_cap;
     const int* __restrict__ id0;
     const int* __restrict__ id1;
+    const int* __restrict__ pidx0;  // entry 0's index in the current list (null: via id0)
     // fused force reduction (LBG_FORCE_FUSED)
     const lbg_snapshot* __restrict__ snaps;
     int n_snaps;
@@ -143,15 +144,27 @@ __device__ __forceinline__ void solid_velocity(const SweepArgs& a, int e, long l
     }
 }
 
+// snapshot index of entry 0 of cell fc for the inline solid velocity: the mapping's own index
+// (a.pidx0, written by the mapping kernel) while the current snapshot list is the mapping list —
+// one dependent load instead of id0 -> id table -> index — else snapshot_index(id0)
+// (psm.cpp:46-51). For an uncovered cell the value is stale and selected away by the caller.
+__device__ __forceinline__ int entry0_index(const SweepArgs& a, long long fc) {
+    if (a.pidx0) {
+        const int p = a.pidx0[fc];
+        return (unsigned)p < (unsigned)a.n_snaps ? p : -1;
+    }
+    return a.sidx(a.id0[fc]);
+}
+
 // solid velocity of the first entry of a one-entry-segment lane, selected to 0 where the cell
-// is not covered. Every index load (id0, the id -> index table, the snapshot) is issued
-// without waiting for the cell's count, so the chain seg_list -> cell fields -> table ->
-// snapshot overlaps the 19 population loads instead of following them.
+// is not covered. Every index load (id0 or the direct index, the id -> index table, the
+// snapshot) is issued without waiting for the cell's count, so the chain seg_list -> cell
+// fields -> table -> snapshot overlaps the 19 population loads instead of following them.
+// `p` is the entry's snapshot index (kVsnap; -1 if unknown).
 template <bool kVsnap>
 __device__ __forceinline__ void solid_velocity_sel(const SweepArgs& a, bool cov, long long fc, int i, int j,
-                                                   int k, double (&v)[3], int id0 = 0) {
+                                                   int k, double (&v)[3], int p = -1) {
     if constexpr (kVsnap) {
-        const int p = a.sidx(id0);  // id0 of an uncovered cell is stale: selected away
         if (cov && p < 0) atomicAdd(&a.err->unknown, 1ull);
         double x[3] = {0.0, 0.0, 0.0}, u[3] = {0.0, 0.0, 0.0}, w[3] = {0.0, 0.0, 0.0};
         if (p >= 0) {
@@ -372,7 +385,8 @@ __device__ __forceinline__ bool coupled_lane(const SweepArgs& a, int i, int j, i
         // cell fields loaded unconditionally (fc is an interior cell), selected by cov
         const double bt = a.btot[fc], b0 = a.b0[fc];
         double v[3];
-        solid_velocity_sel<kVsnap>(a, cov, fc, i, j, k, v, kVsnap ? a.id0[fc] : 0);
+        const int pe = kVsnap ? entry0_index(a, fc) : -1;
+        solid_velocity_sel<kVsnap>(a, cov, fc, i, j, k, v, pe);
         double f[kQ];
         pull(a, i, j, k, base, f);
         ok = psm_cell_one<kForced>(f, a.inv_tau, a.F, cov ? bt : 0.0, cov ? b0 : 0.0, v[0], v[1], v[2], a.dst,
@@ -399,7 +413,8 @@ __device__ __forceinline__ bool coupled_lane(const SweepArgs& a, int i, int j, i
         const long long base = L.idx(i, j, k);
         const double bt = a.btot[fc], b0 = a.b0[fc], b1 = a.b1[fc];
         double v0[3], v1[3] = {0.0, 0.0, 0.0};
-        solid_velocity_sel<kVsnap>(a, cov, fc, i, j, k, v0, kVsnap ? a.id0[fc] : 0);
+        const int pe = kVsnap ? entry0_index(a, fc) : -1;
+        solid_velocity_sel<kVsnap>(a, cov, fc, i, j, k, v0, pe);
         if (two) solid_velocity<kVsnap>(a, 1, fc, i, j, k, v1);
         double f[kQ];
         pull(a, i, j, k, base, f);
@@ -419,7 +434,7 @@ __device__ __forceinline__ bool coupled_lane(const SweepArgs& a, int i, int j, i
             cc[0] = (double)(a.blk_lo[0] + i) + 0.5;
             cc[1] = (double)(a.blk_lo[1] + j) + 0.5;
             cc[2] = (double)(a.blk_lo[2] + k) + 0.5;
-            p0 = a.sidx(a.id0[fc]);
+            p0 = entry0_index(a, fc);
             if (cnt > 1) p1 = a.sidx(a.id1[fc]);
             if (p0 < 0 || (cnt > 1 && p1 < 0)) atomicAdd(&a.err->unknown, 1ull);
         }
@@ -506,7 +521,7 @@ struct SegPre {
 template <bool kVsnap>
 __device__ __forceinline__ void seg_pre(const SweepArgs& a, const SegIn& in, SegPre& pre) {
     if (!in.act) return;
-    solid_velocity_sel<kVsnap>(a, in.cnt > 0, in.fc, in.i, in.j, in.k, pre.v, in.id0);
+    solid_velocity_sel<kVsnap>(a, in.cnt > 0, in.fc, in.i, in.j, in.k, pre.v, kVsnap ? a.sidx(in.id0) : -1);
     moments(in.f, pre.rho, pre.ux, pre.uy, pre.uz);
     pre.usq = (pre.ux * pre.ux + pre.uy * pre.uy) + pre.uz * pre.uz;
     pre.ok = pre.rho > 0.0 && pre.usq <= kMaxVelocity * kMaxVelocity && isfinite(pre.rho);
@@ -666,7 +681,7 @@ __device__ __forceinline__ void seg_from_tma(const SweepArgs& a, unsigned c0, in
             for (int q = 0; q < kQ; ++q) f[q] = st.f[q][4 + lane - cx(q)];
         }
         double v[3];
-        solid_velocity_sel<kVsnap>(a, cov, fc, i, j, k, v, id0);
+        solid_velocity_sel<kVsnap>(a, cov, fc, i, j, k, v, kVsnap ? a.sidx(id0) : -1);
         ok = psm_cell_one<false>(f, a.inv_tau, a.F, cov ? bt : 0.0, cov ? b0 : 0.0, v[0], v[1], v[2], a.dst,
                                  L.plane, base, m);
         if constexpr (!kFused) {
@@ -719,6 +734,55 @@ __global__ void __launch_bounds__(32 * kTmaWarps) psm_seg_tma_kernel(const Sweep
     }
 }
 
+// ---------------------------------------------------------------- K12: unified coupled sweep
+// One persistent kernel for the fluid and the one-entry segments of a coupled block (default;
+// LBG_K12=0 restores the K1 || K2 split): each warp walks the aligned 32-cell row segments of
+// the box in memory order (grid stride), reads the segment's 32 count bytes and runs the SRT
+// operator (no covered cell) or the pair-scheduled one-entry operator on every lane (max count
+// 1; fluid lanes with B = b = 0 when unforced). Segments holding a two-entry cell are left to
+// psm_seg_kernel<two> (the segment list's back), so every PDF sector is still swept by exactly
+// one kernel. One kernel keeps the SM's warps mixing memory-bound SRT segments with the
+// fp64-heavy PSM segments (the split had early-exit K1 warps and, the register file being
+// full with K2, no real K1 || K2 concurrency). Config 3: 1.09 ms vs 1.13 ms for the split
+// (profiles/r02_ab_k12.txt, where the variants that measured slower are listed: L2 bulk or
+// line prefetch of the next segment, a dynamic segment counter, a low-register L1-re-read
+// operator, 4 or 6 CTAs per SM).
+template <bool kForced, bool kFused, bool kVsnap, int kMinBlocks>
+__global__ void __launch_bounds__(128, kMinBlocks) coupled_unified_kernel(const SweepArgs a) {
+    const Layout& L = a.L;
+    const int lane = threadIdx.x & 31;
+    const long long warp = (long long)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const long long nwarps = (long long)((gridDim.x * blockDim.x) >> 5);
+    const int segs_x = (a.hi[0] - a.i0 + 31) >> 5;
+    const int ny_b = a.hi[1] - a.lo[1];
+    const long long nseg = (long long)segs_x * ny_b * (a.hi[2] - a.lo[2]);
+    for (long long s = warp; s < nseg; s += nwarps) {
+        const long long r = s / segs_x;
+        const int i0 = a.i0 + 32 * (int)(s - r * segs_x);
+        const int j = a.lo[1] + (int)(r % ny_b);
+        const int k = a.lo[2] + (int)(r / ny_b);
+        const int i = i0 + lane;
+        const bool inx = i < L.nx;
+        const long long fc = L.frac(inx ? i : L.nx - 1, j, k);
+        const int cnt = inx ? (int)a.count[fc] : 0;
+        const int mx = __reduce_max_sync(0xffffffffu, (unsigned)cnt);
+        if (mx >= 2) continue;  // psm_seg_kernel<two> sweeps this segment
+        const bool act = inx && i >= a.lo[0] && i < a.hi[0];
+        bool ok = true;
+        if (mx == 0) {
+            if (act) ok = srt_cell_at<kForced, false>(a, i, j, k);
+            count_bad(a.err, !ok);
+            continue;
+        }
+        double m[2][3] = {{0, 0, 0}, {0, 0, 0}};
+        double cc[3] = {0, 0, 0};
+        int p0 = -1, p1 = -1;
+        if (act) ok = coupled_lane<kForced, kFused, false, kVsnap>(a, i, j, k, fc, cnt, m, p0, p1, cc);
+        count_bad(a.err, !ok);
+        if constexpr (kFused) fused_accumulate(a, p0, m[0], cc);
+    }
+}
+
 // Thin boxes of a coupled block (the boundary shell), split like K1/K2 by the operator a cell
 // needs rather than by segment: kTwo = false sweeps every shell cell with count <= 1 (the
 // ~94-register one-entry path), kTwo = true only the two-entry cells (general operator), so
@@ -768,6 +832,15 @@ static bool empty_box(const lbg_box& r) {
     return r.hi[0] <= r.lo[0] || r.hi[1] <= r.lo[1] || r.hi[2] <= r.lo[2];
 }
 
+// LBG_DIRECT_INDEX=0: the inline solid velocity always goes through id0 -> id table (A/B)
+static bool lbg_direct_index_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("LBG_DIRECT_INDEX");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
 // the fused force mode needs its per-particle accumulators for the current snapshot list
 static lbg_status check_fused(lbg_block b) {
     if (b->coupling && b->force_mode == LBG_FORCE_FUSED && b->n_snaps > 0 &&
@@ -802,6 +875,7 @@ static SweepArgs make_args(lbg_block b, const lbg_fluid* fl) {
         a.snaps = b->snaps_d;
         a.n_snaps = b->n_snaps;
         a.sidx = snap_index(b);
+        a.pidx0 = (b->v_snap && b->p_direct && lbg_direct_index_enabled()) ? b->pidx0 : nullptr;
         for (int c = 0; c < 3; ++c) a.blk_lo[c] = b->lo[c];
         a.facc = b->facc;
         a.fused_used = b->fused_used;
@@ -923,6 +997,42 @@ static void launch_psm_segments(lbg_block b, const SweepArgs& a, bool forced, cu
     });
 }
 
+// K12 (coupled_unified_kernel) settings: LBG_K12=0 restores the K1 || K2 split, LBG_K12_SM =
+// CTAs per SM (4, 5 or 6: also the register cap; 5 measured best)
+static int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+static bool k12_on() {
+    static const bool v = env_int("LBG_K12", 1) != 0;
+    return v;
+}
+
+static void launch_unified(lbg_block b, const SweepArgs& a, bool forced, cudaStream_t st) {
+    static const int per_sm = std::min(6, std::max(4, env_int("LBG_K12_SM", 5)));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, b->device);
+    const bool fused = b->force_mode == LBG_FORCE_FUSED;
+    const long long nseg = (long long)((a.hi[0] - a.i0 + 31) / 32) * (a.hi[1] - a.lo[1]) * (a.hi[2] - a.lo[2]);
+    with_flags(forced, fused, b->v_snap, [&](auto F, auto U, auto V) {
+        constexpr bool kF = decltype(F)::value, kU = decltype(U)::value, kV = decltype(V)::value;
+        auto go = [&](auto kern, int ctas) {
+            const long long want = (nseg + 3) / 4;  // CTAs of 4 warps, one segment each
+            const unsigned grid = (unsigned)std::max(1LL, std::min<long long>(want, (long long)sms * ctas));
+            kern<<<grid, 128, 0, st>>>(a);
+        };
+        if (kF || per_sm == 4)
+            go(coupled_unified_kernel<kF, kU, kV, 4>, 4);
+        else if (per_sm == 6)
+            go(coupled_unified_kernel<kF, kU, kV, 6>, 6);
+        else
+            go(coupled_unified_kernel<kF, kU, kV, 5>, 5);
+        count_launch();
+        // segments holding a two-entry cell (particle contacts): pair-scheduled two-entry operator
+        psm_seg_kernel<kF, kU, true, kV><<<(unsigned)(sms * 4), 128, 0, st>>>(a);
+    });
+}
+
 // LBG_K2_CONCURRENT=0 runs K2 after K1 on the compute stream (A/B measurement)
 static bool k2_concurrent() {
     static const bool v = [] {
@@ -969,6 +1079,11 @@ lbg_status lbg_sweep(lbg_block b, const lbg_fluid* fl, const lbg_box* range) {
     Span span(b, LBG_CAT_PSM);
     const bool fo = forced(fl);
     if (b->coupling) {
+        if (k12_on()) {
+            launch_unified(b, a, fo, b->stream);
+            LBG_LAUNCH_CHECK();
+            return LBG_OK;
+        }
         if (k2_concurrent()) {
             // K1 and K2 touch disjoint cells (K1 skips K2's segments): K2 runs on the aux stream
             // beside K1, with fewer persistent CTAs so K1's blocks find room on every SM

@@ -10,4 +10,7 @@ import bench  # noqa: E402
 
 r = bench.coupled_sweep_roofline(steps=int(os.environ.get("AB_STEPS", "20")))
 env = {k: v for k, v in os.environ.items() if k.startswith("LBG_")}
-print(json.dumps({"env": env, "sweep_ms": r["sweep_ms"], "bc_ms": r["bc_ms"], "frac": r["roofline"]["frac"]}))
+rec = {"env": env, "sweep_ms": r["sweep_ms"], "bc_ms": r["bc_ms"], "frac": r["roofline"]["frac"]}
+if os.environ.get("AB_REDUCE_MS"):
+    rec["reduce_ms"] = os.environ["AB_REDUCE_MS"]
+print(json.dumps(rec))
