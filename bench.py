@@ -413,6 +413,55 @@ def coupled_b0_roofline(n=512, tau=0.8, steps=10, warmup=3):
                          "frac": round(achieved / peak, 4)}}
 
 
+def aa_roofline(n=512, tau=0.8, steps=10, warmup=4):
+    """Config 2 with the AA-pattern in-place streaming (lbg_set_streaming(LBG_STREAM_AA)): the
+    same 512^3 periodic shear wave and 304 B per LUP in ONE PDF buffer (the second is released:
+    half the HBM). Even step counts (both AA phases per pair of steps); CUDA events on the
+    block's stream."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2303_11811_b200 import lbdem
+    from paper_2303_11811_b200 import lbg as abi
+    blk = lbdem.Block((n, n, n))
+    try:
+        mem = C.c_longlong()
+        abi.load().lbg_block_info(blk.h, None, None, None, C.byref(mem))
+        mem_ab = mem.value
+        blk.init_shear_wave((n, n, n))
+        blk.set_periodic_wrap((1, 1, 1))
+        blk.set_streaming(abi.STREAM_AA)
+        abi.load().lbg_block_info(blk.h, None, None, None, C.byref(mem))
+        p = lbdem.FluidParams(tau)
+        box = lbdem.CellBox((0, 0, 0), (n, n, n))
+        stream = torch.cuda.ExternalStream(blk.stream)
+        for _ in range(warmup):
+            blk.sweep(p, box)
+            blk.swap()
+        blk.sync()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            blk.sweep(p, box)
+            blk.swap()
+        e1.record(stream)
+        e1.synchronize()
+        blk.sync()
+        ms = e0.elapsed_time(e1) / steps
+    finally:
+        blk.close()
+    cells = n ** 3
+    pk = peaks()
+    peak = pk["hbm_gbs"] if pk and pk.get("hbm_gbs") else 6650.0
+    achieved = BYTES_PER_LUP * cells / (ms / 1e3) / 1e9
+    return {"workload": f"config 2 with AA in-place streaming: {n}^3 periodic shear wave, tau {tau}",
+            "device_bytes": mem.value, "device_bytes_double_buffer": mem_ab,
+            "sweep_ms": round(ms, 4), "mlups": round(cells / (ms / 1e3) / 1e6, 1),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4)}}
+
+
 def host_mem_available():
     """MemAvailable of this host in bytes (None if unknown)."""
     try:
@@ -686,6 +735,10 @@ def run_lbg(args):
             out["coupled_b0"] = coupled_b0_roofline(n, args.tau)
         except Exception as e:  # noqa: BLE001
             out["coupled_b0"] = {"unavailable": f"{type(e).__name__}: {e}"}
+        try:
+            out["aa_streaming"] = aa_roofline(n, args.tau)
+        except Exception as e:  # noqa: BLE001
+            out["aa_streaming"] = {"unavailable": f"{type(e).__name__}: {e}"}
     if rank == 0:
         if N == 1 and not args.no_coupled:
             try:

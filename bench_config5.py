@@ -9,10 +9,11 @@ its GPU-side operators on liblbg; host DEM = the reference's code).
 Weak scaling as SURVEY §8(d): domain (edge*N) x edge x edge, block grid {N,1,1} (x-slabs, so
 the bottom-settled bed splits evenly), edge^3 cells and `per_gpu` spheres (d = 10) per GPU.
 Strong scaling: the fixed 1024 x 512 x 512 bed (2.7e8 cells, 10^5 spheres; about 120 GB on a
-single GPU) split into {N,1,1} x-slabs. Either way one block per GPU (LBDEM_GPU_SPREAD=1), one
-reference worker thread per block, no host PDF mirror (LBDEM_GPU_HOST_MIRROR=0). Prints one
-JSON line with the reference's own per-category TimingReport (perf.hpp:17-51) and
-MLUPS = cells * steps / wall time.
+single GPU) split into {N,1,1} x-slabs. Either way `--blocks-per-gpu` consecutive x-slab blocks
+per GPU (LBDEM_GPU_SPREAD=1), one reference worker thread per block, no host PDF mirror
+(LBDEM_GPU_HOST_MIRROR=0), the pushed halo between blocks (LBDEM_GPU_HALO, default push).
+Prints one JSON line with, per force mode (scratch = bitwise PARITY partials, fused), the
+reference's own per-category TimingReport (perf.hpp:17-51) and MLUPS = cells * steps / wall time.
 """
 import argparse
 import json
@@ -39,14 +40,15 @@ def main():
     ap.add_argument("--edge", type=int, default=512)
     ap.add_argument("--per-gpu", type=int, default=12500)
     ap.add_argument("--settle", type=int, default=100)
-    ap.add_argument("--force", choices=["scratch", "fused"], default="fused")
+    ap.add_argument("--force", choices=["scratch", "fused", "both"], default="both",
+                    help="scratch: reference semantics, bitwise PARITY partials; fused: per-particle sums "
+                         "inside the PSM kernel (tolerance); both: one run each, scratch first")
     ap.add_argument("--mode", choices=["weak", "strong"], default="weak")
-    ap.add_argument("--blocks-per-gpu", type=int, default=1,
+    ap.add_argument("--blocks-per-gpu", type=int, default=4,
                     help="x-slab blocks per GPU (consecutive ids), one host worker each: spreads the host DEM")
     args = ap.parse_args()
     os.environ["LBDEM_GPU_SPREAD"] = "1"
     os.environ["LBDEM_GPU_HOST_MIRROR"] = "0"
-    os.environ["LBDEM_GPU_FORCE"] = args.force
     os.environ["LBDEM_GPU_BLOCKS_PER_DEVICE"] = str(args.blocks_per_gpu)
     import torch  # noqa: F401  (CUDA plumbing)
     import dropin
@@ -57,28 +59,31 @@ def main():
         nx, particles = n * g, args.per_gpu * g
     nb = g * args.blocks_per_gpu
     cfg = CFG.format(nx=nx, n=n, g=nb, p=particles, settle=args.settle)
-    t0 = time.perf_counter()
-    sim = dropin.DropinSim(cfg, (nx, n, n))
-    setup = time.perf_counter() - t0
-    sim.run(1)
-    sim.reset_timers()
-    t0 = time.perf_counter()
-    sim.run(args.steps)
-    dt = time.perf_counter() - t0
-    cat = sim.timings()
     cells = nx * n * n
-    print(json.dumps({
-        "workload": f"config 5 {args.mode}: {nx}x{n}x{n} fluidized bed, {particles} spheres d=10, "
-                    f"blocks {{{nb},1,1}}, {args.blocks_per_gpu} per GPU (one host worker each), "
-                    f"host DEM (reference), force mode {args.force}",
-        "blocks_per_gpu": args.blocks_per_gpu,
-        "scaling": args.mode,
-        "n_gpus": g, "steps": args.steps, "ms_per_step": round(dt * 1e3 / args.steps, 2),
-        "mlups": round(cells * args.steps / dt / 1e6, 1),
-        "mlups_per_gpu": round(cells * args.steps / dt / 1e6 / g, 1),
-        "categories_ms_per_step": {c: round(v * 1e3 / args.steps, 3) for c, v in zip(CATS, cat)},
-        "particles": particles, "setup_s": round(setup, 1)}))
-    sim.close()
+    out = {"workload": f"config 5 {args.mode}: {nx}x{n}x{n} fluidized bed, {particles} spheres d=10, "
+                       f"blocks {{{nb},1,1}}, {args.blocks_per_gpu} per GPU (one host worker each), "
+                       f"host DEM (reference)",
+           "blocks_per_gpu": args.blocks_per_gpu, "scaling": args.mode, "n_gpus": g, "steps": args.steps,
+           "particles": particles, "halo": os.environ.get("LBDEM_GPU_HALO", "push")}
+    for mode in (("scratch", "fused") if args.force == "both" else (args.force,)):
+        os.environ["LBDEM_GPU_FORCE"] = mode
+        t0 = time.perf_counter()
+        sim = dropin.DropinSim(cfg, (nx, n, n))
+        setup = time.perf_counter() - t0
+        sim.run(1)
+        sim.reset_timers()
+        t0 = time.perf_counter()
+        sim.run(args.steps)
+        dt = time.perf_counter() - t0
+        cat = sim.timings()
+        out[mode] = {
+            "force_mode": mode, "ms_per_step": round(dt * 1e3 / args.steps, 2),
+            "mlups": round(cells * args.steps / dt / 1e6, 1),
+            "mlups_per_gpu": round(cells * args.steps / dt / 1e6 / g, 1),
+            "categories_ms_per_step": {c: round(v * 1e3 / args.steps, 3) for c, v in zip(CATS, cat)},
+            "setup_s": round(setup, 1)}
+        sim.close()
+    print(json.dumps(out))
 
 
 if __name__ == "__main__":

@@ -139,10 +139,36 @@ public:
                                  static_cast<int>(s.size())));
     }
 
+    /// Sender-pushed halo (lbg_halo_push*): the neighbours this block pushes into; then per
+    /// step push_halo() after the whole-block sweep and push_wait() before the next one.
+    void push_connect(const std::vector<std::pair<Vec3i, const DeviceBlock*>>& to) {
+        std::vector<std::array<int, 3>> d;
+        std::vector<lbg_block> s;
+        for (const auto& [v, blk] : to) {
+            d.push_back({v.x, v.y, v.z});
+            s.push_back(blk->b_);
+        }
+        check(lbg_halo_push_connect(b_, reinterpret_cast<const int(*)[3]>(d.data()), s.data(),
+                                    static_cast<int>(s.size())));
+    }
+    void push_halo() { check(lbg_halo_push(b_)); }
+    void push_wait() { check(lbg_halo_push_wait(b_)); }
+
     void map(const std::vector<psm::ParticleSnapshot>& snaps, int subdivisions) {
         to_c(snaps);
         check(lbg_map(b_, cs_.data(), static_cast<int>(cs_.size()), subdivisions));
     }
+    /// the next step's mapping into the shadow fraction field (lbg_map_prepare) / make it current
+    void map_prepare(const std::vector<psm::ParticleSnapshot>& snaps, int subdivisions) {
+        std::vector<lbg_snapshot> c(snaps.size());
+        for (std::size_t i = 0; i < snaps.size(); ++i) {
+            const auto& s = snaps[i];
+            c[i] = lbg_snapshot{s.id, 0, {s.x.x, s.x.y, s.x.z}, s.r, s.f_r,
+                                {s.u.x, s.u.y, s.u.z}, {s.omega.x, s.omega.y, s.omega.z}};
+        }
+        check(lbg_map_prepare(b_, c.data(), static_cast<int>(c.size()), subdivisions));
+    }
+    void map_commit() { check(lbg_map_commit(b_)); }
     void set_solid_velocities(const std::vector<psm::ParticleSnapshot>& snaps) {
         to_c(snaps);
         check(lbg_set_solid_velocities(b_, cs_.data(), static_cast<int>(cs_.size())));

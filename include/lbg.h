@@ -171,6 +171,16 @@ lbg_status lbg_sweep_boxes(lbg_block b, const lbg_fluid* fluid, const lbg_box* b
  * wrapped interior cell instead — the value fill_periodic_ghosts would have put there — so
  * the ghost fill for that axis is not needed. Bitwise identical interior results. */
 lbg_status lbg_set_periodic_wrap(lbg_block b, const int wrap[3]);
+/* Streaming layout of a plain-fluid block. LBG_STREAM_AB (default): the reference's two
+ * buffers, pull sweep into dst, lbg_swap (field.hpp:36-78). LBG_STREAM_AA: in-place AA pattern
+ * in ONE buffer (half the HBM; the other buffer is released): alternating steps read and write
+ * each cell's own slots or its neighbours' (lbg_aa.cu), bitwise the same populations. Needs a
+ * single periodic block with the in-kernel wrap on every axis (no BC, halo or coupling); each
+ * step is lbg_sweep over the whole block + lbg_swap. lbg_download_src returns the double-buffer
+ * src image in either phase; dst transfers, BCs, halos and box sweeps return LBG_INVALID;
+ * moments and totals only after an even number of steps. Switching back re-allocates dst. */
+enum { LBG_STREAM_AB = 0, LBG_STREAM_AA = 1 };
+lbg_status lbg_set_streaming(lbg_block b, int mode);
 /* Unfused pull stream (lbm.cpp:6-17), debug/tests. */
 lbg_status lbg_stream(lbg_block b, const lbg_box* range);
 
@@ -187,6 +197,13 @@ lbg_status lbg_apply_boundaries(lbg_block b, const lbg_face_bc faces[6], const i
  * pinned memory and copied H2D on the block's side stream. `subdivisions` is accepted for
  * API parity (the device binning is finer and gives the same candidate order). */
 lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisions);
+/* lbg_map into a second fraction field while the block keeps using the current one (its
+ * sweeps, reductions and observers are unaffected): the next step's mapping can be issued as
+ * soon as its inputs (ids, positions, radii) are final, overlapping host work. lbg_map_commit
+ * makes the prepared field current (pointer swap); errors of the prepared mapping (overfull
+ * cells) are reported by lbg_sync like lbg_map's. */
+lbg_status lbg_map_prepare(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisions);
+lbg_status lbg_map_commit(lbg_block b);
 /* set_solid_velocities (psm.cpp:138-169), replaces Simulation::phase_setu_inner's call
  * (sim.cpp:296-297). Uploads the (post velocity-sync) snapshots; the PSM sweep evaluates
  * u + omega x (c - x) per entry from them. If the list lost an id of the mapping list (or
@@ -277,6 +294,22 @@ lbg_status lbg_halo_fetch(lbg_block dst, const int dir[3], lbg_block src);
  * (dirs[t], srcs[t]) as in lbg_halo_fetch, one unpack launch (the ghost regions of distinct
  * directions are disjoint, so the order of the reference's loop does not matter). */
 lbg_status lbg_halo_fetch_all(lbg_block dst, const int (*dirs)[3], const lbg_block* srcs, int n);
+
+/* The halo pushed by its sender, for several blocks of one process on any GPUs (replaces
+ * begin/complete_halo_exchange, sim.cpp:156-201, once the ghosts have been filled by one
+ * lbg_halo_stage / lbg_halo_fetch_all exchange). lbg_halo_push_connect registers the block's
+ * neighbours (offset, block; not itself) and enables peer access to their GPUs. After each
+ * sweep of the whole block (before any lbg_swap), lbg_halo_push stores the post-collision
+ * populations that stream out through each face (5 q per face cell) and edge (1 q per edge
+ * cell) straight into the neighbours' next-step ghost cells — the only ghost slots a pull sweep
+ * reads — on the block's comm stream (NVLink peer stores across GPUs; no staging, no unpack),
+ * asynchronous to the caller. lbg_halo_push_wait, at the start of the next step, orders the
+ * block's stream after its neighbours' pushes (complete_halo_exchange). Interior results are
+ * bitwise those of the full 19-q exchange; ghost slots no sweep reads are not written. Steps
+ * must be lockstep across the registered blocks (every block pushes once per step). */
+lbg_status lbg_halo_push_connect(lbg_block b, const int (*offs)[3], const lbg_block* nbrs, int n);
+lbg_status lbg_halo_push(lbg_block b);
+lbg_status lbg_halo_push_wait(lbg_block b);
 
 /* The slab halo fused into the outer sweep over NVLink peer memory (one process per GPU,
  * >= 2 ranks, plain-fluid blocks). lbg_p2p_handles exports 208 bytes per rank: CUDA IPC

@@ -31,13 +31,17 @@ SIM_HPP_EDITS = [
      "    mutable bool host_stale = false;        ///< host field copy behind the device\n"
      "    mutable std::vector<double> moments;    ///< device moments cache (observers)\n"
      "    mutable bool moments_stale = true;\n"
-     "    bool outer_done = false;                ///< whole block swept in phase_setu_inner\n"),
+     "    bool outer_done = false;                ///< whole block swept in phase_setu_inner\n"
+     "    bool push_connected = false;            ///< lbg_halo_push neighbours registered\n"
+     "    bool push_ready = false;                ///< ghosts kept current by the neighbours' pushes\n"
+     "    bool premapped = false;                 ///< next step's fraction field already mapped\n"
+     "    std::vector<psm::ParticleSnapshot> premap;  ///< the snapshots it was mapped from\n"),
 ]
 
 SIM_CPP_EDITS = [
     # includes + host-copy refresh used by the observers
     ("#include <set>\n",
-     "#include <set>\n#include <cstdlib>\n\n#include \"lbdem_gpu.hpp\"\n#include \"dropin_observe.hpp\"\n"),
+     "#include <set>\n#include <cstdlib>\n#include <cstring>\n\n#include \"lbdem_gpu.hpp\"\n#include \"dropin_observe.hpp\"\n"),
     ("namespace lbdem {\n\nusing partition::MsgKind;",
      "namespace lbdem {\n\n"
      "namespace {\n"
@@ -61,11 +65,17 @@ SIM_CPP_EDITS = [
      "    return !(e && std::atoi(e) == 0);\n"
      "}\n"
      "int mirror_dim(int d) { return host_mirror() ? d : 1; }\n"
-     "/// PDF halo device to device (default) or through the MessageBus (LBDEM_GPU_HALO=host).\n"
-     "bool device_halo() {\n"
+     "/// PDF halo (LBDEM_GPU_HALO): push (default) - after the first step every block stores the\n"
+     "/// populations leaving through its faces/edges into its neighbours' next-step ghosts right\n"
+     "/// after its sweep (lbg_halo_push, 5 q per face cell, peer stores across GPUs); stage - the\n"
+     "/// 19-q source slabs staged and fetched device to device every step; host - the MessageBus.\n"
+     "int halo_mode() {\n"
      "    const char* e = std::getenv(\"LBDEM_GPU_HALO\");\n"
-     "    return !(e && std::string(e) == \"host\");\n"
+     "    if (e && std::string(e) == \"host\") return 0;\n"
+     "    if (e && std::string(e) == \"stage\") return 1;\n"
+     "    return 2;\n"
      "}\n"
+     "bool device_halo() { return halo_mode() != 0; }\n"
      "/// LBDEM_GPU_SWEEP=split: the reference's inner sweep / halo / BCs / outer-shell sweep;\n"
      "/// default one sweep of the whole block in phase_setu_inner after the halo and BCs (the\n"
      "/// halo messages were posted in phase_post_and_map; the inner sweep reads no ghost, so\n"
@@ -73,6 +83,31 @@ SIM_CPP_EDITS = [
      "bool full_sweep() {\n"
      "    const char* e = std::getenv(\"LBDEM_GPU_SWEEP\");\n"
      "    return !(e && std::string(e) == \"split\");\n"
+     "}\n"
+     "/// the pushed halo needs the whole-block sweep (it follows the only sweep of a step)\n"
+     "bool push_halo() { return halo_mode() == 2 && full_sweep(); }\n"
+     "/// LBDEM_GPU_PREMAP=1: the next step's fraction field is mapped as soon as its inputs are\n"
+     "/// final - in the last sub-cycle, right\n"
+     "/// after the particle sync that fixes positions (sub_integrate_and_sync) and the block's\n"
+     "/// particle/ghost membership (apply_particle_sync) - so the device mapping runs under the\n"
+     "/// rest of that sub-cycle's host DEM (PAPER.md:576-583), into the block's second fraction\n"
+     "/// field (observers after the step still see this step's). phase_post_and_map commits it\n"
+     "/// when the snapshots it builds have the same ids, positions and radii (what the mapping\n"
+     "/// reads), else maps as usual. Off by default: on config 3 it did not shorten the step\n"
+     "/// (profiles/r02_premap.txt); the default maps in phase_post_and_map like the reference.\n"
+     "bool premap_on() {\n"
+     "    const char* e = std::getenv(\"LBDEM_GPU_PREMAP\");\n"
+     "    return e && std::atoi(e) != 0;\n"
+     "}\n"
+     "bool same_geometry(const std::vector<psm::ParticleSnapshot>& a,\n"
+     "                   const std::vector<psm::ParticleSnapshot>& b) {\n"
+     "    if (a.size() != b.size()) return false;\n"
+     "    for (std::size_t i = 0; i < a.size(); ++i)\n"
+     "        if (a[i].id != b[i].id || std::memcmp(&a[i].x, &b[i].x, sizeof(Vec3)) != 0 ||\n"
+     "            std::memcmp(&a[i].r, &b[i].r, sizeof(double)) != 0 ||\n"
+     "            std::memcmp(&a[i].f_r, &b[i].f_r, sizeof(double)) != 0)\n"
+     "            return false;\n"
+     "    return true;\n"
      "}\n"
      "/// Observers read the host copies; refresh them from the device after a step.\n"
      "void refresh_host(const std::vector<std::unique_ptr<BlockState>>& blocks, bool coupling) {\n"
@@ -108,8 +143,11 @@ SIM_CPP_EDITS = [
     ("void Simulation::begin_halo_exchange(int b) {\n    BlockState& blk = *blocks_[b];\n",
      "void Simulation::begin_halo_exchange(int b) {\n    BlockState& blk = *blocks_[b];\n"
      "    if (device_halo()) {\n"
+     "        // once pushing, only periodic self-neighbours still go through the staging\n"
+     "        const bool pushed = push_halo() && blk.push_ready;\n"
      "        std::vector<Vec3i> offs;\n"
-     "        for (const auto& n : decomp_.blocks[b].neighbors) offs.push_back(n.offset);\n"
+     "        for (const auto& n : decomp_.blocks[b].neighbors)\n"
+     "            if (!(pushed && n.block != b)) offs.push_back(n.offset);\n"
      "        blk.dev->stage_slabs(offs);\n"
      "        blk.halo_pending = true;\n"
      "        return;\n"
@@ -119,10 +157,12 @@ SIM_CPP_EDITS = [
     ("    if (!blk.halo_pending) throw SyncError(\"halo completion without a pending exchange\");\n",
      "    if (!blk.halo_pending) throw SyncError(\"halo completion without a pending exchange\");\n"
      "    if (device_halo()) {\n"
+     "        const bool pushed = push_halo() && blk.push_ready;\n"
      "        std::vector<std::pair<Vec3i, const gpu::DeviceBlock*>> from;\n"
      "        for (const auto& n : decomp_.blocks[b].neighbors)\n"
-     "            from.emplace_back(n.offset, blocks_[n.block]->dev.get());\n"
-     "        blk.dev->fetch_slabs(from);  // every neighbour entry in one unpack launch\n"
+     "            if (!(pushed && n.block != b)) from.emplace_back(n.offset, blocks_[n.block]->dev.get());\n"
+     "        if (!from.empty()) blk.dev->fetch_slabs(from);  // all staged entries in one unpack launch\n"
+     "        if (pushed) blk.dev->push_wait();  // the neighbours' pushes of the previous step\n"
      "        blk.halo_pending = false;\n"
      "        return;\n"
      "    }\n"),
@@ -168,8 +208,26 @@ SIM_CPP_EDITS = [
     ("        blk.registry.build(blk.box, blk.snapshots, params_.subdivisions);\n"
      "        psm::build_fraction_field(blk.frac, blk.box, blk.registry, blk.snapshots,\n"
      "                                  params_.kernels == KernelMode::openmp);\n",
-     "        blk.dev->map(blk.snapshots, params_.subdivisions);\n"
+     "        if (blk.premapped && same_geometry(blk.premap, blk.snapshots))\n"
+     "            blk.dev->map_commit();  // mapped during the last sub-cycle\n"
+     "        else\n"
+     "            blk.dev->map(blk.snapshots, params_.subdivisions);\n"
+     "        blk.premapped = false;\n"
      "        blk.dev->sync();\n"),
+    # sim.cpp:623-628 - the next step's mapping issued once its inputs are final (premap_on())
+    ("        ScopedTimer t(blk.timings, Category::kPdComm);\n"
+     "        apply_particle_sync(blk, s);\n"
+     "    }\n",
+     "        ScopedTimer t(blk.timings, Category::kPdComm);\n"
+     "        apply_particle_sync(blk, s);\n"
+     "    }\n"
+     "    if (params_.coupling && premap_on() && s == params_.dem.subcycles - 1) {\n"
+     "        ScopedTimer t(blk.timings, Category::kMapping);\n"
+     "        build_snapshots(blk);\n"
+     "        blk.premap = blk.snapshots;\n"
+     "        blk.dev->map_prepare(blk.premap, params_.subdivisions);  // asynchronous, shadow field\n"
+     "        blk.premapped = true;\n"
+     "    }\n"),
     # sim.cpp:296-297 — set_solid_velocities on the device (post velocity-sync snapshots):
     # an asynchronous snapshot upload the PSM sweep evaluates u + omega x (c - x) from; it
     # raises SyncError itself when the exact per-entry walk finds unknown ids, so no sync here
@@ -192,6 +250,18 @@ SIM_CPP_EDITS = [
      "        blk.dev->apply_boundaries(params_.bc, blk.domain_faces);\n"
      "        ScopedTimer t(blk.timings, Category::kPsm);\n"
      "        run_kernel(blk, {{0, 0, 0}, {d.x, d.y, d.z}});\n"
+     "        if (device_halo() && push_halo()) {\n"
+     "            // the next step's halo leaves now, overlapping everything until then\n"
+     "            if (!blk.push_connected) {\n"
+     "                std::vector<std::pair<Vec3i, const gpu::DeviceBlock*>> to;\n"
+     "                for (const auto& n : decomp_.blocks[b].neighbors)\n"
+     "                    if (n.block != b) to.emplace_back(n.offset, blocks_[n.block]->dev.get());\n"
+     "                blk.dev->push_connect(to);\n"
+     "                blk.push_connected = true;\n"
+     "            }\n"
+     "            blk.dev->push_halo();\n"
+     "            blk.push_ready = true;\n"
+     "        }\n"
      "        blk.dev->sync();\n"
      "        blk.outer_done = true;\n"
      "    } else {\n"

@@ -100,6 +100,7 @@ struct BcArgs {
     int faces[6];  // processed faces in order
     int nfaces;
     long long fstart[7];
+    DeviceErrors* err;
 };
 
 // boundary.cpp:75-80
@@ -154,12 +155,12 @@ __global__ void __launch_bounds__(256) bc_fill_kernel(const BcArgs a) {
     const bool multi = multi_lo[0] || multi_lo[1] || multi_lo[2] || multi_hi[0] || multi_hi[1] ||
                        multi_hi[2];
     const int kind = a.kind[face];
-    const long long gi = L.idx(g[0], g[1], g[2]);
+    const long long gi = LBG_IDX(L.idx(g[0], g[1], g[2]), L.plane, a.err);
 #pragma unroll
     for (int q = 1; q < kQ; ++q) {
         const int s0 = g[0] + cx(q), s1 = g[1] + cy(q), s2 = g[2] + cz(q);
         if (!(s0 >= 0 && s0 < n[0] && s1 >= 0 && s1 < n[1] && s2 >= 0 && s2 < n[2])) continue;
-        const long long si = L.idx(s0, s1, s2);
+        const long long si = LBG_IDX(L.idx(s0, s1, s2), L.plane, a.err);
         const double out = a.src[opposite(q) * L.plane + si];
         double v;
         if (multi || kind == LBG_BC_NO_SLIP) {
@@ -187,6 +188,7 @@ using namespace lbg;
 extern "C" {
 
 lbg_status lbg_fill_periodic(lbg_block b, const int periodic[3], int full) {
+    if (lbg_status s_ = aa_refuse(b, "lbg_fill_periodic")) return s_;
     if (!b || !periodic) return set_error(LBG_INVALID, "null argument");
     if (!periodic[0] && !periodic[1] && !periodic[2]) return LBG_OK;
     LBG_CUDA(cudaSetDevice(b->device));
@@ -208,6 +210,7 @@ lbg_status lbg_fill_periodic(lbg_block b, const int periodic[3], int full) {
 }
 
 lbg_status lbg_apply_boundaries(lbg_block b, const lbg_face_bc faces[6], const int touches[6]) {
+    if (lbg_status s_ = aa_refuse(b, "lbg_apply_boundaries")) return s_;
     if (!b || !faces || !touches) return set_error(LBG_INVALID, "null argument");
     // BcSpec::validate (boundary.cpp:8-16)
     for (int axis = 0; axis < 3; ++axis) {
@@ -221,6 +224,7 @@ lbg_status lbg_apply_boundaries(lbg_block b, const lbg_face_bc faces[6], const i
     BcArgs a{};
     a.src = b->src();
     a.L = b->L;
+    a.err = b->err_d;
     const Layout& L = b->L;
     const int n[3] = {L.nx, L.ny, L.nz};
     a.fstart[0] = 0;

@@ -271,6 +271,7 @@ using namespace lbg;
 extern "C" {
 
 lbg_status lbg_observe(lbg_block b, const double f_ext[3], double out[6]) {
+    if (lbg_status s_ = aa_refuse(b, "lbg_observe", true)) return s_;
     if (!b || !out) return set_error(LBG_INVALID, "null argument");
     LBG_CUDA(cudaSetDevice(b->device));
     int sms = 148;
@@ -313,6 +314,7 @@ lbg_status lbg_observe(lbg_block b, const double f_ext[3], double out[6]) {
 }
 
 lbg_status lbg_moments(lbg_block b, int with_frac, double* out) {
+    if (lbg_status s_ = aa_refuse(b, "lbg_moments", true)) return s_;
     if (!b || !out) return set_error(LBG_INVALID, "null argument");
     LBG_CUDA(cudaSetDevice(b->device));
     const Layout& L = b->L;
@@ -339,7 +341,13 @@ lbg_status lbg_moments(lbg_block b, int with_frac, double* out) {
 }
 
 const char* lbg_last_error(void) { return g_last_error.c_str(); }
-const char* lbg_version(void) { return "lbg 0.1 (sm_100a)"; }
+const char* lbg_version(void) {
+#ifdef LBG_CHECKED
+    return "lbg 0.2 (sm_100a, checked)";
+#else
+    return "lbg 0.2 (sm_100a)";
+#endif
+}
 
 int lbg_device_count(void) {
     int n = 0;
@@ -445,6 +453,7 @@ lbg_status lbg_block_create(int device, const int box_lo[3], const int dims[3], 
 
 lbg_status lbg_comm_destroy(lbg_block b);  // lbg_halo.cu
 lbg_status lbg_p2p_destroy(lbg_block b);   // lbg_p2p.cu
+lbg_status lbg_halo_push_destroy(lbg_block b);  // lbg_push.cu
 
 lbg_status lbg_block_destroy(lbg_block b) {
     if (!b) return LBG_OK;
@@ -454,10 +463,12 @@ lbg_status lbg_block_destroy(lbg_block b) {
     if (b->aux) cudaStreamSynchronize(b->aux);
     if (b->comm) lbg_comm_destroy(b);
     if (b->p2p) lbg_p2p_destroy(b);
+    if (b->push) lbg_halo_push_destroy(b);
+    lbg::free_shadow(b);
     void* dev[] = {b->buf[0], b->buf[1], b->count, b->id0, b->id1, b->b0, b->b1, b->btot,
                    b->v0, b->v1, b->m0, b->m1, b->snaps_d, b->bin_count, b->bin_start,
                    b->bin_items, b->red_rows, b->red_used, b->err_d, b->facc, b->fused_used,
-                   b->obs_d, b->mom_d, b->seg_list, b->seg_n, b->snap_tab, b->red_box, b->pidx0};
+                   b->obs_d, b->mom_d, b->seg_list, b->seg_n, b->snap_tab, b->red_box, b->pidx0, b->wcount};
     for (void* p : dev)
         if (p) cudaFree(p);
     void* host[] = {b->snaps_h, b->err_h, b->red_rows_h, b->red_used_h, b->obs_h};
@@ -594,10 +605,35 @@ static lbg_status copy_pdf(lbg_block b, double* dev, const double* host_in, doub
     return LBG_OK;
 }
 
-lbg_status lbg_upload_src(lbg_block b, const double* host) { return copy_pdf(b, b->src(), host, nullptr); }
-lbg_status lbg_download_src(lbg_block b, double* host) { return copy_pdf(b, b->src(), nullptr, host); }
-lbg_status lbg_upload_dst(lbg_block b, const double* host) { return copy_pdf(b, b->dst(), host, nullptr); }
-lbg_status lbg_download_dst(lbg_block b, double* host) { return copy_pdf(b, b->dst(), nullptr, host); }
+lbg_status lbg_upload_src(lbg_block b, const double* host) {
+    if (b && b->aa) {  // an AA block takes the double-buffer src as its state S0
+        b->aa_phase = 0;
+        b->aa_pending = false;
+    }
+    return copy_pdf(b, b->src(), host, nullptr);
+}
+lbg_status lbg_download_src(lbg_block b, double* host) {
+    if (b && b->aa && b->aa_phase == 1) {  // S1: the S0 image (post-collision, unstreamed) first
+        LBG_CUDA(cudaSetDevice(b->device));
+        double* tmp = nullptr;
+        const size_t bytes = sizeof(double) * (kQ * (size_t)b->L.plane + 128);
+        LBG_CUDA(cudaMallocAsync(&tmp, bytes, b->stream));
+        LBG_CUDA(cudaMemsetAsync(tmp, 0, bytes, b->stream));
+        lbg_status s = aa_unstream(b, tmp);
+        if (s == LBG_OK) s = copy_pdf(b, tmp, nullptr, host);
+        cudaFreeAsync(tmp, b->stream);
+        return s;
+    }
+    return copy_pdf(b, b->src(), nullptr, host);
+}
+lbg_status lbg_upload_dst(lbg_block b, const double* host) {
+    if (lbg_status s_ = aa_refuse(b, "lbg_upload_dst")) return s_;
+    return copy_pdf(b, b->dst(), host, nullptr);
+}
+lbg_status lbg_download_dst(lbg_block b, double* host) {
+    if (lbg_status s_ = aa_refuse(b, "lbg_download_dst")) return s_;
+    return copy_pdf(b, b->dst(), nullptr, host);
+}
 
 lbg_status lbg_set_periodic_wrap(lbg_block b, const int wrap[3]) {
     if (!b || !wrap) return set_error(LBG_INVALID, "null argument");
@@ -606,11 +642,20 @@ lbg_status lbg_set_periodic_wrap(lbg_block b, const int wrap[3]) {
 }
 
 lbg_status lbg_swap(lbg_block b) {
+    if (b->aa) {  // in place: the swap completes the AA step (state S0 <-> S1)
+        if (b->aa_pending) b->aa_phase ^= 1;
+        b->aa_pending = false;
+        return LBG_OK;
+    }
     b->cur ^= 1;
     return LBG_OK;
 }
 
 lbg_status lbg_fill_equilibrium(lbg_block b, double rho, const double u[3]) {
+    if (b->aa) {  // writes the src state: S0
+        b->aa_phase = 0;
+        b->aa_pending = false;
+    }
     Feq f;
     equilibrium_host(rho, u, f.v);
     const Layout& L = b->L;
@@ -622,6 +667,10 @@ lbg_status lbg_fill_equilibrium(lbg_block b, double rho, const double u[3]) {
 }
 
 lbg_status lbg_init_shear_wave(lbg_block b, const int domain[3]) {
+    if (b->aa) {  // writes the src state: S0
+        b->aa_phase = 0;
+        b->aa_pending = false;
+    }
     const Layout& L = b->L;
     LBG_CUDA(cudaSetDevice(b->device));
     dim3 grid((L.nx + 127) / 128, L.ny, L.nz);
@@ -653,6 +702,12 @@ lbg_status lbg_sync(lbg_block b, lbg_errors* out) {
         out->overfull_cells = (long long)e.overfull;
         out->unknown_ids = (long long)e.unknown;
     }
+    if (e.oob > 0)
+        return set_error(LBG_CUDA_ERROR, "checked build: " + std::to_string(e.oob) +
+                                             " out-of-range buffer indices (accesses skipped)");
+    if (e.race > 0)
+        return set_error(LBG_CUDA_ERROR, "checked build: " + std::to_string(e.race) +
+                                             " cells written other than exactly once by a sweep");
     if (e.p2p_timeout > 0)
         return set_error(LBG_CUDA_ERROR, "P2P halo: neighbour did not publish its step (wait timed out)");
     if (e.overfull > 0)
@@ -711,6 +766,7 @@ static lbg_status moments(lbg_block b, double out[4]) {
 }
 
 lbg_status lbg_total_mass(lbg_block b, double* out) {
+    if (lbg_status s_ = aa_refuse(b, "lbg_total_mass", true)) return s_;
     double m[4];
     lbg_status s = moments(b, m);
     if (s == LBG_OK) *out = m[0];
@@ -718,6 +774,7 @@ lbg_status lbg_total_mass(lbg_block b, double* out) {
 }
 
 lbg_status lbg_total_momentum(lbg_block b, double out[3]) {
+    if (lbg_status s_ = aa_refuse(b, "lbg_total_momentum", true)) return s_;
     double m[4];
     lbg_status s = moments(b, m);
     if (s == LBG_OK)

@@ -208,6 +208,7 @@ lbg_status lbg_comm_unique_id(char out[128]) {
 
 lbg_status lbg_comm_init(lbg_block b, int nranks, int rank, const char id[128], int axis,
                          const int periodic[3]) {
+    if (lbg_status s_ = aa_refuse(b, "lbg_comm_init")) return s_;
     if (!b) return set_error(LBG_INVALID, "null block");
     if (axis < 0 || axis > 2 || nranks < 1 || rank < 0 || rank >= nranks)
         return set_error(LBG_INVALID, "bad comm arguments");
@@ -397,14 +398,17 @@ lbg_status note_consumed(lbg_block dst, const lbg_block* srcs, int n) {
 extern "C" {
 
 lbg_status lbg_pack_slab(lbg_block b, const int off[3], double* out, long long capacity, long long* n_out) {
+    if (lbg_status s_ = aa_refuse(b, "lbg_pack_slab")) return s_;
     return slab_io(b, off, false, out, capacity, n_out, true);
 }
 
 lbg_status lbg_unpack_slab(lbg_block b, const int dir[3], const double* in, long long n) {
+    if (lbg_status s_ = aa_refuse(b, "lbg_unpack_slab")) return s_;
     return slab_io(b, dir, true, const_cast<double*>(in), n, nullptr, false);
 }
 
 lbg_status lbg_halo_stage(lbg_block b, const int (*offs)[3], int n) {
+    if (lbg_status s_ = aa_refuse(b, "lbg_halo_stage")) return s_;
     using namespace lbg;
     if (!b || (n > 0 && !offs)) return set_error(LBG_INVALID, "null argument");
     LBG_CUDA(cudaSetDevice(b->device));

@@ -70,7 +70,28 @@ struct DeviceErrors {
     unsigned long long overfull;
     unsigned long long unknown;
     unsigned long long p2p_timeout;  // lbg_p2p.cu wait gave up
+    unsigned long long oob;          // checked build: an index outside its buffer (access skipped)
+    unsigned long long race;         // checked build: a cell written != once by one sweep
 };
+
+// Checked build (make checked, -DLBG_CHECKED): the hot kernels check every computed index
+// against its buffer (an out-of-range one is counted and redirected to element 0, so the run
+// goes on and lbg_sync reports it) and every sweep counts the cells it writes (each cell of
+// the swept box exactly once across all the kernels of the sweep: K12 || two-entry K2, K1 ||
+// K2, ... — a double write is a race between them, a missing one a hole). compute-sanitizer is
+// closed on the GPU pool; this is the repository's own memcheck/racecheck substitute.
+#ifdef LBG_CHECKED
+#define LBG_IDX(idx, limit, err) ::lbg::checked_idx((long long)(idx), (long long)(limit), (err))
+#else
+#define LBG_IDX(idx, limit, err) (idx)
+#endif
+__device__ __forceinline__ long long checked_idx(long long idx, long long limit, DeviceErrors* err) {
+    if (idx < 0 || idx >= limit) {
+        atomicAdd(&err->oob, 1ull);
+        return 0;
+    }
+    return idx;
+}
 
 struct TimedSpan {
     int cat;
@@ -104,8 +125,38 @@ struct SnapIndex {
     }
 };
 
+// The state one mapping produces (the fraction field, its segment lists, the snapshot list it
+// was mapped from with its index, and the host bookkeeping about that list). lbg_map_prepare
+// maps into a shadow copy while the block keeps using (and observers keep seeing) the current
+// one; lbg_map_commit swaps the two by pointer.
+struct MapState {
+    uint8_t* count = nullptr;
+    int* id0 = nullptr;
+    int* id1 = nullptr;
+    int* pidx0 = nullptr;
+    double* b0 = nullptr;
+    double* b1 = nullptr;
+    double* btot = nullptr;
+    unsigned* seg_list = nullptr;
+    int* seg_n = nullptr;
+    lbg_snapshot* snaps_d = nullptr;
+    int snaps_dcap = 0;
+    int n_snaps = 0;
+    int* snap_tab = nullptr;
+    long long snap_tab_cap = 0;
+    int snap_id_min = 0;
+    int snap_range = 0;
+    std::vector<int> map_ids;
+    std::vector<lbg_snapshot> map_snaps;
+    bool map_ids_valid = false;
+    bool v_snap = false;
+    bool p_direct = false;
+    bool cov_dirty = true;
+};
+
 struct Comm;  // lbg_halo.cu
 struct P2P;   // lbg_p2p.cu
+struct Push;  // lbg_push.cu
 
 }  // namespace lbg
 
@@ -163,12 +214,15 @@ struct lbg_block_s {
     // particle snapshots: pinned staging + device copy (H2D on the side stream)
     lbg_snapshot* snaps_h = nullptr;
     lbg_snapshot* snaps_d = nullptr;
-    int snaps_cap = 0;
+    int snaps_cap = 0;   // pinned staging
+    int snaps_dcap = 0;  // device list
     int n_snaps = 0;
     int* snap_tab = nullptr;  // dense id -> index table (SnapIndex)
     long long snap_tab_cap = 0;
     int snap_id_min = 0;
     int snap_range = 0;  // 0: no table (sparse ids)
+    lbg::MapState* shadow = nullptr;  // lbg_map_prepare's target
+    bool prepared = false;
     // device binning for the mapping kernel (lbg_psm.cu)
     int* bin_count = nullptr;
     int* bin_start = nullptr;
@@ -189,6 +243,7 @@ struct lbg_block_s {
     cudaEvent_t ev_red = nullptr;
 
     lbg::DeviceErrors* err_d = nullptr;
+    int* wcount = nullptr;  // checked build: per-cell write counts of the current sweep
     lbg::DeviceErrors* err_h = nullptr;  // pinned
 
     cudaStream_t stream = nullptr;  // compute
@@ -207,6 +262,7 @@ struct lbg_block_s {
 
     lbg::Comm* comm = nullptr;
     lbg::P2P* p2p = nullptr;
+    lbg::Push* push = nullptr;
     long long device_bytes = 0;
     double* obs_d = nullptr;  // observer partials (lbg_observe)
     double* obs_h = nullptr;
@@ -234,12 +290,23 @@ struct lbg_block_s {
     cudaEvent_t ev_copy[2] = {nullptr, nullptr};
     cudaEvent_t ev_done[2] = {nullptr, nullptr};
 
+    // AA in-place streaming (lbg_aa.cu): one buffer (buf[cur]); aa_phase 0: state S0 (the
+    // double-buffer src), 1: S1 (streamed, slots swapped); aa_pending: swept, not yet swapped
+    bool aa = false;
+    int aa_phase = 0;
+    bool aa_pending = false;
+
     double* src() const { return buf[cur]; }
     double* dst() const { return buf[cur ^ 1]; }
 };
 
 namespace lbg {
 
+// AA streaming (lbg_aa.cu): one step of the in-place sweep; the S0 image of an S1 buffer
+lbg_status aa_sweep(lbg_block b, const lbg_fluid* fl);
+lbg_status aa_unstream(lbg_block b, double* out);
+// frees the shadow mapping state of lbg_map_prepare (lbg_psm.cu)
+void free_shadow(lbg_block b);
 // covered-cell counts and segment lists rebuilt from `count` (lbg_psm.cu)
 lbg_status rebuild_covered(lbg_block b);
 // the block's current snapshot index
@@ -264,6 +331,14 @@ __device__ __forceinline__ void warp_append(bool pred, unsigned v, unsigned* lis
 lbg_status set_error(lbg_status s, const std::string& msg);
 lbg_status cuda_check(cudaError_t e, const char* what);
 void count_launch();
+// operations defined on the double-buffered layout refuse an AA block (`state1`: only while it
+// holds the streamed state S1)
+inline lbg_status aa_refuse(lbg_block b, const char* what, bool state1 = false) {
+    if (b && b->aa && (!state1 || b->aa_phase == 1))
+        return set_error(LBG_INVALID, std::string(what) + ": not available on an AA-streaming block" +
+                                          (state1 ? " after an odd number of steps" : ""));
+    return LBG_OK;
+}
 
 // Grow-only device buffer: holds at least `need` elements afterwards (`want` when it has to
 // grow, for geometric growth). The old buffer is freed first; on failure the pointer is null

@@ -222,6 +222,7 @@ lbg_status lbg_p2p_handles(lbg_block b, void* out, size_t* bytes) {
 }
 
 lbg_status lbg_p2p_connect(lbg_block b, int nranks, int rank, const void* all, int axis, const int periodic[3]) {
+    if (lbg_status s_ = aa_refuse(b, "lbg_p2p_connect")) return s_;
     if (!b || !all || !periodic) return set_error(LBG_INVALID, "null argument");
     if (axis < 0 || axis > 2 || nranks < 2 || rank < 0 || rank >= nranks)
         return set_error(LBG_INVALID, "p2p halo needs >= 2 ranks and a slab axis");

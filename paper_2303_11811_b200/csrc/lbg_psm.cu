@@ -158,6 +158,8 @@ struct MapArgs {
     double* __restrict__ b1;
     double* __restrict__ btot;
     DeviceErrors* err;
+    long long items_cap;
+    long long cells;
 };
 
 // K3 mapping (psm.cpp:28-32 overlap_fraction, psm.cpp:93-136 per-cell entry rule): one warp
@@ -190,7 +192,7 @@ struct MapCand {
 __device__ __forceinline__ void stage_cands(const MapArgs& a, const int* list, int base, int m, int lane,
                                             MapCand& sc) {
     if (lane < m) {
-        const int ix = list[base + lane];
+        const int ix = list[LBG_IDX((list - a.items) + base + lane, a.items_cap, a.err) - (list - a.items)];
         const lbg_snapshot& p = a.s[ix];
         sc.idx[lane] = ix;
         sc.x0[lane] = p.x[0];
@@ -231,7 +233,7 @@ __global__ void __launch_bounds__(32 * kMapWarps) map_warp_kernel(const MapArgs 
         const int k = bz * kBin + zz;
         if (k >= g.dims[2]) break;  // warp-uniform
         const double cc2 = (double)(g.lo[2] + k) + 0.5;
-        const long long c = ((long long)k * g.dims[1] + j) * g.dims[0] + i;
+        const long long c = inxy ? LBG_IDX(((long long)k * g.dims[1] + j) * g.dims[0] + i, a.cells, a.err) : 0;
         int cnt = 0;
         double sum = 0.0;
         bool over = false;
@@ -402,8 +404,8 @@ __device__ __forceinline__ void nm_add(double& sum, double& comp, double v) {  /
 //   box source: the snapshot's reach (r + max(1/2, f_r), the mapping's candidate test) when
 //   the fraction field was mapped from these positions; otherwise entry_box_kernel takes the
 //   min/max cell of every particle's entries from the field itself (order-independent).
-constexpr int kWalkWarps = 4;
-constexpr int kWalkBuf = 128;  // staged terms per warp: flushed at >= 32, a step adds <= 128
+constexpr int kWalkWarps = 8;
+constexpr int kWalkKeys = 1024;  // entry keys staged per warp before a replay flush
 
 struct WalkArgs {
     const lbg_snapshot* __restrict__ s;
@@ -418,35 +420,88 @@ struct WalkArgs {
     double* __restrict__ rows;
     int* __restrict__ used;
     int fast;
+    DeviceErrors* err;
+    long long cells;
 };
 
-__device__ __forceinline__ void nm_replay(double (*terms)[7], int nbuf, int lane, bool fast, double& sum,
-                                          double& comp) {
-    if (lane < 6) {
-        for (int e = 0; e < nbuf; ++e) {
-            const double v = terms[e][lane];
-            if (fast)
-                sum += v;
-            else
-                nm_add(sum, comp, v);
-        }
-    }
-    __syncwarp();
+// vec3.hpp:75-82 without a branch: the larger-magnitude operand first, as the reference's if
+__device__ __forceinline__ void nm_add_sel(double& sum, double& comp, double v) {
+    const double t = sum + v;
+    const bool a = fabs(sum) >= fabs(v);
+    const double big = a ? sum : v, small = a ? v : sum;
+    comp += (big - t) + small;
+    sum = t;
 }
 
-// the walk's per-lane state: two consecutive box cells (t, t + 1) with their cell fields
-struct WalkCells {
-    long long c[2];
-    int i[2], j[2], k[2];
-    int cnt[2], e0[2], e1[2];
-};
+// replay of staged keys kb[0, nk): 32 entries per batch (m gathered one batch ahead, zeroed as
+// consumed), their six terms into the warp's tile, lanes 0..5 add them in entry order
+__device__ __forceinline__ void walk_flush(const WalkArgs& a, const unsigned* kb, int nk, double (*tw)[7],
+                                           int lane, double x0, double x1, double x2, double& sum, double& comp) {
+    const BinGeom& g = a.g;
+    auto gather = [&](int base, long long& c, double (&m)[3]) {
+        c = -1;
+        m[0] = m[1] = m[2] = 0.0;
+        if (base + lane < nk) {
+            const unsigned key = kb[base + lane];
+            c = LBG_IDX((long long)(key >> 1), a.cells, a.err);
+            double* mp = ((key & 1u) ? a.m1 : a.m0) + 3 * c;
+            m[0] = mp[0];
+            m[1] = mp[1];
+            m[2] = mp[2];
+            c = (c << 1) | (key & 1u);
+        }
+    };
+    long long c;
+    double m[3];
+    gather(0, c, m);
+    for (int base = 0; base < nk; base += 32) {
+        const int nb = min(32, nk - base);
+        if (c >= 0) {
+            const long long cell = c >> 1;
+            const int ci = (int)(cell % g.dims[0]), cj = (int)((cell / g.dims[0]) % g.dims[1]),
+                      ck = (int)(cell / ((long long)g.dims[0] * g.dims[1]));
+            const double r0 = ((double)(g.lo[0] + ci) + 0.5) - x0;
+            const double r1 = ((double)(g.lo[1] + cj) + 0.5) - x1;
+            const double r2 = ((double)(g.lo[2] + ck) + 0.5) - x2;
+            tw[lane][0] = m[0];
+            tw[lane][1] = m[1];
+            tw[lane][2] = m[2];
+            tw[lane][3] = r1 * m[2] - r2 * m[1];
+            tw[lane][4] = r2 * m[0] - r0 * m[2];
+            tw[lane][5] = r0 * m[1] - r1 * m[0];
+            double* mp = ((c & 1) ? a.m1 : a.m0) + 3 * cell;  // psm.cpp:305: the entry is cleared
+            mp[0] = 0.0;
+            mp[1] = 0.0;
+            mp[2] = 0.0;
+        }
+        __syncwarp();
+        gather(base + 32, c, m);  // the next batch's momenta in flight during the replay
+        if (lane < 6) {
+#pragma unroll 4
+            for (int e = 0; e < nb; ++e) {
+                const double v = tw[e][lane];
+                if (a.fast)
+                    sum += v;
+                else
+                    nm_add_sel(sum, comp, v);
+            }
+        }
+        __syncwarp();
+    }
+}
 
+// One warp per particle. Pass 1 walks the box (32 cells per step, the next step's cell fields
+// in flight) and stages the keys (cell << 1 | entry) of the particle's entries in walk order —
+// only count and ids are read; pass 2 (a flush whenever the key stage fills, and at the end)
+// gathers the momenta 32 at a time and replays them.
 __global__ void __launch_bounds__(32 * kWalkWarps) walk_chain_kernel(const WalkArgs a) {
-    __shared__ double terms_all[kWalkWarps][kWalkBuf + 32][7];
+    __shared__ unsigned keys_all[kWalkWarps][kWalkKeys];
+    __shared__ double terms_all[kWalkWarps][32][7];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int p = blockIdx.x * kWalkWarps + w;
     if (p >= a.n) return;  // warp-uniform
-    double (*terms)[7] = terms_all[w];
+    unsigned* kb = keys_all[w];
+    double (*tw)[7] = terms_all[w];
     const BinGeom& g = a.g;
     const lbg_snapshot& sp = a.s[p];
     const int id = sp.id;
@@ -473,90 +528,58 @@ __global__ void __launch_bounds__(32 * kWalkWarps) walk_chain_kernel(const WalkA
     if (hi[0] >= lo[0] && hi[1] >= lo[1] && hi[2] >= lo[2]) {
         const int ex = hi[0] - lo[0] + 1, ey = hi[1] - lo[1] + 1;
         const long long total = (long long)ex * ey * (hi[2] - lo[2] + 1);
-        int nbuf = 0;
-        // 64 box cells per step (two per lane), the next step's cell fields in flight
-        auto fetch = [&](long long base, WalkCells& w2) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const long long t = base + 2 * lane + h;
-                w2.cnt[h] = 0;
-                w2.c[h] = 0;
-                if (t < total) {
-                    const long long r = t / ex;
-                    w2.i[h] = lo[0] + (int)(t - r * ex);
-                    w2.j[h] = lo[1] + (int)(r % ey);
-                    w2.k[h] = lo[2] + (int)(r / ey);
-                    const long long c = ((long long)w2.k[h] * g.dims[1] + w2.j[h]) * g.dims[0] + w2.i[h];
-                    w2.c[h] = c;
-                    w2.cnt[h] = a.count[c];
-                    w2.e0[h] = a.id0[c];
-                    w2.e1[h] = a.id1[c];
+        const unsigned lt = (1u << lane) - 1u;
+        struct Cell {
+            long long c;
+            int cnt, e0, e1;
+        };
+        auto fetch = [&](long long t, Cell& f) {
+            f.cnt = 0;
+            f.c = 0;
+            f.e0 = f.e1 = -1;
+            if (t < total) {
+                const long long r = t / ex;
+                const int i = lo[0] + (int)(t - r * ex), j = lo[1] + (int)(r % ey), k = lo[2] + (int)(r / ey);
+                f.c = LBG_IDX(((long long)k * g.dims[1] + j) * g.dims[0] + i, a.cells, a.err);
+                f.cnt = a.count[f.c];
+                f.e0 = a.id0[f.c];
+                f.e1 = a.id1[f.c];
+            }
+        };
+        int nk = 0;
+        // one step of the walk on `use`; `ahead` receives the fields two steps on. The three
+        // register sets rotate roles through the unrolled loop, so no in-flight load is ever
+        // copied (a copy would wait for it)
+        auto step = [&](long long base, const Cell& use, Cell& ahead) {
+            fetch(base + 64 + lane, ahead);
+            const bool h0 = use.cnt >= 1 && use.e0 == id, h1 = use.cnt >= 2 && use.e1 == id;
+            const unsigned b0 = __ballot_sync(0xffffffffu, h0), b1 = __ballot_sync(0xffffffffu, h1);
+            if (b0 | b1) {
+                any = true;
+                const int s0 = nk + __popc(b0 & lt) + __popc(b1 & lt);
+                if (h0) kb[LBG_IDX(s0, kWalkKeys, a.err)] = (unsigned)(use.c << 1);
+                if (h1) kb[LBG_IDX(s0 + (h0 ? 1 : 0), kWalkKeys, a.err)] = (unsigned)((use.c << 1) | 1);
+                nk += __popc(b0) + __popc(b1);
+                if (nk > kWalkKeys - 64) {
+                    __syncwarp();
+                    walk_flush(a, kb, nk, tw, lane, x0, x1, x2, sum, comp);
+                    nk = 0;
                 }
             }
         };
-        WalkCells cur, nxt;
-        fetch(0, cur);
-        for (long long base = 0; base < total; base += 64) {
-            fetch(base + 64, nxt);
-            bool h0[2], h1[2];
-            int mine = 0;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                h0[h] = cur.cnt[h] >= 1 && cur.e0[h] == id;
-                h1[h] = cur.cnt[h] >= 2 && cur.e1[h] == id;
-                mine += (int)h0[h] + (int)h1[h];
-            }
-            // entries before this lane's cells: exclusive warp scan (walk order = lane order)
-            int incl = mine;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
-            }
-            const int step_total = __shfl_sync(0xffffffffu, incl, 31);
-            if (step_total > 0) {
-                any = true;
-                double mv[2][2][3];
-#pragma unroll
-                for (int h = 0; h < 2; ++h)
-#pragma unroll
-                    for (int d = 0; d < 3; ++d) {
-                        mv[h][0][d] = h0[h] ? a.m0[3 * cur.c[h] + d] : 0.0;
-                        mv[h][1][d] = h1[h] ? a.m1[3 * cur.c[h] + d] : 0.0;
-                    }
-                int slot = nbuf + incl - mine;
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const double r0 = ((double)(g.lo[0] + cur.i[h]) + 0.5) - x0;
-                    const double r1 = ((double)(g.lo[1] + cur.j[h]) + 0.5) - x1;
-                    const double r2 = ((double)(g.lo[2] + cur.k[h]) + 0.5) - x2;
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        if (!(e == 0 ? h0[h] : h1[h])) continue;
-                        const double* m = mv[h][e];
-                        double* t = terms[slot++];
-                        t[0] = m[0];
-                        t[1] = m[1];
-                        t[2] = m[2];
-                        t[3] = r1 * m[2] - r2 * m[1];
-                        t[4] = r2 * m[0] - r0 * m[2];
-                        t[5] = r0 * m[1] - r1 * m[0];
-                        double* z = (e == 0 ? a.m0 : a.m1) + 3 * cur.c[h];  // psm.cpp:305
-                        z[0] = 0.0;
-                        z[1] = 0.0;
-                        z[2] = 0.0;
-                    }
-                }
-                nbuf += step_total;
-                __syncwarp();
-                if (nbuf >= 32) {
-                    nm_replay(terms, nbuf, lane, a.fast, sum, comp);
-                    nbuf = 0;
-                }
-            }
-            cur = nxt;
+        Cell A, B, Cc;
+        fetch(lane, A);
+        fetch(32 + lane, B);
+        for (long long base = 0;;) {
+            step(base, A, Cc);
+            if ((base += 32) >= total) break;
+            step(base, B, A);
+            if ((base += 32) >= total) break;
+            step(base, Cc, B);
+            if ((base += 32) >= total) break;
         }
-        nm_replay(terms, nbuf, lane, a.fast, sum, comp);
+        __syncwarp();
+        walk_flush(a, kb, nk, tw, lane, x0, x1, x2, sum, comp);
     }
     if (lane < 6) {
         const int slot = lane < 3 ? lane : 6 + (lane - 3);
@@ -621,9 +644,13 @@ static lbg_status upload_snapshots(lbg_block b, const lbg_snapshot* snaps, int n
         const int cap = std::max(n, 2 * b->snaps_cap);
         b->snaps_cap = 0;
         LBG_CUDA(cudaMallocHost(&b->snaps_h, sizeof(lbg_snapshot) * cap));
-        int dcap = 0;
-        if (lbg_status s = grow_device(b->snaps_d, dcap, cap, cap, "cudaMalloc(snapshots)")) return s;
         b->snaps_cap = cap;
+    }
+    if (n > b->snaps_dcap || !b->snaps_d) {
+        LBG_CUDA(cudaStreamSynchronize(b->stream));
+        if (lbg_status s = grow_device(b->snaps_d, b->snaps_dcap, std::max(n, 1), std::max(b->snaps_cap, 1),
+                                       "cudaMalloc(snapshots)"))
+            return s;
     }
     // staging buffer may still feed the previous copy
     LBG_CUDA(cudaEventSynchronize(b->ev_side));
@@ -676,6 +703,66 @@ lbg_status rebuild_covered(lbg_block b) {
     return LBG_OK;
 }
 
+// the block's mapping state <-> the shadow (pointer swaps only)
+void swap_map_state(lbg_block b) {
+    MapState& m = *b->shadow;
+    std::swap(b->count, m.count);
+    std::swap(b->id0, m.id0);
+    std::swap(b->id1, m.id1);
+    std::swap(b->pidx0, m.pidx0);
+    std::swap(b->b0, m.b0);
+    std::swap(b->b1, m.b1);
+    std::swap(b->btot, m.btot);
+    std::swap(b->seg_list, m.seg_list);
+    std::swap(b->seg_n, m.seg_n);
+    std::swap(b->snaps_d, m.snaps_d);
+    std::swap(b->snaps_dcap, m.snaps_dcap);
+    std::swap(b->n_snaps, m.n_snaps);
+    std::swap(b->snap_tab, m.snap_tab);
+    std::swap(b->snap_tab_cap, m.snap_tab_cap);
+    std::swap(b->snap_id_min, m.snap_id_min);
+    std::swap(b->snap_range, m.snap_range);
+    std::swap(b->map_ids, m.map_ids);
+    std::swap(b->map_snaps, m.map_snaps);
+    std::swap(b->map_ids_valid, m.map_ids_valid);
+    std::swap(b->v_snap, m.v_snap);
+    std::swap(b->p_direct, m.p_direct);
+    std::swap(b->cov_dirty, m.cov_dirty);
+}
+
+lbg_status ensure_shadow(lbg_block b) {
+    if (b->shadow) return LBG_OK;
+    auto* m = new MapState;
+    b->shadow = m;
+    const size_t n = (size_t)b->L.nx * b->L.ny * b->L.nz + 64;
+    struct A {
+        void** p;
+        size_t bytes;
+    } allocs[] = {{(void**)&m->count, n},     {(void**)&m->id0, n * 4}, {(void**)&m->id1, n * 4},
+                  {(void**)&m->pidx0, n * 4}, {(void**)&m->b0, n * 8},  {(void**)&m->b1, n * 8},
+                  {(void**)&m->btot, n * 8},  {(void**)&m->seg_list, sizeof(unsigned) * (size_t)b->seg_cap},
+                  {(void**)&m->seg_n, 2 * sizeof(int)}};
+    for (auto& a : allocs) {
+        LBG_CUDA(cudaMalloc(a.p, a.bytes));
+        LBG_CUDA(cudaMemset(*a.p, 0, a.bytes));
+        b->device_bytes += (long long)a.bytes;
+    }
+    LBG_CUDA(cudaMemset(m->id0, 0xff, n * 4));  // FractionField::resize (field.cpp:37-46)
+    LBG_CUDA(cudaMemset(m->id1, 0xff, n * 4));
+    return LBG_OK;
+}
+
+void free_shadow(lbg_block b) {
+    MapState* m = b->shadow;
+    if (!m) return;
+    void* dev[] = {m->count, m->id0, m->id1, m->pidx0, m->b0, m->b1, m->btot, m->seg_list, m->seg_n,
+                   m->snaps_d, m->snap_tab};
+    for (void* p : dev)
+        if (p) cudaFree(p);
+    delete m;
+    b->shadow = nullptr;
+}
+
 }  // namespace lbg
 
 using namespace lbg;
@@ -718,6 +805,7 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
     if (lbg_status s = need_coupling(b)) return s;
     if (subdivisions < 1) return set_error(LBG_CONFIG_ERROR, "subdivisions must be >= 1");
     LBG_CUDA(cudaSetDevice(b->device));
+    b->prepared = false;
     Span span(b, LBG_CAT_MAPPING);
     if (lbg_status s = upload_snapshots(b, snaps, n)) return s;
     if (lbg_status s = prepare_fused(b, n)) return s;
@@ -772,6 +860,8 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
         a.b1 = b->b1;
         a.btot = b->btot;
         a.err = b->err_d;
+        a.items_cap = b->bin_items_cap;
+        a.cells = cells;
         // count and btot of every cell were zeroed by map_zero_kernel, so the mapping kernel
         // skips bins without candidates and writes only covered cells
         const long long units = 2 * nbins;
@@ -807,6 +897,29 @@ static lbg_status run_setu(lbg_block b) {
 static lbg_status materialize_velocity(lbg_block b) {
     if (!b->v_snap) return LBG_OK;
     return run_setu(b);
+}
+
+lbg_status lbg_map_prepare(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisions) {
+    if (lbg_status s = need_coupling(b)) return s;
+    LBG_CUDA(cudaSetDevice(b->device));
+    if (lbg_status s = ensure_shadow(b)) return s;
+    b->prepared = false;
+    swap_map_state(b);  // map into the shadow; the current state stays in use meanwhile
+    const lbg_status st = lbg_map(b, snaps, n, subdivisions);
+    swap_map_state(b);
+    if (st != LBG_OK) return st;
+    b->prepared = true;
+    return LBG_OK;
+}
+
+lbg_status lbg_map_commit(lbg_block b) {
+    if (lbg_status s = need_coupling(b)) return s;
+    if (!b->prepared) return set_error(LBG_INVALID, "lbg_map_commit without lbg_map_prepare");
+    // later work on the stream uses the new state; in-flight work holds the old pointers, and
+    // the old state is only written again by the next prepare (stream order)
+    swap_map_state(b);
+    b->prepared = false;
+    return LBG_OK;
 }
 
 lbg_status lbg_set_solid_velocities(lbg_block b, const lbg_snapshot* snaps, int n) {
@@ -937,6 +1050,8 @@ lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int c
         a.rows = b->red_rows;
         a.used = b->red_used;
         a.fast = mode == LBG_REDUCE_FAST;
+        a.err = b->err_d;
+        a.cells = cells;
         if (!reach_ok) {
             if (std::max(n, 1) > b->red_box_cap || !b->red_box) {
                 const int cap = std::max(std::max(n, 1), 2 * b->red_box_cap);

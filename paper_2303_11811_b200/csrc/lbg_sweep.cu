@@ -79,7 +79,16 @@ struct SweepArgs {
     int blo[8][3];
     int bext[8][3];
     long long bstart[9];
+    int* wc;          // checked build: per-cell write counts
+    long long cells;  // interior cells (field length)
 };
+
+// checked build: the cell (i, j, k) was written by this sweep
+__device__ __forceinline__ void mark_write(const SweepArgs& a, int i, int j, int k) {
+#ifdef LBG_CHECKED
+    atomicAdd(&a.wc[LBG_IDX(a.L.frac(i, j, k), a.cells, a.err)], 1);
+#endif
+}
 
 // pull the 19 populations of cell (i,j,k), wrapping periodic axes in-kernel
 __device__ __forceinline__ void pull(const SweepArgs& a, int i, int j, int k, long long base,
@@ -97,7 +106,7 @@ __device__ __forceinline__ void pull(const SweepArgs& a, int i, int j, int k, lo
         const long long corr = (cx(q) == 1 ? xl : (cx(q) == -1 ? xh : 0)) +
                                (cy(q) == 1 ? yl : (cy(q) == -1 ? yh : 0)) +
                                (cz(q) == 1 ? zl : (cz(q) == -1 ? zh : 0));
-        f[q] = a.src[q * L.plane + base - L.shift(q) + corr];
+        f[q] = a.src[q * L.plane + LBG_IDX(base - L.shift(q) + corr, L.plane, a.err)];
     }
 }
 
@@ -107,12 +116,13 @@ __device__ __forceinline__ bool srt_cell_at(const SweepArgs& a, int i, int j, in
     if constexpr (kSkipCovered) {
         if (a.count[a.L.frac(i, j, k)] != 0) return true;
     }
-    const long long base = a.L.idx(i, j, k);
+    const long long base = LBG_IDX(a.L.idx(i, j, k), a.L.plane, a.err);
     double f[kQ];
     pull(a, i, j, k, base, f);
     const bool ok = srt_cell<kForced>(f, a.inv_tau, a.F);
 #pragma unroll
     for (int q = 0; q < kQ; ++q) a.dst[q * a.L.plane + base] = f[q];
+    mark_write(a, i, j, k);
     return ok;
 }
 
@@ -284,7 +294,9 @@ __global__ void __launch_bounds__(256, 2) sweep_pair_kernel(const SweepArgs a) {
     }
     const bool okA = srt_cell<kForced>(fa, a.inv_tau, a.F);
     const bool okB = srt_cell<kForced>(fb, a.inv_tau, a.F);
-    double* d = a.dst + base;
+    double* d = a.dst + LBG_IDX(base, L.plane, a.err);
+    if (actA) mark_write(a, i, j, k);
+    if (actB) mark_write(a, i + 1, j, k);
     if (actA && actB) {
 #pragma unroll
         for (int q = 0; q < kQ; ++q)
@@ -374,6 +386,8 @@ template <bool kForced, bool kFused, bool kGeneral, bool kVsnap>
 __device__ __forceinline__ bool coupled_lane(const SweepArgs& a, int i, int j, int k, long long fc, int cnt,
                                              double (&m)[2][3], int& p0, int& p1, double (&cc)[3]) {
     const Layout& L = a.L;
+    fc = LBG_IDX(fc, a.cells, a.err);
+    (void)LBG_IDX(L.idx(i, j, k), L.plane, a.err);
     bool ok;
     if (!kGeneral && !kForced) {
         // unforced one-entry lanes: fluid lanes run the same operator with B = b = 0 and
@@ -429,6 +443,9 @@ __device__ __forceinline__ bool coupled_lane(const SweepArgs& a, int i, int j, i
     } else {
         ok = srt_cell_at<kForced, false>(a, i, j, k);
     }
+    // the psm branches store through the pair operators: count their cell here (the forced
+    // fluid lanes went through srt_cell_at, which counts its own)
+    if (!(kForced && cnt == 0)) mark_write(a, i, j, k);
     if constexpr (kFused) {
         if (cnt > 0) {
             cc[0] = (double)(a.blk_lo[0] + i) + 0.5;
@@ -498,8 +515,8 @@ __device__ __forceinline__ void seg_load(const SweepArgs& a, unsigned c0, int la
     in.act = in.i < L.nx && in_boxes(a, in.i, in.j, in.k);
     in.cnt = 0;
     if (in.act) {
-        in.fc = L.frac(in.i, in.j, in.k);
-        in.base = L.idx(in.i, in.j, in.k);
+        in.fc = LBG_IDX(L.frac(in.i, in.j, in.k), a.cells, a.err);
+        in.base = LBG_IDX(L.idx(in.i, in.j, in.k), L.plane, a.err);
         in.cnt = a.count[in.fc];
         in.bt = a.btot[in.fc];
         in.b0 = a.b0[in.fc];
@@ -539,6 +556,7 @@ __device__ __forceinline__ void seg_finish(const SweepArgs& a, const SegIn& in, 
                                   cov ? in.bt : 0.0, cov ? in.b0 : 0.0, pre.v[0], pre.v[1], pre.v[2], a.dst,
                                   a.L.plane, in.base, m);
         ok = pre.ok;
+        mark_write(a, in.i, in.j, in.k);
         if constexpr (!kFused) {
             if (cov)
                 for (int d = 0; d < 3; ++d) a.m0[3 * in.fc + d] = m[d];
@@ -668,7 +686,8 @@ __device__ __forceinline__ void seg_from_tma(const SweepArgs& a, unsigned c0, in
     double cc[3] = {0, 0, 0};
     int p0 = -1;
     if (act) {
-        const long long base = L.idx(i, j, k), fc = L.frac(i, j, k);
+        const long long base = LBG_IDX(L.idx(i, j, k), L.plane, a.err), fc = LBG_IDX(L.frac(i, j, k), a.cells, a.err);
+        mark_write(a, i, j, k);
         const int cnt = st.cnt[lane + (int)(c0 & 15u)];
         const bool cov = cnt > 0;
         const int id0 = kVsnap ? st.id0[lane + (int)(c0 & 3u)] : 0;
@@ -821,6 +840,42 @@ __global__ void stream_kernel(const double* __restrict__ src, double* __restrict
     for (int q = 0; q < kQ; ++q) dst[q * L.plane + base] = src[q * L.plane + base - L.shift(q)];
 }
 
+#ifdef LBG_CHECKED
+// every cell of the sweep's boxes written exactly once, no other cell written; counts reset
+__global__ void __launch_bounds__(256) verify_writes_kernel(SweepArgs a) {
+    const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= a.cells) return;
+    const int i = (int)(c % a.L.nx), j = (int)((c / a.L.nx) % a.L.ny), k = (int)(c / ((long long)a.L.nx * a.L.ny));
+    const int want = in_boxes(a, i, j, k) ? 1 : 0;
+    if (a.wc[c] != want) atomicAdd(&a.err->race, 1ull);
+    a.wc[c] = 0;
+}
+#endif
+
+static lbg_status verify_writes(lbg_block b, const SweepArgs& a) {
+#ifdef LBG_CHECKED
+    verify_writes_kernel<<<(unsigned)((a.cells + 255) / 256), 256, 0, b->stream>>>(a);
+    LBG_LAUNCH_CHECK();
+#else
+    (void)b;
+    (void)a;
+#endif
+    return LBG_OK;
+}
+
+static lbg_status ensure_wcount(lbg_block b) {
+#ifdef LBG_CHECKED
+    if (!b->wcount) {
+        const size_t n = (size_t)b->L.nx * b->L.ny * b->L.nz;
+        LBG_CUDA(cudaMalloc(&b->wcount, sizeof(int) * n));
+        LBG_CUDA(cudaMemset(b->wcount, 0, sizeof(int) * n));
+    }
+#else
+    (void)b;
+#endif
+    return LBG_OK;
+}
+
 static bool valid_box(const Layout& L, const lbg_box& r) {
     const int d[3] = {L.nx, L.ny, L.nz};
     for (int a = 0; a < 3; ++a)
@@ -857,6 +912,8 @@ static SweepArgs make_args(lbg_block b, const lbg_fluid* fl) {
     a.inv_tau = 1.0 / fl->tau;  // kDt / params.tau (lbm.cpp:30)
     a.F = {fl->f_ext[0], fl->f_ext[1], fl->f_ext[2]};
     a.err = b->err_d;
+    a.wc = b->wcount;
+    a.cells = (long long)b->L.nx * b->L.ny * b->L.nz;
     for (int c = 0; c < 3; ++c) a.wrap[c] = b->wrap[c];
     if (b->coupling) {
         a.count = b->count;
@@ -1066,9 +1123,20 @@ lbg_status lbg_sweep(lbg_block b, const lbg_fluid* fl, const lbg_box* range) {
     if (empty_box(*range)) return LBG_OK;  // run_kernel skips empty ranges (sim.cpp:222)
     if (!valid_box(b->L, *range)) return set_error(LBG_INVALID, "sweep range outside the block");
     LBG_CUDA(cudaSetDevice(b->device));
+    if (b->aa) {  // AA in-place streaming: whole block, every axis wrapped
+        if (range->lo[0] != 0 || range->lo[1] != 0 || range->lo[2] != 0 || range->hi[0] != b->L.nx ||
+            range->hi[1] != b->L.ny || range->hi[2] != b->L.nz)
+            return set_error(LBG_INVALID, "AA streaming sweeps the whole block");
+        if (!(b->wrap[0] && b->wrap[1] && b->wrap[2]))
+            return set_error(LBG_INVALID, "AA streaming needs the in-kernel periodic wrap on every axis");
+        if (b->aa_pending) return set_error(LBG_INVALID, "AA streaming: lbg_swap between sweeps");
+        Span span(b, LBG_CAT_PSM);
+        return aa_sweep(b, fl);
+    }
     if (b->coupling && b->cov_dirty)
         if (lbg_status s = rebuild_covered(b)) return s;
     if (lbg_status s = check_fused(b)) return s;
+    if (lbg_status s = ensure_wcount(b)) return s;
     SweepArgs a = make_args(b, fl);
     for (int c = 0; c < 3; ++c) {
         a.lo[c] = range->lo[c];
@@ -1082,7 +1150,7 @@ lbg_status lbg_sweep(lbg_block b, const lbg_fluid* fl, const lbg_box* range) {
         if (k12_on()) {
             launch_unified(b, a, fo, b->stream);
             LBG_LAUNCH_CHECK();
-            return LBG_OK;
+            return verify_writes(b, a);
         }
         if (k2_concurrent()) {
             // K1 and K2 touch disjoint cells (K1 skips K2's segments): K2 runs on the aux stream
@@ -1095,7 +1163,7 @@ lbg_status lbg_sweep(lbg_block b, const lbg_fluid* fl, const lbg_box* range) {
             LBG_LAUNCH_CHECK();
             LBG_CUDA(cudaEventRecord(b->ev_join, b->aux));
             LBG_CUDA(cudaStreamWaitEvent(b->stream, b->ev_join, 0));
-            return LBG_OK;
+            return verify_writes(b, a);
         }
         fo ? launch_box<true, true>(a, b->stream) : launch_box<false, true>(a, b->stream);
         LBG_LAUNCH_CHECK();
@@ -1106,10 +1174,11 @@ lbg_status lbg_sweep(lbg_block b, const lbg_fluid* fl, const lbg_box* range) {
         fo ? launch_box<true, false>(a, b->stream) : launch_box<false, false>(a, b->stream);
     }
     LBG_LAUNCH_CHECK();
-    return LBG_OK;
+    return verify_writes(b, a);
 }
 
 lbg_status lbg_sweep_boxes(lbg_block b, const lbg_fluid* fl, const lbg_box* boxes, int n) {
+    if (lbg_status s_ = aa_refuse(b, "lbg_sweep_boxes")) return s_;
     if (!b || (!boxes && n > 0)) return set_error(LBG_INVALID, "null argument");
     if (lbg_status s = check_fluid(fl)) return s;
     if (n > 8) return set_error(LBG_INVALID, "at most 8 boxes per launch");
@@ -1117,6 +1186,7 @@ lbg_status lbg_sweep_boxes(lbg_block b, const lbg_fluid* fl, const lbg_box* boxe
     if (b->coupling && b->cov_dirty)
         if (lbg_status s = rebuild_covered(b)) return s;
     if (lbg_status s = check_fused(b)) return s;
+    if (lbg_status s = ensure_wcount(b)) return s;
     SweepArgs a = make_args(b, fl);
     if (lbg_status s = add_boxes(a, b->L, boxes, n)) return s;
     if (a.nbox == 0) return LBG_OK;
@@ -1136,10 +1206,11 @@ lbg_status lbg_sweep_boxes(lbg_block b, const lbg_fluid* fl, const lbg_box* boxe
         fo ? launch_flat<true, false>(a, b->stream) : launch_flat<false, false>(a, b->stream);
     }
     LBG_LAUNCH_CHECK();
-    return LBG_OK;
+    return verify_writes(b, a);
 }
 
 lbg_status lbg_stream(lbg_block b, const lbg_box* r) {
+    if (lbg_status s_ = aa_refuse(b, "lbg_stream")) return s_;
     if (!b || !r) return set_error(LBG_INVALID, "null argument");
     if (empty_box(*r)) return LBG_OK;
     if (!valid_box(b->L, *r)) return set_error(LBG_INVALID, "stream range outside the block");

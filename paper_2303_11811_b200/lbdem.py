@@ -325,6 +325,10 @@ class Block:
         """Periodic axes the sweep wraps in-kernel (replaces the ghost fill for them)."""
         check(_lib().lbg_set_periodic_wrap(self.h, (C.c_int * 3)(*[int(bool(w)) for w in wrap])))
 
+    def set_streaming(self, mode):
+        """lbg.STREAM_AB (two buffers, default) or lbg.STREAM_AA (in-place, one buffer)."""
+        check(_lib().lbg_set_streaming(self.h, int(mode)))
+
     def stream_only(self, box: CellBox):
         bx = box.c()
         check(_lib().lbg_stream(self.h, C.byref(bx)))
@@ -338,6 +342,14 @@ class Block:
     def map(self, snaps, subdivisions=8):
         arr, n = snapshot_array(snaps)
         check(_lib().lbg_map(self.h, arr, n, subdivisions))
+
+    def map_prepare(self, snaps, subdivisions=8):
+        """Map into the shadow fraction field (the current one stays in use)."""
+        arr, n = snapshot_array(snaps)
+        check(_lib().lbg_map_prepare(self.h, arr, n, subdivisions))
+
+    def map_commit(self):
+        check(_lib().lbg_map_commit(self.h))
 
     def set_force_mode(self, mode):
         """lbg.FORCE_SCRATCH (reference scratch + finalize) or lbg.FORCE_FUSED (the PSM
@@ -478,6 +490,19 @@ class Block:
         dirs = (C.c_int * (3 * max(n, 1)))(*[v for d, _ in entries for v in d])
         srcs = (C.c_void_p * max(n, 1))(*[s.h.value for _, s in entries])
         check(_lib().lbg_halo_fetch_all(self.h, dirs, srcs, n))
+
+    def halo_push_connect(self, entries):
+        """entries: [(offset (ox, oy, oz), Block)] — the neighbours this block pushes into."""
+        n = len(entries)
+        offs = (C.c_int * (3 * max(n, 1)))(*[v for o, _ in entries for v in o])
+        blks = (C.c_void_p * max(n, 1))(*[b.h.value for _, b in entries])
+        check(_lib().lbg_halo_push_connect(self.h, offs, blks, n))
+
+    def halo_push(self):
+        check(_lib().lbg_halo_push(self.h))
+
+    def halo_push_wait(self):
+        check(_lib().lbg_halo_push_wait(self.h))
 
     def set_timing(self, on=True):
         check(_lib().lbg_set_timing(self.h, int(on)))

@@ -10,12 +10,15 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblbg.so")
+# LBG_LIB: another build of the same library (the bounds/race-checked build,
+# build_checked/liblbg.so from `make checked`); never a different implementation
+LIB_PATH = os.environ.get("LBG_LIB") or os.path.join(HERE, "liblbg.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include", "lbg.h")
 
 OK, CONFIG_ERROR, NUMERIC_ERROR, SYNC_ERROR, IO_ERROR, CUDA_ERROR, INVALID = range(7)
 BC_PERIODIC, BC_NO_SLIP, BC_VELOCITY, BC_PRESSURE = range(4)
 REDUCE_PARITY, REDUCE_FAST = 0, 1
+STREAM_AB, STREAM_AA = 0, 1
 FORCE_SCRATCH, FORCE_FUSED = 0, 1
 CATEGORIES = ("PSM", "PSM-comm", "mapping", "setU", "redF", "PD", "PD-comm", "other")  # perf.hpp:17-26
 
@@ -83,10 +86,13 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "lbg_sweep": (st, [blk, C.POINTER(Fluid), C.POINTER(Box)]),
         "lbg_sweep_boxes": (st, [blk, C.POINTER(Fluid), C.POINTER(Box), C.c_int]),
         "lbg_stream": (st, [blk, C.POINTER(Box)]),
+        "lbg_set_streaming": (st, [blk, C.c_int]),
         "lbg_set_periodic_wrap": (st, [blk, i3]),
         "lbg_fill_periodic": (st, [blk, i3, C.c_int]),
         "lbg_apply_boundaries": (st, [blk, C.POINTER(FaceBc), i3]),
         "lbg_map": (st, [blk, C.POINTER(Snapshot), C.c_int, C.c_int]),
+        "lbg_map_prepare": (st, [blk, C.POINTER(Snapshot), C.c_int, C.c_int]),
+        "lbg_map_commit": (st, [blk]),
         "lbg_set_solid_velocities": (st, [blk, C.POINTER(Snapshot), C.c_int]),
         "lbg_set_force_mode": (st, [blk, C.c_int]),
         "lbg_reduce_hydro": (st, [blk, C.c_int, C.POINTER(HydroPartial), C.c_int, C.POINTER(C.c_int)]),
@@ -111,6 +117,9 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "lbg_halo_stage": (st, [blk, i3, C.c_int]),
         "lbg_halo_fetch": (st, [blk, i3, blk]),
         "lbg_halo_fetch_all": (st, [blk, i3, C.POINTER(C.c_void_p), C.c_int]),
+        "lbg_halo_push_connect": (st, [blk, i3, C.POINTER(C.c_void_p), C.c_int]),
+        "lbg_halo_push": (st, [blk]),
+        "lbg_halo_push_wait": (st, [blk]),
         "lbg_p2p_handles": (st, [blk, vp, C.POINTER(C.c_size_t)]),
         "lbg_p2p_connect": (st, [blk, C.c_int, C.c_int, C.c_char_p, C.c_int, i3]),
         "lbg_p2p_prime": (st, [blk]),

@@ -46,13 +46,14 @@ def test_config4_full_size_two_gpus_vs_one_block(halo):
     assert "rank 1: 0 of 512 z-planes differ" in r.stdout
 
 
-@pytest.mark.parametrize("halo,per", [("device", 1), ("host", 1), ("device", 2)])
+@pytest.mark.parametrize("halo,per", [("push", 1), ("stage", 1), ("host", 1), ("push", 2), ("push", 4)])
 def test_dropin_bed_spread_over_gpus_bitwise(halo, per, monkeypatch):
     """The drop-in with its blocks dealt over the GPUs (LBDEM_GPU_SPREAD=1: `per` consecutive
     blocks per GPU, one worker thread per block): a config-3-shaped bed on {N*per,1,1} x-slabs
-    (N = 2..4) with host DEM, the PDF halo peer-to-peer between GPUs and on-device between
-    slabs of one GPU (or through host slabs), PARITY force partials — every PDF and particle
-    state bitwise equal to the CPU reference."""
+    (N = 2..4; per = 4 is config 5's layout) with host DEM, the PDF halo pushed by each sender
+    after its sweep (5 q per face cell, NVLink peer stores between GPUs, device stores between
+    slabs of one GPU), or staged 19-q slabs, or host slabs; PARITY force partials — every PDF
+    and particle state bitwise equal to the CPU reference."""
     n = _ngpus()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
