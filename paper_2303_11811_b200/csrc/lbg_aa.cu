@@ -69,8 +69,8 @@ __global__ void __launch_bounds__(256) sweep_aa_kernel(const AAArgs a) {
     if (m && (threadIdx.x & 31) == 0) atomicAdd(&a.err->unstable, (unsigned long long)__popc(m));
 }
 
-// S1 -> S0 without a collision: slot q of x in `out` = slot q̄ of x + c_q in `in` (the post-
-// collision values before their streaming); `in` and `out` distinct
+// S1 -> S0 without a collision: slot q of x in `out` = slot q̄ of x + c_q in `in` (where the odd
+// step stored x's post-collision f_q); `in` and `out` distinct
 __global__ void __launch_bounds__(256) aa_unstream_kernel(const double* __restrict__ in, double* __restrict__ out,
                                                           Layout L) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(256) aa_unstream_kernel(const double* __restri
     if (i >= L.nx) return;
     const long long base = L.idx(i, j, k);
 #pragma unroll
-    for (int q = 0; q < kQ; ++q) out[q * L.plane + base] = in[aa_off(L, i, j, k, opposite(q), 1)];
+    for (int q = 0; q < kQ; ++q) out[q * L.plane + base] = in[aa_off(L, i, j, k, opposite(q), -1)];
 }
 
 lbg_status aa_sweep(lbg_block b, const lbg_fluid* fl) {

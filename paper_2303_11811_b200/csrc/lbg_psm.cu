@@ -404,8 +404,9 @@ __device__ __forceinline__ void nm_add(double& sum, double& comp, double v) {  /
 //   box source: the snapshot's reach (r + max(1/2, f_r), the mapping's candidate test) when
 //   the fraction field was mapped from these positions; otherwise entry_box_kernel takes the
 //   min/max cell of every particle's entries from the field itself (order-independent).
-constexpr int kWalkWarps = 8;
-constexpr int kWalkKeys = 1024;  // entry keys staged per warp before a replay flush
+constexpr int kWalkWarps = 4;   // warps per CTA
+constexpr int kWalkGroups = 4;  // particles per warp: lane groups of 8
+constexpr int kWalkKeys = 256;  // entry keys staged per particle before a replay flush
 
 struct WalkArgs {
     const lbg_snapshot* __restrict__ s;
@@ -433,160 +434,192 @@ __device__ __forceinline__ void nm_add_sel(double& sum, double& comp, double v) 
     sum = t;
 }
 
-// replay of staged keys kb[0, nk): 32 entries per batch (m gathered one batch ahead, zeroed as
-// consumed), their six terms into the warp's tile, lanes 0..5 add them in entry order
-__device__ __forceinline__ void walk_flush(const WalkArgs& a, const unsigned* kb, int nk, double (*tw)[7],
-                                           int lane, double x0, double x1, double x2, double& sum, double& comp) {
+// four cells of one lane per walk step (cell t = step * 32 + u * 8 + lane-in-group)
+struct WalkQuad {
+    long long c[4];
+    int cnt[4], e0[4], e1[4];
+};
+
+// One warp walks four particles, one per 8-lane group (so the six Neumaier chains of each
+// particle run in lanes 0..5 of its group and every replay instruction serves four particles).
+// Pass 1 walks each particle's box 32 cells per step (4 per lane, the next step's cell fields
+// in flight) and stages the keys (cell << 1 | entry) of the particle's entries in walk order —
+// only count and ids are read; pass 2 (whenever a group's stage nears full, and at the end)
+// gathers the momenta 32 per group at a time, writes the six terms of each entry, zeroes the
+// entry's scratch (psm.cpp:305), and lanes 0..5 of each group replay them in order.
+template <int kMinBlocks>
+__global__ void __launch_bounds__(32 * kWalkWarps, kMinBlocks) walk_chain_kernel(const WalkArgs a) {
+    __shared__ unsigned keys_all[kWalkWarps][kWalkGroups][kWalkKeys];
+    __shared__ double terms_all[kWalkWarps][kWalkGroups][32][7];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int grp = lane >> 3, gl = lane & 7;
+    const long long pw = (long long)(blockIdx.x * kWalkWarps + w) * kWalkGroups;
+    if (pw >= a.n) return;  // warp-uniform
+    const int p = (int)pw + grp;
+    const bool valid = p < a.n;
+    unsigned* kb = keys_all[w][grp];
+    double (*tw)[7] = terms_all[w][grp];
     const BinGeom& g = a.g;
-    auto gather = [&](int base, long long& c, double (&m)[3]) {
-        c = -1;
-        m[0] = m[1] = m[2] = 0.0;
-        if (base + lane < nk) {
-            const unsigned key = kb[base + lane];
-            c = LBG_IDX((long long)(key >> 1), a.cells, a.err);
-            double* mp = ((key & 1u) ? a.m1 : a.m0) + 3 * c;
-            m[0] = mp[0];
-            m[1] = mp[1];
-            m[2] = mp[2];
-            c = (c << 1) | (key & 1u);
-        }
-    };
-    long long c;
-    double m[3];
-    gather(0, c, m);
-    for (int base = 0; base < nk; base += 32) {
-        const int nb = min(32, nk - base);
-        if (c >= 0) {
-            const long long cell = c >> 1;
-            const int ci = (int)(cell % g.dims[0]), cj = (int)((cell / g.dims[0]) % g.dims[1]),
-                      ck = (int)(cell / ((long long)g.dims[0] * g.dims[1]));
-            const double r0 = ((double)(g.lo[0] + ci) + 0.5) - x0;
-            const double r1 = ((double)(g.lo[1] + cj) + 0.5) - x1;
-            const double r2 = ((double)(g.lo[2] + ck) + 0.5) - x2;
-            tw[lane][0] = m[0];
-            tw[lane][1] = m[1];
-            tw[lane][2] = m[2];
-            tw[lane][3] = r1 * m[2] - r2 * m[1];
-            tw[lane][4] = r2 * m[0] - r0 * m[2];
-            tw[lane][5] = r0 * m[1] - r1 * m[0];
-            double* mp = ((c & 1) ? a.m1 : a.m0) + 3 * cell;  // psm.cpp:305: the entry is cleared
-            mp[0] = 0.0;
-            mp[1] = 0.0;
-            mp[2] = 0.0;
-        }
-        __syncwarp();
-        gather(base + 32, c, m);  // the next batch's momenta in flight during the replay
-        if (lane < 6) {
-#pragma unroll 4
-            for (int e = 0; e < nb; ++e) {
-                const double v = tw[e][lane];
-                if (a.fast)
-                    sum += v;
-                else
-                    nm_add_sel(sum, comp, v);
+    int id = -2;
+    double x0 = 0.0, x1 = 0.0, x2 = 0.0;
+    int lo[3] = {0, 0, 0}, hi[3] = {-1, -1, -1};
+    if (valid) {
+        const lbg_snapshot& sp = a.s[p];
+        id = sp.id;
+        x0 = sp.x[0];
+        x1 = sp.x[1];
+        x2 = sp.x[2];
+        if (a.box) {
+            for (int d = 0; d < 3; ++d) {
+                lo[d] = -a.box[6 * p + d];
+                hi[d] = a.box[6 * p + 3 + d];
+            }
+        } else {
+            // every cell with eps > 0 has |c - x| < r + f_r (psm.cpp:28-32), c = lo + i + 1/2:
+            // the cells within R = r + max(1/2, f_r) of x per axis, one cell of margin
+            const double R = sp.r + (sp.f_r > 0.5 ? sp.f_r : 0.5);
+            const double xs[3] = {x0, x1, x2};
+            for (int d = 0; d < 3; ++d) {
+                const double o = xs[d] - (double)g.lo[d] - 0.5;
+                lo[d] = max((int)ceil(o - R) - 1, 0);
+                hi[d] = min((int)floor(o + R) + 1, g.dims[d] - 1);
             }
         }
-        __syncwarp();
     }
-}
-
-// One warp per particle. Pass 1 walks the box (32 cells per step, the next step's cell fields
-// in flight) and stages the keys (cell << 1 | entry) of the particle's entries in walk order —
-// only count and ids are read; pass 2 (a flush whenever the key stage fills, and at the end)
-// gathers the momenta 32 at a time and replays them.
-__global__ void __launch_bounds__(32 * kWalkWarps) walk_chain_kernel(const WalkArgs a) {
-    __shared__ unsigned keys_all[kWalkWarps][kWalkKeys];
-    __shared__ double terms_all[kWalkWarps][32][7];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int p = blockIdx.x * kWalkWarps + w;
-    if (p >= a.n) return;  // warp-uniform
-    unsigned* kb = keys_all[w];
-    double (*tw)[7] = terms_all[w];
-    const BinGeom& g = a.g;
-    const lbg_snapshot& sp = a.s[p];
-    const int id = sp.id;
-    const double x0 = sp.x[0], x1 = sp.x[1], x2 = sp.x[2];
-    int lo[3], hi[3];
-    if (a.box) {
-        for (int d = 0; d < 3; ++d) {
-            lo[d] = -a.box[6 * p + d];
-            hi[d] = a.box[6 * p + 3 + d];
-        }
-    } else {
-        // every cell with eps > 0 has |c - x| < r + f_r (psm.cpp:28-32), c = lo + i + 1/2: the
-        // cells within R = r + max(1/2, f_r) of x per axis, one cell of margin for rounding
-        const double R = sp.r + (sp.f_r > 0.5 ? sp.f_r : 0.5);
-        const double xs[3] = {x0, x1, x2};
-        for (int d = 0; d < 3; ++d) {
-            const double o = xs[d] - (double)g.lo[d] - 0.5;
-            lo[d] = max((int)ceil(o - R) - 1, 0);
-            hi[d] = min((int)floor(o + R) + 1, g.dims[d] - 1);
-        }
-    }
+    const bool nonempty = hi[0] >= lo[0] && hi[1] >= lo[1] && hi[2] >= lo[2];
+    const int ex = nonempty ? hi[0] - lo[0] + 1 : 1, ey = nonempty ? hi[1] - lo[1] + 1 : 1;
+    const long long total = nonempty ? (long long)ex * ey * (hi[2] - lo[2] + 1) : 0;
+    const unsigned gmask = 0xffu << (8 * grp);
+    const unsigned lt = ((1u << lane) - 1u) & gmask;
     double sum = 0.0, comp = 0.0;
     bool any = false;
-    if (hi[0] >= lo[0] && hi[1] >= lo[1] && hi[2] >= lo[2]) {
-        const int ex = hi[0] - lo[0] + 1, ey = hi[1] - lo[1] + 1;
-        const long long total = (long long)ex * ey * (hi[2] - lo[2] + 1);
-        const unsigned lt = (1u << lane) - 1u;
-        struct Cell {
-            long long c;
-            int cnt, e0, e1;
-        };
-        auto fetch = [&](long long t, Cell& f) {
-            f.cnt = 0;
-            f.c = 0;
-            f.e0 = f.e1 = -1;
+    int nk = 0;
+
+    auto fetch = [&](long long step, WalkQuad& q) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const long long t = step * 32 + u * 8 + gl;
+            q.cnt[u] = 0;
+            q.c[u] = 0;
+            q.e0[u] = q.e1[u] = -1;
             if (t < total) {
-                const long long r = t / ex;
-                const int i = lo[0] + (int)(t - r * ex), j = lo[1] + (int)(r % ey), k = lo[2] + (int)(r / ey);
-                f.c = LBG_IDX(((long long)k * g.dims[1] + j) * g.dims[0] + i, a.cells, a.err);
-                f.cnt = a.count[f.c];
-                f.e0 = a.id0[f.c];
-                f.e1 = a.id1[f.c];
+                // 32-bit index math (boxes hold < 2^31 cells; 64-bit division is a long routine)
+                const unsigned tu = (unsigned)t, r = tu / (unsigned)ex;
+                const int i = lo[0] + (int)(tu - r * (unsigned)ex), j = lo[1] + (int)(r % (unsigned)ey),
+                          k = lo[2] + (int)(r / (unsigned)ey);
+                q.c[u] = LBG_IDX(((long long)k * g.dims[1] + j) * g.dims[0] + i, a.cells, a.err);
+                q.cnt[u] = a.count[q.c[u]];
+                q.e0[u] = a.id0[q.c[u]];
+                q.e1[u] = a.id1[q.c[u]];
             }
-        };
-        int nk = 0;
-        // one step of the walk on `use`; `ahead` receives the fields two steps on. The three
-        // register sets rotate roles through the unrolled loop, so no in-flight load is ever
-        // copied (a copy would wait for it)
-        auto step = [&](long long base, const Cell& use, Cell& ahead) {
-            fetch(base + 64 + lane, ahead);
-            const bool h0 = use.cnt >= 1 && use.e0 == id, h1 = use.cnt >= 2 && use.e1 == id;
-            const unsigned b0 = __ballot_sync(0xffffffffu, h0), b1 = __ballot_sync(0xffffffffu, h1);
-            if (b0 | b1) {
-                any = true;
-                const int s0 = nk + __popc(b0 & lt) + __popc(b1 & lt);
-                if (h0) kb[LBG_IDX(s0, kWalkKeys, a.err)] = (unsigned)(use.c << 1);
-                if (h1) kb[LBG_IDX(s0 + (h0 ? 1 : 0), kWalkKeys, a.err)] = (unsigned)((use.c << 1) | 1);
-                nk += __popc(b0) + __popc(b1);
-                if (nk > kWalkKeys - 64) {
-                    __syncwarp();
-                    walk_flush(a, kb, nk, tw, lane, x0, x1, x2, sum, comp);
-                    nk = 0;
+        }
+    };
+    // pass 2 over the staged keys of every group (lockstep batches; groups with fewer idle)
+    auto flush = [&]() {
+        __syncwarp();
+        const int nb = (nk + 31) / 32;
+        const int nbmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)nb);
+        long long gc[4];
+        double gm[4][3];
+        auto gather = [&](int b) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = b * 32 + u * 8 + gl;
+                gc[u] = -1;
+                gm[u][0] = gm[u][1] = gm[u][2] = 0.0;
+                if (e < nk) {
+                    const unsigned key = kb[e];
+                    const long long c = LBG_IDX((long long)(key >> 1), a.cells, a.err);
+                    const double* mp = ((key & 1u) ? a.m1 : a.m0) + 3 * c;
+                    gm[u][0] = mp[0];
+                    gm[u][1] = mp[1];
+                    gm[u][2] = mp[2];
+                    gc[u] = (c << 1) | (key & 1u);
                 }
             }
         };
-        Cell A, B, Cc;
-        fetch(lane, A);
-        fetch(32 + lane, B);
-        for (long long base = 0;;) {
-            step(base, A, Cc);
-            if ((base += 32) >= total) break;
-            step(base, B, A);
-            if ((base += 32) >= total) break;
-            step(base, Cc, B);
-            if ((base += 32) >= total) break;
+        gather(0);
+        for (int b = 0; b < nbmax; ++b) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (gc[u] < 0) continue;
+                const long long cell = gc[u] >> 1;
+                const unsigned cu = (unsigned)cell, row = cu / (unsigned)g.dims[0];
+                const int ci = (int)(cu - row * (unsigned)g.dims[0]), cj = (int)(row % (unsigned)g.dims[1]),
+                          ck = (int)(row / (unsigned)g.dims[1]);
+                const double r0 = ((double)(g.lo[0] + ci) + 0.5) - x0;
+                const double r1 = ((double)(g.lo[1] + cj) + 0.5) - x1;
+                const double r2 = ((double)(g.lo[2] + ck) + 0.5) - x2;
+                const double* m = gm[u];
+                double* t = tw[u * 8 + gl];
+                t[0] = m[0];
+                t[1] = m[1];
+                t[2] = m[2];
+                t[3] = r1 * m[2] - r2 * m[1];
+                t[4] = r2 * m[0] - r0 * m[2];
+                t[5] = r0 * m[1] - r1 * m[0];
+                double* z = ((gc[u] & 1) ? a.m1 : a.m0) + 3 * cell;  // the visited entry is cleared
+                z[0] = 0.0;
+                z[1] = 0.0;
+                z[2] = 0.0;
+            }
+            __syncwarp();
+            const int ne = min(32, nk - b * 32);
+            gather(b + 1);  // the next batch's momenta in flight during the replay
+            if (gl < 6) {
+#pragma unroll 4
+                for (int e = 0; e < ne; ++e) {
+                    const double v = tw[e][gl];
+                    if (a.fast)
+                        sum += v;
+                    else
+                        nm_add_sel(sum, comp, v);
+                }
+            }
+            __syncwarp();
         }
-        __syncwarp();
-        walk_flush(a, kb, nk, tw, lane, x0, x1, x2, sum, comp);
+        nk = 0;
+    };
+    auto step = [&](const WalkQuad& q) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const bool h0 = q.cnt[u] >= 1 && q.e0[u] == id, h1 = q.cnt[u] >= 2 && q.e1[u] == id;
+            const unsigned b0 = __ballot_sync(0xffffffffu, h0), b1 = __ballot_sync(0xffffffffu, h1);
+            const int s0 = nk + __popc(b0 & lt) + __popc(b1 & lt);
+            if (h0) kb[LBG_IDX(s0, kWalkKeys, a.err)] = (unsigned)(q.c[u] << 1);
+            if (h1) kb[LBG_IDX(s0 + (h0 ? 1 : 0), kWalkKeys, a.err)] = (unsigned)((q.c[u] << 1) | 1);
+            nk += __popc(b0 & gmask) + __popc(b1 & gmask);
+            any = any || ((b0 | b1) & gmask) != 0;
+        }
+    };
+    const long long steps = (total + 31) / 32;
+    long long smax = steps;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) smax = max(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+    // two register quads swap roles (copying an in-flight load would wait for it); one flush
+    // call site (the flush is most of the code: a second inlined copy would spill the
+    // instruction cache), taken after every pair of steps that may have filled a stage
+    WalkQuad A, B;
+    fetch(0, A);
+    for (long long st = 0;; st += 2) {
+        if (st < smax) {
+            fetch(st + 1, B);
+            step(A);
+        }
+        if (st + 1 < smax) {
+            fetch(st + 2, A);
+            step(B);
+        }
+        const bool done = st + 2 >= smax;
+        if (done || __any_sync(0xffffffffu, nk > kWalkKeys - 128)) flush();  // 2 steps add <= 128
+        if (done) break;
     }
-    if (lane < 6) {
-        const int slot = lane < 3 ? lane : 6 + (lane - 3);
+    if (valid && gl < 6) {
+        const int slot = gl < 3 ? gl : 6 + (gl - 3);
         a.rows[12 * (size_t)p + slot] = sum;
         a.rows[12 * (size_t)p + slot + 3] = comp;
     }
-    if (lane == 0) a.used[p] = any ? 1 : 0;
+    if (valid && gl == 0) a.used[p] = any ? 1 : 0;
 }
 
 // generic box source: per particle the min/max cell of its entries (atomic max on -lo / hi:
@@ -1071,7 +1104,16 @@ lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int c
             a.box = b->red_box;
         }
         if (n > 0) {
-            walk_chain_kernel<<<(unsigned)((n + kWalkWarps - 1) / kWalkWarps), 32 * kWalkWarps, 0, b->stream>>>(a);
+            const int per_cta = kWalkWarps * kWalkGroups;
+            static const int minb = [] {
+                const char* e = std::getenv("LBG_WALK_MINB");
+                return e ? std::atoi(e) : 4;
+            }();
+            const unsigned grid = (unsigned)((n + per_cta - 1) / per_cta);
+            if (minb == 5)
+                walk_chain_kernel<5><<<grid, 32 * kWalkWarps, 0, b->stream>>>(a);
+            else
+                walk_chain_kernel<4><<<grid, 32 * kWalkWarps, 0, b->stream>>>(a);
             LBG_LAUNCH_CHECK();
             // partials D2H on the side stream (pinned), ordered after the walk by an event
             LBG_CUDA(cudaEventRecord(b->ev_red, b->stream));

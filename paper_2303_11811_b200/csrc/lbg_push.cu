@@ -60,13 +60,14 @@ __global__ void __launch_bounds__(256) halo_push_kernel(const double* __restrict
     if (t >= a.begin[a.n]) return;
     int s = 0;
     while (t >= a.begin[s + 1]) ++s;
-    const long long u = t - a.begin[s];
-    const long long cells = (long long)a.ext[s][0] * a.ext[s][1] * a.ext[s][2];
+    // 32-bit index math within a slab (a face has < 2^31 cells)
+    const unsigned u = (unsigned)(t - a.begin[s]);
+    const unsigned cells = (unsigned)a.ext[s][0] * a.ext[s][1] * a.ext[s][2];
     const int qi = (int)(u / cells);
-    const long long r = u - qi * cells;
-    const int i = a.lo[s][0] + (int)(r % a.ext[s][0]);
-    const int j = a.lo[s][1] + (int)((r / a.ext[s][0]) % a.ext[s][1]);
-    const int k = a.lo[s][2] + (int)(r / ((long long)a.ext[s][0] * a.ext[s][1]));
+    const unsigned r = u - qi * cells, row = r / (unsigned)a.ext[s][0];
+    const int i = a.lo[s][0] + (int)(r - row * (unsigned)a.ext[s][0]);
+    const int j = a.lo[s][1] + (int)(row % (unsigned)a.ext[s][1]);
+    const int k = a.lo[s][2] + (int)(row / (unsigned)a.ext[s][1]);
     const int q = a.q[s][qi];
     const double v = src[q * L.plane + LBG_IDX(L.idx(i, j, k), L.plane, a.err)];
     const long long bi = i + a.sh[s][0], bj = j + a.sh[s][1], bk = k + a.sh[s][2];

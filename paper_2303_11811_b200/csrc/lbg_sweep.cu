@@ -775,30 +775,158 @@ __global__ void __launch_bounds__(128, kMinBlocks) coupled_unified_kernel(const 
     const int segs_x = (a.hi[0] - a.i0 + 31) >> 5;
     const int ny_b = a.hi[1] - a.lo[1];
     const long long nseg = (long long)segs_x * ny_b * (a.hi[2] - a.lo[2]);
-    for (long long s = warp; s < nseg; s += nwarps) {
-        const long long r = s / segs_x;
-        const int i0 = a.i0 + 32 * (int)(s - r * segs_x);
-        const int j = a.lo[1] + (int)(r % ny_b);
-        const int k = a.lo[2] + (int)(r / ny_b);
-        const int i = i0 + lane;
-        const bool inx = i < L.nx;
-        const long long fc = L.frac(inx ? i : L.nx - 1, j, k);
-        const int cnt = inx ? (int)a.count[fc] : 0;
+    if (warp >= nseg) return;  // warp-uniform
+    // the count byte of a segment is loaded one segment ahead, so the operator choice never
+    // waits on HBM and every segment's loads (populations, cell fields) go out in one batch
+    auto count_of = [&](long long s) -> int {
+        if (s >= nseg) return 0;
+        // 32-bit index math (a 64-bit division is a ~100-instruction software routine)
+        const unsigned su = (unsigned)s, r = su / (unsigned)segs_x;
+        const int i = a.i0 + 32 * (int)(su - r * (unsigned)segs_x) + lane;
+        if (i >= L.nx) return 0;
+        return (int)a.count[LBG_IDX(L.frac(i, a.lo[1] + (int)(r % (unsigned)ny_b), a.lo[2] + (int)(r / (unsigned)ny_b)),
+                                    a.cells, a.err)];
+    };
+    auto sweep_seg = [&](long long s, int cnt) {
+        const unsigned su = (unsigned)s, r = su / (unsigned)segs_x;
+        const int i = a.i0 + 32 * (int)(su - r * (unsigned)segs_x) + lane;
+        const int j = a.lo[1] + (int)(r % (unsigned)ny_b);
+        const int k = a.lo[2] + (int)(r / (unsigned)ny_b);
         const int mx = __reduce_max_sync(0xffffffffu, (unsigned)cnt);
-        if (mx >= 2) continue;  // psm_seg_kernel<two> sweeps this segment
-        const bool act = inx && i >= a.lo[0] && i < a.hi[0];
+        if (mx >= 2) return;  // psm_seg_kernel<two> sweeps this segment
+        const bool act = i < L.nx && i >= a.lo[0] && i < a.hi[0];
         bool ok = true;
         if (mx == 0) {
             if (act) ok = srt_cell_at<kForced, false>(a, i, j, k);
             count_bad(a.err, !ok);
-            continue;
+            return;
         }
         double m[2][3] = {{0, 0, 0}, {0, 0, 0}};
         double cc[3] = {0, 0, 0};
         int p0 = -1, p1 = -1;
-        if (act) ok = coupled_lane<kForced, kFused, false, kVsnap>(a, i, j, k, fc, cnt, m, p0, p1, cc);
+        if (act) ok = coupled_lane<kForced, kFused, false, kVsnap>(a, i, j, k, L.frac(i, j, k), cnt, m, p0, p1, cc);
         count_bad(a.err, !ok);
         if constexpr (kFused) fused_accumulate(a, p0, m[0], cc);
+    };
+    // one body (a second inlined copy of both operators overflows the instruction cache): the
+    // copy of the count loaded a whole segment earlier never waits
+    int cnt_next = count_of(warp);
+    for (long long s = warp; s < nseg; s += nwarps) {
+        const int cnt = cnt_next;
+        cnt_next = count_of(s + nwarps);
+        sweep_seg(s, cnt);
+    }
+}
+
+// K12, register-pipelined (default; LBG_K12_PIPE=0 selects the plain loop above; unforced,
+// inline solid velocities through the mapping's direct index): the next segment's
+// populations and cell fields (count, btot, b0, entry index: all loaded, the operator is only
+// known when the count arrives) are loaded while the
+// current one is finished. pre() consumes everything the current segment loaded (count ballot,
+// moments, solid velocity) before the next loads are issued, so no wait on the current data is
+// also a wait on the next (loads share the warp's scoreboards); the register sets swap roles
+// through the unrolled loop (a copy of an in-flight register would wait for it).
+struct USeg {
+    double f[kQ];
+    double bt, b0;
+    long long fc, base;
+    int i, j, k, cnt, pe;
+    bool act;
+};
+
+struct UPre {
+    double rho, ux, uy, uz, usq, v[3];
+    int mx;
+    bool ok;
+};
+
+__device__ __forceinline__ void useg_issue(const SweepArgs& a, long long s, int segs_x, int ny_b, int lane,
+                                           USeg& u) {
+    const Layout& L = a.L;
+    // 32-bit index math (a 64-bit division is a ~100-instruction software routine)
+    const unsigned su = (unsigned)s, r = su / (unsigned)segs_x;
+    u.i = a.i0 + 32 * (int)(su - r * (unsigned)segs_x) + lane;
+    u.j = a.lo[1] + (int)(r % (unsigned)ny_b);
+    u.k = a.lo[2] + (int)(r / (unsigned)ny_b);
+    const bool inx = u.i < L.nx;
+    u.fc = LBG_IDX(L.frac(inx ? u.i : L.nx - 1, u.j, u.k), a.cells, a.err);
+    u.act = inx && u.i >= a.lo[0] && u.i < a.hi[0];
+    u.cnt = inx ? (int)a.count[u.fc] : 0;
+    u.bt = a.btot[u.fc];
+    u.b0 = a.b0[u.fc];
+    u.pe = a.pidx0[u.fc];
+    if (u.act) {
+        u.base = LBG_IDX(L.idx(u.i, u.j, u.k), L.plane, a.err);
+        pull(a, u.i, u.j, u.k, u.base, u.f);
+    }
+}
+
+template <bool kVsnap>
+__device__ __forceinline__ void useg_pre(const SweepArgs& a, const USeg& u, UPre& pre) {
+    pre.mx = (int)__reduce_max_sync(0xffffffffu, (unsigned)u.cnt);
+    pre.ok = true;
+    if (pre.mx >= 2 || !u.act) return;
+    const bool cov = u.cnt > 0;
+    if (pre.mx == 1) {
+        const int p = kVsnap ? ((unsigned)u.pe < (unsigned)a.n_snaps ? u.pe : -1) : -1;
+        solid_velocity_sel<kVsnap>(a, cov, u.fc, u.i, u.j, u.k, pre.v, p);
+    }
+    moments(u.f, pre.rho, pre.ux, pre.uy, pre.uz);
+    pre.usq = (pre.ux * pre.ux + pre.uy * pre.uy) + pre.uz * pre.uz;
+    pre.ok = pre.rho > 0.0 && pre.usq <= kMaxVelocity * kMaxVelocity && isfinite(pre.rho);
+}
+
+template <bool kFused, bool kVsnap>
+__device__ __forceinline__ void useg_finish(const SweepArgs& a, const USeg& u, const UPre& pre) {
+    if (pre.mx >= 2) return;  // psm_seg_kernel<two> sweeps this segment
+    double m[3] = {0, 0, 0};
+    double cc[3] = {0, 0, 0};
+    int p0 = -1;
+    if (u.act) {
+        const auto g = [&](int q) { return u.f[q]; };
+        if (pre.mx == 0) {
+            srt_pairs_g(g, pre.rho, pre.ux, pre.uy, pre.uz, pre.usq, a.inv_tau, a.dst, a.L.plane, u.base);
+        } else {
+            const bool cov = u.cnt > 0;
+            psm_one_pairs_g<false>(g, pre.rho, pre.ux, pre.uy, pre.uz, pre.usq, a.inv_tau, a.F, cov ? u.bt : 0.0,
+                                   cov ? u.b0 : 0.0, pre.v[0], pre.v[1], pre.v[2], a.dst, a.L.plane, u.base, m);
+            if constexpr (!kFused) {
+                if (cov)
+                    for (int d = 0; d < 3; ++d) a.m0[3 * u.fc + d] = m[d];
+            } else if (cov) {
+                cc[0] = (double)(a.blk_lo[0] + u.i) + 0.5;
+                cc[1] = (double)(a.blk_lo[1] + u.j) + 0.5;
+                cc[2] = (double)(a.blk_lo[2] + u.k) + 0.5;
+                p0 = (unsigned)u.pe < (unsigned)a.n_snaps ? u.pe : -1;
+                if (p0 < 0) atomicAdd(&a.err->unknown, 1ull);
+            }
+        }
+        mark_write(a, u.i, u.j, u.k);
+    }
+    count_bad(a.err, !pre.ok);
+    if constexpr (kFused)
+        if (pre.mx == 1) fused_accumulate(a, p0, m, cc);
+}
+
+template <bool kFused, bool kVsnap>
+__global__ void __launch_bounds__(128, 3) coupled_unified_pipe_kernel(const SweepArgs a) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = (long long)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const long long nwarps = (long long)((gridDim.x * blockDim.x) >> 5);
+    const int segs_x = (a.hi[0] - a.i0 + 31) >> 5;
+    const int ny_b = a.hi[1] - a.lo[1];
+    const long long nseg = (long long)segs_x * ny_b * (a.hi[2] - a.lo[2]);
+    if (warp >= nseg) return;  // warp-uniform
+    // one body: a second inlined copy of the operators would overflow the instruction cache.
+    // The copy cur = nxt happens a whole finish() after nxt's loads were issued.
+    USeg cur, nxt;
+    UPre pre;
+    useg_issue(a, warp, segs_x, ny_b, lane, nxt);
+    for (long long s = warp; s < nseg; s += nwarps) {
+        cur = nxt;
+        useg_pre<kVsnap>(a, cur, pre);
+        if (s + nwarps < nseg) useg_issue(a, s + nwarps, segs_x, ny_b, lane, nxt);
+        useg_finish<kFused, kVsnap>(a, cur, pre);
     }
 }
 
@@ -1078,7 +1206,10 @@ static void launch_unified(lbg_block b, const SweepArgs& a, bool forced, cudaStr
             const unsigned grid = (unsigned)std::max(1LL, std::min<long long>(want, (long long)sms * ctas));
             kern<<<grid, 128, 0, st>>>(a);
         };
-        if (kF || per_sm == 4)
+        static const int pipe = env_int("LBG_K12_PIPE", 1);
+        if (!kF && pipe && a.pidx0)
+            go(coupled_unified_pipe_kernel<kU, kV>, 3);
+        else if (kF || per_sm == 4)
             go(coupled_unified_kernel<kF, kU, kV, 4>, 4);
         else if (per_sm == 6)
             go(coupled_unified_kernel<kF, kU, kV, 6>, 6);
@@ -1146,6 +1277,14 @@ lbg_status lbg_sweep(lbg_block b, const lbg_fluid* fl, const lbg_box* range) {
     if (lbg_status s = add_boxes(a, b->L, range, 1)) return s;
     Span span(b, LBG_CAT_PSM);
     const bool fo = forced(fl);
+    // a coupled block mapped from an empty particle list has count 0 everywhere: the PSM sweep
+    // is collide_cell in every cell (psm.cpp:236-240), so it is the plain K1 sweep exactly
+    const bool no_cover = b->coupling && b->v_snap && b->map_ids_valid && b->map_ids.empty() && !b->cov_dirty;
+    if (no_cover) {
+        fo ? launch_box<true, false>(a, b->stream) : launch_box<false, false>(a, b->stream);
+        LBG_LAUNCH_CHECK();
+        return verify_writes(b, a);
+    }
     if (b->coupling) {
         if (k12_on()) {
             launch_unified(b, a, fo, b->stream);

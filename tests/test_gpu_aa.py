@@ -44,7 +44,7 @@ def test_aa_matches_double_buffer_every_step(gpu, oracle, dims, fext):
         blk.swap()
         got = interior(blk.download_src())
         assert equal_bits(got, ref[s]), f"step {s + 1}"
-    assert blk.sync()["unstable_cells"] == 0
+    assert blk.sync()["unstable"] == 0
     # the oracle's first step too (pull from periodically filled ghosts)
     o = src0.copy()
     oracle.fill_periodic(dims, o, ALL_P)

@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+timeout 900 python -m pytest tests/test_gpu_aa.py tests/test_gpu_parity.py tests/test_dropin.py -m gpu -q -x > gpurun_out/r02_g15_pytest.log 2>&1; echo rc=$? >> gpurun_out/r02_g15_pytest.log
+for env in "LBG_K12_PIPE=1" "LBG_K12_PIPE=0" "LBG_K12_PIPE=1"; do
+  env $env AB_REDUCE=1 AB_STEPS=30 timeout 300 python tests/ab_coupled_sweep.py >> gpurun_out/r02_g15_ab.log 2>&1
+done
+AB_REDUCE=1 AB_STEPS=3 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02_g15_launches.csv python tests/ab_coupled_sweep.py > /dev/null 2>&1
+AB_STEPS=2 timeout 900 ncu --set full --import-source on --clock-control none -k regex:unified_pipe -s 3 -c 1 -o gpurun_out/r02_pipe2 python tests/ab_coupled_sweep.py > /dev/null 2>&1
