@@ -110,6 +110,18 @@ __device__ __forceinline__ void pull(const SweepArgs& a, int i, int j, int k, lo
     }
 }
 
+// pull() for a block with no in-kernel wrap: no per-population wrap selects
+template <bool kWrap>
+__device__ __forceinline__ void pull_t(const SweepArgs& a, int i, int j, int k, long long base, double (&f)[kQ]) {
+    if constexpr (kWrap) {
+        pull(a, i, j, k, base, f);
+    } else {
+        const Layout& L = a.L;
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) f[q] = a.src[q * L.plane + LBG_IDX(base - L.shift(q), L.plane, a.err)];
+    }
+}
+
 // plain cell; in a coupled block covered cells are left to K2 (kSkipCovered)
 template <bool kForced, bool kSkipCovered>
 __device__ __forceinline__ bool srt_cell_at(const SweepArgs& a, int i, int j, int k) {
@@ -164,6 +176,32 @@ __device__ __forceinline__ int entry0_index(const SweepArgs& a, long long fc) {
         return (unsigned)p < (unsigned)a.n_snaps ? p : -1;
     }
     return a.sidx(a.id0[fc]);
+}
+
+// solid velocity of an entry named by its particle id (entry 1 of a two-entry cell)
+template <bool kVsnap>
+__device__ __forceinline__ void solid_velocity_id(const SweepArgs& a, int id, long long fc, int i, int j, int k,
+                                                  double (&v)[3]) {
+    if constexpr (kVsnap) {
+        const int p = a.sidx(id);
+        if (p < 0) {
+            atomicAdd(&a.err->unknown, 1ull);
+            v[0] = v[1] = v[2] = 0.0;
+            return;
+        }
+        const lbg_snapshot& s = a.snaps[p];
+        const double r0 = ((double)(a.blk_lo[0] + i) + 0.5) - s.x[0];
+        const double r1 = ((double)(a.blk_lo[1] + j) + 0.5) - s.x[1];
+        const double r2 = ((double)(a.blk_lo[2] + k) + 0.5) - s.x[2];
+        v[0] = s.u[0] + (s.omega[1] * r2 - s.omega[2] * r1);
+        v[1] = s.u[1] + (s.omega[2] * r0 - s.omega[0] * r2);
+        v[2] = s.u[2] + (s.omega[0] * r1 - s.omega[1] * r0);
+    } else {
+        const double* w = a.v1 + 3 * fc;
+        v[0] = w[0];
+        v[1] = w[1];
+        v[2] = w[2];
+    }
 }
 
 // solid velocity of the first entry of a one-entry-segment lane, selected to 0 where the cell
@@ -828,19 +866,34 @@ __global__ void __launch_bounds__(128, kMinBlocks) coupled_unified_kernel(const 
 // through the unrolled loop (a copy of an in-flight register would wait for it).
 struct USeg {
     double f[kQ];
-    double bt, b0;
+    double bt, b0, b1;
     long long fc, base;
-    int i, j, k, cnt, pe;
+    int i, j, k, cnt, pe, id1, mx;
     bool act;
 };
 
 struct UPre {
-    double rho, ux, uy, uz, usq, v[3];
-    int mx;
+    double rho, ux, uy, uz, usq, v[3], v1[3];
     bool ok;
 };
 
-__device__ __forceinline__ void useg_issue(const SweepArgs& a, long long s, int segs_x, int ny_b, int lane,
+// the count bytes of segment s (32 lanes), 0 past the end
+__device__ __forceinline__ int useg_count(const SweepArgs& a, long long s, long long nseg, int segs_x, int ny_b,
+                                          int lane) {
+    if (s >= nseg) return 0;
+    const Layout& L = a.L;
+    const unsigned su = (unsigned)s, r = su / (unsigned)segs_x;
+    const int i = a.i0 + 32 * (int)(su - r * (unsigned)segs_x) + lane;
+    if (i >= L.nx) return 0;
+    return (int)a.count[LBG_IDX(L.frac(i, a.lo[1] + (int)(r % (unsigned)ny_b), a.lo[2] + (int)(r / (unsigned)ny_b)),
+                                a.cells, a.err)];
+}
+
+// the loads of segment s, whose counts `cnt` arrived one segment earlier: the populations
+// unless it is a two-entry segment (psm_seg_kernel<two> sweeps those), the cell fields only
+// for a one-entry segment — nothing an SRT segment does not use
+template <bool kTwoInline, bool kWrap>
+__device__ __forceinline__ void useg_issue(const SweepArgs& a, long long s, int segs_x, int ny_b, int lane, int cnt,
                                            USeg& u) {
     const Layout& L = a.L;
     // 32-bit index math (a 64-bit division is a ~100-instruction software routine)
@@ -851,40 +904,82 @@ __device__ __forceinline__ void useg_issue(const SweepArgs& a, long long s, int 
     const bool inx = u.i < L.nx;
     u.fc = LBG_IDX(L.frac(inx ? u.i : L.nx - 1, u.j, u.k), a.cells, a.err);
     u.act = inx && u.i >= a.lo[0] && u.i < a.hi[0];
-    u.cnt = inx ? (int)a.count[u.fc] : 0;
-    u.bt = a.btot[u.fc];
-    u.b0 = a.b0[u.fc];
-    u.pe = a.pidx0[u.fc];
-    if (u.act) {
+    u.cnt = cnt;
+    u.mx = (int)__reduce_max_sync(0xffffffffu, (unsigned)cnt);
+    if (u.mx >= 1) {
+        u.bt = a.btot[u.fc];
+        u.b0 = a.b0[u.fc];
+        u.pe = a.pidx0[u.fc];
+    }
+    if (kTwoInline && u.mx >= 2) {
+        u.b1 = a.b1[u.fc];
+        u.id1 = a.id1[u.fc];
+    }
+    if (u.act && (kTwoInline || u.mx <= 1)) {
         u.base = LBG_IDX(L.idx(u.i, u.j, u.k), L.plane, a.err);
-        pull(a, u.i, u.j, u.k, u.base, u.f);
+        pull_t<kWrap>(a, u.i, u.j, u.k, u.base, u.f);
     }
 }
 
-template <bool kVsnap>
+template <bool kVsnap, bool kTwoInline>
 __device__ __forceinline__ void useg_pre(const SweepArgs& a, const USeg& u, UPre& pre) {
-    pre.mx = (int)__reduce_max_sync(0xffffffffu, (unsigned)u.cnt);
     pre.ok = true;
-    if (pre.mx >= 2 || !u.act) return;
+    if ((!kTwoInline && u.mx >= 2) || !u.act) return;
     const bool cov = u.cnt > 0;
-    if (pre.mx == 1) {
+    if (u.mx >= 1) {
         const int p = kVsnap ? ((unsigned)u.pe < (unsigned)a.n_snaps ? u.pe : -1) : -1;
         solid_velocity_sel<kVsnap>(a, cov, u.fc, u.i, u.j, u.k, pre.v, p);
+    }
+    if (kTwoInline && u.mx >= 2) {
+        pre.v1[0] = pre.v1[1] = pre.v1[2] = 0.0;
+        if (u.cnt > 1) solid_velocity_id<kVsnap>(a, u.id1, u.fc, u.i, u.j, u.k, pre.v1);
     }
     moments(u.f, pre.rho, pre.ux, pre.uy, pre.uz);
     pre.usq = (pre.ux * pre.ux + pre.uy * pre.uy) + pre.uz * pre.uz;
     pre.ok = pre.rho > 0.0 && pre.usq <= kMaxVelocity * kMaxVelocity && isfinite(pre.rho);
 }
 
-template <bool kFused, bool kVsnap>
+template <bool kFused, bool kVsnap, bool kTwoInline>
 __device__ __forceinline__ void useg_finish(const SweepArgs& a, const USeg& u, const UPre& pre) {
-    if (pre.mx >= 2) return;  // psm_seg_kernel<two> sweeps this segment
+    if (!kTwoInline && u.mx >= 2) return;  // psm_seg_kernel<two> sweeps this segment
+    if (kTwoInline && u.mx >= 2) {
+        // two-entry segment: the pair-scheduled two-entry operator (entry 1 where count 2)
+        double m2[2][3] = {{0, 0, 0}, {0, 0, 0}};
+        double cc[3] = {0, 0, 0};
+        int p0 = -1, p1 = -1;
+        bool ok = true;
+        if (u.act) {
+            const bool cov = u.cnt > 0, two = u.cnt > 1;
+            ok = psm_cell_two<false>(u.f, a.inv_tau, a.F, cov ? u.bt : 0.0, cov ? u.b0 : 0.0, pre.v, two ? u.b1 : 0.0,
+                                     pre.v1, two, a.dst, a.L.plane, u.base, m2);
+            if constexpr (!kFused) {
+                if (cov)
+                    for (int d = 0; d < 3; ++d) a.m0[3 * u.fc + d] = m2[0][d];
+                if (two)
+                    for (int d = 0; d < 3; ++d) a.m1[3 * u.fc + d] = m2[1][d];
+            } else if (cov) {
+                cc[0] = (double)(a.blk_lo[0] + u.i) + 0.5;
+                cc[1] = (double)(a.blk_lo[1] + u.j) + 0.5;
+                cc[2] = (double)(a.blk_lo[2] + u.k) + 0.5;
+                p0 = (unsigned)u.pe < (unsigned)a.n_snaps ? u.pe : -1;
+                if (two) p1 = a.sidx(u.id1);
+                if (p0 < 0 || (two && p1 < 0)) atomicAdd(&a.err->unknown, 1ull);
+            }
+            mark_write(a, u.i, u.j, u.k);
+        }
+        count_bad(a.err, !ok);
+        if constexpr (kFused) {
+            fused_accumulate(a, p0, m2[0], cc);
+            fused_accumulate(a, p1, m2[1], cc);
+        }
+        return;
+    }
     double m[3] = {0, 0, 0};
     double cc[3] = {0, 0, 0};
     int p0 = -1;
     if (u.act) {
         const auto g = [&](int q) { return u.f[q]; };
-        if (pre.mx == 0) {
+        if (u.mx == 0) {
             srt_pairs_g(g, pre.rho, pre.ux, pre.uy, pre.uz, pre.usq, a.inv_tau, a.dst, a.L.plane, u.base);
         } else {
             const bool cov = u.cnt > 0;
@@ -905,10 +1000,10 @@ __device__ __forceinline__ void useg_finish(const SweepArgs& a, const USeg& u, c
     }
     count_bad(a.err, !pre.ok);
     if constexpr (kFused)
-        if (pre.mx == 1) fused_accumulate(a, p0, m, cc);
+        if (u.mx == 1) fused_accumulate(a, p0, m, cc);
 }
 
-template <bool kFused, bool kVsnap>
+template <bool kFused, bool kVsnap, bool kTwoInline, bool kWrap>
 __global__ void __launch_bounds__(128, 3) coupled_unified_pipe_kernel(const SweepArgs a) {
     const int lane = threadIdx.x & 31;
     const long long warp = (long long)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
@@ -918,15 +1013,19 @@ __global__ void __launch_bounds__(128, 3) coupled_unified_pipe_kernel(const Swee
     const long long nseg = (long long)segs_x * ny_b * (a.hi[2] - a.lo[2]);
     if (warp >= nseg) return;  // warp-uniform
     // one body: a second inlined copy of the operators would overflow the instruction cache.
-    // The copy cur = nxt happens a whole finish() after nxt's loads were issued.
+    // Counts run two segments ahead of the sweep and the loads one segment ahead; the copies
+    // (cur = nxt, c1 = cfar) happen a whole finish() after their loads were issued.
     USeg cur, nxt;
     UPre pre;
-    useg_issue(a, warp, segs_x, ny_b, lane, nxt);
+    useg_issue<kTwoInline, kWrap>(a, warp, segs_x, ny_b, lane, useg_count(a, warp, nseg, segs_x, ny_b, lane), nxt);
+    int cfar = useg_count(a, warp + nwarps, nseg, segs_x, ny_b, lane);
     for (long long s = warp; s < nseg; s += nwarps) {
         cur = nxt;
-        useg_pre<kVsnap>(a, cur, pre);
-        if (s + nwarps < nseg) useg_issue(a, s + nwarps, segs_x, ny_b, lane, nxt);
-        useg_finish<kFused, kVsnap>(a, cur, pre);
+        useg_pre<kVsnap, kTwoInline>(a, cur, pre);
+        const int c1 = cfar;
+        cfar = useg_count(a, s + 2 * nwarps, nseg, segs_x, ny_b, lane);
+        if (s + nwarps < nseg) useg_issue<kTwoInline, kWrap>(a, s + nwarps, segs_x, ny_b, lane, c1, nxt);
+        useg_finish<kFused, kVsnap, kTwoInline>(a, cur, pre);
     }
 }
 
@@ -1207,8 +1306,18 @@ static void launch_unified(lbg_block b, const SweepArgs& a, bool forced, cudaStr
             kern<<<grid, 128, 0, st>>>(a);
         };
         static const int pipe = env_int("LBG_K12_PIPE", 1);
+        static const int two_inline = env_int("LBG_K12_TWO", 1);
+        static const int nowrap = env_int("LBG_K12_NOWRAP", 1);  // 0: the generic pull (A/B)
+        const bool wrapped = a.wrap[0] || a.wrap[1] || a.wrap[2] || !nowrap;
+        if (!kF && pipe && a.pidx0 && two_inline) {
+            if (wrapped)
+                go(coupled_unified_pipe_kernel<kU, kV, true, true>, 3);
+            else
+                go(coupled_unified_pipe_kernel<kU, kV, true, false>, 3);
+            return;  // every segment swept by the one kernel
+        }
         if (!kF && pipe && a.pidx0)
-            go(coupled_unified_pipe_kernel<kU, kV>, 3);
+            go(coupled_unified_pipe_kernel<kU, kV, false, true>, 3);
         else if (kF || per_sm == 4)
             go(coupled_unified_kernel<kF, kU, kV, 4>, 4);
         else if (per_sm == 6)

@@ -2,7 +2,8 @@
 -DLBG_CHECKED): every computed buffer index in the sweep, mapping, reduction, boundary and halo
 kernels is range-checked, and every sweep verifies that it wrote each cell of its box exactly
 once across all of its kernels (the unified coupled sweep || the two-entry kernel, K1 || K2 on
-two streams, TMA-fed K2, shell sweeps) and nothing outside. lbg_sync turns a violation into an
+two streams, TMA-fed K2, shell sweeps, the pipelined and plain unified sweeps with two-entry
+segments inline or in their own kernel) and nothing outside. lbg_sync turns a violation into an
 error, so any out-of-range index or double/missing write fails the suite. This is the
 repository's memcheck/racecheck (compute-sanitizer is closed on the GPU pool). The library is
 the same sources; LBG_LIB points the ctypes binding at it and LD_LIBRARY_PATH the drop-in."""
@@ -68,7 +69,8 @@ def test_dropin_suites_checked():
     _run(["test_gpu_checked.py", "test_dropin.py", "test_gpu_multi.py"], k=SELF)
 
 
-@pytest.mark.parametrize("env", [{"LBG_K12": "0"}, {"LBG_K12": "0", "LBG_K2_MODE": "2"},
+@pytest.mark.parametrize("env", [{"LBG_K12_PIPE": "0"}, {"LBG_K12_TWO": "0"},
+                                 {"LBG_K12": "0"}, {"LBG_K12": "0", "LBG_K2_MODE": "2"},
                                  {"LBG_K12": "0", "LBG_K2_CONCURRENT": "0"}, {"LBG_SWEEP_PAIR": "1"}])
 def test_sweep_variants_checked(env):
     _run(["test_gpu_parity.py", "test_dropin.py"], extra_env=env,

@@ -1,9 +1,12 @@
 """The coupled-sweep parity tests under every selectable kernel variant (the switches are read
 once per process, so each variant runs the tests in a subprocess):
+  LBG_K12_PIPE=0 the unified coupled sweep without the register pipeline (LBG_K12_SM=4/6 its
+  occupancy caps), LBG_K12_TWO=0 two-entry segments in their own kernel, LBG_K12_NOWRAP=0 the
+  generic pull for unwrapped blocks;
   LBG_K12=0 the K1 || K2 split instead of the unified coupled sweep, with LBG_K2_MODE=0 plain
   segment loop, 1 register-pipelined (split default), 2 TMA-fed one-entry K2, LBG_K2_CONCURRENT=0
   K2 after K1 on one stream; LBG_DIRECT_INDEX=0 solid velocities through id0 -> id table;
-  LBG_K12_SM=4/6 other occupancy caps; LBG_SWEEP_PAIR=1 the 128-bit K1;
+  LBG_SWEEP_PAIR=1 the 128-bit K1;
   LBDEM_GPU_SWEEP=split the drop-in in the reference's inner / halo / BC / outer-shell order;
   LBDEM_GPU_PREMAP=1 the next step's mapping prepared during the last DEM sub-cycle;
   LBDEM_GPU_HALO=stage the staged 19-q device halo instead of the pushed one."""
@@ -21,9 +24,11 @@ SELECT = "coupled or setu or fused or mapping_and_solid or shear or sweep"
 DROPIN = "config1_known_answers or particle_bed or decomposition_invariance or config5_layout_scratch"
 
 
-@pytest.mark.parametrize("env", [{"LBG_K12": "0"}, {"LBG_K12": "0", "LBG_K2_MODE": "0"},
+@pytest.mark.parametrize("env", [{"LBG_K12_PIPE": "0"}, {"LBG_K12_TWO": "0"}, {"LBG_K12_NOWRAP": "0"},
+                                 {"LBG_K12": "0"}, {"LBG_K12": "0", "LBG_K2_MODE": "0"},
                                  {"LBG_K12": "0", "LBG_K2_MODE": "2"}, {"LBG_K12": "0", "LBG_K2_CONCURRENT": "0"},
-                                 {"LBG_DIRECT_INDEX": "0"}, {"LBG_K12_SM": "4"}, {"LBG_K12_SM": "6"},
+                                 {"LBG_DIRECT_INDEX": "0"}, {"LBG_K12_PIPE": "0", "LBG_K12_SM": "4"},
+                                 {"LBG_K12_PIPE": "0", "LBG_K12_SM": "6"},
                                  {"LBG_SWEEP_PAIR": "1"}, {"LBDEM_GPU_SWEEP": "split"}, {"LBDEM_GPU_PREMAP": "1"},
                                  {"LBDEM_GPU_HALO": "stage"}])
 def test_parity_suite_under_variant(env):
