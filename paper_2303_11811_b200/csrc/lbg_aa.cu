@@ -23,7 +23,10 @@
 namespace lbg {
 
 struct AAArgs {
-    double* buf;  // one buffer: loads and stores alias (no __restrict__)
+    // the one buffer, passed twice: with one pointer the compiler keeps the 19 load addresses
+    // live for the stores (124 registers); as two it recomputes them (70, like K1)
+    const double* buf_r;
+    double* buf_w;
     Layout L;
     double inv_tau;
     Force F;
@@ -42,6 +45,11 @@ __device__ __forceinline__ long long aa_off(const Layout& L, int i, int j, int k
 template <bool kForced, bool kOdd>
 __global__ void __launch_bounds__(256) sweep_aa_kernel(const AAArgs a) {
     const Layout& L = a.L;
+    // read and write views of the one buffer: every value a thread stores depends on all 19 it
+    // loaded (the density), so no store can precede a load of the same slot, and no two threads
+    // touch one slot — the views never alias in any order the compiler can produce
+    const double* __restrict__ rd = a.buf_r;
+    double* __restrict__ wr = a.buf_w;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y * blockDim.y + threadIdx.y;
     const int k = blockIdx.z;
@@ -49,20 +57,32 @@ __global__ void __launch_bounds__(256) sweep_aa_kernel(const AAArgs a) {
     if (i < L.nx && j < L.ny) {
         double f[kQ];
         const long long base = L.idx(i, j, k);
+        // odd step: the wrapped neighbour coordinates once per cell; the 9 (dy, dz) rows D3Q19
+        // reaches serve both the pulls (x - c_q) and the stores (x + c_q)
+        int xs[3] = {i == 0 ? L.nx - 1 : i - 1, i, i == L.nx - 1 ? 0 : i + 1};
+        int ys[3] = {j == 0 ? L.ny - 1 : j - 1, j, j == L.ny - 1 ? 0 : j + 1};
+        int zs[3] = {k == 0 ? L.nz - 1 : k - 1, k, k == L.nz - 1 ? 0 : k + 1};
+        auto at = [&](int q, int sgn) {  // slot q of the cell at (i, j, k) + sgn * c_q
+            return (long long)q * L.plane + L.row(ys[1 + sgn * cy(q)], zs[1 + sgn * cz(q)]) + xs[1 + sgn * cx(q)];
+        };
         if (kOdd) {
 #pragma unroll
-            for (int q = 0; q < kQ; ++q) f[q] = a.buf[aa_off(L, i, j, k, q, -1)];
+            for (int q = 0; q < kQ; ++q) f[q] = rd[at(q, -1)];
         } else {
 #pragma unroll
-            for (int q = 0; q < kQ; ++q) f[q] = a.buf[opposite(q) * L.plane + base];
+            for (int q = 0; q < kQ; ++q) f[q] = rd[opposite(q) * L.plane + base];
         }
         ok = srt_cell<kForced>(f, a.inv_tau, a.F);
         if (kOdd) {
+            // the store addresses are the load addresses of the opposite populations: make the
+            // coordinates opaque here so they are recomputed rather than held in 38 registers
+            asm volatile("" : "+r"(xs[0]), "+r"(xs[1]), "+r"(xs[2]), "+r"(ys[0]), "+r"(ys[1]), "+r"(ys[2]),
+                         "+r"(zs[0]), "+r"(zs[1]), "+r"(zs[2]));
 #pragma unroll
-            for (int q = 0; q < kQ; ++q) a.buf[aa_off(L, i, j, k, opposite(q), -1)] = f[q];
+            for (int q = 0; q < kQ; ++q) wr[at(opposite(q), -1)] = f[q];
         } else {
 #pragma unroll
-            for (int q = 0; q < kQ; ++q) a.buf[q * L.plane + base] = f[q];
+            for (int q = 0; q < kQ; ++q) wr[q * L.plane + base] = f[q];
         }
     }
     const unsigned m = __ballot_sync(0xffffffffu, !ok);
@@ -84,7 +104,8 @@ __global__ void __launch_bounds__(256) aa_unstream_kernel(const double* __restri
 
 lbg_status aa_sweep(lbg_block b, const lbg_fluid* fl) {
     AAArgs a{};
-    a.buf = b->buf[b->cur];
+    a.buf_r = b->buf[b->cur];
+    a.buf_w = b->buf[b->cur];
     a.L = b->L;
     a.inv_tau = 1.0 / fl->tau;  // lbm.cpp:30
     a.F = {fl->f_ext[0], fl->f_ext[1], fl->f_ext[2]};
