@@ -185,12 +185,14 @@ __device__ __forceinline__ double axis_gap(double lo, double hi, double x) {
 }
 
 struct MapCand {
-    double x0[32], x1[32], x2[32], r[32], fr[32], out2[32], in2[32];
+    double x0[32], x1[32], x2[32], r[32], fr[32], out2[32], in2[32], gxy[32];
     int id[32], idx[32];
 };
 
+// stage candidates [base, base + m) of the bin list; gxy = the squared x/y gap between the
+// candidate and the warp's 8 x 4 column of cell centres (the z-independent part of the cull)
 __device__ __forceinline__ void stage_cands(const MapArgs& a, const int* list, int base, int m, int lane,
-                                            MapCand& sc) {
+                                            double wx0, double wx1, double wy0, double wy1, MapCand& sc) {
     if (lane < m) {
         const int ix = list[LBG_IDX((list - a.items) + base + lane, a.items_cap, a.err) - (list - a.items)];
         const lbg_snapshot& p = a.s[ix];
@@ -203,12 +205,15 @@ __device__ __forceinline__ void stage_cands(const MapArgs& a, const int* list, i
         const double ro = p.r + p.f_r, ri = ro - 1.0;
         sc.out2[lane] = (ro * ro) * (1.0 + 1e-9);
         sc.in2[lane] = ri > 0.0 ? (ri * ri) * (1.0 - 1e-9) : -1.0;
+        const double g0 = axis_gap(wx0, wx1, p.x[0]), g1 = axis_gap(wy0, wy1, p.x[1]);
+        sc.gxy[lane] = g0 * g0 + g1 * g1;
         sc.id[lane] = p.id;
     }
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(32 * kMapWarps) map_warp_kernel(const MapArgs a) {
+template <int kMinBlocks>
+__global__ void __launch_bounds__(32 * kMapWarps, kMinBlocks) map_warp_kernel(const MapArgs a) {
     __shared__ MapCand cand_all[kMapWarps];
     const BinGeom& g = a.g;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -227,7 +232,7 @@ __global__ void __launch_bounds__(32 * kMapWarps) map_warp_kernel(const MapArgs 
     const double wx0 = (double)(g.lo[0] + bx * kBin) + 0.5, wx1 = wx0 + 7.0;
     const double wy0 = (double)(g.lo[1] + by * kBin + yh * 4) + 0.5, wy1 = wy0 + 3.0;
     const bool inxy = i < g.dims[0] && j < g.dims[1];
-    if (n <= 32) stage_cands(a, list, 0, n, lane, sc);
+    if (n <= 32) stage_cands(a, list, 0, n, lane, wx0, wx1, wy0, wy1, sc);
     unsigned long long overfull = 0;
     for (int zz = 0; zz < kBin; ++zz) {
         const int k = bz * kBin + zz;
@@ -241,7 +246,7 @@ __global__ void __launch_bounds__(32 * kMapWarps) map_warp_kernel(const MapArgs 
             const int m = min(32, n - base);
             if (n > 32) {
                 __syncwarp();  // every lane is done with the previous chunk
-                stage_cands(a, list, base, m, lane, sc);
+                stage_cands(a, list, base, m, lane, wx0, wx1, wy0, wy1, sc);
             }
             // warp-level cull: the squared gap between the candidate and the slab's box of cell
             // centres bounds every cell's radicand from below in floating point too (each
@@ -249,9 +254,8 @@ __global__ void __launch_bounds__(32 * kMapWarps) map_warp_kernel(const MapArgs 
             // the box rejects only candidates every cell rejects (rad > out2)
             bool rl = false;
             if (lane < m) {
-                const double g0 = axis_gap(wx0, wx1, sc.x0[lane]), g1 = axis_gap(wy0, wy1, sc.x1[lane]);
                 const double g2 = axis_gap(cc2, cc2, sc.x2[lane]);
-                rl = !((g0 * g0 + g1 * g1) + g2 * g2 > sc.out2[lane]);
+                rl = !(sc.gxy[lane] + g2 * g2 > sc.out2[lane]);  // (g0 g0 + g1 g1) + g2 g2
             }
             const unsigned rel = __ballot_sync(0xffffffffu, rl);
             if (!inxy || over) continue;
@@ -495,22 +499,41 @@ __global__ void __launch_bounds__(32 * kWalkWarps, kMinBlocks) walk_chain_kernel
     bool any = false;
     int nk = 0;
 
+    // keys: box-local (di, dj, dk) packed in 10 bits each when the box allows (no division to
+    // recover the cell in pass 2), else the cell index
+    const bool packed = ex <= 1024 && ey <= 1024 && hi[2] - lo[2] + 1 <= 1024;
+    // each lane's next cells (t = step * 32 + u * 8 + lane-in-group) as running coordinates:
+    // fetch() is called for consecutive steps and advances them by 32 cells (no division)
+    int ci[4], cj[4], ck[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const unsigned tu = (unsigned)(u * 8 + gl), r = tu / (unsigned)ex;
+        ci[u] = lo[0] + (int)(tu - r * (unsigned)ex);
+        cj[u] = lo[1] + (int)(r % (unsigned)ey);
+        ck[u] = lo[2] + (int)(r / (unsigned)ey);
+    }
     auto fetch = [&](long long step, WalkQuad& q) {
+        (void)step;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const long long t = step * 32 + u * 8 + gl;
             q.cnt[u] = 0;
             q.c[u] = 0;
             q.e0[u] = q.e1[u] = -1;
-            if (t < total) {
-                // 32-bit index math (boxes hold < 2^31 cells; 64-bit division is a long routine)
-                const unsigned tu = (unsigned)t, r = tu / (unsigned)ex;
-                const int i = lo[0] + (int)(tu - r * (unsigned)ex), j = lo[1] + (int)(r % (unsigned)ey),
-                          k = lo[2] + (int)(r / (unsigned)ey);
-                q.c[u] = LBG_IDX(((long long)k * g.dims[1] + j) * g.dims[0] + i, a.cells, a.err);
-                q.cnt[u] = a.count[q.c[u]];
-                q.e0[u] = a.id0[q.c[u]];
-                q.e1[u] = a.id1[q.c[u]];
+            if (nonempty && ck[u] <= hi[2]) {
+                const long long c =
+                    LBG_IDX(((long long)ck[u] * g.dims[1] + cj[u]) * g.dims[0] + ci[u], a.cells, a.err);
+                q.cnt[u] = a.count[c];
+                q.e0[u] = a.id0[c];
+                q.e1[u] = a.id1[c];
+                q.c[u] = packed ? (((long long)(ck[u] - lo[2]) << 20) | ((cj[u] - lo[1]) << 10) | (ci[u] - lo[0])) : c;
+                ci[u] += 32;
+                while (ci[u] > hi[0]) {
+                    ci[u] -= ex;
+                    if (++cj[u] > hi[1]) {
+                        cj[u] = lo[1];
+                        ++ck[u];
+                    }
+                }
             }
         }
     };
@@ -529,12 +552,21 @@ __global__ void __launch_bounds__(32 * kWalkWarps, kMinBlocks) walk_chain_kernel
                 gm[u][0] = gm[u][1] = gm[u][2] = 0.0;
                 if (e < nk) {
                     const unsigned key = kb[e];
-                    const long long c = LBG_IDX((long long)(key >> 1), a.cells, a.err);
+                    long long c;
+                    if (packed) {
+                        const unsigned v = key >> 1;
+                        c = ((long long)(lo[2] + (int)(v >> 20)) * g.dims[1] + (lo[1] + (int)((v >> 10) & 1023u))) *
+                                g.dims[0] +
+                            (lo[0] + (int)(v & 1023u));
+                    } else {
+                        c = (long long)(key >> 1);
+                    }
+                    c = LBG_IDX(c, a.cells, a.err);
                     const double* mp = ((key & 1u) ? a.m1 : a.m0) + 3 * c;
                     gm[u][0] = mp[0];
                     gm[u][1] = mp[1];
                     gm[u][2] = mp[2];
-                    gc[u] = (c << 1) | (key & 1u);
+                    gc[u] = packed ? (long long)key : ((c << 1) | (key & 1u));
                 }
             }
         };
@@ -543,13 +575,24 @@ __global__ void __launch_bounds__(32 * kWalkWarps, kMinBlocks) walk_chain_kernel
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 if (gc[u] < 0) continue;
-                const long long cell = gc[u] >> 1;
-                const unsigned cu = (unsigned)cell, row = cu / (unsigned)g.dims[0];
-                const int ci = (int)(cu - row * (unsigned)g.dims[0]), cj = (int)(row % (unsigned)g.dims[1]),
-                          ck = (int)(row / (unsigned)g.dims[1]);
-                const double r0 = ((double)(g.lo[0] + ci) + 0.5) - x0;
-                const double r1 = ((double)(g.lo[1] + cj) + 0.5) - x1;
-                const double r2 = ((double)(g.lo[2] + ck) + 0.5) - x2;
+                int xi, xj, xk;
+                long long cell;
+                if (packed) {
+                    const unsigned v = (unsigned)(gc[u] >> 1);
+                    xi = lo[0] + (int)(v & 1023u);
+                    xj = lo[1] + (int)((v >> 10) & 1023u);
+                    xk = lo[2] + (int)(v >> 20);
+                    cell = ((long long)xk * g.dims[1] + xj) * g.dims[0] + xi;
+                } else {
+                    cell = gc[u] >> 1;
+                    const unsigned cu = (unsigned)cell, row = cu / (unsigned)g.dims[0];
+                    xi = (int)(cu - row * (unsigned)g.dims[0]);
+                    xj = (int)(row % (unsigned)g.dims[1]);
+                    xk = (int)(row / (unsigned)g.dims[1]);
+                }
+                const double r0 = ((double)(g.lo[0] + xi) + 0.5) - x0;
+                const double r1 = ((double)(g.lo[1] + xj) + 0.5) - x1;
+                const double r2 = ((double)(g.lo[2] + xk) + 0.5) - x2;
                 const double* m = gm[u];
                 double* t = tw[u * 8 + gl];
                 t[0] = m[0];
@@ -898,7 +941,15 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
         // count and btot of every cell were zeroed by map_zero_kernel, so the mapping kernel
         // skips bins without candidates and writes only covered cells
         const long long units = 2 * nbins;
-        map_warp_kernel<<<(unsigned)((units + kMapWarps - 1) / kMapWarps), 32 * kMapWarps, 0, b->stream>>>(a);
+        static const int minb = [] {  // LBG_MAP_MINB: 5 caps the registers at 48 (A/B)
+            const char* e = std::getenv("LBG_MAP_MINB");
+            return e ? std::atoi(e) : 4;
+        }();
+        const unsigned mgrid = (unsigned)((units + kMapWarps - 1) / kMapWarps);
+        if (minb == 5)
+            map_warp_kernel<5><<<mgrid, 32 * kMapWarps, 0, b->stream>>>(a);
+        else
+            map_warp_kernel<4><<<mgrid, 32 * kMapWarps, 0, b->stream>>>(a);
         LBG_LAUNCH_CHECK();
         const long long rows = (long long)b->L.ny * b->L.nz;
         const long long nseg = rows * ((b->L.nx + 31) / 32);
