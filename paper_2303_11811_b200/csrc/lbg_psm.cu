@@ -408,7 +408,7 @@ __device__ __forceinline__ void nm_add(double& sum, double& comp, double v) {  /
 //   box source: the snapshot's reach (r + max(1/2, f_r), the mapping's candidate test) when
 //   the fraction field was mapped from these positions; otherwise entry_box_kernel takes the
 //   min/max cell of every particle's entries from the field itself (order-independent).
-constexpr int kWalkWarps = 4;   // warps per CTA
+constexpr int kWalkWarps = 1;   // warps per CTA (one: register-limited residency is per warp)
 constexpr int kWalkGroups = 4;  // particles per warp: lane groups of 8
 constexpr int kWalkKeys = 256;  // entry keys staged per particle before a replay flush
 
@@ -451,8 +451,10 @@ struct WalkQuad {
 // only count and ids are read; pass 2 (whenever a group's stage nears full, and at the end)
 // gathers the momenta 32 per group at a time, writes the six terms of each entry, zeroes the
 // entry's scratch (psm.cpp:305), and lanes 0..5 of each group replay them in order.
-template <int kMinBlocks>
-__global__ void __launch_bounds__(32 * kWalkWarps, kMinBlocks) walk_chain_kernel(const WalkArgs a) {
+// __maxnreg__(120): 17 resident warps per SM hold 68 particles, so a 10^4-particle block
+// (67.6 per SM) runs in one wave instead of 1.06 (16 warps at the natural 125 registers)
+template <int kRegs>
+__global__ void __maxnreg__(kRegs) walk_chain_kernel(const WalkArgs a) {
     __shared__ unsigned keys_all[kWalkWarps][kWalkGroups][kWalkKeys];
     __shared__ double terms_all[kWalkWarps][kWalkGroups][32][7];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1156,15 +1158,15 @@ lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int c
         }
         if (n > 0) {
             const int per_cta = kWalkWarps * kWalkGroups;
-            static const int minb = [] {
-                const char* e = std::getenv("LBG_WALK_MINB");
-                return e ? std::atoi(e) : 4;
+            static const int regs = [] {  // LBG_WALK_REGS: 128 (natural) or 120 (A/B)
+                const char* e = std::getenv("LBG_WALK_REGS");
+                return e ? std::atoi(e) : 120;
             }();
             const unsigned grid = (unsigned)((n + per_cta - 1) / per_cta);
-            if (minb == 5)
-                walk_chain_kernel<5><<<grid, 32 * kWalkWarps, 0, b->stream>>>(a);
+            if (regs >= 128)
+                walk_chain_kernel<128><<<grid, 32 * kWalkWarps, 0, b->stream>>>(a);
             else
-                walk_chain_kernel<4><<<grid, 32 * kWalkWarps, 0, b->stream>>>(a);
+                walk_chain_kernel<120><<<grid, 32 * kWalkWarps, 0, b->stream>>>(a);
             LBG_LAUNCH_CHECK();
             // partials D2H on the side stream (pinned), ordered after the walk by an event
             LBG_CUDA(cudaEventRecord(b->ev_red, b->stream));

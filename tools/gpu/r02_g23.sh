@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_dropin.py -m gpu -q -x -k "hydro or reduce or partial or bed or config or fused or coupled" > gpurun_out/r02_g23_pytest.log 2>&1; echo rc=$? >> gpurun_out/r02_g23_pytest.log
+for env in "LBG_WALK_REGS=120" "LBG_WALK_REGS=128" "LBG_WALK_REGS=120"; do
+env $env AB_REDUCE=1 AB_STEPS=10 timeout 300 python tests/ab_coupled_sweep.py >> gpurun_out/r02_g23_ab.log 2>&1
+done
+AB_REDUCE=1 AB_STEPS=3 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02_g23_launches.csv python tests/ab_coupled_sweep.py > /dev/null 2>&1
+LBG_WALK_REGS=128 AB_REDUCE=1 AB_STEPS=3 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02_g23_launches128.csv python tests/ab_coupled_sweep.py > /dev/null 2>&1
