@@ -451,8 +451,8 @@ struct WalkQuad {
 // only count and ids are read; pass 2 (whenever a group's stage nears full, and at the end)
 // gathers the momenta 32 per group at a time, writes the six terms of each entry, zeroes the
 // entry's scratch (psm.cpp:305), and lanes 0..5 of each group replay them in order.
-// __maxnreg__(120): 17 resident warps per SM hold 68 particles, so a 10^4-particle block
-// (67.6 per SM) runs in one wave instead of 1.06 (16 warps at the natural 125 registers)
+// register cap: 128 (the natural 125; default) or 120 (17 resident warps per SM, so a
+// 10^4-particle block fits one wave: measured no faster, 275 vs 263 us on config 3)
 template <int kRegs>
 __global__ void __maxnreg__(kRegs) walk_chain_kernel(const WalkArgs a) {
     __shared__ unsigned keys_all[kWalkWarps][kWalkGroups][kWalkKeys];
@@ -1160,7 +1160,7 @@ lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int c
             const int per_cta = kWalkWarps * kWalkGroups;
             static const int regs = [] {  // LBG_WALK_REGS: 128 (natural) or 120 (A/B)
                 const char* e = std::getenv("LBG_WALK_REGS");
-                return e ? std::atoi(e) : 120;
+                return e ? std::atoi(e) : 128;
             }();
             const unsigned grid = (unsigned)((n + per_cta - 1) / per_cta);
             if (regs >= 128)

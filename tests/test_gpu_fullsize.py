@@ -105,3 +105,41 @@ def test_config2_512_windows_bitwise_and_mass(gpu, oracle):
         assert abs(m1 - m0) <= 1e-12 * abs(m0), (m0, m1)
     finally:
         blk.close()
+
+
+def test_config2_aa_streaming_full_size_bitwise(gpu):
+    """The AA in-place layout at config 2's size: the 512^3 periodic shear wave stepped 4 times
+    in one buffer and 4 times double-buffered from the same device-initialised state give
+    bitwise equal per-cell moments (rho and the bare momentum, lbg_moments) over all 1.3e8
+    cells — an even step count, so the AA buffer holds the double-buffer state S0 — and, after
+    a fifth (odd) step, bitwise equal populations in sampled planes of the downloaded src."""
+    from paper_2303_11811_b200 import lbg
+    n = 512
+    if mem_available() < 60e9:
+        pytest.skip("needs ~60 GB of host memory for two moment arrays and one PDF field")
+    p = gpu.FluidParams(0.8)
+    box = gpu.CellBox((0, 0, 0), (n, n, n))
+    out = {}
+    for mode in ("ab", "aa"):
+        blk = gpu.Block((n, n, n))
+        try:
+            blk.init_shear_wave((n, n, n))
+            blk.set_periodic_wrap((1, 1, 1))
+            if mode == "aa":
+                blk.set_streaming(lbg.STREAM_AA)
+            for _ in range(4):
+                blk.sweep(p, box)
+                blk.swap()
+            assert blk.sync()["unstable"] == 0
+            mom = blk.moments()
+            out[mode] = np.ascontiguousarray(mom).view(np.uint64).copy()
+            del mom
+            blk.sweep(p, box)
+            blk.swap()
+            f = blk.download_src()
+            out[mode + "_planes"] = np.ascontiguousarray(f[:, [1, 2, n // 2, n - 1, n], :, :]).copy()
+            del f
+        finally:
+            blk.close()
+    assert np.array_equal(out["ab"], out["aa"])
+    assert np.array_equal(out["ab_planes"].view(np.uint64), out["aa_planes"].view(np.uint64))
