@@ -855,3 +855,45 @@ def test_poisoned_halos_never_leak(gpu, oracle, grid, batched):
         got = interior(b.download_dst())
         assert np.isfinite(got).all()
         assert n_bit_mismatch(got, want[:, lo[2]:lo[2] + bd[2], lo[1]:lo[1] + bd[1], lo[0]:lo[0] + bd[0]]) == 0
+
+
+def test_fused_mode_switched_after_map_with_longer_setu_list(gpu, oracle):
+    """The fused accumulators follow the force mode and the snapshot list (advisor findings):
+    the mode is switched to FUSED after the mapping, and set_solid_velocities then registers a
+    LONGER list than the mapping's (two extra ghost ids). The accumulators must cover the longer
+    list (sized and zeroed by set_solid_velocities), the sweep must not run without them, and
+    the FAST partials match the oracle's walk over the same list within the L1 tolerance."""
+    dims = (24, 22, 26)
+    src0 = random_pdf(dims, seed=95)
+    s_map = spheres(oracle, [(8.2, 9.1, 10.7), (15.5, 11.4, 13.2)], [4.5, 4.0], ids=[2, 5])
+    s_all = spheres(oracle, [(8.2, 9.1, 10.7), (15.5, 11.4, 13.2), (60.0, 60.0, 60.0), (70.0, 2.0, 3.0)],
+                    [4.5, 4.0, 3.0, 3.0], ids=[2, 5, 9, 11],
+                    u=[(0.001, 0.0, -0.002), (0.0, 0.003, 0.0), (0, 0, 0), (0, 0, 0)],
+                    w=[(0.0, 0.0005, 0.0), (0.0002, 0.0, 0.0), (0, 0, 0), (0, 0, 0)])
+    tau = 0.75
+    f_o, _ = oracle.build_fraction_field((0, 0, 0), dims, s_map)
+    sv_o, _ = oracle.set_solid_velocities((0, 0, 0), dims, s_all, f_o)
+    src_o = src0.copy()
+    oracle.fill_periodic(dims, src_o, ALL_P)
+    dst_o = np.zeros_like(src_o)
+    scr = new_scratch(dims)
+    oracle.psm_collide_stream(dims, src_o, dst_o, tau, (0.0, 0.0, 0.0), (0, 0, 0), dims, f_o, sv_o, scr)
+    ids_o, rows_o = oracle.finalize_hydro((0, 0, 0), dims, s_all, f_o, scr)
+    l1 = {}
+    for e, mk in ((0, "m0"), (1, "m1")):
+        sel = f_o["count"] > e
+        for pid, mv in zip(f_o["id0" if e == 0 else "id1"][sel], scr[mk][sel]):
+            l1[int(pid)] = l1.get(int(pid), 0) + np.abs(mv)
+    blk = gpu.Block(dims, coupling=True)
+    blk.upload_src(src0)
+    blk.map(s_map)          # scratch mode: no accumulators yet
+    blk.set_force_mode(1)   # takes effect at once: accumulators for the mapping's list
+    blk.set_solid_velocities(s_all)  # a longer list: accumulators resized and zeroed
+    blk.fill_periodic(ALL_P)
+    blk.sweep(gpu.FluidParams(tau), gpu.CellBox((0, 0, 0), dims))
+    blk.sync()
+    assert equal_bits(interior(blk.download_dst()), interior(dst_o))
+    parts = gpu.finalize_hydro_forces(blk, 1)
+    assert [q.id for q in parts] == list(ids_o)
+    for q, r in zip(parts, rows_o):
+        assert np.all(np.abs(q.f - (r[0:3] + r[3:6])) <= 1e-12 * l1[q.id])
