@@ -189,6 +189,9 @@ def run_reference(args):
     except FileNotFoundError as e:
         print(json.dumps({"impl": "reference", "unavailable": f"reference build missing: {e}"}))
         return 0
+    except MemoryError as e:  # the host cannot hold the full block: said so, never a smaller domain
+        print(json.dumps({"impl": "reference", "unavailable": str(e)}))
+        return 0
     line = {"metric": METRIC, "value": round(mlups, 3), "unit": "MLUPS", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(per_step * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
