@@ -17,6 +17,8 @@
 // boundary cell touches across a face are the wrapped interior ones; no ghost layer is read or
 // written): single-block periodic plain-fluid blocks (configs 1-2). Roofline: 304 B per LUP
 // either way; the even step's accesses are all unshifted.
+#include <cstdlib>
+
 #include "lbg_cell.cuh"
 #include "lbg_internal.cuh"
 
@@ -112,8 +114,16 @@ lbg_status aa_sweep(lbg_block b, const lbg_fluid* fl) {
     a.err = b->err_d;
     const bool forced = fl->f_ext[0] != 0.0 || fl->f_ext[1] != 0.0 || fl->f_ext[2] != 0.0;
     const bool odd = b->aa_phase == 0;  // S0 -> S1
-    dim3 block(128, 2, 1);
-    dim3 grid((b->L.nx + 127) / 128, (b->L.ny + 1) / 2, b->L.nz);
+    // CTAs of 256 threads along x (LBG_AA_BX = 128/64/32 for A/B: 256 measured best, the odd
+    // step's x-shifted stores then split fewer lines between CTAs; profiles/r02_ab_k12.txt)
+    static const int bx = [] {
+        const char* e = std::getenv("LBG_AA_BX");
+        const int v = e ? std::atoi(e) : 256;
+        return (v == 32 || v == 64 || v == 128) ? v : 256;
+    }();
+    const int by = 256 / bx;
+    dim3 block(bx, by, 1);
+    dim3 grid((b->L.nx + bx - 1) / bx, (b->L.ny + by - 1) / by, b->L.nz);
     if (forced)
         odd ? sweep_aa_kernel<true, true><<<grid, block, 0, b->stream>>>(a)
             : sweep_aa_kernel<true, false><<<grid, block, 0, b->stream>>>(a);

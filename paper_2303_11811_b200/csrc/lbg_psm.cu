@@ -453,9 +453,13 @@ struct WalkQuad {
 // entry's scratch (psm.cpp:305), and lanes 0..5 of each group replay them in order.
 // register cap: 128 (the natural 125; default) or 120 (17 resident warps per SM, so a
 // 10^4-particle block fits one wave: measured no faster, 275 vs 263 us on config 3)
-template <int kRegs>
+// kRows: the row walk (rows of at most 16 cells: every box of the reach path for r + f_r
+// below 6.5, checked on the host) — each lane of a group takes a whole box row, loads its
+// cells' fields at once, and a group prefix over the lanes (rows in order) places the row's
+// keys: the per-cell bookkeeping of the cell walk disappears.
+template <int kRegs, bool kRows, int kKeys>
 __global__ void __maxnreg__(kRegs) walk_chain_kernel(const WalkArgs a) {
-    __shared__ unsigned keys_all[kWalkWarps][kWalkGroups][kWalkKeys];
+    __shared__ unsigned keys_all[kWalkWarps][kWalkGroups][kKeys];
     __shared__ double terms_all[kWalkWarps][kWalkGroups][32][7];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = lane >> 3, gl = lane & 7;
@@ -631,8 +635,8 @@ __global__ void __maxnreg__(kRegs) walk_chain_kernel(const WalkArgs a) {
             const bool h0 = q.cnt[u] >= 1 && q.e0[u] == id, h1 = q.cnt[u] >= 2 && q.e1[u] == id;
             const unsigned b0 = __ballot_sync(0xffffffffu, h0), b1 = __ballot_sync(0xffffffffu, h1);
             const int s0 = nk + __popc(b0 & lt) + __popc(b1 & lt);
-            if (h0) kb[LBG_IDX(s0, kWalkKeys, a.err)] = (unsigned)(q.c[u] << 1);
-            if (h1) kb[LBG_IDX(s0 + (h0 ? 1 : 0), kWalkKeys, a.err)] = (unsigned)((q.c[u] << 1) | 1);
+            if (h0) kb[LBG_IDX(s0, kKeys, a.err)] = (unsigned)(q.c[u] << 1);
+            if (h1) kb[LBG_IDX(s0 + (h0 ? 1 : 0), kKeys, a.err)] = (unsigned)((q.c[u] << 1) | 1);
             nk += __popc(b0 & gmask) + __popc(b1 & gmask);
             any = any || ((b0 | b1) & gmask) != 0;
         }
@@ -641,23 +645,77 @@ __global__ void __maxnreg__(kRegs) walk_chain_kernel(const WalkArgs a) {
     long long smax = steps;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) smax = max(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+    if constexpr (kRows) {
+        const int ez = nonempty ? hi[2] - lo[2] + 1 : 0;
+        const int rows = nonempty ? ey * ez : 0;
+        const int rsteps = (rows + 7) / 8;
+        const int rsmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)rsteps);
+        for (int rs = 0; rs < rsmax; ++rs) {
+            const int r = rs * 8 + gl;
+            const bool rv = r < rows;
+            int j = 0, k = 0;
+            if (rv) {
+                j = lo[1] + (int)((unsigned)r % (unsigned)ey);
+                k = lo[2] + (int)((unsigned)r / (unsigned)ey);
+            }
+            const long long c0 = ((long long)k * g.dims[1] + j) * g.dims[0] + lo[0];
+            int cnt[16], f0[16], f1[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                cnt[u] = 0;
+                f0[u] = f1[u] = -1;
+                if (rv && u < ex) {
+                    const long long c = LBG_IDX(c0 + u, a.cells, a.err);
+                    cnt[u] = a.count[c];
+                    f0[u] = a.id0[c];
+                    f1[u] = a.id1[c];
+                }
+            }
+            unsigned hm = 0;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                if (cnt[u] >= 1 && f0[u] == id) hm |= 1u << (2 * u);
+                if (cnt[u] >= 2 && f1[u] == id) hm |= 1u << (2 * u + 1);
+            }
+            const int mine = __popc(hm);
+            int incl = mine;
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o, 8);
+                if (gl >= o) incl += v;
+            }
+            const int gtotal = __shfl_sync(0xffffffffu, incl, 7, 8);
+            int slot = nk + incl - mine;
+            const unsigned rowkey = ((unsigned)(k - lo[2]) << 20) | ((unsigned)(j - lo[1]) << 10);
+            while (hm) {  // the row's entries in (cell, entry) order
+                const int bit = __ffs(hm) - 1;
+                hm &= hm - 1;
+                kb[LBG_IDX(slot++, kKeys, a.err)] = ((rowkey | (unsigned)(bit >> 1)) << 1) | (unsigned)(bit & 1);
+            }
+            nk += gtotal;
+            any = any || gtotal > 0;
+            if (__any_sync(0xffffffffu, nk > kKeys - 256)) flush();  // a row step adds <= 8 x 32
+        }
+        flush();
+    } else {
     // two register quads swap roles (copying an in-flight load would wait for it); one flush
-    // call site (the flush is most of the code: a second inlined copy would spill the
-    // instruction cache), taken after every pair of steps that may have filled a stage
-    WalkQuad A, B;
-    fetch(0, A);
-    for (long long st = 0;; st += 2) {
-        if (st < smax) {
-            fetch(st + 1, B);
-            step(A);
+        // call site (the flush is most of the code: a second inlined copy would spill the
+        // instruction cache), taken after every pair of steps that may have filled a stage
+        WalkQuad A, B;
+        fetch(0, A);
+        for (long long st = 0;; st += 2) {
+            if (st < smax) {
+                fetch(st + 1, B);
+                step(A);
+            }
+            if (st + 1 < smax) {
+                fetch(st + 2, A);
+                step(B);
+            }
+            const bool done = st + 2 >= smax;
+            if (done || __any_sync(0xffffffffu, nk > kKeys - 128)) flush();  // 2 steps add <= 128
+            if (done) break;
         }
-        if (st + 1 < smax) {
-            fetch(st + 2, A);
-            step(B);
-        }
-        const bool done = st + 2 >= smax;
-        if (done || __any_sync(0xffffffffu, nk > kWalkKeys - 128)) flush();  // 2 steps add <= 128
-        if (done) break;
     }
     if (valid && gl < 6) {
         const int slot = gl < 3 ? gl : 6 + (gl - 3);
@@ -1162,11 +1220,25 @@ lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int c
                 const char* e = std::getenv("LBG_WALK_REGS");
                 return e ? std::atoi(e) : 128;
             }();
+            static const int rows_ok = [] {  // LBG_WALK_ROWS=0: the cell walk always (A/B)
+                const char* e = std::getenv("LBG_WALK_ROWS");
+                return !(e && e[0] == '0');
+            }();
+            // the row walk needs every reach-box row within 16 cells: 2 R + 3 <= 16 with
+            // R = r + max(1/2, f_r) (the box is x +- R widened by one cell each side)
+            bool rows = rows_ok && reach_ok;
+            for (int q = 0; rows && q < n; ++q) {
+                const lbg_snapshot& sp = b->snaps_h[q];
+                const double R = sp.r + (sp.f_r > 0.5 ? sp.f_r : 0.5);
+                rows = 2.0 * R + 3.0 <= 16.0;
+            }
             const unsigned grid = (unsigned)((n + per_cta - 1) / per_cta);
-            if (regs >= 128)
-                walk_chain_kernel<128><<<grid, 32 * kWalkWarps, 0, b->stream>>>(a);
+            if (rows)
+                walk_chain_kernel<128, true, 512><<<grid, 32 * kWalkWarps, 0, b->stream>>>(a);
+            else if (regs >= 128)
+                walk_chain_kernel<128, false, kWalkKeys><<<grid, 32 * kWalkWarps, 0, b->stream>>>(a);
             else
-                walk_chain_kernel<120><<<grid, 32 * kWalkWarps, 0, b->stream>>>(a);
+                walk_chain_kernel<120, false, kWalkKeys><<<grid, 32 * kWalkWarps, 0, b->stream>>>(a);
             LBG_LAUNCH_CHECK();
             // partials D2H on the side stream (pinned), ordered after the walk by an event
             LBG_CUDA(cudaEventRecord(b->ev_red, b->stream));
