@@ -453,10 +453,11 @@ struct WalkQuad {
 // entry's scratch (psm.cpp:305), and lanes 0..5 of each group replay them in order.
 // register cap: 128 (the natural 125; default) or 120 (17 resident warps per SM, so a
 // 10^4-particle block fits one wave: measured no faster, 275 vs 263 us on config 3)
-// kRows: the row walk (rows of at most 16 cells: every box of the reach path for r + f_r
-// below 6.5, checked on the host) — each lane of a group takes a whole box row, loads its
+// kRows (LBG_WALK_ROWS=1; rows of at most 16 cells: every box of the reach path for r + f_r
+// below 6.5, checked on the host): each lane of a group takes a whole box row, loads its
 // cells' fields at once, and a group prefix over the lanes (rows in order) places the row's
-// keys: the per-cell bookkeeping of the cell walk disappears.
+// keys. Fewer instructions than the cell walk but a full load latency per row step: measured
+// slower on config 3 (432 vs 263 us), so the cell walk is the default.
 template <int kRegs, bool kRows, int kKeys>
 __global__ void __maxnreg__(kRegs) walk_chain_kernel(const WalkArgs a) {
     __shared__ unsigned keys_all[kWalkWarps][kWalkGroups][kKeys];
@@ -1220,9 +1221,9 @@ lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int c
                 const char* e = std::getenv("LBG_WALK_REGS");
                 return e ? std::atoi(e) : 128;
             }();
-            static const int rows_ok = [] {  // LBG_WALK_ROWS=0: the cell walk always (A/B)
-                const char* e = std::getenv("LBG_WALK_ROWS");
-                return !(e && e[0] == '0');
+            static const int rows_ok = [] {  // LBG_WALK_ROWS=1: the row walk where it applies (A/B;
+                const char* e = std::getenv("LBG_WALK_ROWS");  // measured slower: 432 vs 263 us)
+                return e && e[0] == '1';
             }();
             // the row walk needs every reach-box row within 16 cells: 2 R + 3 <= 16 with
             // R = r + max(1/2, f_r) (the box is x +- R widened by one cell each side)

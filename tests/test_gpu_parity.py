@@ -878,12 +878,12 @@ def test_fused_mode_switched_after_map_with_longer_setu_list(gpu, oracle):
     dst_o = np.zeros_like(src_o)
     scr = new_scratch(dims)
     oracle.psm_collide_stream(dims, src_o, dst_o, tau, (0.0, 0.0, 0.0), (0, 0, 0), dims, f_o, sv_o, scr)
-    ids_o, rows_o = oracle.finalize_hydro((0, 0, 0), dims, s_all, f_o, scr)
-    l1 = {}
+    l1 = {}  # before the finalize walk, which clears the scratch (psm.cpp:305)
     for e, mk in ((0, "m0"), (1, "m1")):
         sel = f_o["count"] > e
         for pid, mv in zip(f_o["id0" if e == 0 else "id1"][sel], scr[mk][sel]):
             l1[int(pid)] = l1.get(int(pid), 0) + np.abs(mv)
+    ids_o, rows_o = oracle.finalize_hydro((0, 0, 0), dims, s_all, f_o, scr)
     blk = gpu.Block(dims, coupling=True)
     blk.upload_src(src0)
     blk.map(s_map)          # scratch mode: no accumulators yet

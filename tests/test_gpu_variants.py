@@ -9,7 +9,9 @@ once per process, so each variant runs the tests in a subprocess):
   LBG_SWEEP_PAIR=1 the 128-bit K1;
   LBDEM_GPU_SWEEP=split the drop-in in the reference's inner / halo / BC / outer-shell order;
   LBDEM_GPU_PREMAP=1 the next step's mapping prepared during the last DEM sub-cycle;
-  LBDEM_GPU_HALO=stage the staged 19-q device halo instead of the pushed one."""
+  LBDEM_GPU_HALO=stage the staged 19-q device halo instead of the pushed one; LBG_WALK_ROWS=1 /
+  LBG_WALK_REGS=120 the force reduction's row walk / register cap; LBG_MAP_MINB=5 the mapping
+  kernel at 48 registers."""
 import os
 import subprocess
 import sys
@@ -20,7 +22,7 @@ from conftest import ROOT
 
 pytestmark = pytest.mark.gpu
 
-SELECT = "coupled or setu or fused or mapping_and_solid or shear or sweep"
+SELECT = "coupled or setu or fused or mapping_and_solid or shear or sweep or finalize or hydro"
 DROPIN = "config1_known_answers or particle_bed or decomposition_invariance or config5_layout_scratch"
 
 
@@ -30,7 +32,8 @@ DROPIN = "config1_known_answers or particle_bed or decomposition_invariance or c
                                  {"LBG_DIRECT_INDEX": "0"}, {"LBG_K12_PIPE": "0", "LBG_K12_SM": "4"},
                                  {"LBG_K12_PIPE": "0", "LBG_K12_SM": "6"},
                                  {"LBG_SWEEP_PAIR": "1"}, {"LBDEM_GPU_SWEEP": "split"}, {"LBDEM_GPU_PREMAP": "1"},
-                                 {"LBDEM_GPU_HALO": "stage"}])
+                                 {"LBDEM_GPU_HALO": "stage"}, {"LBG_WALK_ROWS": "1"}, {"LBG_WALK_REGS": "120"},
+                                 {"LBG_MAP_MINB": "5"}])
 def test_parity_suite_under_variant(env):
     e = dict(os.environ, **env)
     # the parity cases, and drop-in runs vs the reference (config 1: periodic block, in-kernel
