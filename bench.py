@@ -286,7 +286,15 @@ def coupled_step(steps, with_reference, ref_steps=1, blocks=(1, 1, 1), workers=1
     return out
 
 
-def coupled_sweep_roofline(steps=10, warmup=3):
+CONFIG5_1GPU = ('{"scenario":"fluidized_bed_dense","domain":[512,512,512],"blocks":[1,1,1],"workers":1,'
+                '"particles":{"count":12500},"physical":{"diameter_cells":10},'
+                '"fluid":{"bc":{"xm":"no_slip","xp":"no_slip","ym":"no_slip","yp":"no_slip",'
+                '"zm":"velocity","zp":"pressure"}},'
+                '"dem":{"k_n":230,"d_n":520,"k_t":65,"d_t":260,"subcycles":10,"settle_subcycles":100}}')
+
+
+def coupled_sweep_roofline(steps=10, warmup=3, cfg=None, n=256, label="config 3 bed (reference scenario "
+                           "particles), one 256^3 block, tau 0.567416"):
     """Device-side roofline of the coupled fluid step on config 3's bed (one 256^3 block):
     the particle list is the reference scenario's own (drop-in construction, 10^4 spheres
     d = 10 after settling), mapped once (K3); each step is the bed BCs (K5) followed by the
@@ -302,8 +310,7 @@ def coupled_sweep_roofline(steps=10, warmup=3):
     from paper_2303_11811_b200 import lbdem
     sys.path.insert(0, os.path.join(ROOT, "integration"))
     import dropin
-    n = 256
-    sim = dropin.DropinSim(config3(), (n, n, n))
+    sim = dropin.DropinSim(cfg or config3(), (n, n, n))
     rows = sim.particles()
     sim.close()
     r = 5.0  # physical.diameter_cells / 2
@@ -363,8 +370,8 @@ def coupled_sweep_roofline(steps=10, warmup=3):
     pk = peaks()
     peak = pk["hbm_gbs"] if pk and pk.get("hbm_gbs") else 6650.0
     achieved = algo / (sweep_ms / 1e3) / 1e9
-    return {"workload": "config 3 bed (reference scenario particles), one 256^3 block, tau 0.567416",
-            "kernels": "K1 sweep_box_kernel<skip> || K2 psm_seg_kernel (one-entry, two-entry segments)",
+    return {"workload": label,
+            "kernels": "K12 coupled_unified_pipe_kernel (fluid, one-entry and two-entry segments in one kernel)",
             "cells": cells, "one_entry_cells": n1, "two_entry_cells": n2,
             "algorithmic_bytes_per_step": algo, "sweep_ms": round(sweep_ms, 4), "bc_ms": round(bc_ms / steps, 4),
             "mlups": round(cells / (sweep_ms / 1e3) / 1e6, 1),
@@ -754,6 +761,10 @@ def run_lbg(args):
                 out["coupled_step"]["single_block"] = {k: single[k] for k in (
                     "ms_per_step", "categories_ms_per_step", "gpu_side_ms_per_step", "fused_force_mode")}
                 out["coupled_step"]["psm_sweep"] = coupled_sweep_roofline()
+                # config 5's dilute bed (12,500 spheres in 512^3, 4.9 % solid) as one block
+                out["coupled_step"]["psm_sweep_config5"] = coupled_sweep_roofline(
+                    cfg=CONFIG5_1GPU, n=512, label="config 5 bed (12,500 spheres d = 10 after 100 settling "
+                    "sub-cycles), one 512^3 block, tau 0.567416")
             except Exception as e:  # noqa: BLE001
                 out["coupled_step"] = {"unavailable": f"{type(e).__name__}: {e}"}
         print(json.dumps(out))
