@@ -471,7 +471,7 @@ lbg_status lbg_block_destroy(lbg_block b) {
                    b->obs_d, b->mom_d, b->seg_list, b->seg_n, b->snap_tab, b->red_box, b->pidx0, b->wcount};
     for (void* p : dev)
         if (p) cudaFree(p);
-    void* host[] = {b->snaps_h, b->err_h, b->red_rows_h, b->red_used_h, b->obs_h};
+    void* host[] = {b->snaps_h, b->err_h, b->red_rows_h, b->red_used_h, b->obs_h, b->segn_h};
     for (void* p : host)
         if (p) cudaFreeHost(p);
     for (auto& s : b->spans) {
@@ -485,6 +485,7 @@ lbg_status lbg_block_destroy(lbg_block b) {
     if (b->ev_stage) cudaEventDestroy(b->ev_stage);
     if (b->ev_fetched) cudaEventDestroy(b->ev_fetched);
     if (b->ev_red) cudaEventDestroy(b->ev_red);
+    if (b->ev_segn) cudaEventDestroy(b->ev_segn);
     for (int s = 0; s < 2; ++s) {
         if (b->xfer[s]) cudaFree(b->xfer[s]);
         if (b->ev_copy[s]) cudaEventDestroy(b->ev_copy[s]);

@@ -138,6 +138,11 @@ struct MapState {
     double* b1 = nullptr;
     double* btot = nullptr;
     unsigned* seg_list = nullptr;
+    // covered-segment counts of the last mapping, copied to the host asynchronously (the
+    // coupled sweep picks the unified kernel or the split by the covered fraction)
+    int* segn_h = nullptr;
+    cudaEvent_t ev_segn = nullptr;
+    bool segn_pending = false;
     int* seg_n = nullptr;
     lbg_snapshot* snaps_d = nullptr;
     int snaps_dcap = 0;
@@ -197,6 +202,11 @@ struct lbg_block_s {
     // aligned 32-cell row segments holding covered cells (first cell index): segments with
     // one-entry cells only from the front (seg_n[0]), with a two-entry cell from the back
     unsigned* seg_list = nullptr;
+    // covered-segment counts of the last mapping, copied to the host asynchronously (the
+    // coupled sweep picks the unified kernel or the split by the covered fraction)
+    int* segn_h = nullptr;
+    cudaEvent_t ev_segn = nullptr;
+    bool segn_pending = false;
     int* seg_n = nullptr;
     long long seg_cap = 0;
 
@@ -223,6 +233,7 @@ struct lbg_block_s {
     int snap_range = 0;  // 0: no table (sparse ids)
     lbg::MapState* shadow = nullptr;  // lbg_map_prepare's target
     bool prepared = false;
+    bool preparing = false;
     // device binning for the mapping kernel (lbg_psm.cu)
     int* bin_count = nullptr;
     int* bin_start = nullptr;
@@ -309,6 +320,8 @@ lbg_status aa_unstream(lbg_block b, double* out);
 void free_shadow(lbg_block b);
 // covered-cell counts and segment lists rebuilt from `count` (lbg_psm.cu)
 lbg_status rebuild_covered(lbg_block b);
+// the covered-segment counts to the host, asynchronously (lbg_psm.cu)
+lbg_status post_segment_counts(lbg_block b);
 // the block's current snapshot index
 inline SnapIndex snap_index(const lbg_block_s* b) {
     return SnapIndex{b->snaps_d, b->n_snaps, b->snap_range > 0 ? b->snap_tab : nullptr, b->snap_id_min,

@@ -829,6 +829,16 @@ static lbg_status ensure_bins(lbg_block b, long long nbins) {
     return LBG_OK;
 }
 
+// the covered-segment counts to the host (pinned, asynchronous) for the sweep's kernel choice
+lbg_status post_segment_counts(lbg_block b) {
+    if (!b->segn_h) LBG_CUDA(cudaMallocHost(&b->segn_h, 2 * sizeof(int)));
+    if (!b->ev_segn) LBG_CUDA(cudaEventCreateWithFlags(&b->ev_segn, cudaEventDisableTiming));
+    LBG_CUDA(cudaMemcpyAsync(b->segn_h, b->seg_n, 2 * sizeof(int), cudaMemcpyDeviceToHost, b->stream));
+    LBG_CUDA(cudaEventRecord(b->ev_segn, b->stream));
+    b->segn_pending = true;
+    return LBG_OK;
+}
+
 lbg_status rebuild_covered(lbg_block b) {
     const long long rows = (long long)b->L.ny * b->L.nz;
     const long long nseg = rows * ((b->L.nx + 31) / 32);
@@ -837,7 +847,7 @@ lbg_status rebuild_covered(lbg_block b) {
                                                                            b->seg_n, b->seg_cap);
     LBG_LAUNCH_CHECK();
     b->cov_dirty = false;
-    return LBG_OK;
+    return post_segment_counts(b);
 }
 
 // the block's mapping state <-> the shadow (pointer swaps only)
@@ -1018,6 +1028,8 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
                                                                                b->seg_list, b->seg_n, b->seg_cap);
         LBG_LAUNCH_CHECK();
     }
+    if (!b->preparing)  // a prepared mapping posts its counts when committed
+        if (lbg_status s = post_segment_counts(b)) return s;
     b->cov_dirty = false;
     b->v_snap = true;
     b->p_direct = true;
@@ -1050,7 +1062,9 @@ lbg_status lbg_map_prepare(lbg_block b, const lbg_snapshot* snaps, int n, int su
     if (lbg_status s = ensure_shadow(b)) return s;
     b->prepared = false;
     swap_map_state(b);  // map into the shadow; the current state stays in use meanwhile
+    b->preparing = true;
     const lbg_status st = lbg_map(b, snaps, n, subdivisions);
+    b->preparing = false;
     swap_map_state(b);
     if (st != LBG_OK) return st;
     b->prepared = true;
@@ -1064,7 +1078,9 @@ lbg_status lbg_map_commit(lbg_block b) {
     // the old state is only written again by the next prepare (stream order)
     swap_map_state(b);
     b->prepared = false;
-    return LBG_OK;
+    // the committed field's counts (the shadow's were never posted)
+    LBG_CUDA(cudaSetDevice(b->device));
+    return post_segment_counts(b);
 }
 
 lbg_status lbg_set_solid_velocities(lbg_block b, const lbg_snapshot* snaps, int n) {

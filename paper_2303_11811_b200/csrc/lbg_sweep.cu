@@ -877,33 +877,59 @@ struct UPre {
     bool ok;
 };
 
-// the count bytes of segment s (32 lanes), 0 past the end
-__device__ __forceinline__ int useg_count(const SweepArgs& a, long long s, long long nseg, int segs_x, int ny_b,
-                                          int lane) {
-    if (s >= nseg) return 0;
-    const Layout& L = a.L;
-    const unsigned su = (unsigned)s, r = su / (unsigned)segs_x;
-    const int i = a.i0 + 32 * (int)(su - r * (unsigned)segs_x) + lane;
-    if (i >= L.nx) return 0;
-    return (int)a.count[LBG_IDX(L.frac(i, a.lo[1] + (int)(r % (unsigned)ny_b), a.lo[2] + (int)(r / (unsigned)ny_b)),
-                                a.cells, a.err)];
+// segment s's first cell: dense mode — the s-th aligned 32-cell row segment of the box; list
+// mode (kList) — the s-th entry of the mapping's covered-segment list (one-entry segments from
+// the front, segments with a two-entry cell from the back)
+struct USegId {
+    int i0, j, k;
+};
+
+// list mode: the list entry of segment s (its first cell index)
+__device__ __forceinline__ unsigned useg_raw(const SweepArgs& a, long long s, long long nseg, int n1) {
+    if (s >= nseg) return 0u;
+    return (s < n1) ? a.seg_list[s] : a.seg_list[a.seg_cap - 1 - (s - n1)];
 }
 
-// the loads of segment s, whose counts `cnt` arrived one segment earlier: the populations
-// unless it is a two-entry segment (psm_seg_kernel<two> sweeps those), the cell fields only
-// for a one-entry segment — nothing an SRT segment does not use
-template <bool kTwoInline, bool kWrap>
-__device__ __forceinline__ void useg_issue(const SweepArgs& a, long long s, int segs_x, int ny_b, int lane, int cnt,
-                                           USeg& u) {
-    const Layout& L = a.L;
+__device__ __forceinline__ USegId useg_decode(const Layout& L, unsigned c0) {
+    USegId id;
+    const unsigned row = c0 / (unsigned)L.nx;
+    id.i0 = (int)(c0 - row * (unsigned)L.nx);
+    id.j = (int)(row % (unsigned)L.ny);
+    id.k = (int)(row / (unsigned)L.ny);
+    return id;
+}
+
+__device__ __forceinline__ USegId useg_dense(const SweepArgs& a, long long s, int segs_x, int ny_b) {
     // 32-bit index math (a 64-bit division is a ~100-instruction software routine)
+    USegId id;
     const unsigned su = (unsigned)s, r = su / (unsigned)segs_x;
-    u.i = a.i0 + 32 * (int)(su - r * (unsigned)segs_x) + lane;
-    u.j = a.lo[1] + (int)(r % (unsigned)ny_b);
-    u.k = a.lo[2] + (int)(r / (unsigned)ny_b);
+    id.i0 = a.i0 + 32 * (int)(su - r * (unsigned)segs_x);
+    id.j = a.lo[1] + (int)(r % (unsigned)ny_b);
+    id.k = a.lo[2] + (int)(r / (unsigned)ny_b);
+    return id;
+}
+
+// the count bytes of segment `id` (32 lanes)
+__device__ __forceinline__ int useg_count(const SweepArgs& a, const USegId& id, bool valid, int lane) {
+    const Layout& L = a.L;
+    const int i = id.i0 + lane;
+    if (!valid || i >= L.nx) return 0;
+    return (int)a.count[LBG_IDX(L.frac(i, id.j, id.k), a.cells, a.err)];
+}
+
+// the loads of segment `id`, whose counts `cnt` arrived one segment earlier: the populations
+// unless it is a two-entry segment swept elsewhere, the cell fields only for a covered
+// segment — nothing an SRT segment does not use
+template <bool kTwoInline, bool kWrap>
+__device__ __forceinline__ void useg_issue(const SweepArgs& a, const USegId& id, int lane, int cnt, USeg& u) {
+    const Layout& L = a.L;
+    u.i = id.i0 + lane;
+    u.j = id.j;
+    u.k = id.k;
     const bool inx = u.i < L.nx;
     u.fc = LBG_IDX(L.frac(inx ? u.i : L.nx - 1, u.j, u.k), a.cells, a.err);
-    u.act = inx && u.i >= a.lo[0] && u.i < a.hi[0];
+    u.act = inx && u.i >= a.lo[0] && u.i < a.hi[0] && u.j >= a.lo[1] && u.j < a.hi[1] && u.k >= a.lo[2] &&
+            u.k < a.hi[2];
     u.cnt = cnt;
     u.mx = (int)__reduce_max_sync(0xffffffffu, (unsigned)cnt);
     if (u.mx >= 1) {
@@ -1003,28 +1029,44 @@ __device__ __forceinline__ void useg_finish(const SweepArgs& a, const USeg& u, c
         if (u.mx == 1) fused_accumulate(a, p0, m, cc);
 }
 
-template <bool kFused, bool kVsnap, bool kTwoInline, bool kWrap>
+template <bool kFused, bool kVsnap, bool kTwoInline, bool kWrap, bool kList = false>
 __global__ void __launch_bounds__(128, 3) coupled_unified_pipe_kernel(const SweepArgs a) {
     const int lane = threadIdx.x & 31;
     const long long warp = (long long)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const long long nwarps = (long long)((gridDim.x * blockDim.x) >> 5);
     const int segs_x = (a.hi[0] - a.i0 + 31) >> 5;
     const int ny_b = a.hi[1] - a.lo[1];
-    const long long nseg = (long long)segs_x * ny_b * (a.hi[2] - a.lo[2]);
+    const int n1 = kList ? a.seg_n[0] : 0;
+    const long long nseg = kList ? (long long)n1 + a.seg_n[1] : (long long)segs_x * ny_b * (a.hi[2] - a.lo[2]);
     if (warp >= nseg) return;  // warp-uniform
+    // list mode: list entries three segments ahead, decoded when their counts are loaded
+    auto locate = [&](long long s, unsigned raw) {
+        if constexpr (kList)
+            return useg_decode(a.L, raw);
+        else
+            return useg_dense(a, s < nseg ? s : 0, segs_x, ny_b);
+    };
     // one body: a second inlined copy of the operators would overflow the instruction cache.
     // Counts run two segments ahead of the sweep and the loads one segment ahead; the copies
     // (cur = nxt, c1 = cfar) happen a whole finish() after their loads were issued.
     USeg cur, nxt;
     UPre pre;
-    useg_issue<kTwoInline, kWrap>(a, warp, segs_x, ny_b, lane, useg_count(a, warp, nseg, segs_x, ny_b, lane), nxt);
-    int cfar = useg_count(a, warp + nwarps, nseg, segs_x, ny_b, lane);
+    {
+        const USegId id0 = locate(warp, kList ? useg_raw(a, warp, nseg, n1) : 0u);
+        useg_issue<kTwoInline, kWrap>(a, id0, lane, useg_count(a, id0, true, lane), nxt);
+    }
+    USegId idfar = locate(warp + nwarps, kList ? useg_raw(a, warp + nwarps, nseg, n1) : 0u);
+    int cfar = useg_count(a, idfar, warp + nwarps < nseg, lane);
+    unsigned rawfar = kList ? useg_raw(a, warp + 2 * nwarps, nseg, n1) : 0u;
     for (long long s = warp; s < nseg; s += nwarps) {
         cur = nxt;
         useg_pre<kVsnap, kTwoInline>(a, cur, pre);
         const int c1 = cfar;
-        cfar = useg_count(a, s + 2 * nwarps, nseg, segs_x, ny_b, lane);
-        if (s + nwarps < nseg) useg_issue<kTwoInline, kWrap>(a, s + nwarps, segs_x, ny_b, lane, c1, nxt);
+        const USegId id1 = idfar;
+        idfar = locate(s + 2 * nwarps, rawfar);
+        cfar = useg_count(a, idfar, s + 2 * nwarps < nseg, lane);
+        if constexpr (kList) rawfar = useg_raw(a, s + 3 * nwarps, nseg, n1);
+        if (s + nwarps < nseg) useg_issue<kTwoInline, kWrap>(a, id1, lane, c1, nxt);
         useg_finish<kFused, kVsnap, kTwoInline>(a, cur, pre);
     }
 }
@@ -1292,6 +1334,32 @@ static bool k12_on() {
     return v;
 }
 
+template <bool kForced, bool kSkip>
+static void launch_box(const SweepArgs& a, cudaStream_t s);
+
+// Coupled sweep kernel choice (LBG_K12): 0 round 1's K1 || K2 split; 2 the unified kernel; 3 the
+// covered-list split (K1 over the segments without a covered cell, K12 over the mapping's
+// covered-segment list); 1 (default) picks 2 or 3 by the block's covered fraction of the last
+// mapping: above LBG_K12_SPLIT_BELOW (default 0.35) the unified kernel (config 3's dense bed,
+// 62 % covered segments: 1.03 ms vs 1.13 split), below it the split (config 5's dilute bed,
+// ~12 %: 6.7 ms vs 8.0 unified; profiles/r02_ab_k12.txt)
+static int k12_mode() {
+    static const int v = env_int("LBG_K12", 1);
+    return v;
+}
+
+// the covered fraction of the block's segments, from the counts the last mapping posted (-1
+// while they are not on the host yet)
+static double covered_fraction(lbg_block b) {
+    if (!b->segn_pending || !b->segn_h || !b->ev_segn) return -1.0;
+    if (cudaEventQuery(b->ev_segn) != cudaSuccess) {
+        cudaGetLastError();  // cudaErrorNotReady is not an error
+        return -1.0;
+    }
+    const double total = (double)((b->L.nx + 31) / 32) * b->L.ny * b->L.nz;
+    return total > 0 ? (b->segn_h[0] + b->segn_h[1]) / total : 0.0;
+}
+
 static void launch_unified(lbg_block b, const SweepArgs& a, bool forced, cudaStream_t st) {
     static const int per_sm = std::min(6, std::max(4, env_int("LBG_K12_SM", 5)));
     int sms = 148;
@@ -1327,6 +1395,20 @@ static void launch_unified(lbg_block b, const SweepArgs& a, bool forced, cudaStr
         count_launch();
         // segments holding a two-entry cell (particle contacts): pair-scheduled two-entry operator
         psm_seg_kernel<kF, kU, true, kV><<<(unsigned)(sms * 4), 128, 0, st>>>(a);
+    });
+}
+
+// K12 over the covered-segment list only (unforced, direct snapshot index): one- and
+// two-entry segments, the pipelined operator loop
+static void launch_covered_list(lbg_block b, const SweepArgs& a, cudaStream_t st) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, b->device);
+    const bool fused = b->force_mode == LBG_FORCE_FUSED;
+    const bool wrapped = a.wrap[0] || a.wrap[1] || a.wrap[2];
+    const unsigned grid = (unsigned)(sms * 3);
+    with_flags(fused, b->v_snap, wrapped, [&](auto U, auto V, auto W) {
+        constexpr bool kU = decltype(U)::value, kV = decltype(V)::value, kW = decltype(W)::value;
+        coupled_unified_pipe_kernel<kU, kV, true, kW, true><<<grid, 128, 0, st>>>(a);
     });
 }
 
@@ -1396,6 +1478,21 @@ lbg_status lbg_sweep(lbg_block b, const lbg_fluid* fl, const lbg_box* range) {
     }
     if (b->coupling) {
         if (k12_on()) {
+            static const double split_below = [] {
+                const char* e = std::getenv("LBG_K12_SPLIT_BELOW");
+                return e ? std::atof(e) : 0.35;
+            }();
+            const int mode = k12_mode();
+            const double cf = mode == 1 ? covered_fraction(b) : -1.0;
+            const bool list_ok = !fo && a.pidx0;
+            if (list_ok && (mode == 3 || (mode == 1 && cf >= 0.0 && cf < split_below))) {
+                // K1 over the fluid segments, then K12 over the covered-segment list
+                launch_box<false, true>(a, b->stream);
+                LBG_LAUNCH_CHECK();
+                launch_covered_list(b, a, b->stream);
+                LBG_LAUNCH_CHECK();
+                return verify_writes(b, a);
+            }
             launch_unified(b, a, fo, b->stream);
             LBG_LAUNCH_CHECK();
             return verify_writes(b, a);

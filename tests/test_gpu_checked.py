@@ -69,7 +69,7 @@ def test_dropin_suites_checked():
     _run(["test_gpu_checked.py", "test_dropin.py", "test_gpu_multi.py"], k=SELF)
 
 
-@pytest.mark.parametrize("env", [{"LBG_K12_PIPE": "0"}, {"LBG_K12_TWO": "0"},
+@pytest.mark.parametrize("env", [{"LBG_K12": "2"}, {"LBG_K12": "3"}, {"LBG_K12_PIPE": "0"}, {"LBG_K12_TWO": "0"},
                                  {"LBG_K12": "0"}, {"LBG_K12": "0", "LBG_K2_MODE": "2"},
                                  {"LBG_K12": "0", "LBG_K2_CONCURRENT": "0"}, {"LBG_SWEEP_PAIR": "1"}])
 def test_sweep_variants_checked(env):

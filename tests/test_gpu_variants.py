@@ -1,6 +1,8 @@
 """The coupled-sweep parity tests under every selectable kernel variant (the switches are read
 once per process, so each variant runs the tests in a subprocess):
-  LBG_K12_PIPE=0 the unified coupled sweep without the register pipeline (LBG_K12_SM=4/6 its
+  LBG_K12=2 / 3 the unified coupled sweep / the covered-list split always (the default picks one
+  per block by its covered fraction); LBG_K12_PIPE=0 the unified coupled sweep without the
+  register pipeline (LBG_K12_SM=4/6 its
   occupancy caps), LBG_K12_TWO=0 two-entry segments in their own kernel, LBG_K12_NOWRAP=0 the
   generic pull for unwrapped blocks;
   LBG_K12=0 the K1 || K2 split instead of the unified coupled sweep, with LBG_K2_MODE=0 plain
@@ -26,7 +28,8 @@ SELECT = "coupled or setu or fused or mapping_and_solid or shear or sweep or fin
 DROPIN = "config1_known_answers or particle_bed or decomposition_invariance or config5_layout_scratch"
 
 
-@pytest.mark.parametrize("env", [{"LBG_K12_PIPE": "0"}, {"LBG_K12_TWO": "0"}, {"LBG_K12_NOWRAP": "0"},
+@pytest.mark.parametrize("env", [{"LBG_K12": "2"}, {"LBG_K12": "3"}, {"LBG_K12_PIPE": "0"}, {"LBG_K12_TWO": "0"},
+                                 {"LBG_K12_NOWRAP": "0"},
                                  {"LBG_K12": "0"}, {"LBG_K12": "0", "LBG_K2_MODE": "0"},
                                  {"LBG_K12": "0", "LBG_K2_MODE": "2"}, {"LBG_K12": "0", "LBG_K2_CONCURRENT": "0"},
                                  {"LBG_DIRECT_INDEX": "0"}, {"LBG_K12_PIPE": "0", "LBG_K12_SM": "4"},
