@@ -468,7 +468,7 @@ lbg_status lbg_block_destroy(lbg_block b) {
     void* dev[] = {b->buf[0], b->buf[1], b->count, b->id0, b->id1, b->b0, b->b1, b->btot,
                    b->v0, b->v1, b->m0, b->m1, b->snaps_d, b->bin_count, b->bin_start,
                    b->bin_items, b->red_rows, b->red_used, b->err_d, b->facc, b->fused_used,
-                   b->obs_d, b->mom_d, b->seg_list, b->seg_n, b->snap_tab, b->red_box, b->pidx0, b->wcount};
+                   b->obs_d, b->mom_d, b->seg_list, b->seg_n, b->snap_tab, b->red_box, b->pidx0, b->wcount, b->bin_rec};
     for (void* p : dev)
         if (p) cudaFree(p);
     void* host[] = {b->snaps_h, b->err_h, b->red_rows_h, b->red_used_h, b->obs_h, b->segn_h};

@@ -163,6 +163,8 @@ struct Comm;  // lbg_halo.cu
 struct P2P;   // lbg_p2p.cu
 struct Push;  // lbg_push.cu
 
+struct MapRec;  // lbg_psm.cu
+
 }  // namespace lbg
 
 struct lbg_block_s {
@@ -239,6 +241,8 @@ struct lbg_block_s {
     int* bin_start = nullptr;
     int* bin_items = nullptr;
     long long bin_items_cap = 0;
+    lbg::MapRec* bin_rec = nullptr;  // the items' candidate records (sorted like the items)
+    long long bin_rec_cap = 0;
     long long n_bins_cap = 0;
     // hydro reduction scratch
     double* red_rows = nullptr;  // n_snaps x 12

@@ -110,16 +110,45 @@ __global__ void __launch_bounds__(256) bin_alloc_kernel(const int* __restrict__ 
 constexpr int kSortWarps = 8;
 constexpr int kSortSmem = 1024;
 
+// the mapping's per-candidate record, in the bin's sorted order (one load per candidate when
+// the mapping kernel stages a bin instead of a list load and a dependent snapshot load)
+struct MapRec {
+    double x[3];
+    double r, fr;
+    int id, idx;
+};
+static_assert(sizeof(MapRec) == 48, "MapRec layout");
+
+__device__ __forceinline__ void put_rec(MapRec* __restrict__ rec, const lbg_snapshot* __restrict__ s, int ix) {
+    const lbg_snapshot& p = s[ix];
+    MapRec r;
+    r.x[0] = p.x[0];
+    r.x[1] = p.x[1];
+    r.x[2] = p.x[2];
+    r.r = p.r;
+    r.fr = p.f_r;
+    r.id = p.id;
+    r.idx = ix;
+    *rec = r;
+}
+
 __global__ void __launch_bounds__(32 * kSortWarps) bin_sort_kernel(const int* __restrict__ start,
                                                                    const int* __restrict__ cnt, int nbins,
-                                                                   int* __restrict__ items) {
+                                                                   int* __restrict__ items,
+                                                                   const lbg_snapshot* __restrict__ snaps,
+                                                                   MapRec* __restrict__ rec) {
     __shared__ int buf[kSortWarps][kSortSmem];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int b = blockIdx.x * kSortWarps + w;
     if (b >= nbins) return;  // warp-uniform
     const int n = cnt[b];
-    if (n < 2) return;
+    if (n == 0) return;
     int* a = items + start[b];
+    MapRec* r = rec + start[b];
+    if (n == 1) {
+        if (lane == 0) put_rec(r, snaps, a[0]);
+        return;
+    }
     if (n > kSortSmem) {
         if (lane == 0)
             for (int i = 1; i < n; ++i) {
@@ -131,6 +160,8 @@ __global__ void __launch_bounds__(32 * kSortWarps) bin_sort_kernel(const int* __
                 }
                 a[j + 1] = v;
             }
+        __syncwarp();
+        for (int t = lane; t < n; t += 32) put_rec(r + t, snaps, a[t]);
         return;
     }
     int* sb = buf[w];
@@ -138,9 +169,10 @@ __global__ void __launch_bounds__(32 * kSortWarps) bin_sort_kernel(const int* __
     __syncwarp();
     for (int t = lane; t < n; t += 32) {
         const int v = sb[t];
-        int r = 0;
-        for (int u = 0; u < n; ++u) r += sb[u] < v;
-        a[r] = v;
+        int rk = 0;
+        for (int u = 0; u < n; ++u) rk += sb[u] < v;
+        a[rk] = v;
+        put_rec(r + rk, snaps, v);
     }
 }
 
@@ -150,6 +182,7 @@ struct MapArgs {
     const int* __restrict__ start;
     const int* __restrict__ cnt;
     const int* __restrict__ items;
+    const MapRec* __restrict__ rec;    // the bins' candidate records (sorted like items)
     uint8_t* __restrict__ count;
     int* __restrict__ id0;
     int* __restrict__ id1;
@@ -295,6 +328,149 @@ __global__ void __launch_bounds__(32 * kMapWarps, kMinBlocks) map_warp_kernel(co
         overfull += (unsigned long long)__popc(__ballot_sync(0xffffffffu, inxy && over));
     }
     if (overfull && lane == 0) atomicAdd(&a.err->overfull, overfull);
+}
+
+// K3 (default): candidate-outer, one warp per unit. A unit is an 8 x 4 x 8 cell
+// column of an occupied 8^3 bin (lane = 8 x 4 cells of a level), and each lane keeps the state
+// of its 8 cells (one per z-level: count, running sum, overfull flag) in registers while the
+// loop runs the bin's candidates outside and the levels inside. A cell still visits its
+// candidates in ascending (id) order with the same operations — rad = (d0*d0 + d1*d1) + d2*d2,
+// whose z-independent d0*d0 + d1*d1 is now computed once per candidate instead of once per
+// level — so the entries are bitwise those of map_warp_kernel. The per-level cull (the
+// column's x/y gap plus the level's z gap against (r + f_r)^2 (1 + 1e-9)) runs once per
+// candidate at staging time (lane = candidate) into a bit mask of the levels it can reach.
+// Candidates are staged from the bins' sorted records (one load instead of list -> snapshot).
+// LBG_MAP_COL=0 selects map_warp_kernel.
+struct MapCandZ {
+    double x0[32], x1[32], x2[32], r[32], fr[32], out2[32], in2[32];
+    int id[32], idx[32];
+    unsigned zm[32];
+};
+
+__device__ __forceinline__ void stage_recs(const MapRec* rec, int m, int lane, double wx0, double wx1, double wy0,
+                                           double wy1, double z0c, int nz, MapCandZ& sc) {
+    if (lane < m) {
+        const MapRec p = rec[lane];
+        sc.idx[lane] = p.idx;
+        sc.x0[lane] = p.x[0];
+        sc.x1[lane] = p.x[1];
+        sc.x2[lane] = p.x[2];
+        sc.r[lane] = p.r;
+        sc.fr[lane] = p.fr;
+        const double ro = p.r + p.fr, ri = ro - 1.0;
+        const double out2 = (ro * ro) * (1.0 + 1e-9);
+        sc.out2[lane] = out2;
+        sc.in2[lane] = ri > 0.0 ? (ri * ri) * (1.0 - 1e-9) : -1.0;
+        const double g0 = axis_gap(wx0, wx1, p.x[0]), g1 = axis_gap(wy0, wy1, p.x[1]);
+        const double gxy = g0 * g0 + g1 * g1;
+        unsigned zm = 0;
+        for (int zz = 0; zz < nz; ++zz) {
+            const double cc2 = z0c + (double)zz;  // = (double)(lo + k) + 0.5 exactly
+            const double g2 = axis_gap(cc2, cc2, p.x[2]);
+            if (!(gxy + g2 * g2 > out2)) zm |= 1u << zz;
+        }
+        sc.zm[lane] = zm;
+        sc.id[lane] = p.id;
+    }
+    __syncwarp();
+}
+
+// one unit (bin b, y half yh; the bin's n candidate records from `start`); returns the number
+// of the warp's cells found overfull (lane 0's value counts)
+__device__ __forceinline__ unsigned map_unit(const MapArgs& a, int b, int yh, int start, int n, int lane,
+                                             MapCandZ& sc) {
+    const BinGeom& g = a.g;
+    const int bx = b % g.nb[0], by = (b / g.nb[0]) % g.nb[1], bz = b / (g.nb[0] * g.nb[1]);
+    const int i = bx * kBin + (lane & 7), j = by * kBin + yh * 4 + (lane >> 3);
+    const double cc0 = (double)(g.lo[0] + i) + 0.5, cc1 = (double)(g.lo[1] + j) + 0.5;
+    const double wx0 = (double)(g.lo[0] + bx * kBin) + 0.5, wx1 = wx0 + 7.0;
+    const double wy0 = (double)(g.lo[1] + by * kBin + yh * 4) + 0.5, wy1 = wy0 + 3.0;
+    const int kz0 = bz * kBin;
+    const int nz = min(kBin, g.dims[2] - kz0);
+    const double z0c = (double)(g.lo[2] + kz0) + 0.5;
+    const bool inxy = i < g.dims[0] && j < g.dims[1];
+    const long long plane = (long long)g.dims[0] * g.dims[1];
+    const long long c0 = inxy ? ((long long)kz0 * g.dims[1] + j) * g.dims[0] + i : 0;
+    unsigned cnts = 0;  // 2 bits per level
+    unsigned over = 0;  // 1 bit per level
+    double sum[kBin];
+#pragma unroll
+    for (int zz = 0; zz < kBin; ++zz) sum[zz] = 0.0;
+    for (int base = 0; base < n; base += 32) {
+        const int m = min(32, n - base);
+        __syncwarp();  // every lane is done with the previous chunk / unit
+        stage_recs(a.rec + LBG_IDX((long long)start + base, a.items_cap, a.err), m, lane, wx0, wx1, wy0, wy1,
+                   z0c, nz, sc);
+        const unsigned rel = __ballot_sync(0xffffffffu, lane < m && sc.zm[lane] != 0u);
+        if (!inxy) continue;
+        for (unsigned mask = rel; mask; mask &= mask - 1) {  // ascending = id order
+            const int q = __ffs(mask) - 1;
+            const unsigned zm = sc.zm[q];
+            const double d0 = cc0 - sc.x0[q], d1 = cc1 - sc.x1[q];
+            const double dxy = d0 * d0 + d1 * d1;
+            const double x2 = sc.x2[q], out2 = sc.out2[q], in2 = sc.in2[q];
+#pragma unroll
+            for (int zz = 0; zz < kBin; ++zz) {
+                if (!((zm >> zz) & 1u)) continue;  // warp-uniform
+                const double d2 = (z0c + (double)zz) - x2;
+                const double rad = dxy + d2 * d2;
+                if (rad > out2) continue;
+                double eps;
+                if (rad < in2) {
+                    eps = 1.0;
+                } else {
+                    eps = -(sqrt(rad) - sc.r[q]) + sc.fr[q];
+                    eps = eps < 0.0 ? 0.0 : (1.0 < eps ? 1.0 : eps);  // std::clamp
+                    if (eps <= 0.0) continue;
+                }
+                if ((over >> zz) & 1u) continue;
+                const unsigned cnt = (cnts >> (2 * zz)) & 3u;
+                if (cnt >= 2) {
+                    over |= 1u << zz;
+                    continue;
+                }
+                const long long c = LBG_IDX(c0 + zz * plane, a.cells, a.err);
+                if (cnt == 0) {
+                    a.id0[c] = sc.id[q];
+                    a.pidx0[c] = sc.idx[q];
+                    a.b0[c] = eps;
+                } else {
+                    a.id1[c] = sc.id[q];
+                    a.b1[c] = eps;
+                }
+                cnts += 1u << (2 * zz);
+                sum[zz] += eps;
+            }
+        }
+    }
+#pragma unroll
+    for (int zz = 0; zz < kBin; ++zz) {
+        const unsigned cnt = (cnts >> (2 * zz)) & 3u;
+        if (inxy && zz < nz && cnt > 0) {  // uncovered cells keep the zeroed count and btot (+0.0)
+            const long long c = c0 + zz * plane;
+            a.count[c] = (uint8_t)cnt;
+            a.btot[c] = sum[zz] < 1.0 ? sum[zz] : 1.0;  // std::min(1.0, sum)
+        }
+    }
+    return __reduce_add_sync(0xffffffffu, (unsigned)__popc(over));
+}
+
+// one warp per unit of every bin (empty bins exit), kWarps warps per CTA. Measured slower
+// (profiles/r02_ab_k12.txt): a persistent grid over a list of the occupied bins' units (static
+// or counter-driven) and a grid over that list — the bin-ordered grid keeps neighbouring bins,
+// which write the same 128-byte lines, on one SM at one time.
+template <int kWarps>
+__global__ void __launch_bounds__(32 * kWarps, 32 / kWarps) map_col_kernel(const MapArgs a) {
+    __shared__ MapCandZ cand_all[kWarps];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long unit = (long long)blockIdx.x * kWarps + w;
+    const long long nbins = (long long)a.g.nb[0] * a.g.nb[1] * a.g.nb[2];
+    if (unit >= 2 * nbins) return;  // warp-uniform
+    const int b = (int)(unit >> 1);
+    const int n = a.cnt[b];
+    if (n == 0) return;
+    const unsigned over = map_unit(a, b, (int)(unit & 1), a.start[b], n, lane, cand_all[w]);
+    if (over && lane == 0) atomicAdd(&a.err->overfull, (unsigned long long)over);
 }
 
 // the zero fills of one mapping in one launch (instead of separate memsets, each an API call
@@ -982,6 +1158,9 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
         if (lbg_status s = grow_device(b->bin_items, b->bin_items_cap, bound, 2 * b->bin_items_cap,
                                        "cudaMalloc(bin items)"))
             return s;
+        if (lbg_status s = grow_device(b->bin_rec, b->bin_rec_cap, b->bin_items_cap, b->bin_items_cap,
+                                       "cudaMalloc(bin records)"))
+            return s;
         bin_count_kernel<<<(n + 127) / 128, 128, 0, b->stream>>>(b->snaps_d, n, g, cnt);
         LBG_LAUNCH_CHECK();
         bin_alloc_kernel<<<(unsigned)((nbins + 255) / 256), 256, 0, b->stream>>>(cnt, (int)nbins, b->bin_start,
@@ -991,7 +1170,7 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
                                                                 b->bin_items);
         LBG_LAUNCH_CHECK();
         bin_sort_kernel<<<(unsigned)((nbins + kSortWarps - 1) / kSortWarps), 32 * kSortWarps, 0, b->stream>>>(
-            b->bin_start, cnt, (int)nbins, b->bin_items);
+            b->bin_start, cnt, (int)nbins, b->bin_items, b->snaps_d, b->bin_rec);
         LBG_LAUNCH_CHECK();
         MapArgs a{};
         a.s = b->snaps_d;
@@ -999,6 +1178,7 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
         a.start = b->bin_start;
         a.cnt = cnt;
         a.items = b->bin_items;
+        a.rec = b->bin_rec;
         a.count = b->count;
         a.id0 = b->id0;
         a.id1 = b->id1;
@@ -1012,15 +1192,27 @@ lbg_status lbg_map(lbg_block b, const lbg_snapshot* snaps, int n, int subdivisio
         // count and btot of every cell were zeroed by map_zero_kernel, so the mapping kernel
         // skips bins without candidates and writes only covered cells
         const long long units = 2 * nbins;
-        static const int minb = [] {  // LBG_MAP_MINB: 5 caps the registers at 48 (A/B)
+        static const int minb = [] {  // LBG_MAP_MINB: 5 caps the registers at 48, 3 at 80 (A/B)
             const char* e = std::getenv("LBG_MAP_MINB");
             return e ? std::atoi(e) : 4;
         }();
         const unsigned mgrid = (unsigned)((units + kMapWarps - 1) / kMapWarps);
-        if (minb == 5)
+        static const int col = [] {  // LBG_MAP_COL=0: the level-outer kernel (A/B)
+            const char* e = std::getenv("LBG_MAP_COL");
+            return e ? std::atoi(e) : 1;
+        }();
+        static const int cw = [] {  // LBG_MAP_CTA_WARPS: 4 or 8 warps per CTA (A/B)
+            const char* e = std::getenv("LBG_MAP_CTA_WARPS");
+            return e && std::atoi(e) == 4 ? 4 : 8;
+        }();
+        if (col) {
+            const unsigned grid = (unsigned)((units + cw - 1) / cw);
+            cw == 4 ? map_col_kernel<4><<<grid, 128, 0, b->stream>>>(a) : map_col_kernel<8><<<grid, 256, 0, b->stream>>>(a);
+        } else if (minb == 5) {
             map_warp_kernel<5><<<mgrid, 32 * kMapWarps, 0, b->stream>>>(a);
-        else
+        } else {
             map_warp_kernel<4><<<mgrid, 32 * kMapWarps, 0, b->stream>>>(a);
+        }
         LBG_LAUNCH_CHECK();
         const long long rows = (long long)b->L.ny * b->L.nz;
         const long long nseg = rows * ((b->L.nx + 31) / 32);

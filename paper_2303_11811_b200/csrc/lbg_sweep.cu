@@ -1400,12 +1400,12 @@ static void launch_unified(lbg_block b, const SweepArgs& a, bool forced, cudaStr
 
 // K12 over the covered-segment list only (unforced, direct snapshot index): one- and
 // two-entry segments, the pipelined operator loop
-static void launch_covered_list(lbg_block b, const SweepArgs& a, cudaStream_t st, int per_sm = 3) {
+static void launch_covered_list(lbg_block b, const SweepArgs& a, cudaStream_t st) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, b->device);
     const bool fused = b->force_mode == LBG_FORCE_FUSED;
     const bool wrapped = a.wrap[0] || a.wrap[1] || a.wrap[2];
-    const unsigned grid = (unsigned)(sms * per_sm);
+    const unsigned grid = (unsigned)(sms * 3);
     with_flags(fused, b->v_snap, wrapped, [&](auto U, auto V, auto W) {
         constexpr bool kU = decltype(U)::value, kV = decltype(V)::value, kW = decltype(W)::value;
         coupled_unified_pipe_kernel<kU, kV, true, kW, true><<<grid, 128, 0, st>>>(a);
@@ -1486,20 +1486,7 @@ lbg_status lbg_sweep(lbg_block b, const lbg_fluid* fl, const lbg_box* range) {
             const double cf = mode == 1 ? covered_fraction(b) : -1.0;
             const bool list_ok = !fo && a.pidx0;
             if (list_ok && (mode == 3 || (mode == 1 && cf >= 0.0 && cf < split_below))) {
-                // K1 over the fluid segments, then K12 over the covered-segment list (or, with
-                // LBG_K12_SPLIT_CONC=1, the list on the aux stream beside K1 at 2 CTAs per SM)
-                static const int conc = env_int("LBG_K12_SPLIT_CONC", 0);
-                if (conc) {
-                    LBG_CUDA(cudaEventRecord(b->ev_fork, b->stream));
-                    LBG_CUDA(cudaStreamWaitEvent(b->aux, b->ev_fork, 0));
-                    launch_covered_list(b, a, b->aux, 2);
-                    LBG_LAUNCH_CHECK();
-                    launch_box<false, true>(a, b->stream);
-                    LBG_LAUNCH_CHECK();
-                    LBG_CUDA(cudaEventRecord(b->ev_join, b->aux));
-                    LBG_CUDA(cudaStreamWaitEvent(b->stream, b->ev_join, 0));
-                    return verify_writes(b, a);
-                }
+                // K1 over the fluid segments, then K12 over the covered-segment list
                 launch_box<false, true>(a, b->stream);
                 LBG_LAUNCH_CHECK();
                 launch_covered_list(b, a, b->stream);

@@ -12,8 +12,9 @@ once per process, so each variant runs the tests in a subprocess):
   LBDEM_GPU_SWEEP=split the drop-in in the reference's inner / halo / BC / outer-shell order;
   LBDEM_GPU_PREMAP=1 the next step's mapping prepared during the last DEM sub-cycle;
   LBDEM_GPU_HALO=stage the staged 19-q device halo instead of the pushed one; LBG_WALK_ROWS=1 /
-  LBG_WALK_REGS=120 the force reduction's row walk / register cap; LBG_MAP_MINB=5 the mapping
-  kernel at 48 registers."""
+  LBG_WALK_REGS=120 the force reduction's row walk / register cap; LBG_MAP_COL=0 the level-outer
+  mapping kernel (LBG_MAP_MINB=5: at 48 registers), LBG_MAP_CTA_WARPS=4 the column mapping kernel
+  in CTAs of 4 warps."""
 import os
 import subprocess
 import sys
@@ -36,7 +37,8 @@ DROPIN = "config1_known_answers or particle_bed or decomposition_invariance or c
                                  {"LBG_K12_PIPE": "0", "LBG_K12_SM": "6"},
                                  {"LBG_SWEEP_PAIR": "1"}, {"LBDEM_GPU_SWEEP": "split"}, {"LBDEM_GPU_PREMAP": "1"},
                                  {"LBDEM_GPU_HALO": "stage"}, {"LBG_WALK_ROWS": "1"}, {"LBG_WALK_REGS": "120"},
-                                 {"LBG_MAP_MINB": "5"}])
+                                 {"LBG_MAP_COL": "0"}, {"LBG_MAP_COL": "0", "LBG_MAP_MINB": "5"},
+                                 {"LBG_MAP_CTA_WARPS": "4"}])
 def test_parity_suite_under_variant(env):
     e = dict(os.environ, **env)
     # the parity cases, and drop-in runs vs the reference (config 1: periodic block, in-kernel
