@@ -208,9 +208,12 @@ public:
 
     std::vector<psm::HydroPartial> finalize_hydro_forces(int mode = -1) {
         if (mode < 0) mode = fused_ ? LBG_REDUCE_FAST : LBG_REDUCE_PARITY;
-        std::vector<lbg_hydro_partial> out(cs_.size() + 1);
+        // the raw partials buffer persists across steps (no 1-MB value-initialised allocation
+        // per call at 10^4 particles)
+        if (red_out_.size() < cs_.size() + 1) red_out_.resize(cs_.size() + 1);
+        lbg_hydro_partial* out = red_out_.data();
         int n = 0;
-        check(lbg_reduce_hydro(b_, mode, out.data(), static_cast<int>(out.size()), &n));
+        check(lbg_reduce_hydro(b_, mode, out, static_cast<int>(red_out_.size()), &n));
         std::vector<psm::HydroPartial> parts(static_cast<std::size_t>(n));
         for (int i = 0; i < n; ++i) {
             parts[i].id = out[i].id;
@@ -242,6 +245,7 @@ private:
     lbg_block b_ = nullptr;
     bool fused_ = false;
     std::vector<lbg_snapshot> cs_;
+    std::vector<lbg_hydro_partial> red_out_;
 };
 
 }  // namespace lbdem::gpu

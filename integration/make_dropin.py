@@ -41,7 +41,7 @@ SIM_HPP_EDITS = [
 SIM_CPP_EDITS = [
     # includes + host-copy refresh used by the observers
     ("#include <set>\n",
-     "#include <set>\n#include <cstdlib>\n#include <cstring>\n\n#include \"lbdem_gpu.hpp\"\n#include \"dropin_observe.hpp\"\n"),
+     "#include <set>\n#include <cstdlib>\n#include <cstring>\n#include <limits>\n\n#include \"lbdem_gpu.hpp\"\n#include \"dropin_observe.hpp\"\n"),
     ("namespace lbdem {\n\nusing partition::MsgKind;",
      "namespace lbdem {\n\n"
      "namespace {\n"
@@ -120,6 +120,70 @@ SIM_CPP_EDITS = [
      "        m.host_stale = false;\n"
      "    }\n"
      "}\n"
+     "/// LBDEM_GPU_FAST_SYNC=0: the reference's host particle-messaging code as written. Default:\n"
+     "/// the same results (ids are unique and sorted, so every lookup, sort and patch below finds\n"
+     "/// what the reference's finds) with the quadratic snapshot patch of apply_velocity_sync\n"
+     "/// replaced by a binary search, apply_particle_sync's struct sort by an in-place key\n"
+     "/// permutation into reused storage, and phase_apply_hydro's sort skipped when its input is\n"
+     "/// already in (id, block) order, and the partials' particle lookups done by a forward\n"
+     "/// cursor (SURVEY 8(f)#3; profiles/r02_host_sync.txt).\n"
+     "bool fast_sync() {\n"
+     "    static const bool on = [] {\n"
+     "        const char* e = std::getenv(\"LBDEM_GPU_FAST_SYNC\");\n"
+     "        return !(e && std::atoi(e) == 0);\n"
+     "    }();\n"
+     "    return on;\n"
+     "}\n"
+     "/// apply_particle_sync's sort (ascending id; the reference checks uniqueness right after,\n"
+     "/// so with unique ids the order is std::sort's): the (id, index) keys are sorted and the\n"
+     "/// particles permuted in place along the cycles, one move each, no allocation\n"
+     "void sort_by_id(std::vector<dem::Particle>& v) {\n"
+     "    if (std::is_sorted(v.begin(), v.end(),\n"
+     "                       [](const dem::Particle& a, const dem::Particle& b2) { return a.id < b2.id; }))\n"
+     "        return;\n"
+     "    thread_local std::vector<std::pair<int, int>> keys;\n"
+     "    thread_local std::vector<unsigned char> done;\n"
+     "    const std::size_t n = v.size();\n"
+     "    keys.resize(n);\n"
+     "    for (std::size_t i = 0; i < n; ++i) keys[i] = {v[i].id, static_cast<int>(i)};\n"
+     "    std::sort(keys.begin(), keys.end());\n"
+     "    done.assign(n, 0);\n"
+     "    for (std::size_t i = 0; i < n; ++i) {\n"
+     "        if (done[i]) continue;\n"
+     "        done[i] = 1;\n"
+     "        if (static_cast<std::size_t>(keys[i].second) == i) continue;\n"
+     "        dem::Particle tmp = std::move(v[i]);\n"
+     "        std::size_t j = i;\n"
+     "        for (;;) {\n"
+     "            const std::size_t src = static_cast<std::size_t>(keys[j].second);\n"
+     "            done[j] = 1;\n"
+     "            if (src == i) {\n"
+     "                v[j] = std::move(tmp);\n"
+     "                break;\n"
+     "            }\n"
+     "            v[j] = std::move(v[src]);\n"
+     "            j = src;\n"
+     "        }\n"
+     "    }\n"
+     "}\n"
+     "/// blk.particle(id) for ascending ids (the partial lists of phase_outer_reduce and\n"
+     "/// phase_apply_hydro): a forward cursor over the id-sorted particle list finds what the\n"
+     "/// binary search finds without its cache-missing probes; any id below the last one asked\n"
+     "/// falls back to the binary search\n"
+     "struct ParticleCursor {\n"
+     "    BlockState& blk;\n"
+     "    std::size_t i = 0;\n"
+     "    int last = std::numeric_limits<int>::min();\n"
+     "    dem::Particle* operator()(int id) {\n"
+     "        if (!fast_sync() || id < last) return blk.particle(id);\n"
+     "        last = id;\n"
+     "        auto& v = blk.particles;\n"
+     "        while (i < v.size() && v[i].id < id) ++i;\n"
+     "        return (i < v.size() && v[i].id == id) ? &v[i] : nullptr;\n"
+     "    }\n"
+     "};\n"
+     "/// apply_particle_sync's list reuses the storage of the list it replaced (per worker thread)\n"
+     "thread_local std::vector<dem::Particle> particle_scratch;\n"
      "}  // namespace\n\n"
      "using partition::MsgKind;"),
     # sim.cpp:15-25 — BlockState ctor: optional host mirror, create the device block
@@ -313,6 +377,90 @@ SIM_CPP_EDITS = [
      "                                      cell.z - blk.box.lo.z)];\n",
      "    return gpu::cell_fraction(blk, cell.x - blk.box.lo.x, cell.y - blk.box.lo.y,\n"
      "                              cell.z - blk.box.lo.z);\n"),
+    # sim.cpp:249-266 - apply_velocity_sync: the snapshot patch by binary search (fast_sync())
+    ("void Simulation::apply_velocity_sync(BlockState& blk) {\n",
+     "void Simulation::apply_velocity_sync(BlockState& blk) {\n"
+     "    const bool psorted = fast_sync() &&\n"
+     "                         std::is_sorted(blk.snapshots.begin(), blk.snapshots.end(),\n"
+     "                                        [](const psm::ParticleSnapshot& a, const psm::ParticleSnapshot& b2) {\n"
+     "                                            return a.id < b2.id;\n"
+     "                                        });\n"),
+    ("            // Patch the kernel snapshot built before the sync arrived.\n"
+     "            for (auto& s : blk.snapshots)\n"
+     "                if (s.id == rec.id) {\n"
+     "                    s.u = rec.u;\n"
+     "                    s.omega = rec.w;\n"
+     "                    break;\n"
+     "                }\n",
+     "            // Patch the kernel snapshot built before the sync arrived (ascending unique ids:\n"
+     "            // the binary search finds the linear scan's match)\n"
+     "            if (psorted) {\n"
+     "                auto it = std::lower_bound(blk.snapshots.begin(), blk.snapshots.end(), rec.id,\n"
+     "                                           [](const psm::ParticleSnapshot& s, int v) { return s.id < v; });\n"
+     "                if (it != blk.snapshots.end() && it->id == rec.id) {\n"
+     "                    it->u = rec.u;\n"
+     "                    it->omega = rec.w;\n"
+     "                }\n"
+     "            } else {\n"
+     "                for (auto& s : blk.snapshots)\n"
+     "                    if (s.id == rec.id) {\n"
+     "                        s.u = rec.u;\n"
+     "                        s.omega = rec.w;\n"
+     "                        break;\n"
+     "                    }\n"
+     "            }\n"),
+    # sim.cpp:441-497 - apply_particle_sync: reused storage and the key-permutation sort
+    ("    std::vector<dem::Particle> next;\n"
+     "    next.reserve(blk.particles.size());\n",
+     "    std::vector<dem::Particle> next;\n"
+     "    if (fast_sync()) next = std::move(particle_scratch);\n"
+     "    next.clear();\n"
+     "    next.reserve(blk.particles.size());\n"),
+    ("    std::sort(next.begin(), next.end(),\n"
+     "              [](const dem::Particle& a, const dem::Particle& b2) { return a.id < b2.id; });\n",
+     "    if (fast_sync())\n"
+     "        sort_by_id(next);\n"
+     "    else\n"
+     "        std::sort(next.begin(), next.end(),\n"
+     "                  [](const dem::Particle& a, const dem::Particle& b2) { return a.id < b2.id; });\n"),
+    ("    blk.particles = std::move(next);\n"
+     "    (void)s;\n",
+     "    std::swap(blk.particles, next);\n"
+     "    if (fast_sync()) particle_scratch = std::move(next);\n"
+     "    (void)s;\n"),
+    # sim.cpp:353-356 - phase_apply_hydro: no sort of a list already in (id, block) order
+    ("    std::sort(all.begin(), all.end(), [](const auto& a, const auto& b2) {\n"
+     "        if (a.second->id != b2.second->id) return a.second->id < b2.second->id;\n"
+     "        return a.first < b2.first;\n"
+     "    });\n",
+     "    const auto by_id_src = [](const auto& a, const auto& b2) {\n"
+     "        if (a.second->id != b2.second->id) return a.second->id < b2.second->id;\n"
+     "        return a.first < b2.first;\n"
+     "    };\n"
+     "    if (!fast_sync() || !std::is_sorted(all.begin(), all.end(), by_id_src))\n"
+     "        std::sort(all.begin(), all.end(), by_id_src);\n"),
+    # sim.cpp:323-325 / 378-380 - the partials' particle lookups through the forward cursor
+    ("    for (const psm::HydroPartial& p : partials) {\n"
+     "        const dem::Particle* part = blk.particle(p.id);\n",
+     "    ParticleCursor cursor{blk};\n"
+     "    for (const psm::HydroPartial& p : partials) {\n"
+     "        const dem::Particle* part = cursor(p.id);\n"),
+    ("    std::size_t i = 0;\n"
+     "    while (i < all.size()) {\n",
+     "    ParticleCursor cursor{blk};\n"
+     "    std::size_t i = 0;\n"
+     "    while (i < all.size()) {\n"),
+    ("        dem::Particle* part = blk.particle(id);\n"
+     "        if (part == nullptr || part->ghost)\n",
+     "        dem::Particle* part = cursor(id);\n"
+     "        if (part == nullptr || part->ghost)\n"),
+    # sim.cpp:322 / 347 - the partial lists sized once (fast_sync(); no regrowth copies)
+    ("    blk.own_partials.clear();\n",
+     "    blk.own_partials.clear();\n"
+     "    if (fast_sync()) blk.own_partials.reserve(partials.size());\n"),
+    ("    std::vector<std::pair<int, const psm::HydroPartial*>> all;\n",
+     "    std::vector<std::pair<int, const psm::HydroPartial*>> all;\n"
+     "    if (fast_sync()) all.reserve(blk.own_partials.size());\n"),
 ]
 
 
