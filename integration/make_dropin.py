@@ -125,8 +125,9 @@ SIM_CPP_EDITS = [
      "/// what the reference's finds) with the quadratic snapshot patch of apply_velocity_sync\n"
      "/// replaced by a binary search, apply_particle_sync's struct sort by an in-place key\n"
      "/// permutation into reused storage, and phase_apply_hydro's sort skipped when its input is\n"
-     "/// already in (id, block) order, and the partials' particle lookups done by a forward\n"
-     "/// cursor (SURVEY 8(f)#3; profiles/r02_host_sync.txt).\n"
+     "/// already in (id, block) order, the partials' particle lookups done by a forward cursor,\n"
+     "/// and the ghost-eligibility loops skipping particles deep inside the block (SURVEY\n"
+     "/// 8(f)#3; profiles/r02_host_sync.txt).\n"
      "bool fast_sync() {\n"
      "    static const bool on = [] {\n"
      "        const char* e = std::getenv(\"LBDEM_GPU_FAST_SYNC\");\n"
@@ -182,6 +183,20 @@ SIM_CPP_EDITS = [
      "        return (i < v.size() && v[i].id == id) ? &v[i] : nullptr;\n"
      "    }\n"
      "};\n"
+     "/// a particle of the block whose distance to every face of the block box exceeds its ghost\n"
+     "/// reach (r + margin, with a 1e-9 relative guard far above rounding) is ghost-eligible for\n"
+     "/// no other block: any other block's box lies outside this one, so ghost_eligible's d2 is at\n"
+     "/// least that distance squared. The neighbour loops skip it (false for a particle outside).\n"
+     "bool deep_inside(const dem::Particle& p, const CellBox& box, double margin) {\n"
+     "    const double reach = p.r + margin;\n"
+     "    double dmin = std::numeric_limits<double>::infinity();\n"
+     "    for (int a = 0; a < 3; ++a) {\n"
+     "        const double lo = box.lo[a], hi = box.hi[a];\n"
+     "        if (!(p.x[a] >= lo && p.x[a] <= hi)) return false;\n"
+     "        dmin = std::min(dmin, std::min(p.x[a] - lo, hi - p.x[a]));\n"
+     "    }\n"
+     "    return dmin > reach * (1.0 + 1e-9);\n"
+     "}\n"
      "/// apply_particle_sync's list reuses the storage of the list it replaced (per worker thread)\n"
      "thread_local std::vector<dem::Particle> particle_scratch;\n"
      "}  // namespace\n\n"
@@ -461,6 +476,19 @@ SIM_CPP_EDITS = [
     ("    std::vector<std::pair<int, const psm::HydroPartial*>> all;\n",
      "    std::vector<std::pair<int, const psm::HydroPartial*>> all;\n"
      "    if (fast_sync()) all.reserve(blk.own_partials.size());\n"),
+    # sim.cpp:243-246 / 433-437 - the ghost loops skip particles deep inside the block
+    ("        for (const dem::Particle& p : blk.particles) {\n"
+     "            if (p.ghost) continue;\n"
+     "            if (ghost_eligible(p, nb)) per_dst[nb].push_back({p.id, p.u, p.w});\n",
+     "        for (const dem::Particle& p : blk.particles) {\n"
+     "            if (p.ghost) continue;\n"
+     "            if (fast_sync() && deep_inside(p, blk.box, ghost_margin())) continue;\n"
+     "            if (ghost_eligible(p, nb)) per_dst[nb].push_back({p.id, p.u, p.w});\n"),
+    ("        rec.migrate = false;\n"
+     "        for (int nb : neighbors) {\n",
+     "        rec.migrate = false;\n"
+     "        if (fast_sync() && owner == blk.id && deep_inside(p, blk.box, ghost_margin())) continue;\n"
+     "        for (int nb : neighbors) {\n"),
 ]
 
 
