@@ -34,6 +34,7 @@ def load(path: str = SO):
         L.dropin_sim_create.argtypes = [C.c_char_p]
         L.dropin_sim_destroy.argtypes = [vp]
         L.dropin_sim_run.argtypes = [vp, C.c_long]
+        L.dropin_sim_add_particles.argtypes = [vp, C.c_int, dp]
         L.dropin_sim_cells.restype = C.c_long
         L.dropin_sim_cells.argtypes = [vp]
         L.dropin_sim_num_particles.restype = C.c_int
@@ -73,6 +74,11 @@ class DropinSim:
 
     def run(self, steps):
         self._check(self.L.dropin_sim_run(self.h, steps))
+
+    def add_particles(self, rows):
+        """rows: (n, 6) of id, x, y, z, r, m (Simulation::add_particles)"""
+        rows = np.ascontiguousarray(rows, dtype=np.float64)
+        self._check(self.L.dropin_sim_add_particles(self.h, len(rows), rows))
 
     def shear_wave(self):
         self._check(self.L.dropin_sim_shear_wave(self.h))

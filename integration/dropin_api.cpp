@@ -9,6 +9,7 @@
 #include <cmath>
 #include <memory>
 #include <string>
+#include <vector>
 
 #include "lbdem/config.hpp"
 #include "lbdem/errors.hpp"
@@ -76,6 +77,22 @@ void dropin_sim_destroy(void* h) { delete R(h); }
 
 int dropin_sim_run(void* h, long steps) {
     return guarded([&] { R(h)->sim->run(steps); });
+}
+
+// Simulation::add_particles (sim.cpp:67-94) with rows {id, x, y, z, r, m}: test scenarios
+// the presets cannot make (e.g. three spheres sharing cells)
+int dropin_sim_add_particles(void* h, int n, const double* rows) {
+    return guarded([&] {
+        std::vector<dem::Particle> ps(static_cast<std::size_t>(n));
+        for (int i = 0; i < n; ++i) {
+            const double* r = rows + 6 * i;
+            ps[i].id = static_cast<int>(r[0]);
+            ps[i].x = {r[1], r[2], r[3]};
+            ps[i].r = r[4];
+            ps[i].m = r[5];
+        }
+        R(h)->sim->add_particles(ps);
+    });
 }
 
 long dropin_sim_cells(void* h) {

@@ -292,7 +292,19 @@ SIM_CPP_EDITS = [
      "        else\n"
      "            blk.dev->map(blk.snapshots, params_.subdivisions);\n"
      "        blk.premapped = false;\n"
-     "        blk.dev->sync();\n"),
+     "        // no wait here: the mapping runs under post_velocity_sync, checked right after it\n"),
+    # sim.cpp:282-285 - the mapping's end-of-operator check (overfull cells: NumericError, the
+    # reference's text) once the velocity records are posted
+    ("        ScopedTimer t(blk.timings, Category::kPdComm);\n"
+     "        post_velocity_sync(blk);\n"
+     "    }\n",
+     "        ScopedTimer t(blk.timings, Category::kPdComm);\n"
+     "        post_velocity_sync(blk);\n"
+     "    }\n"
+     "    if (params_.coupling) {\n"
+     "        ScopedTimer t(blk.timings, Category::kMapping);\n"
+     "        blk.dev->sync();\n"
+     "    }\n"),
     # sim.cpp:623-628 - the next step's mapping issued once its inputs are final (premap_on())
     ("        ScopedTimer t(blk.timings, Category::kPdComm);\n"
      "        apply_particle_sync(blk, s);\n"
@@ -484,11 +496,14 @@ SIM_CPP_EDITS = [
      "            if (p.ghost) continue;\n"
      "            if (fast_sync() && deep_inside(p, blk.box, ghost_margin())) continue;\n"
      "            if (ghost_eligible(p, nb)) per_dst[nb].push_back({p.id, p.u, p.w});\n"),
-    ("        rec.migrate = false;\n"
-     "        for (int nb : neighbors) {\n",
-     "        rec.migrate = false;\n"
+    ("        const int owner = decomp_.block_of_position(p.x);\n"
+     "\n"
+     "        partition::StateRecord rec;\n",
+     "        const int owner = decomp_.block_of_position(p.x);\n"
+     "        // neither migrating nor a ghost anywhere: nothing to send\n"
      "        if (fast_sync() && owner == blk.id && deep_inside(p, blk.box, ghost_margin())) continue;\n"
-     "        for (int nb : neighbors) {\n"),
+     "\n"
+     "        partition::StateRecord rec;\n"),
 ]
 
 

@@ -277,6 +277,7 @@ class RefLib:
         L.ref_sim_create.argtypes = [C.c_char_p]
         L.ref_sim_destroy.argtypes = [vp]
         L.ref_sim_run.argtypes = [vp, C.c_long]
+        L.ref_sim_add_particles.argtypes = [vp, C.c_int, _dp]
         L.ref_sim_params.argtypes = [vp, C.POINTER(C.c_double), _dp, _ip]
         L.ref_sim_shear_wave.argtypes = [vp]
         L.ref_sim_pdfs.argtypes = [vp, _dp]
@@ -429,6 +430,11 @@ class RefSim:
 
     def run(self, steps):
         self.lib.check(self.L.ref_sim_run(self.h, steps))
+
+    def add_particles(self, rows):
+        """rows: (n, 6) of id, x, y, z, r, m (Simulation::add_particles)"""
+        rows = np.ascontiguousarray(rows, dtype=np.float64)
+        self.lib.check(self.L.ref_sim_add_particles(self.h, len(rows), rows))
 
     def shear_wave(self):
         self.L.ref_sim_shear_wave(self.h)

@@ -322,6 +322,21 @@ int ref_sim_run(void* h, long steps) {
     return guarded([&] { static_cast<RefSim*>(h)->sim->run(steps); });
 }
 
+// Simulation::add_particles with rows {id, x, y, z, r, m} (dropin_sim_add_particles' twin)
+int ref_sim_add_particles(void* h, int n, const double* rows) {
+    return guarded([&] {
+        std::vector<dem::Particle> ps(static_cast<std::size_t>(n));
+        for (int i = 0; i < n; ++i) {
+            const double* r = rows + 6 * i;
+            ps[i].id = static_cast<int>(r[0]);
+            ps[i].x = {r[1], r[2], r[3]};
+            ps[i].r = r[4];
+            ps[i].m = r[5];
+        }
+        static_cast<RefSim*>(h)->sim->add_particles(ps);
+    });
+}
+
 void ref_sim_params(void* h, double* tau, double fext[3], int domain[3]) {
     const auto& c = static_cast<RefSim*>(h)->cfg;
     *tau = c.fluid.tau;

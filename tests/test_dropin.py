@@ -119,6 +119,30 @@ def test_errors_propagate_as_reference_exceptions(dropin):
     assert "tau" in str(e.value)
 
 
+@pytest.mark.parametrize("blocks", [[1, 1, 1], [2, 1, 1]])
+def test_overfull_cells_raise_the_reference_error(dropin, ref, blocks):
+    """Three spheres sharing cells: build_fraction_field's NumericError (psm.cpp:132-135) with
+    the reference's text and count, raised by the step as the reference's is (the drop-in
+    checks the mapping after posting the velocity records)."""
+    cfg = ('{"scenario":"custom","domain":[32,24,24],"blocks":%s,"workers":%d,'
+           '"fluid":{"tau":0.8,"coupling":true},"particles":{"count":0},"dem":{"subcycles":2}}'
+           % (json.dumps(blocks), blocks[0]))
+    # inside block 0 (and no other block's ghost), so one block raises
+    rows = np.array([[1, 7.2, 12.0, 12.0, 3.0, 1.0], [2, 8.1, 12.3, 11.8, 3.0, 1.0],
+                     [3, 7.7, 11.6, 12.4, 3.0, 1.0]])
+    a = dropin.DropinSim(cfg, (32, 24, 24))
+    b = ref.sim(cfg)
+    a.add_particles(rows)
+    b.add_particles(rows)
+    with pytest.raises(dropin.DropinError) as ea:
+        a.run(1)
+    with pytest.raises(Exception) as eb:
+        b.run(1)
+    assert ea.value.code == 2 and getattr(eb.value, "code", None) == 2
+    assert "more than two particles overlap a single cell" in str(ea.value)
+    assert str(ea.value).split("] ", 1)[1] == str(eb.value).split("] ", 1)[1]
+
+
 @pytest.mark.parametrize("blocks,workers", [([1, 1, 1], 1), ([2, 1, 2], 2)])
 def test_fused_force_mode_tracks_reference(dropin, ref, blocks, workers, monkeypatch):
     """SURVEY §8(c) parity contract for the non-bitwise force path: with LBDEM_GPU_FORCE=fused
