@@ -324,7 +324,11 @@ def coupled_sweep_roofline(steps=10, warmup=3, cfg=None, n=256, label="config 3 
         blk.sync()
         cnt = blk.download_fraction()["count"]
         n1, n2 = int((cnt == 1).sum()), int((cnt == 2).sum())
-        del cnt
+        # the sweep's per-block kernel choice (lbg_sweep.cu, LBG_K12=1): the covered fraction of
+        # the aligned 32-cell row segments against LBG_K12_SPLIT_BELOW (0.35)
+        segs = cnt.reshape(n, n, -1, 32).max(axis=3) if n % 32 == 0 else None
+        cov_frac = float((segs > 0).mean()) if segs is not None else None
+        del cnt, segs
         F = lbdem.FaceBc
         spec = lbdem.BcSpec([F(lbdem.BcKind.no_slip)] * 4 +
                             [F(lbdem.BcKind.velocity, (0.0, 0.0, u_in)), F(lbdem.BcKind.pressure, rho=1.0)])
@@ -370,8 +374,12 @@ def coupled_sweep_roofline(steps=10, warmup=3, cfg=None, n=256, label="config 3 
     pk = peaks()
     peak = pk["hbm_gbs"] if pk and pk.get("hbm_gbs") else 6650.0
     achieved = algo / (sweep_ms / 1e3) / 1e9
+    split = cov_frac is not None and cov_frac < float(os.environ.get("LBG_K12_SPLIT_BELOW", "0.35"))
+    kernels = ("K1 sweep_box_kernel over the fluid segments + K12 coupled_unified_pipe_kernel over the "
+               "covered-segment list" if split else
+               "K12 coupled_unified_pipe_kernel (fluid, one-entry and two-entry segments in one kernel)")
     return {"workload": label,
-            "kernels": "K12 coupled_unified_pipe_kernel (fluid, one-entry and two-entry segments in one kernel)",
+            "kernels": kernels, "covered_segment_fraction": None if cov_frac is None else round(cov_frac, 4),
             "cells": cells, "one_entry_cells": n1, "two_entry_cells": n2,
             "algorithmic_bytes_per_step": algo, "sweep_ms": round(sweep_ms, 4), "bc_ms": round(bc_ms / steps, 4),
             "mlups": round(cells / (sweep_ms / 1e3) / 1e6, 1),
