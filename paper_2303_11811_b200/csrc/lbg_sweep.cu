@@ -1029,8 +1029,11 @@ __device__ __forceinline__ void useg_finish(const SweepArgs& a, const USeg& u, c
         if (u.mx == 1) fused_accumulate(a, p0, m, cc);
 }
 
+#ifndef LBG_K12_MINB
+#define LBG_K12_MINB 3  // CTAs per SM the register budget is set for (A/B builds: 4)
+#endif
 template <bool kFused, bool kVsnap, bool kTwoInline, bool kWrap, bool kList = false>
-__global__ void __launch_bounds__(128, 3) coupled_unified_pipe_kernel(const SweepArgs a) {
+__global__ void __launch_bounds__(128, LBG_K12_MINB) coupled_unified_pipe_kernel(const SweepArgs a) {
     const int lane = threadIdx.x & 31;
     const long long warp = (long long)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const long long nwarps = (long long)((gridDim.x * blockDim.x) >> 5);
@@ -1068,6 +1071,171 @@ __global__ void __launch_bounds__(128, 3) coupled_unified_pipe_kernel(const Swee
         if constexpr (kList) rawfar = useg_raw(a, s + 3 * nwarps, nseg, n1);
         if (s + nwarps < nseg) useg_issue<kTwoInline, kWrap>(a, id1, lane, c1, nxt);
         useg_finish<kFused, kVsnap, kTwoInline>(a, cur, pre);
+    }
+}
+
+// K12, TMA-fed (LBG_K12_TMA=1; unforced, non-fused, direct snapshot index, unwrapped blocks):
+// the register-pipelined kernel above keeps the next segment's 19 populations and cell fields
+// in registers (166 registers, 3 CTAs of 4 warps per SM) and still waits for them in most of
+// its stall samples. Here each warp owns kTStages shared-memory stages, filled by 1-D bulk
+// copies (one per pulled q-row, issued by lanes 0..18 in parallel, plus the btot / b0 / pidx0
+// windows of a covered segment by lanes 19..21) completing on the stage's mbarrier — nothing in
+// flight occupies registers or the LSU. The row windows are the sectors the lanes' pulls touch
+// and no more: [i0, i0 + 32) for c_x = 0, [i0 - 2, i0 + 32) for c_x = +1 (pull from x - 1),
+// [i0, i0 + 34) for c_x = -1 (16-byte aligned starts). The lanes store their count bytes
+// (loaded one segment before the copies are issued) into the stage. The consumer rebuilds the
+// USeg from the stage and runs the same useg_pre / useg_finish as the register-pipelined
+// kernel, so the results are bitwise the same.
+struct TStage {
+    double f[kQ][34];
+    double bt[34];
+    double b0[34];
+    int pe[36];
+    int cnt[32];
+    int mx, pad[3];
+};
+static_assert(sizeof(TStage) % 16 == 0, "TMA stage must keep 16-byte alignment");
+constexpr int kTWarps = 4;   // warps per CTA
+constexpr int kTStages = 2;  // stages per warp
+
+__host__ __device__ constexpr size_t tma_smem_bytes() {
+    return sizeof(TStage) * kTStages * kTWarps + sizeof(unsigned long long) * kTStages * kTWarps;
+}
+
+// the row window of population q: first element (relative to i0) and bytes
+__device__ __forceinline__ int trow_first(int q) { return cx(q) == 1 ? -2 : 0; }
+__device__ __forceinline__ unsigned trow_bytes(int q) { return cx(q) == 0 ? 256u : 272u; }
+// index of lane l's pulled value (x = i0 + l - c_x) in its row window
+__device__ __forceinline__ int trow_at(int q, int l) { return l - cx(q) - trow_first(q); }
+
+// the whole warp: the copies of segment `id` (warp max count mx) into `st`; lane q < 19 copies
+// row q
+__device__ __forceinline__ void tseg_issue(const SweepArgs& a, const USegId& id, int mx, TStage& st,
+                                           unsigned long long* bar, int lane) {
+    const Layout& L = a.L;
+    // lane q: the offset of its row window from the segment's cell index, and its size
+    // (compile-time per q: a select chain, no local-memory table)
+    long long roff = 0;
+    unsigned rbytes = 0;
+#pragma unroll
+    for (int q = 0; q < kQ; ++q)
+        if (lane == q) {
+            roff = (long long)q * L.plane + trow_first(q) - cy(q) * (long long)L.px -
+                   cz(q) * (long long)L.px * L.py;
+            rbytes = trow_bytes(q);
+        }
+    const long long c = L.frac(id.i0, id.j, id.k);
+    const long long c2 = c & ~1LL, c4 = c & ~3LL;
+    const unsigned bb = (unsigned)(((c + 32 - c2) + 1) & ~1LL) * 8u;  // 256 or 272
+    const unsigned pb = (unsigned)(((c + 32 - c4) + 3) & ~3LL) * 4u;  // 128 .. 144
+    if (lane == 0) {
+        unsigned tx = 9u * 256u + 10u * 272u;
+        if (mx >= 1) tx += 2u * bb + pb;
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // the consumer's reads of st
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(tx)
+                     : "memory");
+    }
+    __syncwarp();
+    if (lane < kQ) {
+        tma_bulk(&st.f[0][0] + 34 * lane, a.src + (L.idx(id.i0, id.j, id.k) + roff), rbytes, bar);
+    } else if (mx >= 1) {
+        if (lane == kQ) tma_bulk(st.bt, a.btot + c2, bb, bar);
+        if (lane == kQ + 1) tma_bulk(st.b0, a.b0 + c2, bb, bar);
+        if (lane == kQ + 2) tma_bulk(st.pe, a.pidx0 + c4, pb, bar);
+    }
+}
+
+template <bool kVsnap>
+__global__ void __launch_bounds__(32 * kTWarps, 4) coupled_tma_kernel(const SweepArgs a) {
+    extern __shared__ __align__(128) unsigned char tsm[];
+    const Layout& L = a.L;
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const long long warp = (long long)blockIdx.x * kTWarps + wl;
+    const long long nwarps = (long long)gridDim.x * kTWarps;
+    const int segs_x = (a.hi[0] - a.i0 + 31) >> 5;
+    const int ny_b = a.hi[1] - a.lo[1];
+    const long long nseg = (long long)segs_x * ny_b * (a.hi[2] - a.lo[2]);
+    TStage* st = reinterpret_cast<TStage*>(tsm) + kTStages * wl;
+    unsigned long long* bar =
+        reinterpret_cast<unsigned long long*>(tsm + sizeof(TStage) * kTStages * kTWarps) + kTStages * wl;
+    if (warp >= nseg) return;  // warp-uniform
+    if (lane == 0) {
+        for (int t = 0; t < kTStages; ++t)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bar[t])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    // issue segment s into stage t: counts into the stage (this lane's), the copies
+    auto issue = [&](long long s, int cnt, int t) {
+        const USegId id = useg_dense(a, s, segs_x, ny_b);
+        const int mx = (int)__reduce_max_sync(0xffffffffu, (unsigned)cnt);
+        st[t].cnt[lane] = cnt;
+        if (lane == 0) st[t].mx = mx;
+        tseg_issue(a, id, mx, st[t], &bar[t], lane);
+    };
+    // prologue: the first kTStages segments in flight, the counts of the next one loaded
+#pragma unroll
+    for (int t = 0; t < kTStages; ++t) {
+        const long long s = warp + t * nwarps;
+        if (s < nseg) issue(s, useg_count(a, useg_dense(a, s, segs_x, ny_b), true, lane), t);
+    }
+    long long sfar = warp + kTStages * nwarps;
+    int cfar = useg_count(a, useg_dense(a, sfar < nseg ? sfar : 0, segs_x, ny_b), sfar < nseg, lane);
+    unsigned phase = 0;  // bit t: parity of stage t
+    int t = 0;
+    for (long long s = warp; s < nseg; s += nwarps) {
+        {
+            unsigned done = 0;
+            const unsigned par = (phase >> t) & 1u;
+            do {
+                asm volatile(
+                    "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                    " selp.u32 %0, 1, 0, p;\n}\n"
+                    : "=r"(done)
+                    : "r"(smem_u32(&bar[t])), "r"(par)
+                    : "memory");
+            } while (!done);
+            phase ^= 1u << t;
+        }
+        __syncwarp();  // the lanes' count stores of this stage are visible
+        // rebuild the segment from the stage
+        USeg u;
+        {
+            const TStage& S = st[t];
+            const USegId id = useg_dense(a, s, segs_x, ny_b);
+            u.i = id.i0 + lane;
+            u.j = id.j;
+            u.k = id.k;
+            const bool inx = u.i < L.nx;
+            u.fc = LBG_IDX(L.frac(inx ? u.i : L.nx - 1, u.j, u.k), a.cells, a.err);
+            u.act = inx && u.i >= a.lo[0] && u.i < a.hi[0];
+            u.cnt = S.cnt[lane];
+            u.mx = S.mx;
+            const long long c0 = L.frac(id.i0, id.j, id.k);
+            if (u.mx >= 1) {
+                u.bt = S.bt[lane + (int)(c0 & 1)];
+                u.b0 = S.b0[lane + (int)(c0 & 1)];
+                u.pe = S.pe[lane + (int)(c0 & 3)];
+            }
+            if (u.mx >= 2) {  // two-entry segment (rare): entry 1 from global
+                u.b1 = a.b1[u.fc];
+                u.id1 = a.id1[u.fc];
+            }
+            u.base = LBG_IDX(L.idx(u.i, u.j, u.k), L.plane, a.err);
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) u.f[q] = S.f[q][trow_at(q, lane)];
+        }
+        UPre pre;
+        useg_pre<kVsnap, true>(a, u, pre);
+        // the next count set (one segment ahead of its copies)
+        const int c1 = cfar;
+        const long long s1 = sfar;
+        sfar += nwarps;
+        cfar = useg_count(a, useg_dense(a, sfar < nseg ? sfar : 0, segs_x, ny_b), sfar < nseg, lane);
+        __syncwarp();  // every lane has read stage t
+        if (s1 < nseg) issue(s1, c1, t);
+        useg_finish<false, kVsnap, true>(a, u, pre);
+        t = (t + 1 == kTStages) ? 0 : t + 1;
     }
 }
 
@@ -1377,15 +1545,28 @@ static void launch_unified(lbg_block b, const SweepArgs& a, bool forced, cudaStr
         static const int two_inline = env_int("LBG_K12_TWO", 1);
         static const int nowrap = env_int("LBG_K12_NOWRAP", 1);  // 0: the generic pull (A/B)
         const bool wrapped = a.wrap[0] || a.wrap[1] || a.wrap[2] || !nowrap;
+        static const int tma = env_int("LBG_K12_TMA", 0);
+        if (!kF && !kU && pipe && a.pidx0 && two_inline && tma && !wrapped) {
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(coupled_tma_kernel<kV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)tma_smem_bytes());
+                attr = true;
+            }
+            const long long want = (nseg + kTWarps - 1) / kTWarps;
+            const unsigned grid = (unsigned)std::max(1LL, std::min<long long>(want, (long long)sms * 4));
+            coupled_tma_kernel<kV><<<grid, 32 * kTWarps, tma_smem_bytes(), st>>>(a);
+            return;
+        }
         if (!kF && pipe && a.pidx0 && two_inline) {
             if (wrapped)
-                go(coupled_unified_pipe_kernel<kU, kV, true, true>, 3);
+                go(coupled_unified_pipe_kernel<kU, kV, true, true>, LBG_K12_MINB);
             else
-                go(coupled_unified_pipe_kernel<kU, kV, true, false>, 3);
+                go(coupled_unified_pipe_kernel<kU, kV, true, false>, LBG_K12_MINB);
             return;  // every segment swept by the one kernel
         }
         if (!kF && pipe && a.pidx0)
-            go(coupled_unified_pipe_kernel<kU, kV, false, true>, 3);
+            go(coupled_unified_pipe_kernel<kU, kV, false, true>, LBG_K12_MINB);
         else if (kF || per_sm == 4)
             go(coupled_unified_kernel<kF, kU, kV, 4>, 4);
         else if (per_sm == 6)
@@ -1405,7 +1586,7 @@ static void launch_covered_list(lbg_block b, const SweepArgs& a, cudaStream_t st
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, b->device);
     const bool fused = b->force_mode == LBG_FORCE_FUSED;
     const bool wrapped = a.wrap[0] || a.wrap[1] || a.wrap[2];
-    const unsigned grid = (unsigned)(sms * 3);
+    const unsigned grid = (unsigned)(sms * LBG_K12_MINB);
     with_flags(fused, b->v_snap, wrapped, [&](auto U, auto V, auto W) {
         constexpr bool kU = decltype(U)::value, kV = decltype(V)::value, kW = decltype(W)::value;
         coupled_unified_pipe_kernel<kU, kV, true, kW, true><<<grid, 128, 0, st>>>(a);

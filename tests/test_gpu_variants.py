@@ -15,7 +15,7 @@ once per process, so each variant runs the tests in a subprocess):
   LBG_WALK_REGS=120 the force reduction's row walk / register cap; LBG_MAP_COL=0 the level-outer
   mapping kernel (LBG_MAP_MINB=5: at 48 registers), LBG_MAP_CTA_WARPS=4 the column mapping kernel
   in CTAs of 4 warps; LBDEM_GPU_FAST_SYNC=0 the drop-in's host particle messaging exactly as the
-  reference writes it."""
+  reference writes it; LBG_K12_TMA=1 the TMA-fed unified coupled sweep."""
 import os
 import subprocess
 import sys
@@ -39,7 +39,8 @@ DROPIN = "config1_known_answers or particle_bed or decomposition_invariance or c
                                  {"LBG_SWEEP_PAIR": "1"}, {"LBDEM_GPU_SWEEP": "split"}, {"LBDEM_GPU_PREMAP": "1"},
                                  {"LBDEM_GPU_HALO": "stage"}, {"LBG_WALK_ROWS": "1"}, {"LBG_WALK_REGS": "120"},
                                  {"LBG_MAP_COL": "0"}, {"LBG_MAP_COL": "0", "LBG_MAP_MINB": "5"},
-                                 {"LBG_MAP_CTA_WARPS": "4"}, {"LBDEM_GPU_FAST_SYNC": "0"}],
+                                 {"LBG_MAP_CTA_WARPS": "4"}, {"LBDEM_GPU_FAST_SYNC": "0"},
+                                 {"LBG_K12_TMA": "1"}, {"LBG_K12_TMA": "1", "LBG_K12": "2"}],
                          ids=lambda env: "-".join(f"{k}_{v}" for k, v in env.items()))
 def test_parity_suite_under_variant(env):
     e = dict(os.environ, **env)
