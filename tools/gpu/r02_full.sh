@@ -1,7 +1,7 @@
 # the driver's round-end checks at HEAD: full GPU suite, smoke, bench (N = 1) + launch list
 cd $GRAFT_REPO_ROOT
-timeout 5400 python -m pytest tests -m gpu -q -x > gpurun_out/r02_full_pytest.log 2>&1; echo rc=$? >> gpurun_out/r02_full_pytest.log
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02_full_smoke.log 2>&1; echo rc=$? >> gpurun_out/r02_full_smoke.log
-timeout 1200 python bench.py --steps 20 --warmup 5 > gpurun_out/r02_full_bench.log 2>&1; echo rc=$? >> gpurun_out/r02_full_bench.log
-timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/r02_full_ref.log 2>&1; echo rc=$? >> gpurun_out/r02_full_ref.log
-timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r02_full_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+timeout 5400 python -m pytest tests -m gpu -q -x > gpurun_out/r02_full2_pytest.log 2>&1; echo rc=$? >> gpurun_out/r02_full2_pytest.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02_full2_smoke.log 2>&1; echo rc=$? >> gpurun_out/r02_full2_smoke.log
+timeout 1200 python bench.py --steps 20 --warmup 5 > gpurun_out/r02_full2_bench.log 2>&1; echo rc=$? >> gpurun_out/r02_full2_bench.log
+timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/r02_full2_ref.log 2>&1; echo rc=$? >> gpurun_out/r02_full2_ref.log
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r02_full2_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
