@@ -41,7 +41,7 @@ SIM_HPP_EDITS = [
 SIM_CPP_EDITS = [
     # includes + host-copy refresh used by the observers
     ("#include <set>\n",
-     "#include <set>\n#include <cstdlib>\n#include <cstring>\n#include <limits>\n\n#include \"lbdem_gpu.hpp\"\n#include \"dropin_observe.hpp\"\n"),
+     "#include <set>\n#include <cstdlib>\n#include <cstring>\n#include <limits>\n\n#include \"lbdem_gpu.hpp\"\n#include \"dropin_observe.hpp\"\n#include \"dropin_sched.hpp\"\n"),
     ("namespace lbdem {\n\nusing partition::MsgKind;",
      "namespace lbdem {\n\n"
      "namespace {\n"
@@ -196,6 +196,13 @@ SIM_CPP_EDITS = [
      "        dmin = std::min(dmin, std::min(p.x[a] - lo, hi - p.x[a]));\n"
      "    }\n"
      "    return dmin > reach * (1.0 + 1e-9);\n"
+     "}\n"
+     "/// LBDEM_GPU_SPIN_PHASES=0: the reference's ThreadPoolScheduler as built by the scenario;\n"
+     "/// default: the same contract with spin-published phases (dropin_sched.hpp)\n"
+     "std::unique_ptr<partition::Scheduler> phase_scheduler(std::unique_ptr<partition::Scheduler> s) {\n"
+     "    const char* e = std::getenv(\"LBDEM_GPU_SPIN_PHASES\");\n"
+     "    if ((e && std::atoi(e) == 0) || !dynamic_cast<partition::ThreadPoolScheduler*>(s.get())) return s;\n"
+     "    return std::make_unique<gpu::SpinPhaseScheduler>(s->workers());\n"
      "}\n"
      "/// apply_particle_sync's list reuses the storage of the list it replaced (per worker thread)\n"
      "thread_local std::vector<dem::Particle> particle_scratch;\n"
@@ -504,6 +511,9 @@ SIM_CPP_EDITS = [
      "        if (fast_sync() && owner == blk.id && deep_inside(p, blk.box, ghost_margin())) continue;\n"
      "\n"
      "        partition::StateRecord rec;\n"),
+    # sim.cpp:39-44 - the phase scheduler (phase_scheduler(): spin-published phases)
+    ("      scheduler_(std::move(scheduler)) {\n",
+     "      scheduler_(phase_scheduler(std::move(scheduler))) {\n"),
 ]
 
 
