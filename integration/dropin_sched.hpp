@@ -35,7 +35,8 @@ namespace lbdem::gpu {
 class SpinPhaseScheduler final : public partition::Scheduler {
 public:
     /// spin_us: how long an idle thread polls before it blocks
-    explicit SpinPhaseScheduler(int workers, int spin_us = 2000) : spin_(std::chrono::microseconds(spin_us)) {
+    explicit SpinPhaseScheduler(int workers, int spin_us = 2000)
+        : nw_(workers), spin_(std::chrono::microseconds(spin_us)) {
         threads_.reserve(workers);
         for (int w = 0; w < workers; ++w) threads_.emplace_back([this, w] { worker_loop(w); });
     }
@@ -52,7 +53,7 @@ public:
     void run_phase(int n_blocks, const std::function<void(int)>& fn) override {
         fn_ = &fn;
         n_blocks_ = n_blocks;
-        remaining_.store(static_cast<int>(threads_.size()), std::memory_order_relaxed);
+        remaining_.store(nw_, std::memory_order_relaxed);
         {
             std::lock_guard<std::mutex> lock(m_);  // a worker between its check and its wait sees it
             epoch_.fetch_add(1, std::memory_order_release);
@@ -70,7 +71,7 @@ public:
         }
     }
 
-    int workers() const override { return static_cast<int>(threads_.size()); }
+    int workers() const override { return nw_; }
 
 private:
     template <class Pred>
@@ -85,7 +86,7 @@ private:
 
     void worker_loop(int w) {
         long seen = 0;
-        const int nw = static_cast<int>(threads_.size());
+        const int nw = nw_;  // (threads_ is still being filled while the first workers start)
         for (;;) {
             auto ready = [&] {
                 return stop_.load(std::memory_order_acquire) || epoch_.load(std::memory_order_acquire) > seen;
@@ -115,6 +116,7 @@ private:
         }
     }
 
+    const int nw_;
     std::vector<std::thread> threads_;
     std::mutex m_;
     std::condition_variable cv_main_, cv_work_;

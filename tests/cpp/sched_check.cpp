@@ -13,6 +13,16 @@
 #include "dropin_sched.hpp"
 
 int main() {
+    // fresh schedulers: the first phase may start while the later workers are still starting
+    for (int rep = 0; rep < 200; ++rep) {
+        lbdem::gpu::SpinPhaseScheduler s(8, 100);
+        for (int p = 0; p < 3; ++p) {
+            std::vector<std::atomic<int>> seen(8);
+            s.run_phase(8, [&](int b) { seen[b].fetch_add(1); });
+            for (int b = 0; b < 8; ++b)
+                if (seen[b].load() != 1) return 7;
+        }
+    }
     const int workers = 4, blocks = 11, phases = 2000;
     lbdem::gpu::SpinPhaseScheduler s(workers, 200);
     if (s.workers() != workers) return 1;
