@@ -202,7 +202,8 @@ SIM_CPP_EDITS = [
      "std::unique_ptr<partition::Scheduler> phase_scheduler(std::unique_ptr<partition::Scheduler> s) {\n"
      "    const char* e = std::getenv(\"LBDEM_GPU_SPIN_PHASES\");\n"
      "    if ((e && std::atoi(e) == 0) || !dynamic_cast<partition::ThreadPoolScheduler*>(s.get())) return s;\n"
-     "    return std::make_unique<gpu::SpinPhaseScheduler>(s->workers());\n"
+     "    const char* us = std::getenv(\"LBDEM_GPU_SPIN_US\");  // spin budget before blocking (A/B)\n"
+     "    return std::make_unique<gpu::SpinPhaseScheduler>(s->workers(), us ? std::atoi(us) : 2000);\n"
      "}\n"
      "/// apply_particle_sync's list reuses the storage of the list it replaced (per worker thread)\n"
      "thread_local std::vector<dem::Particle> particle_scratch;\n"
