@@ -21,6 +21,9 @@
 #include <thread>
 #include <vector>
 
+#include <pthread.h>
+#include <sched.h>
+
 #include "lbdem/partition.hpp"
 
 #if defined(__x86_64__) || defined(__i386__)
@@ -35,10 +38,19 @@ namespace lbdem::gpu {
 class SpinPhaseScheduler final : public partition::Scheduler {
 public:
     /// spin_us: how long an idle thread polls before it blocks
-    explicit SpinPhaseScheduler(int workers, int spin_us = 2000)
+    /// pin_stride > 0: worker w pinned to CPU (w * pin_stride) mod the CPU count (A/B)
+    explicit SpinPhaseScheduler(int workers, int spin_us = 2000, int pin_stride = 0)
         : nw_(workers), spin_(std::chrono::microseconds(spin_us)) {
         threads_.reserve(workers);
         for (int w = 0; w < workers; ++w) threads_.emplace_back([this, w] { worker_loop(w); });
+        const int ncpu = static_cast<int>(std::thread::hardware_concurrency());
+        if (pin_stride > 0 && ncpu > 0)
+            for (int w = 0; w < workers; ++w) {
+                cpu_set_t set;
+                CPU_ZERO(&set);
+                CPU_SET((w * pin_stride) % ncpu, &set);
+                pthread_setaffinity_np(threads_[w].native_handle(), sizeof(set), &set);
+            }
     }
 
     ~SpinPhaseScheduler() override {

@@ -203,7 +203,9 @@ SIM_CPP_EDITS = [
      "    const char* e = std::getenv(\"LBDEM_GPU_SPIN_PHASES\");\n"
      "    if ((e && std::atoi(e) == 0) || !dynamic_cast<partition::ThreadPoolScheduler*>(s.get())) return s;\n"
      "    const char* us = std::getenv(\"LBDEM_GPU_SPIN_US\");  // spin budget before blocking (A/B)\n"
-     "    return std::make_unique<gpu::SpinPhaseScheduler>(s->workers(), us ? std::atoi(us) : 2000);\n"
+     "    const char* pin = std::getenv(\"LBDEM_GPU_PIN_STRIDE\");  // worker w -> CPU w * stride (A/B)\n"
+     "    return std::make_unique<gpu::SpinPhaseScheduler>(s->workers(), us ? std::atoi(us) : 2000,\n"
+     "                                                     pin ? std::atoi(pin) : 0);\n"
      "}\n"
      "/// apply_particle_sync's list reuses the storage of the list it replaced (per worker thread)\n"
      "thread_local std::vector<dem::Particle> particle_scratch;\n"
