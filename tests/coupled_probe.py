@@ -20,12 +20,13 @@ if blocks:
     cfg = _j.dumps(c)
 for mode in sys.argv[1:] or ["scratch"]:
     os.environ["LBDEM_GPU_FORCE"] = mode
-    sim = dropin.DropinSim(cfg, (256, 256, 256))
-    for s in range(int(os.environ.get("PROBE_STEPS", "6"))):
-        sim.reset_timers()
-        t0 = time.perf_counter()
-        sim.run(1)
-        dt = time.perf_counter() - t0
-        print(json.dumps({"mode": mode, "step": s, "ms": round(dt * 1e3, 2),
-                          "cats": [round(v * 1e3, 2) for v in sim.timings()]}), flush=True)
-    sim.close()
+    for k in range(int(os.environ.get("PROBE_SIMS", "1"))):  # fresh simulations (new workers) in one process
+        sim = dropin.DropinSim(cfg, (256, 256, 256))
+        for s in range(int(os.environ.get("PROBE_STEPS", "6"))):
+            sim.reset_timers()
+            t0 = time.perf_counter()
+            sim.run(1)
+            dt = time.perf_counter() - t0
+            print(json.dumps({"mode": mode, "sim": k, "step": s, "ms": round(dt * 1e3, 2),
+                              "cats": [round(v * 1e3, 2) for v in sim.timings()]}), flush=True)
+        sim.close()
