@@ -480,6 +480,35 @@ def aa_roofline(n=512, tau=0.8, steps=10, warmup=4):
                          "frac": round(achieved / peak, 4)}}
 
 
+def e2e_record(args, n, pdf_bytes, e2e_mlups, loop_mlups, job_mlups, finite, numa_cpus):
+    """The e2e object: with one GPU the streamed job (lbg_run_host; its H2D carries the 19 x nz
+    interior z-planes incl. their x/y ghost rows, its D2H the same planes plus the 48-byte error
+    counters), the unpipelined job beside it; with N > 1 the unpipelined job per rank."""
+    unpiped = {"value": round(e2e_mlups, 1),
+               "h2d_bytes_per_step": round(pdf_bytes / args.steps),
+               "d2h_bytes_per_step": round(pdf_bytes / args.steps) + 24,
+               "how": (f"job of {args.steps} steps through the C-ABI with host buffers: lbg_upload_src "
+                       "from pinned host memory (reference layout), per step sweep [+ halo] + swap + "
+                       "lbg_sync (error-counter D2H, NumericError check), lbg_download_src; wall clock, "
+                       "max over ranks"),
+               "steady_state_loop_mlups": round(loop_mlups, 1)}
+    common = {"result_finite": finite, "host_buffer_numa_cpus": len(numa_cpus) if numa_cpus else None}
+    if job_mlups is None:
+        return {"value": unpiped["value"], "unit": "MLUPS", "h2d_bytes_per_step": unpiped["h2d_bytes_per_step"],
+                "d2h_bytes_per_step": unpiped["d2h_bytes_per_step"], "how": unpiped["how"],
+                "steady_state_loop_mlups": unpiped["steady_state_loop_mlups"], **common}
+    moved = 8 * 19 * n * (n + 2) * (n + 2)
+    return {"value": round(job_mlups, 1), "unit": "MLUPS",
+            "h2d_bytes_per_step": round(moved / args.steps),
+            "d2h_bytes_per_step": round((moved + 48) / args.steps),
+            "how": (f"job of {args.steps} steps through the C-ABI with host buffers: lbg_run_host on the "
+                    "pinned host PdfField (reference layout) — H2D of the state, the K fused sweeps and "
+                    "D2H of the final state pipelined over 16-plane z-slabs on separate streams (both PCIe "
+                    "directions at once), then the accumulated NumericError check (error-counter D2H); "
+                    "wall clock; interior result bitwise that of the unpipelined job (tests/test_gpu_job.py)"),
+            "unpipelined": unpiped, **common}
+
+
 def host_mem_available():
     """MemAvailable of this host in bytes (None if unknown)."""
     try:
@@ -670,7 +699,7 @@ def run_lbg(args):
     avail = host_mem_available()
     fits = avail is None or local_ranks * pdf_bytes <= 0.6 * avail
     fits = all(allgather(fits)) if N > 1 else fits
-    e2e_mlups = loop_mlups = None
+    e2e_mlups = loop_mlups = job_mlups = None
     finite = None
     numa_cpus = None
     saved_affinity = os.sched_getaffinity(0)
@@ -683,6 +712,20 @@ def run_lbg(args):
         lbdem.check(abi.load().lbg_host_alloc(pdf_bytes, C.byref(hp)))
         host = np.ctypeslib.as_array(C.cast(hp, C.POINTER(C.c_double)), shape=(19, n + 2, n + 2, n + 2))
         lbdem.check(abi.load().lbg_download_src(blk.h, hp))  # the current state as the job's input
+        if N == 1:
+            # one GPU, every axis periodic: the streamed job (lbg_run_host) — the same upload,
+            # K steps and download, pipelined over z-slabs so both PCIe directions and the
+            # sweeps overlap; afterwards the unpipelined job below runs for comparison
+            # its slab staging (6 x 0.64 GB) is allocated by one untimed 0-step job (a round
+            # trip), as the unpipelined job's staging is by the untimed download above
+            blk.run_host(p, host, 0)
+            barrier()
+            t0 = time.perf_counter()
+            blk.run_host(p, host, args.steps)
+            t1 = time.perf_counter()
+            job_s = t1 - t0
+            job_mlups = cells * args.steps / job_s / 1e6
+            # (the unpipelined job continues from the streamed job's result: same work)
         barrier()
         t0 = time.perf_counter()
         lbdem.check(abi.load().lbg_upload_src(blk.h, hp))
@@ -730,15 +773,7 @@ def run_lbg(args):
             "hbm_roofline_frac_of_step": round(BYTES_PER_LUP * cells / (ms_step / 1e3) / 1e9 / peak, 4),
             "timings_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in tm.items() if v[1]},
             "halo": (None if N == 1 else halo_record(halo, n, ms_step, tm, args.steps)),
-            "e2e": ({"value": round(e2e_mlups, 1), "unit": "MLUPS",
-                     "h2d_bytes_per_step": round(pdf_bytes / args.steps),
-                     "d2h_bytes_per_step": round(pdf_bytes / args.steps) + 24,
-                     "how": (f"job of {args.steps} steps through the C-ABI with host buffers: lbg_upload_src "
-                             "from pinned host memory (reference layout), per step sweep [+ halo] + swap + "
-                             "lbg_sync (error-counter D2H, NumericError check), lbg_download_src; wall clock, "
-                             "max over ranks"),
-                     "steady_state_loop_mlups": round(loop_mlups, 1), "result_finite": finite,
-                     "host_buffer_numa_cpus": len(numa_cpus) if numa_cpus else None}
+            "e2e": (e2e_record(args, n, pdf_bytes, e2e_mlups, loop_mlups, job_mlups, finite, numa_cpus)
                     if e2e_mlups is not None else
                     {"value": None, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                      "skipped": (f"{local_ranks} host PdfFields of {pdf_bytes / 1e9:.1f} GB exceed 60 % of the "

@@ -158,6 +158,21 @@ lbg_status lbg_init_shear_wave(lbg_block b, const int domain[3]);
 lbg_status lbg_fill_ghosts_src(lbg_block b, double v);
 /* PdfField::swap (field.hpp:64). */
 lbg_status lbg_swap(lbg_block b);
+/* Simulation::run(steps) (sim.cpp:702-704) of a plain-fluid block with every axis periodic and
+ * wrapped in-kernel (lbg_set_periodic_wrap {1,1,1}), for a caller whose PdfField lives on the
+ * host: `host` (reference layout incl. ghosts, as lbg_upload_src) is the state before the
+ * first step and receives, in place, the state after `steps` collide-stream steps. The
+ * upload, the sweeps and the download are pipelined over z-slabs of `slab_planes` planes (0:
+ * 16): slabs are uploaded in z order, step s of a plane range runs as soon as step s-1 of its
+ * neighbour planes is done (the ranges next to the z = 0 seam last), and a slab goes back to
+ * the host as soon as its last step is done, so H2D, D2H (separate streams, both PCIe
+ * directions) and the sweeps overlap. Interior cells are bitwise those of lbg_upload_src +
+ * steps x (lbg_sweep of the block + lbg_swap) + lbg_download_src; ghost cells keep their input
+ * values. Afterwards the block's src holds the final state. The end-of-sweep stability checks
+ * are accumulated and reported once, as lbg_sync does (LBG_NUMERIC_ERROR; `out` optional).
+ * `host` should be pinned (lbg_host_alloc) for the copies to overlap. */
+lbg_status lbg_run_host(lbg_block b, const lbg_fluid* fluid, double* host, int steps, int slab_planes,
+                        lbg_errors* out);
 
 /* ------------------------------------------------------------------ fluid operators */
 /* collide_stream_* / psm_collide_stream_* over a CellBox (lbm.cpp:21-59, psm.cpp:218-276).

@@ -491,6 +491,7 @@ lbg_status lbg_block_destroy(lbg_block b) {
         if (b->ev_copy[s]) cudaEventDestroy(b->ev_copy[s]);
         if (b->ev_done[s]) cudaEventDestroy(b->ev_done[s]);
     }
+    lbg::free_job(b);
     for (double* p : b->stage)
         if (p) cudaFree(p);
     if (b->recv_buf) cudaFree(b->recv_buf);

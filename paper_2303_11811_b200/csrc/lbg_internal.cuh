@@ -305,6 +305,15 @@ struct lbg_block_s {
     cudaEvent_t ev_copy[2] = {nullptr, nullptr};
     cudaEvent_t ev_done[2] = {nullptr, nullptr};
 
+    // streamed host job (lbg_run_host, lbg_job.cu): z-slab staging slots per direction (doubles
+    // per slot: job_cap), the pack and D2H streams, per-slot events (0 uploaded, 1 unpacked,
+    // 2 packed, 3 downloaded)
+    double* job_up[3] = {nullptr, nullptr, nullptr};
+    double* job_dn[3] = {nullptr, nullptr, nullptr};
+    size_t job_cap = 0;
+    cudaStream_t job_pack = nullptr, job_d2h = nullptr;
+    cudaEvent_t job_ev[4][3] = {};
+
     // AA in-place streaming (lbg_aa.cu): one buffer (buf[cur]); aa_phase 0: state S0 (the
     // double-buffer src), 1: S1 (streamed, slots swapped); aa_pending: swept, not yet swapped
     bool aa = false;
@@ -320,6 +329,11 @@ namespace lbg {
 // AA streaming (lbg_aa.cu): one step of the in-place sweep; the S0 image of an S1 buffer
 lbg_status aa_sweep(lbg_block b, const lbg_fluid* fl);
 lbg_status aa_unstream(lbg_block b, double* out);
+// K1 over z-planes [z0, z1) from src into dst on stream st (lbg_sweep.cu; the host job's sweeps)
+lbg_status sweep_planes(lbg_block b, const lbg_fluid* fl, const double* src, double* dst, int z0, int z1,
+                        cudaStream_t st);
+// releases the host job's staging, streams and events (lbg_job.cu)
+void free_job(lbg_block b);
 // frees the shadow mapping state of lbg_map_prepare (lbg_psm.cu)
 void free_shadow(lbg_block b);
 // covered-cell counts and segment lists rebuilt from `count` (lbg_psm.cu)

@@ -1602,6 +1602,30 @@ static bool k2_concurrent() {
     return v;
 }
 
+// K1 over the z-planes [z0, z1) (whole x/y extent) of a plain block from `src` into `dst` on
+// stream `st`: the streamed host job's sweeps (lbg_job.cu), which alternate two buffers per
+// step instead of lbg_swap
+lbg_status sweep_planes(lbg_block b, const lbg_fluid* fl, const double* src, double* dst, int z0, int z1,
+                        cudaStream_t st) {
+    if (z1 <= z0) return LBG_OK;
+    if (lbg_status s = ensure_wcount(b)) return s;
+    SweepArgs a = make_args(b, fl);
+    a.src = src;
+    a.dst = dst;
+    a.lo[0] = a.lo[1] = 0;
+    a.hi[0] = b->L.nx;
+    a.hi[1] = b->L.ny;
+    a.lo[2] = z0;
+    a.hi[2] = z1;
+    a.i0 = 0;
+    const lbg_box box = {{0, 0, z0}, {b->L.nx, b->L.ny, z1}};
+    if (lbg_status s = add_boxes(a, b->L, &box, 1)) return s;
+    const bool fo = fl->f_ext[0] != 0.0 || fl->f_ext[1] != 0.0 || fl->f_ext[2] != 0.0;
+    fo ? launch_box<true, false>(a, st) : launch_box<false, false>(a, st);
+    LBG_LAUNCH_CHECK();
+    return verify_writes(b, a);
+}
+
 }  // namespace lbg
 
 using namespace lbg;

@@ -311,6 +311,17 @@ class Block:
     def swap(self):
         check(_lib().lbg_swap(self.h))
 
+    def run_host(self, params: FluidParams, host, steps: int, slab_planes: int = 0) -> dict:
+        """Simulation::run(steps) (sim.cpp:702-704) of this fully periodic plain block on a
+        host PdfField `host` (pdf_shape, float64, C order; pinned memory for overlapped
+        copies), in place: upload, sweeps and download pipelined over z-slabs (lbg_run_host).
+        Interior cells receive the state after `steps` steps; ghost cells are left as they
+        were. Returns the accumulated error counters (NumericError raised like sync())."""
+        assert host.shape == self.pdf_shape and host.dtype == np.float64 and host.flags.c_contiguous
+        fl, e = params.c(), _abi.Errors()
+        check(_lib().lbg_run_host(self.h, C.byref(fl), _ptr(host), int(steps), int(slab_planes), C.byref(e)))
+        return {"unstable": e.unstable_cells, "overfull": e.overfull_cells, "unknown": e.unknown_ids}
+
     # operators (async)
     def sweep(self, params: FluidParams, box: CellBox):
         fl, bx = params.c(), box.c()

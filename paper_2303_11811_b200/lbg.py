@@ -83,6 +83,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "lbg_fill_ghosts_src": (st, [blk, C.c_double]),
         "lbg_init_shear_wave": (st, [blk, i3]),
         "lbg_swap": (st, [blk]),
+        "lbg_run_host": (st, [blk, C.POINTER(Fluid), vp, C.c_int, C.c_int, C.POINTER(Errors)]),
         "lbg_sweep": (st, [blk, C.POINTER(Fluid), C.POINTER(Box)]),
         "lbg_sweep_boxes": (st, [blk, C.POINTER(Fluid), C.POINTER(Box), C.c_int]),
         "lbg_stream": (st, [blk, C.POINTER(Box)]),
