@@ -504,8 +504,9 @@ def e2e_record(args, n, pdf_bytes, e2e_mlups, loop_mlups, job_mlups, finite, num
             "how": (f"job of {args.steps} steps through the C-ABI with host buffers: lbg_run_host on the "
                     "pinned host PdfField (reference layout) — H2D of the state, the K fused sweeps and "
                     "D2H of the final state pipelined over 16-plane z-slabs on separate streams (both PCIe "
-                    "directions at once), then the accumulated NumericError check (error-counter D2H); "
-                    "wall clock; interior result bitwise that of the unpipelined job (tests/test_gpu_job.py)"),
+                    "directions at once; with N GPUs one NCCL seam exchange per step), then the accumulated "
+                    "NumericError check (error-counter D2H); wall clock, max over ranks; interior result "
+                    "bitwise that of the unpipelined job (tests/test_gpu_job.py, test_gpu_multi.py)"),
             "unpipelined": unpiped, **common}
 
 
@@ -712,20 +713,25 @@ def run_lbg(args):
         lbdem.check(abi.load().lbg_host_alloc(pdf_bytes, C.byref(hp)))
         host = np.ctypeslib.as_array(C.cast(hp, C.POINTER(C.c_double)), shape=(19, n + 2, n + 2, n + 2))
         lbdem.check(abi.load().lbg_download_src(blk.h, hp))  # the current state as the job's input
-        if N == 1:
-            # one GPU, every axis periodic: the streamed job (lbg_run_host) — the same upload,
-            # K steps and download, pipelined over z-slabs so both PCIe directions and the
-            # sweeps overlap; afterwards the unpipelined job below runs for comparison
-            # its slab staging (6 x 0.64 GB) is allocated by one untimed 0-step job (a round
-            # trip), as the unpipelined job's staging is by the untimed download above
-            blk.run_host(p, host, 0)
+        if dec.axis == 2:
+            # the streamed job (lbg_run_host): the same upload, K steps and download, pipelined
+            # over z-slabs so both PCIe directions and the sweeps overlap (one GPU: z wrapped
+            # in-kernel; N GPUs: z-slabs, whose seam planes take one NCCL halo exchange per
+            # step — a P2P-mode block gets an NCCL comm for it); the unpipelined job below
+            # runs afterwards for comparison, continuing from its result (same work)
+            if N > 1 and st.p2p:
+                blk.comm_init(N, rank, uid[0], axis=2, periodic=(1, 1, 1))
+            # its slab staging (6 x 0.64 GB) is allocated, and with N GPUs the NCCL seam
+            # connections are set up, by one untimed 1-step job, as the unpipelined job's
+            # staging is by the untimed download above
+            blk.run_host(p, host, 1)
             barrier()
             t0 = time.perf_counter()
             blk.run_host(p, host, args.steps)
             t1 = time.perf_counter()
-            job_s = t1 - t0
-            job_mlups = cells * args.steps / job_s / 1e6
-            # (the unpipelined job continues from the streamed job's result: same work)
+            barrier()
+            job_s = max_over_ranks(t1 - t0)
+            job_mlups = cells * N * args.steps / job_s / 1e6
         barrier()
         t0 = time.perf_counter()
         lbdem.check(abi.load().lbg_upload_src(blk.h, hp))

@@ -158,13 +158,15 @@ lbg_status lbg_init_shear_wave(lbg_block b, const int domain[3]);
 lbg_status lbg_fill_ghosts_src(lbg_block b, double v);
 /* PdfField::swap (field.hpp:64). */
 lbg_status lbg_swap(lbg_block b);
-/* Simulation::run(steps) (sim.cpp:702-704) of a plain-fluid block with every axis periodic and
- * wrapped in-kernel (lbg_set_periodic_wrap {1,1,1}), for a caller whose PdfField lives on the
- * host: `host` (reference layout incl. ghosts, as lbg_upload_src) is the state before the
+/* Simulation::run(steps) (sim.cpp:702-704) of a periodic plain-fluid block — x and y wrapped
+ * in-kernel, z wrapped too (one block spans the domain) or the slab axis of the block's NCCL
+ * halo (lbg_comm_init, axis 2; one block per rank, every rank calls this with the same
+ * `steps`) — for a caller whose PdfField lives on the host: `host` (reference layout incl. ghosts, as lbg_upload_src) is the state before the
  * first step and receives, in place, the state after `steps` collide-stream steps. The
  * upload, the sweeps and the download are pipelined over z-slabs of `slab_planes` planes (0:
  * 16): slabs are uploaded in z order, step s of a plane range runs as soon as step s-1 of its
- * neighbour planes is done (the ranges next to the z = 0 seam last), and a slab goes back to
+ * neighbour planes is done (the ranges next to the z = 0 seam last; with the NCCL halo the seam
+ * planes take one halo exchange per step), and a slab goes back to
  * the host as soon as its last step is done, so H2D, D2H (separate streams, both PCIe
  * directions) and the sweeps overlap. Interior cells are bitwise those of lbg_upload_src +
  * steps x (lbg_sweep of the block + lbg_swap) + lbg_download_src; ghost cells keep their input

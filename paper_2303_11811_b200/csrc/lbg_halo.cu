@@ -254,6 +254,15 @@ lbg_status lbg_comm_init(lbg_block b, int nranks, int rank, const char id[128], 
     return LBG_OK;
 }
 
+}  // extern "C"
+
+namespace lbg {
+// the slab axis of the block's NCCL halo, -1 without lbg_comm_init (the host job's seam exchange)
+int comm_axis(lbg_block b) { return (b && b->comm) ? b->comm->axis : -1; }
+}  // namespace lbg
+
+extern "C" {
+
 lbg_status lbg_comm_destroy(lbg_block b) {
     if (!b || !b->comm) return LBG_OK;
     Comm* c = b->comm;

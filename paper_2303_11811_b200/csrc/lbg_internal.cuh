@@ -332,6 +332,8 @@ lbg_status aa_unstream(lbg_block b, double* out);
 // K1 over z-planes [z0, z1) from src into dst on stream st (lbg_sweep.cu; the host job's sweeps)
 lbg_status sweep_planes(lbg_block b, const lbg_fluid* fl, const double* src, double* dst, int z0, int z1,
                         cudaStream_t st);
+// the slab axis of the block's NCCL halo (lbg_comm_init), -1 if none (lbg_halo.cu)
+int comm_axis(lbg_block b);
 // releases the host job's staging, streams and events (lbg_job.cu)
 void free_job(lbg_block b);
 // frees the shadow mapping state of lbg_map_prepare (lbg_psm.cu)

@@ -1,8 +1,10 @@
 // SPDX-License-Identifier: Apache-2.0
 //
-// lbg_run_host — Simulation::run(steps) (sim.cpp:702-704) of a fully periodic plain-fluid block
-// whose PdfField lives in (pinned) host memory: upload, `steps` fused sweeps, download, with the
-// three pipelined over z-slabs so both PCIe directions and the sweeps overlap.
+// lbg_run_host — Simulation::run(steps) (sim.cpp:702-704) of a periodic plain-fluid block whose
+// PdfField lives in (pinned) host memory: upload, `steps` fused sweeps, download, with the three
+// pipelined over z-slabs so both PCIe directions and the sweeps overlap. z is either wrapped
+// in-kernel (one block spans the domain) or the slab axis of the NCCL halo (config 4: one block
+// per GPU; the seam planes then take one halo exchange per step, see below).
 //
 // Schedule (one block, every axis wrapped in-kernel, double buffer A = buf[cur] / B):
 //   * slab c (planes [cH, cH + H)) is copied H2D into a staging slot on `side` (19 linear copies,
@@ -13,7 +15,10 @@
 //     (src = step s-1's buffer, dst = step s's). A step s write to a plane p replaces step s-2's
 //     value there, which step s-1 no longer needs: it has already swept up to F[s-1] = F[s] + 1;
 //   * once the last slab is in, every step s (in order) sweeps the rest of the domain: [F[s], nz)
-//     and the seam planes [0, s);
+//     and the seam planes [0, s). With the NCCL halo on z, step s-1's planes 0 and nz-1 go to the
+//     neighbours' z ghosts first (lbg_halo_begin/complete on step s-1's buffer; every rank makes
+//     the same `steps` exchanges), which is the only time the planes next to the seam are pulled
+//     from: the main phase never sweeps plane 0 or nz-1;
 //   * the final step's planes go back to the host as soon as they are done: a pack kernel on its
 //     own stream re-pitches them (interior cells from the final buffer, x/y ghost cells from A,
 //     which holds the uploaded values — sweeps write interior cells only) into a staging slot,
@@ -114,8 +119,12 @@ extern "C" lbg_status lbg_run_host(lbg_block b, const lbg_fluid* fl, double* hos
     if (steps < 0) return set_error(LBG_INVALID, "negative step count");
     if (b->coupling) return set_error(LBG_INVALID, "lbg_run_host: plain-fluid blocks only");
     if (b->aa) return set_error(LBG_INVALID, "lbg_run_host: not available on an AA-streaming block");
-    if (!(b->wrap[0] && b->wrap[1] && b->wrap[2]))
-        return set_error(LBG_INVALID, "lbg_run_host: every axis must be periodic and wrapped in-kernel");
+    // z: wrapped in-kernel (the whole periodic domain), or the slab axis of an NCCL halo
+    // (lbg_comm_init; its exchanges run at the seam, once per step, in the tail)
+    const bool zcomm = !b->wrap[2] && comm_axis(b) == 2;
+    if (!(b->wrap[0] && b->wrap[1] && (b->wrap[2] || zcomm)))
+        return set_error(LBG_INVALID, "lbg_run_host: x and y must be periodic and wrapped in-kernel, z wrapped or "
+                                      "the slab axis of the block's NCCL halo");
     const Layout& L = b->L;
     const int nz = L.nz;
     const int H = std::max(1, std::min({slab_planes > 0 ? slab_planes : 16, nz, 2048}));  // grid.z = 19 H
@@ -207,6 +216,14 @@ extern "C" lbg_status lbg_run_host(lbg_block b, const lbg_fluid* fl, double* hos
         } else {
             // the last slab: every step completes the domain, the seam planes included
             for (int s = 1; s <= steps && st == LBG_OK; ++s) {
+                if (zcomm) {  // step s-1's planes 0 and nz-1 into the neighbours' z ghosts
+                    const int cur0 = b->cur;
+                    b->cur = (src_of(s) == b->buf[0]) ? 0 : 1;
+                    st = lbg_halo_begin(b);
+                    if (st == LBG_OK) st = lbg_halo_complete(b);
+                    b->cur = cur0;
+                    if (st != LBG_OK) break;
+                }
                 st = sweep_planes(b, fl, src_of(s), dst_of(s), std::min(F[s], nz), nz, cs);
                 if (st == LBG_OK) st = sweep_planes(b, fl, src_of(s), dst_of(s), 0, std::min(s, nz), cs);
                 F[s] = nz;

@@ -49,15 +49,25 @@ def main():
         sl[3 - a] = slice(1 + lo[a], 1 + lo[a] + dims[a])
     mine = np.zeros((19, dims[2] + 2, dims[1] + 2, dims[0] + 2))
     mine[:, 1:-1, 1:-1, 1:-1] = glob[tuple(sl)]
-    st.block.upload_src(mine)
-    dist.barrier()
-    st.prime()
-    torch.cuda.synchronize()
-    dist.barrier()
-    for _ in range(steps):
-        st.step()
-    st.block.sync()
-    res = torch.from_numpy(np.ascontiguousarray(st.block.download_src()[:, 1:-1, 1:-1, 1:-1])).cuda()
+    if os.environ.get("SLAB_JOB") == "1":
+        # the streamed host job (lbg_run_host) on each rank's host slab; its seam planes take
+        # the NCCL halo (a P2P-mode stepper gets an NCCL comm for it)
+        if st.p2p:
+            st.block.comm_init(world, rank, uid[0], axis=2, periodic=(1, 1, 1))
+        host = mine.copy()
+        dist.barrier()
+        st.block.run_host(params, host, steps, int(os.environ.get("SLAB_JOB_PLANES", "3")))
+        res = torch.from_numpy(np.ascontiguousarray(host[:, 1:-1, 1:-1, 1:-1])).cuda()
+    else:
+        st.block.upload_src(mine)
+        dist.barrier()
+        st.prime()
+        torch.cuda.synchronize()
+        dist.barrier()
+        for _ in range(steps):
+            st.step()
+        st.block.sync()
+        res = torch.from_numpy(np.ascontiguousarray(st.block.download_src()[:, 1:-1, 1:-1, 1:-1])).cuda()
     parts = [torch.zeros_like(res) for _ in range(world)]
     dist.all_gather(parts, res)
     ok = True

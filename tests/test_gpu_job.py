@@ -76,6 +76,23 @@ def test_run_host_matches_stepwise(gpu, dims, steps, slab, fext):
         free_pinned(p)
 
 
+@pytest.mark.parametrize("steps,slab", [(5, 4), (9, 2), (3, 40)])
+def test_run_host_z_seam_through_the_halo(gpu, steps, slab):
+    """z not wrapped in-kernel but the slab axis of an NCCL halo (one rank: the periodic
+    self-exchange): the seam planes take one halo exchange per step; bitwise the wrapped job"""
+    dims = (12, 10, 40)
+    src0 = random_pdf(dims, seed=8)
+    params = gpu.FluidParams(0.75, (0.0, 2e-6, 0.0))
+    want = stepwise(gpu, dims, src0, params, steps)
+    blk = gpu.Block(dims)
+    blk.set_periodic_wrap((1, 1, 0))
+    blk.comm_init(1, 0, b"\0" * 128, axis=2, periodic=ALL_P)
+    host = src0.copy()
+    blk.run_host(params, host, steps, slab)
+    assert n_bit_mismatch(interior(host), interior(want)) == 0
+    blk.close()
+
+
 def test_run_host_matches_oracle(gpu, oracle):
     dims, steps, tau, fext = (12, 10, 21), 4, 0.7, (1e-5, -1e-5, 0.0)
     src0 = random_pdf(dims, seed=5)

@@ -29,6 +29,23 @@ def test_slab_halo_bitwise(axis, halo):
     assert r.returncode == 0
 
 
+@pytest.mark.parametrize("halo", ["nccl", "p2p"])
+def test_streamed_job_z_slabs_bitwise(halo):
+    """lbg_run_host on every rank's z-slab (upload, sweeps, download pipelined over 3-plane
+    slabs; the seam planes take one NCCL halo exchange per step) against the single-domain
+    oracle: bitwise."""
+    n = _ngpus()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    env = dict(os.environ, SLAB_AXIS="2", SLAB_STEPS="5", SLAB_HALO=halo, SLAB_JOB="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        f"--nproc-per-node={min(n, 4)}", "--master-addr=127.0.0.1",
+                        "--master-port=29537", os.path.join(HERE, "mp_halo_gpu.py")],
+                       env=env, capture_output=True, text=True, timeout=600)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0
+
+
 @pytest.mark.parametrize("halo", ["p2p", "nccl"])
 def test_config4_full_size_two_gpus_vs_one_block(halo):
     """Config 4 at 512^3 per GPU on 2 GPUs against the same 512 x 512 x 1024 domain as one
