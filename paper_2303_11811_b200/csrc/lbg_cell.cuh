@@ -18,6 +18,18 @@
 
 namespace lbg {
 
+// PDF stores of the fused operators. A/B builds (-DLBG_STORE_CS) use the streaming store
+// (st.global.cs: evict-first), so the stored populations do not displace the coupling fields
+// and snapshots from L1/L2.
+__device__ __forceinline__ void pdf_store(double* p, double v) {
+#ifdef LBG_STORE_CS
+    __stcs(p, v);
+#else
+    *p = v;
+#endif
+}
+
+
 // equilibrium numerator pair for +cu / -cu: feq = w (rho + ((+-A + B) - T))  (lbm.hpp:38-45)
 __device__ __forceinline__ void feq_pair(double w, double cu, double rho, double T, double& fp,
                                          double& fm) {
@@ -151,7 +163,7 @@ __device__ __forceinline__ void psm_one_pairs_g(Get f, double rho, double ux, do
         if (cx(q) != 0) mx -= c_solid * (double)cx(q);  // c_q = 0 terms are exact no-ops
         if (cy(q) != 0) my -= c_solid * (double)cy(q);
         if (cz(q) != 0) mz -= c_solid * (double)cz(q);
-        dst[q * plane + base] = base_out + be * c_solid;
+        pdf_store(dst + q * plane + base, base_out + be * c_solid);
     };
     {
         const double f0 = f(0);
@@ -193,15 +205,15 @@ __device__ __forceinline__ void srt_pairs_g(Get f, double rho, double ux, double
     const double T = (0.5 * usq) * 3.0;
     {
         const double f0 = f(0);
-        dst[base] = f0 + inv_tau * (wq(0) * (rho - T) - f0);
+        pdf_store(dst + base, f0 + inv_tau * (wq(0) * (rho - T) - f0));
     }
 #define LBG_SPAIR(qa, qb, cuf)                                  \
     {                                                           \
         const double xa = f(qa), xb = f(qb);                    \
         double fa, fb;                                          \
         feq_pair(wq(qa), (cuf), rho, T, fa, fb);                \
-        dst[qa * plane + base] = xa + inv_tau * (fa - xa);      \
-        dst[qb * plane + base] = xb + inv_tau * (fb - xb);      \
+        pdf_store(dst + qa * plane + base, xa + inv_tau * (fa - xa)); \
+        pdf_store(dst + qb * plane + base, xb + inv_tau * (fb - xb)); \
     }
     LBG_SPAIR(1, 2, ux)
     LBG_SPAIR(3, 4, uy)
@@ -247,7 +259,7 @@ __device__ __forceinline__ bool psm_cell_two(const double (&f)[kQ], double inv_t
         if (cy(q) != 0) m1y -= c1 * (double)cy(q);
         if (cz(q) != 0) m1z -= c1 * (double)cz(q);
         const double r0 = base_out + be0 * c0;
-        dst[q * plane + base] = two ? r0 + be1 * c1 : r0;
+        pdf_store(dst + q * plane + base, two ? r0 + be1 * c1 : r0);
     };
     {
         const double feq0 = wq(0) * (rho - T);

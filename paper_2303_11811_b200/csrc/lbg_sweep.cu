@@ -110,6 +110,20 @@ __device__ __forceinline__ void pull(const SweepArgs& a, int i, int j, int k, lo
     }
 }
 
+// PDF loads of the unwrapped pull. A/B builds: -DLBG_LOAD_HINT=1 the streaming load
+// (ld.global.cs), =2 no L1 allocation (ld.global.nc.L1::no_allocate)
+__device__ __forceinline__ double pdf_load(const double* p) {
+#if defined(LBG_LOAD_HINT) && LBG_LOAD_HINT == 1
+    return __ldcs(p);
+#elif defined(LBG_LOAD_HINT) && LBG_LOAD_HINT == 2
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+#else
+    return *p;
+#endif
+}
+
 // pull() for a block with no in-kernel wrap: no per-population wrap selects
 template <bool kWrap>
 __device__ __forceinline__ void pull_t(const SweepArgs& a, int i, int j, int k, long long base, double (&f)[kQ]) {
@@ -118,7 +132,7 @@ __device__ __forceinline__ void pull_t(const SweepArgs& a, int i, int j, int k, 
     } else {
         const Layout& L = a.L;
 #pragma unroll
-        for (int q = 0; q < kQ; ++q) f[q] = a.src[q * L.plane + LBG_IDX(base - L.shift(q), L.plane, a.err)];
+        for (int q = 0; q < kQ; ++q) f[q] = pdf_load(a.src + q * L.plane + LBG_IDX(base - L.shift(q), L.plane, a.err));
     }
 }
 
