@@ -542,6 +542,7 @@ def gpu_local_cpus(device):
         return None
 
 
+SPEC_HBM_GBS = 8000.0  # B200 HBM3e datasheet figure (report against it too)
 NVLINK_GBS = 900.0  # NVLink 5 per direction per GPU (B200_PROFILING.md)
 
 
@@ -774,6 +775,7 @@ def run_lbg(args):
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "kernel": "sweep_box_kernel<false,false> (K1 fused pull stream-collide)",
                          "bytes_per_lup": BYTES_PER_LUP, "peak_source": peak_src,
+                         "frac_of_spec_8000": round(achieved / SPEC_HBM_GBS, 4),
                          "sweep_ms_per_step": round(sweep_ms_per_step, 4),
                          "sweep_launches": sweep_n},
             "hbm_roofline_frac_of_step": round(BYTES_PER_LUP * cells / (ms_step / 1e3) / 1e9 / peak, 4),

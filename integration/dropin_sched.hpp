@@ -39,8 +39,12 @@ class SpinPhaseScheduler final : public partition::Scheduler {
 public:
     /// spin_us: how long an idle thread polls before it blocks
     /// pin_stride > 0: worker w pinned to CPU (w * pin_stride) mod the CPU count (A/B)
+    /// Spinning needs a CPU per spinning thread: with more threads (workers + the main thread)
+    /// than CPUs this process may run on, a polling thread would hold the CPU a worker with
+    /// work is waiting for (config 3 with 16 workers on 16 CPUs: ~100 ms per step instead of
+    /// ~10), so the scheduler then blocks right away, like the reference's.
     explicit SpinPhaseScheduler(int workers, int spin_us = 2000, int pin_stride = 0)
-        : nw_(workers), spin_(std::chrono::microseconds(spin_us)) {
+        : nw_(workers), spin_(std::chrono::microseconds(workers + 1 <= usable_cpus() ? spin_us : 0)) {
         threads_.reserve(workers);
         for (int w = 0; w < workers; ++w) threads_.emplace_back([this, w] { worker_loop(w); });
         const int ncpu = static_cast<int>(std::thread::hardware_concurrency());
@@ -84,6 +88,17 @@ public:
     }
 
     int workers() const override { return nw_; }
+
+    /// CPUs of this process's affinity mask (hardware_concurrency if unknown)
+    static int usable_cpus() {
+        cpu_set_t set;
+        CPU_ZERO(&set);
+        if (sched_getaffinity(0, sizeof(set), &set) == 0) return CPU_COUNT(&set);
+        const int n = static_cast<int>(std::thread::hardware_concurrency());
+        return n > 0 ? n : 1;
+    }
+
+    bool spinning() const { return spin_.count() > 0; }
 
 private:
     template <class Pred>

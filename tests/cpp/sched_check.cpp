@@ -1,6 +1,7 @@
 // SpinPhaseScheduler (integration/dropin_sched.hpp) against the ThreadPoolScheduler contract
 // (partition.hpp:170-192): every block once per phase, block b always on worker b % workers,
-// the phase's exception rethrown by run_phase, idle threads falling back to blocking.
+// the phase's exception rethrown by run_phase, idle threads falling back to blocking, no
+// spinning when the threads outnumber the CPUs.
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -62,6 +63,18 @@ int main() {
         ++after;
     });
     if (after != blocks) return 6;
+    // more threads than CPUs: no spinning (a polling thread would hold a working one's CPU),
+    // and the contract still holds on the blocking path
+    {
+        const int ncpu = lbdem::gpu::SpinPhaseScheduler::usable_cpus();
+        lbdem::gpu::SpinPhaseScheduler over(ncpu, 2000);
+        if (over.spinning()) return 8;
+        std::vector<std::atomic<int>> seen(2 * ncpu);
+        for (int p = 0; p < 50; ++p) over.run_phase(2 * ncpu, [&](int b) { seen[b].fetch_add(1); });
+        for (auto& v : seen)
+            if (v.load() != 50) return 9;
+        if (ncpu >= 2 && !lbdem::gpu::SpinPhaseScheduler(ncpu - 1, 2000).spinning()) return 10;
+    }
     std::printf("ok\n");
     return 0;
 }
