@@ -480,7 +480,43 @@ def aa_roofline(n=512, tau=0.8, steps=10, warmup=4):
                          "frac": round(achieved / peak, 4)}}
 
 
-def e2e_record(args, n, pdf_bytes, e2e_mlups, loop_mlups, job_mlups, finite, numa_cpus):
+def pcie_rates(host, device, nbytes=2 << 30):
+    """PCIe copy rates (GB/s) on `nbytes` of the pinned host buffer `host` (numpy, float64):
+    H2D alone, D2H alone, and both directions at once (separate streams) — the floor the
+    streamed job's e2e is measured against."""
+    import torch
+    flat = host.reshape(-1)
+    cnt = min(nbytes // 8, flat.size // 2)
+    hb = torch.from_numpy(flat[: 2 * cnt])
+    d1 = torch.empty(cnt, dtype=torch.float64, device=f"cuda:{device}")
+    d2 = torch.empty(cnt, dtype=torch.float64, device=f"cuda:{device}")
+    s1, s2 = torch.cuda.Stream(device), torch.cuda.Stream(device)
+    keep = hb[cnt:].clone()  # the D2H legs overwrite the buffer's second half: restore it
+
+    def timed(fn):
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
+        fn()
+        torch.cuda.synchronize(device)
+        return time.perf_counter() - t0
+
+    d1.copy_(hb[:cnt], non_blocking=True)  # warm
+    h2d = timed(lambda: d1.copy_(hb[:cnt], non_blocking=True))
+    d2h = timed(lambda: hb[cnt:].copy_(d2, non_blocking=True))
+
+    def both():
+        with torch.cuda.stream(s1):
+            d1.copy_(hb[:cnt], non_blocking=True)
+        with torch.cuda.stream(s2):
+            hb[cnt:].copy_(d2, non_blocking=True)
+    bt = timed(both)
+    hb[cnt:].copy_(keep)
+    gb = cnt * 8 / 1e9
+    return {"h2d_gbs": round(gb / h2d, 1), "d2h_gbs": round(gb / d2h, 1), "both_gbs_each": round(gb / bt, 1),
+            "sample_gb": round(gb, 2)}
+
+
+def e2e_record(args, n, pdf_bytes, e2e_mlups, loop_mlups, job_mlups, finite, numa_cpus, pcie=None, job_s=None):
     """The e2e object: with one GPU the streamed job (lbg_run_host; its H2D carries the 19 x nz
     interior z-planes incl. their x/y ghost rows, its D2H the same planes plus the 48-byte error
     counters), the unpipelined job beside it; with N > 1 the unpipelined job per rank."""
@@ -507,7 +543,13 @@ def e2e_record(args, n, pdf_bytes, e2e_mlups, loop_mlups, job_mlups, finite, num
                     "directions at once; with N GPUs one NCCL seam exchange per step), then the accumulated "
                     "NumericError check (error-counter D2H); wall clock, max over ranks; interior result "
                     "bitwise that of the unpipelined job (tests/test_gpu_job.py, test_gpu_multi.py)"),
-            "unpipelined": unpiped, **common}
+            "unpipelined": unpiped,
+            # the PCIe floor: H2D and D2H of the field overlap, so the job cannot beat the
+            # field's bytes at the both-directions rate (per rank)
+            "pcie": (None if pcie is None or job_s is None else
+                     {**pcie, "job_gbs_each": round(moved / job_s / 1e9, 1),
+                      "frac_of_both": round(moved / job_s / 1e9 / pcie["both_gbs_each"], 3)}),
+            **common}
 
 
 def host_mem_available():
@@ -701,7 +743,7 @@ def run_lbg(args):
     avail = host_mem_available()
     fits = avail is None or local_ranks * pdf_bytes <= 0.6 * avail
     fits = all(allgather(fits)) if N > 1 else fits
-    e2e_mlups = loop_mlups = job_mlups = None
+    e2e_mlups = loop_mlups = job_mlups = job_s = pcie = None
     finite = None
     numa_cpus = None
     saved_affinity = os.sched_getaffinity(0)
@@ -733,6 +775,10 @@ def run_lbg(args):
             barrier()
             job_s = max_over_ranks(t1 - t0)
             job_mlups = cells * N * args.steps / job_s / 1e6
+            try:
+                pcie = pcie_rates(host, local)
+            except Exception:  # noqa: BLE001 — a report, not the measurement
+                pcie = None
         barrier()
         t0 = time.perf_counter()
         lbdem.check(abi.load().lbg_upload_src(blk.h, hp))
@@ -781,7 +827,7 @@ def run_lbg(args):
             "hbm_roofline_frac_of_step": round(BYTES_PER_LUP * cells / (ms_step / 1e3) / 1e9 / peak, 4),
             "timings_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in tm.items() if v[1]},
             "halo": (None if N == 1 else halo_record(halo, n, ms_step, tm, args.steps)),
-            "e2e": (e2e_record(args, n, pdf_bytes, e2e_mlups, loop_mlups, job_mlups, finite, numa_cpus)
+            "e2e": (e2e_record(args, n, pdf_bytes, e2e_mlups, loop_mlups, job_mlups, finite, numa_cpus, pcie, job_s)
                     if e2e_mlups is not None else
                     {"value": None, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                      "skipped": (f"{local_ranks} host PdfFields of {pdf_bytes / 1e9:.1f} GB exceed 60 % of the "
