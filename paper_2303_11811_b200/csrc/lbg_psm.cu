@@ -25,6 +25,8 @@
 // (lbg_sweep.cu) sums inside the PSM kernel with warp aggregation + atomics instead.
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -1372,6 +1374,14 @@ lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int c
         return reduce_fused(b, out, capacity, n_out);
     }
     LBG_CUDA(cudaSetDevice(b->device));
+    // LBG_REDUCE_PROFILE=1: host-side phase times of this call on stderr (A/B diagnostics)
+    static const bool prof = [] {
+        const char* e = std::getenv("LBG_REDUCE_PROFILE");
+        return e && e[0] == '1';
+    }();
+    using clk = std::chrono::steady_clock;
+    const auto t_0 = clk::now();
+    auto t_reach = t_0, t_launch = t_0, t_sync = t_0;
     const int n = b->n_snaps;
     if (lbg_status s = reserve_rows(b, n)) return s;
     const BinGeom g = geom(b);
@@ -1388,6 +1398,7 @@ lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int c
         reach_ok = std::memcmp(ms.x, cs.x, sizeof(ms.x)) == 0 && std::memcmp(&ms.r, &cs.r, sizeof(double)) == 0 &&
                    std::memcmp(&ms.f_r, &cs.f_r, sizeof(double)) == 0;
     }
+    t_reach = clk::now();
     {
         Span span(b, LBG_CAT_REDF);
         if (!b->ev_red) LBG_CUDA(cudaEventCreateWithFlags(&b->ev_red, cudaEventDisableTiming));
@@ -1457,12 +1468,14 @@ lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int c
             LBG_CUDA(cudaMemcpyAsync(b->red_used_h, b->red_used, sizeof(int) * n, cudaMemcpyDeviceToHost, b->side));
         }
     }
+    t_launch = clk::now();
     // lbg_sync waits for the side stream's copies and reads the error counters
     if (lbg_status s = lbg_sync(b, nullptr)) {
         if (s == LBG_SYNC_ERROR)
             return set_error(LBG_SYNC_ERROR, "hydrodynamic force for unknown particle id");
         return s;
     }
+    t_sync = clk::now();
     int m = 0;
     for (int p = 0; p < n; ++p) {
         if (!b->red_used_h[p]) continue;
@@ -1478,6 +1491,13 @@ lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int c
         }
     }
     if (n_out) *n_out = m;
+    if (prof) {
+        auto us = [](clk::time_point a, clk::time_point c) {
+            return std::chrono::duration<double, std::micro>(c - a).count();
+        };
+        std::fprintf(stderr, "lbg_reduce_hydro n=%d reach_check %.1f us, launch %.1f us, sync %.1f us, unpack %.1f us\n",
+                     n, us(t_0, t_reach), us(t_reach, t_launch), us(t_launch, t_sync), us(t_sync, clk::now()));
+    }
     return LBG_OK;
 }
 
