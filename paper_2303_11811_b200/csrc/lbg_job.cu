@@ -185,53 +185,59 @@ extern "C" lbg_status lbg_run_host(lbg_block b, const lbg_fluid* fl, double* hos
         return LBG_OK;
     };
 
-    const int nchunks = (nz + H - 1) / H;
-    lbg_status st = LBG_OK;
-    for (int c = 0; c < nchunks && st == LBG_OK; ++c) {
-        const int z0 = c * H, z1 = std::min(nz, z0 + H), nzc = z1 - z0;
-        const int slot = c % kJobSlots;
-        if (c >= kJobSlots) LBG_CUDA(cudaStreamWaitEvent(up, b->job_ev[1][slot], 0));  // slot unpacked
-        for (int q = 0; q < kQ; ++q)
-            LBG_CUDA(cudaMemcpyAsync(b->job_up[slot] + (size_t)q * nzc * run, host + ((size_t)q * L.pz + z0 + 1) * run,
-                                     sizeof(double) * nzc * run, cudaMemcpyHostToDevice, up));
-        LBG_CUDA(cudaEventRecord(b->job_ev[0][slot], up));
-        LBG_CUDA(cudaStreamWaitEvent(cs, b->job_ev[0][slot], 0));
-        slab_unpack_kernel<<<dim3(gx, (unsigned)L.py, (unsigned)(kQ * nzc)), 128, 0, cs>>>(A, b->job_up[slot], L, z0,
-                                                                                         nzc);
-        LBG_LAUNCH_CHECK();
-        LBG_CUDA(cudaEventRecord(b->job_ev[1][slot], cs));
-        F[0] = z1;
-        if (z1 < nz) {
-            for (int s = 1; s <= steps && st == LBG_OK; ++s) {
-                const int nf = z1 - s;
-                if (nf > F[s]) {
-                    st = sweep_planes(b, fl, src_of(s), dst_of(s), F[s], nf, cs);
-                    F[s] = nf;
+    // the whole schedule is enqueued by `schedule`; whatever it returns, every stream of the
+    // job is drained below before the host buffer is handed back (no copy may still target it)
+    auto schedule = [&]() -> lbg_status {
+        const int nchunks = (nz + H - 1) / H;
+        lbg_status st = LBG_OK;
+        for (int c = 0; c < nchunks && st == LBG_OK; ++c) {
+            const int z0 = c * H, z1 = std::min(nz, z0 + H), nzc = z1 - z0;
+            const int slot = c % kJobSlots;
+            if (c >= kJobSlots) LBG_CUDA(cudaStreamWaitEvent(up, b->job_ev[1][slot], 0));  // slot unpacked
+            for (int q = 0; q < kQ; ++q)
+                LBG_CUDA(cudaMemcpyAsync(b->job_up[slot] + (size_t)q * nzc * run, host + ((size_t)q * L.pz + z0 + 1) * run,
+                                         sizeof(double) * nzc * run, cudaMemcpyHostToDevice, up));
+            LBG_CUDA(cudaEventRecord(b->job_ev[0][slot], up));
+            LBG_CUDA(cudaStreamWaitEvent(cs, b->job_ev[0][slot], 0));
+            slab_unpack_kernel<<<dim3(gx, (unsigned)L.py, (unsigned)(kQ * nzc)), 128, 0, cs>>>(A, b->job_up[slot], L, z0,
+                                                                                             nzc);
+            LBG_LAUNCH_CHECK();
+            LBG_CUDA(cudaEventRecord(b->job_ev[1][slot], cs));
+            F[0] = z1;
+            if (z1 < nz) {
+                for (int s = 1; s <= steps && st == LBG_OK; ++s) {
+                    const int nf = z1 - s;
+                    if (nf > F[s]) {
+                        st = sweep_planes(b, fl, src_of(s), dst_of(s), F[s], nf, cs);
+                        F[s] = nf;
+                    }
                 }
-            }
-            if (st == LBG_OK && F[steps] > dl_next) {
-                st = download(dl_next, F[steps]);
-                dl_next = F[steps];
-            }
-        } else {
-            // the last slab: every step completes the domain, the seam planes included
-            for (int s = 1; s <= steps && st == LBG_OK; ++s) {
-                if (zcomm) {  // step s-1's planes 0 and nz-1 into the neighbours' z ghosts
-                    const int cur0 = b->cur;
-                    b->cur = (src_of(s) == b->buf[0]) ? 0 : 1;
-                    st = lbg_halo_begin(b);
-                    if (st == LBG_OK) st = lbg_halo_complete(b);
-                    b->cur = cur0;
-                    if (st != LBG_OK) break;
+                if (st == LBG_OK && F[steps] > dl_next) {
+                    st = download(dl_next, F[steps]);
+                    dl_next = F[steps];
                 }
-                st = sweep_planes(b, fl, src_of(s), dst_of(s), std::min(F[s], nz), nz, cs);
-                if (st == LBG_OK) st = sweep_planes(b, fl, src_of(s), dst_of(s), 0, std::min(s, nz), cs);
-                F[s] = nz;
+            } else {
+                // the last slab: every step completes the domain, the seam planes included
+                for (int s = 1; s <= steps && st == LBG_OK; ++s) {
+                    if (zcomm) {  // step s-1's planes 0 and nz-1 into the neighbours' z ghosts
+                        const int cur0 = b->cur;
+                        b->cur = (src_of(s) == b->buf[0]) ? 0 : 1;
+                        st = lbg_halo_begin(b);
+                        if (st == LBG_OK) st = lbg_halo_complete(b);
+                        b->cur = cur0;
+                        if (st != LBG_OK) break;
+                    }
+                    st = sweep_planes(b, fl, src_of(s), dst_of(s), std::min(F[s], nz), nz, cs);
+                    if (st == LBG_OK) st = sweep_planes(b, fl, src_of(s), dst_of(s), 0, std::min(s, nz), cs);
+                    F[s] = nz;
+                }
+                if (st == LBG_OK && dl_next < nz) st = download(dl_next, nz);
+                if (st == LBG_OK) st = download(0, std::min(steps, nz));
             }
-            if (st == LBG_OK && dl_next < nz) st = download(dl_next, nz);
-            if (st == LBG_OK) st = download(0, std::min(steps, nz));
         }
-    }
+        return st;
+    };
+    const lbg_status st = schedule();
     // drain every stream of the job before touching the host buffer or the block again
     cudaError_t e1 = cudaStreamSynchronize(dl), e2 = cudaStreamSynchronize(pk), e3 = cudaStreamSynchronize(up),
                 e4 = cudaStreamSynchronize(cs);
