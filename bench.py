@@ -849,11 +849,14 @@ def run_lbg(args):
     if rank == 0:
         if N == 1 and not args.no_coupled:
             try:
-                # the reference's own parallelism lever: 2x2x2 blocks, one worker thread each
-                # (host DEM per block in parallel), same blocks/workers for the reference run
-                workers = min(8, os.cpu_count() or 8)
+                # the reference's own parallelism lever: blocks with one worker thread each (host
+                # DEM per block in parallel) — 2x2x4 / 16 workers on a host with >= 16 CPUs (one
+                # polling worker per CPU; 8.6-11 ms vs 11.6-11.7 for 2x2x2 / 8, profiles/
+                # r02_c3blocks4.log), else 2x2x2; the same blocks/workers for the reference run
+                cpus = os.cpu_count() or 8
+                blocks, workers = ((2, 2, 4), 16) if cpus >= 16 else ((2, 2, 2), min(8, cpus))
                 out["coupled_step"] = coupled_step(args.coupled_steps, not args.no_cpu_baseline, ref_steps=1,
-                                                   blocks=(2, 2, 2), workers=workers)
+                                                   blocks=blocks, workers=workers)
                 single = coupled_step(args.coupled_steps, False)
                 out["coupled_step"]["single_block"] = {k: single[k] for k in (
                     "ms_per_step", "categories_ms_per_step", "gpu_side_ms_per_step", "fused_force_mode")}

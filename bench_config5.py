@@ -44,9 +44,20 @@ def main():
                     help="scratch: reference semantics, bitwise PARITY partials; fused: per-particle sums "
                          "inside the PSM kernel (tolerance); both: one run each, scratch first")
     ap.add_argument("--mode", choices=["weak", "strong"], default="weak")
-    ap.add_argument("--blocks-per-gpu", type=int, default=4,
-                    help="x-slab blocks per GPU (consecutive ids), one host worker each: spreads the host DEM")
+    ap.add_argument("--blocks-per-gpu", type=int, default=0,
+                    help="x-slab blocks per GPU (consecutive ids), one host worker each: spreads the host DEM "
+                         "(0: weak 4; strong one worker per host CPU, the largest power of two <= CPUs / GPUs, "
+                         "at most 64 blocks in all — profiles/r02_c5blocks*.log)")
     args = ap.parse_args()
+    if args.blocks_per_gpu <= 0:
+        if args.mode == "strong":
+            per = max(1, (os.cpu_count() or 4) // args.gpus)
+            bpg = 1
+            while 2 * bpg <= per and 2 * bpg * args.gpus <= 64:
+                bpg *= 2
+            args.blocks_per_gpu = bpg
+        else:
+            args.blocks_per_gpu = 4
     os.environ["LBDEM_GPU_SPREAD"] = "1"
     os.environ["LBDEM_GPU_HOST_MIRROR"] = "0"
     os.environ["LBDEM_GPU_BLOCKS_PER_DEVICE"] = str(args.blocks_per_gpu)

@@ -39,12 +39,15 @@ class SpinPhaseScheduler final : public partition::Scheduler {
 public:
     /// spin_us: how long an idle thread polls before it blocks
     /// pin_stride > 0: worker w pinned to CPU (w * pin_stride) mod the CPU count (A/B)
-    /// Spinning needs a CPU per spinning thread: with more threads (workers + the main thread)
-    /// than CPUs this process may run on, a polling thread would hold the CPU a worker with
-    /// work is waiting for (config 3 with 16 workers on 16 CPUs: ~100 ms per step instead of
-    /// ~10), so the scheduler then blocks right away, like the reference's.
+    /// Spinning needs a CPU per spinning thread: a polling thread on an oversubscribed host
+    /// holds the CPU a worker with work is waiting for (config 3 with 16 workers and the main
+    /// thread all polling on 16 CPUs: ~100 ms per step instead of ~10). So the workers poll
+    /// only when each can have a CPU of this process's affinity mask, and the main thread
+    /// only when there is one more; otherwise they block right away, like the reference's.
     explicit SpinPhaseScheduler(int workers, int spin_us = 2000, int pin_stride = 0)
-        : nw_(workers), spin_(std::chrono::microseconds(workers + 1 <= usable_cpus() ? spin_us : 0)) {
+        : nw_(workers),
+          spin_(std::chrono::microseconds(workers <= usable_cpus() ? spin_us : 0)),
+          spin_main_(std::chrono::microseconds(workers + 1 <= usable_cpus() ? spin_us : 0)) {
         threads_.reserve(workers);
         for (int w = 0; w < workers; ++w) threads_.emplace_back([this, w] { worker_loop(w); });
         const int ncpu = static_cast<int>(std::thread::hardware_concurrency());
@@ -75,7 +78,7 @@ public:
             epoch_.fetch_add(1, std::memory_order_release);
         }
         cv_work_.notify_all();
-        if (!spin_until([&] { return remaining_.load(std::memory_order_acquire) == 0; })) {
+        if (!spin_until([&] { return remaining_.load(std::memory_order_acquire) == 0; }, spin_main_)) {
             std::unique_lock<std::mutex> lock(m_);
             cv_main_.wait(lock, [&] { return remaining_.load(std::memory_order_acquire) == 0; });
         }
@@ -99,15 +102,16 @@ public:
     }
 
     bool spinning() const { return spin_.count() > 0; }
+    bool main_spinning() const { return spin_main_.count() > 0; }
 
 private:
     template <class Pred>
-    bool spin_until(Pred&& done) const {
+    bool spin_until(Pred&& done, std::chrono::steady_clock::duration budget) const {
         const auto t0 = std::chrono::steady_clock::now();
         for (int i = 0;; ++i) {
             if (done()) return true;
             LBDEM_CPU_RELAX();
-            if ((i & 255) == 255 && std::chrono::steady_clock::now() - t0 > spin_) return done();
+            if ((i & 255) == 255 && std::chrono::steady_clock::now() - t0 > budget) return done();
         }
     }
 
@@ -118,7 +122,7 @@ private:
             auto ready = [&] {
                 return stop_.load(std::memory_order_acquire) || epoch_.load(std::memory_order_acquire) > seen;
             };
-            if (!spin_until(ready)) {
+            if (!spin_until(ready, spin_)) {
                 std::unique_lock<std::mutex> lock(m_);
                 cv_work_.wait(lock, ready);
             }
@@ -153,7 +157,8 @@ private:
     std::atomic<int> remaining_{0};
     std::atomic<bool> stop_{false};
     std::exception_ptr error_;
-    std::chrono::steady_clock::duration spin_;
+    std::chrono::steady_clock::duration spin_;       // workers' poll budget
+    std::chrono::steady_clock::duration spin_main_;  // the main thread's
 };
 
 }  // namespace lbdem::gpu

@@ -67,13 +67,16 @@ int main() {
     // and the contract still holds on the blocking path
     {
         const int ncpu = lbdem::gpu::SpinPhaseScheduler::usable_cpus();
-        lbdem::gpu::SpinPhaseScheduler over(ncpu, 2000);
-        if (over.spinning()) return 8;
+        lbdem::gpu::SpinPhaseScheduler full(ncpu, 2000);  // a CPU per worker: workers poll, main blocks
+        if (!full.spinning() || full.main_spinning()) return 11;
+        lbdem::gpu::SpinPhaseScheduler over(ncpu + 1, 2000);
+        if (over.spinning() || over.main_spinning()) return 8;
         std::vector<std::atomic<int>> seen(2 * ncpu);
         for (int p = 0; p < 50; ++p) over.run_phase(2 * ncpu, [&](int b) { seen[b].fetch_add(1); });
+        for (int p = 0; p < 50; ++p) full.run_phase(2 * ncpu, [&](int b) { seen[b].fetch_add(1); });
         for (auto& v : seen)
-            if (v.load() != 50) return 9;
-        if (ncpu >= 2 && !lbdem::gpu::SpinPhaseScheduler(ncpu - 1, 2000).spinning()) return 10;
+            if (v.load() != 100) return 9;
+        if (ncpu >= 2 && !lbdem::gpu::SpinPhaseScheduler(ncpu - 1, 2000).main_spinning()) return 10;
     }
     std::printf("ok\n");
     return 0;
