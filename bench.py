@@ -349,6 +349,34 @@ def coupled_sweep_roofline(steps=10, warmup=3, cfg=None, n=256, label="config 3 
                 bc_ms += ev[0].elapsed_time(ev[1])
                 sweep_ms += ev[1].elapsed_time(ev[2])
         blk.sync()
+        # K3 mapping (lbg_map: snapshot H2D + binning + map_col_kernel + segment lists) and K4
+        # PARITY reduction (lbg_reduce_hydro: walk kernel + partials D2H + unpacking), each
+        # timed on its own after the sweeps: CUDA events on the block stream for the mapping,
+        # host wall clock for the reduction call (it returns the partials to the host)
+        import ctypes as C
+        from paper_2303_11811_b200 import lbg as abi
+        lib = abi.load()
+        map_ms, red_ms = [], []
+        for _ in range(5):
+            ev[0].record(stream)
+            blk.map(snaps)
+            ev[1].record(stream)
+            ev[1].synchronize()
+            map_ms.append(ev[0].elapsed_time(ev[1]))
+        blk.sync()
+        cap = len(rows) + 16
+        hp_out = (abi.HydroPartial * cap)()
+        nout = C.c_int()
+        for _ in range(5):
+            blk.sweep(p, box)  # refills the scratch the reduction consumes (and clears)
+            blk.sync()
+            t0 = time.perf_counter()
+            lbdem.check(lib.lbg_reduce_hydro(blk.h, abi.REDUCE_PARITY, hp_out, cap, C.byref(nout)))
+            red_ms.append((time.perf_counter() - t0) * 1e3)
+        map_ms.sort()
+        red_ms.sort()
+        aux = {"mapping_ms": round(map_ms[len(map_ms) // 2], 4), "reduce_hydro_wall_ms": round(red_ms[len(red_ms) // 2], 4),
+               "partials": nout.value}
         if os.environ.get("AB_REDUCE"):
             # wall time of lbg_reduce_hydro (PARITY) after a sweep refilled the scratch:
             # kernels + D2H + host unpacking of the partials, through the raw C-ABI call
@@ -378,8 +406,15 @@ def coupled_sweep_roofline(steps=10, warmup=3, cfg=None, n=256, label="config 3 
     kernels = ("K1 sweep_box_kernel over the fluid segments + K12 coupled_unified_pipe_kernel over the "
                "covered-segment list" if split else
                "K12 coupled_unified_pipe_kernel (fluid, one-entry and two-entry segments in one kernel)")
+    # K3 mapping against HBM: 9 B per cell (count + btot, written for every cell) + 12 B per entry
+    # (id 4, b 8; + the 4-byte entry-0 snapshot index) — an issue-bound kernel, so the fraction
+    # says how far it is from streaming, not what bounds it
+    map_bytes = 9 * cells + 12 * (n1 + 2 * n2) + 4 * (n1 + n2)
+    aux["mapping_algorithmic_bytes"] = map_bytes
+    aux["mapping_frac_of_hbm"] = round(map_bytes / (aux["mapping_ms"] / 1e3) / 1e9 / peak, 4)
     return {"workload": label,
             "kernels": kernels, "covered_segment_fraction": None if cov_frac is None else round(cov_frac, 4),
+            **aux,
             "cells": cells, "one_entry_cells": n1, "two_entry_cells": n2,
             "algorithmic_bytes_per_step": algo, "sweep_ms": round(sweep_ms, 4), "bc_ms": round(bc_ms / steps, 4),
             "mlups": round(cells / (sweep_ms / 1e3) / 1e6, 1),

@@ -41,7 +41,7 @@ constexpr int kJobSlots = 3;
 
 // staging slot [q][zc][jj][ii] (zc < nzc, jj < py, ii < nx + 2: the reference layout's rows of
 // planes z0 .. z0 + nzc - 1, ghost rows and columns included) -> device rows of `dev`
-__global__ void __launch_bounds__(128) slab_unpack_kernel(double* __restrict__ dev, const double* __restrict__ stg,
+__global__ void __launch_bounds__(128) job_unpack_kernel(double* __restrict__ dev, const double* __restrict__ stg,
                                                           Layout L, int z0, int nzc) {
     const int w = L.nx + 2;
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(128) slab_unpack_kernel(double* __restrict__ d
 }
 
 // the reverse for the download: interior cells from `fin`, the x/y ghost cells from `gh`
-__global__ void __launch_bounds__(128) slab_pack_kernel(const double* __restrict__ fin, const double* __restrict__ gh,
+__global__ void __launch_bounds__(128) job_pack_kernel(const double* __restrict__ fin, const double* __restrict__ gh,
                                                         double* __restrict__ stg, Layout L, int z0, int nzc) {
     const int w = L.nx + 2;
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -171,7 +171,7 @@ extern "C" lbg_status lbg_run_host(lbg_block b, const lbg_fluid* fl, double* hos
             LBG_CUDA(cudaEventRecord(ev, cs));
             LBG_CUDA(cudaStreamWaitEvent(pk, ev, 0));
             if (dn_piece >= kJobSlots) LBG_CUDA(cudaStreamWaitEvent(pk, b->job_ev[3][slot], 0));
-            slab_pack_kernel<<<dim3(gx, (unsigned)L.py, (unsigned)(kQ * nzc)), 128, 0, pk>>>(fin, A, b->job_dn[slot], L,
+            job_pack_kernel<<<dim3(gx, (unsigned)L.py, (unsigned)(kQ * nzc)), 128, 0, pk>>>(fin, A, b->job_dn[slot], L,
                                                                                           a, nzc);
             LBG_LAUNCH_CHECK();
             LBG_CUDA(cudaEventRecord(b->job_ev[2][slot], pk));
@@ -199,7 +199,7 @@ extern "C" lbg_status lbg_run_host(lbg_block b, const lbg_fluid* fl, double* hos
                                          sizeof(double) * nzc * run, cudaMemcpyHostToDevice, up));
             LBG_CUDA(cudaEventRecord(b->job_ev[0][slot], up));
             LBG_CUDA(cudaStreamWaitEvent(cs, b->job_ev[0][slot], 0));
-            slab_unpack_kernel<<<dim3(gx, (unsigned)L.py, (unsigned)(kQ * nzc)), 128, 0, cs>>>(A, b->job_up[slot], L, z0,
+            job_unpack_kernel<<<dim3(gx, (unsigned)L.py, (unsigned)(kQ * nzc)), 128, 0, cs>>>(A, b->job_up[slot], L, z0,
                                                                                              nzc);
             LBG_LAUNCH_CHECK();
             LBG_CUDA(cudaEventRecord(b->job_ev[1][slot], cs));
