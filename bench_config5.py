@@ -47,13 +47,14 @@ def main():
     ap.add_argument("--blocks-per-gpu", type=int, default=0,
                     help="x-slab blocks per GPU (consecutive ids), one host worker each: spreads the host DEM "
                          "(0: weak 4; strong one worker per host CPU, the largest power of two <= CPUs / GPUs, "
-                         "at most 64 blocks in all — profiles/r02_c5blocks*.log)")
+                         "at most 16 per GPU — profiles/r02_c5blocks*.log)")
     args = ap.parse_args()
     if args.blocks_per_gpu <= 0:
         if args.mode == "strong":
             per = max(1, (os.cpu_count() or 4) // args.gpus)
             bpg = 1
-            while 2 * bpg <= per and 2 * bpg * args.gpus <= 64:
+            # (at most 16 per GPU: 32 slabs of the 1024 x 512 x 512 bed did not fit one GPU)
+            while 2 * bpg <= per and 2 * bpg <= 16:
                 bpg *= 2
             args.blocks_per_gpu = bpg
         else:
