@@ -62,7 +62,8 @@ SELF = "not suites_checked and not variants_checked"
 
 
 def test_parity_suites_checked():
-    _run(["test_gpu_checked.py", "test_gpu_parity.py", "test_gpu_aa.py", "test_gpu_reference_cases.py"], k=SELF)
+    _run(["test_gpu_checked.py", "test_gpu_parity.py", "test_gpu_aa.py", "test_gpu_reference_cases.py", "test_gpu_job.py"],
+         k=SELF)
 
 
 def test_dropin_suites_checked():
