@@ -642,13 +642,19 @@ struct WalkQuad {
 // cells' fields at once, and a group prefix over the lanes (rows in order) places the row's
 // keys. Fewer instructions than the cell walk but a full load latency per row step: measured
 // slower on config 3 (432 vs 263 us), so the cell walk is the default.
-template <int kRegs, bool kRows, int kKeys>
+// kGroups: particles per warp (4 groups of 8 lanes, default; or 1 group of 32 lanes, for
+// blocks whose particles do not fill the GPU: a quarter of the walk steps per particle, so the
+// latency-bound chain of dependent cell loads is 4x shorter where there are too few warps to
+// hide it; the replay then serves one particle per instruction).
+template <int kRegs, bool kRows, int kKeys, int kGroups = kWalkGroups>
 __global__ void __maxnreg__(kRegs) walk_chain_kernel(const WalkArgs a) {
-    __shared__ unsigned keys_all[kWalkWarps][kWalkGroups][kKeys];
-    __shared__ double terms_all[kWalkWarps][kWalkGroups][32][7];
+    constexpr int kL = 32 / kGroups;  // lanes per particle
+    constexpr int kBatch = 4 * kL;    // entries per replay batch (4 per lane)
+    __shared__ unsigned keys_all[kWalkWarps][kGroups][kKeys];
+    __shared__ double terms_all[kWalkWarps][kGroups][kBatch][7];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int grp = lane >> 3, gl = lane & 7;
-    const long long pw = (long long)(blockIdx.x * kWalkWarps + w) * kWalkGroups;
+    const int grp = lane / kL, gl = lane % kL;
+    const long long pw = (long long)(blockIdx.x * kWalkWarps + w) * kGroups;
     if (pw >= a.n) return;  // warp-uniform
     const int p = (int)pw + grp;
     const bool valid = p < a.n;
@@ -684,7 +690,7 @@ __global__ void __maxnreg__(kRegs) walk_chain_kernel(const WalkArgs a) {
     const bool nonempty = hi[0] >= lo[0] && hi[1] >= lo[1] && hi[2] >= lo[2];
     const int ex = nonempty ? hi[0] - lo[0] + 1 : 1, ey = nonempty ? hi[1] - lo[1] + 1 : 1;
     const long long total = nonempty ? (long long)ex * ey * (hi[2] - lo[2] + 1) : 0;
-    const unsigned gmask = 0xffu << (8 * grp);
+    const unsigned gmask = kL == 32 ? 0xffffffffu : ((1u << kL) - 1u) << (kL * grp);
     const unsigned lt = ((1u << lane) - 1u) & gmask;
     double sum = 0.0, comp = 0.0;
     bool any = false;
@@ -693,12 +699,12 @@ __global__ void __maxnreg__(kRegs) walk_chain_kernel(const WalkArgs a) {
     // keys: box-local (di, dj, dk) packed in 10 bits each when the box allows (no division to
     // recover the cell in pass 2), else the cell index
     const bool packed = ex <= 1024 && ey <= 1024 && hi[2] - lo[2] + 1 <= 1024;
-    // each lane's next cells (t = step * 32 + u * 8 + lane-in-group) as running coordinates:
-    // fetch() is called for consecutive steps and advances them by 32 cells (no division)
+    // each lane's next cells (t = step * kBatch + u * kL + lane-in-group) as running
+    // coordinates: fetch() is called for consecutive steps and advances them by kBatch cells
     int ci[4], cj[4], ck[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-        const unsigned tu = (unsigned)(u * 8 + gl), r = tu / (unsigned)ex;
+        const unsigned tu = (unsigned)(u * kL + gl), r = tu / (unsigned)ex;
         ci[u] = lo[0] + (int)(tu - r * (unsigned)ex);
         cj[u] = lo[1] + (int)(r % (unsigned)ey);
         ck[u] = lo[2] + (int)(r / (unsigned)ey);
@@ -717,7 +723,7 @@ __global__ void __maxnreg__(kRegs) walk_chain_kernel(const WalkArgs a) {
                 q.e0[u] = a.id0[c];
                 q.e1[u] = a.id1[c];
                 q.c[u] = packed ? (((long long)(ck[u] - lo[2]) << 20) | ((cj[u] - lo[1]) << 10) | (ci[u] - lo[0])) : c;
-                ci[u] += 32;
+                ci[u] += kBatch;
                 while (ci[u] > hi[0]) {
                     ci[u] -= ex;
                     if (++cj[u] > hi[1]) {
@@ -731,14 +737,14 @@ __global__ void __maxnreg__(kRegs) walk_chain_kernel(const WalkArgs a) {
     // pass 2 over the staged keys of every group (lockstep batches; groups with fewer idle)
     auto flush = [&]() {
         __syncwarp();
-        const int nb = (nk + 31) / 32;
+        const int nb = (nk + kBatch - 1) / kBatch;
         const int nbmax = (int)__reduce_max_sync(0xffffffffu, (unsigned)nb);
         long long gc[4];
         double gm[4][3];
         auto gather = [&](int b) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int e = b * 32 + u * 8 + gl;
+                const int e = b * kBatch + u * kL + gl;
                 gc[u] = -1;
                 gm[u][0] = gm[u][1] = gm[u][2] = 0.0;
                 if (e < nk) {
@@ -785,7 +791,7 @@ __global__ void __maxnreg__(kRegs) walk_chain_kernel(const WalkArgs a) {
                 const double r1 = ((double)(g.lo[1] + xj) + 0.5) - x1;
                 const double r2 = ((double)(g.lo[2] + xk) + 0.5) - x2;
                 const double* m = gm[u];
-                double* t = tw[u * 8 + gl];
+                double* t = tw[u * kL + gl];
                 t[0] = m[0];
                 t[1] = m[1];
                 t[2] = m[2];
@@ -798,7 +804,7 @@ __global__ void __maxnreg__(kRegs) walk_chain_kernel(const WalkArgs a) {
                 z[2] = 0.0;
             }
             __syncwarp();
-            const int ne = min(32, nk - b * 32);
+            const int ne = min(kBatch, nk - b * kBatch);
             gather(b + 1);  // the next batch's momenta in flight during the replay
             if (gl < 6) {
 #pragma unroll 4
@@ -826,7 +832,7 @@ __global__ void __maxnreg__(kRegs) walk_chain_kernel(const WalkArgs a) {
             any = any || ((b0 | b1) & gmask) != 0;
         }
     };
-    const long long steps = (total + 31) / 32;
+    const long long steps = (total + kBatch - 1) / kBatch;
     long long smax = steps;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) smax = max(smax, __shfl_xor_sync(0xffffffffu, smax, o));
@@ -898,7 +904,7 @@ __global__ void __maxnreg__(kRegs) walk_chain_kernel(const WalkArgs a) {
                 step(B);
             }
             const bool done = st + 2 >= smax;
-            if (done || __any_sync(0xffffffffu, nk > kKeys - 128)) flush();  // 2 steps add <= 128
+            if (done || __any_sync(0xffffffffu, nk > kKeys - 4 * kBatch)) flush();  // 2 steps add <= 4 kBatch
             if (done) break;
         }
     }
@@ -1460,7 +1466,16 @@ lbg_status lbg_reduce_hydro(lbg_block b, int mode, lbg_hydro_partial* out, int c
                 rows = 2.0 * R + 3.0 <= 16.0;
             }
             const unsigned grid = (unsigned)((n + per_cta - 1) / per_cta);
-            if (rows)
+            // one particle per warp (32 lanes) for lists shorter than LBG_WALK_ONE_BELOW
+            // (default 0: off): a 4x shorter chain of dependent cell loads per particle
+            static const int one_below = [] {
+                const char* e = std::getenv("LBG_WALK_ONE_BELOW");
+                return e ? std::atoi(e) : 0;
+            }();
+            if (!rows && n < one_below)
+                walk_chain_kernel<128, false, 1024, 1><<<(unsigned)((n + kWalkWarps - 1) / kWalkWarps), 32 * kWalkWarps, 0,
+                                                          b->stream>>>(a);
+            else if (rows)
                 walk_chain_kernel<128, true, 512><<<grid, 32 * kWalkWarps, 0, b->stream>>>(a);
             else if (regs >= 128)
                 walk_chain_kernel<128, false, kWalkKeys><<<grid, 32 * kWalkWarps, 0, b->stream>>>(a);
