@@ -34,6 +34,7 @@
 #include <vector>
 
 #include "lbg_internal.cuh"
+#include "lbg_job_schedule.hpp"
 
 namespace lbg {
 
@@ -155,87 +156,67 @@ extern "C" lbg_status lbg_run_host(lbg_block b, const lbg_fluid* fl, double* hos
     auto dst_of = [&](int s) { return (s & 1) ? B : A; };
     const unsigned gx = (unsigned)((w + 127) / 128);
 
-    // F[s]: step s is done on [s, F[s]) (F[0]: the uploaded planes)
-    std::vector<int> F(steps + 1);
-    for (int s = 0; s <= steps; ++s) F[s] = s;
-    F[0] = 0;
-    int dl_next = steps;  // the next final plane to download (main phase)
-    int dn_piece = 0;
-
-    auto download = [&](int z0, int z1) -> lbg_status {
-        for (int a = z0; a < z1; a += H) {
-            const int nzc = std::min(H, z1 - a);
-            const int slot = dn_piece % kJobSlots;
-            cudaEvent_t ev;  // the final step is done on [a, a + nzc)
-            if (lbg_status s = fresh_event(ev)) return s;
-            LBG_CUDA(cudaEventRecord(ev, cs));
-            LBG_CUDA(cudaStreamWaitEvent(pk, ev, 0));
-            if (dn_piece >= kJobSlots) LBG_CUDA(cudaStreamWaitEvent(pk, b->job_ev[3][slot], 0));
-            job_pack_kernel<<<dim3(gx, (unsigned)L.py, (unsigned)(kQ * nzc)), 128, 0, pk>>>(fin, A, b->job_dn[slot], L,
-                                                                                          a, nzc);
-            LBG_LAUNCH_CHECK();
-            LBG_CUDA(cudaEventRecord(b->job_ev[2][slot], pk));
-            LBG_CUDA(cudaStreamWaitEvent(dl, b->job_ev[2][slot], 0));
-            for (int q = 0; q < kQ; ++q)
-                LBG_CUDA(cudaMemcpyAsync(host + ((size_t)q * L.pz + a + 1) * run, b->job_dn[slot] + (size_t)q * nzc * run,
-                                         sizeof(double) * nzc * run, cudaMemcpyDeviceToHost, dl));
-            LBG_CUDA(cudaEventRecord(b->job_ev[3][slot], dl));
-            ++dn_piece;
-        }
+    int dn_piece = 0, up_chunk = 0;
+    // one download piece (<= H planes of the final step, done on the compute stream so far)
+    auto download = [&](int a, int nzc) -> lbg_status {
+        const int slot = dn_piece % kJobSlots;
+        cudaEvent_t ev;  // the final step is done on [a, a + nzc)
+        if (lbg_status s = fresh_event(ev)) return s;
+        LBG_CUDA(cudaEventRecord(ev, cs));
+        LBG_CUDA(cudaStreamWaitEvent(pk, ev, 0));
+        if (dn_piece >= kJobSlots) LBG_CUDA(cudaStreamWaitEvent(pk, b->job_ev[3][slot], 0));
+        job_pack_kernel<<<dim3(gx, (unsigned)L.py, (unsigned)(kQ * nzc)), 128, 0, pk>>>(fin, A, b->job_dn[slot], L, a,
+                                                                                      nzc);
+        LBG_LAUNCH_CHECK();
+        LBG_CUDA(cudaEventRecord(b->job_ev[2][slot], pk));
+        LBG_CUDA(cudaStreamWaitEvent(dl, b->job_ev[2][slot], 0));
+        for (int q = 0; q < kQ; ++q)
+            LBG_CUDA(cudaMemcpyAsync(host + ((size_t)q * L.pz + a + 1) * run, b->job_dn[slot] + (size_t)q * nzc * run,
+                                     sizeof(double) * nzc * run, cudaMemcpyDeviceToHost, dl));
+        LBG_CUDA(cudaEventRecord(b->job_ev[3][slot], dl));
+        ++dn_piece;
         return LBG_OK;
     };
-
-    // the whole schedule is enqueued by `schedule`; whatever it returns, every stream of the
-    // job is drained below before the host buffer is handed back (no copy may still target it)
-    auto schedule = [&]() -> lbg_status {
-        const int nchunks = (nz + H - 1) / H;
-        lbg_status st = LBG_OK;
-        for (int c = 0; c < nchunks && st == LBG_OK; ++c) {
-            const int z0 = c * H, z1 = std::min(nz, z0 + H), nzc = z1 - z0;
-            const int slot = c % kJobSlots;
-            if (c >= kJobSlots) LBG_CUDA(cudaStreamWaitEvent(up, b->job_ev[1][slot], 0));  // slot unpacked
-            for (int q = 0; q < kQ; ++q)
-                LBG_CUDA(cudaMemcpyAsync(b->job_up[slot] + (size_t)q * nzc * run, host + ((size_t)q * L.pz + z0 + 1) * run,
-                                         sizeof(double) * nzc * run, cudaMemcpyHostToDevice, up));
-            LBG_CUDA(cudaEventRecord(b->job_ev[0][slot], up));
-            LBG_CUDA(cudaStreamWaitEvent(cs, b->job_ev[0][slot], 0));
-            job_unpack_kernel<<<dim3(gx, (unsigned)L.py, (unsigned)(kQ * nzc)), 128, 0, cs>>>(A, b->job_up[slot], L, z0,
-                                                                                             nzc);
-            LBG_LAUNCH_CHECK();
-            LBG_CUDA(cudaEventRecord(b->job_ev[1][slot], cs));
-            F[0] = z1;
-            if (z1 < nz) {
-                for (int s = 1; s <= steps && st == LBG_OK; ++s) {
-                    const int nf = z1 - s;
-                    if (nf > F[s]) {
-                        st = sweep_planes(b, fl, src_of(s), dst_of(s), F[s], nf, cs);
-                        F[s] = nf;
-                    }
-                }
-                if (st == LBG_OK && F[steps] > dl_next) {
-                    st = download(dl_next, F[steps]);
-                    dl_next = F[steps];
-                }
-            } else {
-                // the last slab: every step completes the domain, the seam planes included
-                for (int s = 1; s <= steps && st == LBG_OK; ++s) {
-                    if (zcomm) {  // step s-1's planes 0 and nz-1 into the neighbours' z ghosts
-                        const int cur0 = b->cur;
-                        b->cur = (src_of(s) == b->buf[0]) ? 0 : 1;
-                        st = lbg_halo_begin(b);
-                        if (st == LBG_OK) st = lbg_halo_complete(b);
-                        b->cur = cur0;
-                        if (st != LBG_OK) break;
-                    }
-                    st = sweep_planes(b, fl, src_of(s), dst_of(s), std::min(F[s], nz), nz, cs);
-                    if (st == LBG_OK) st = sweep_planes(b, fl, src_of(s), dst_of(s), 0, std::min(s, nz), cs);
-                    F[s] = nz;
-                }
-                if (st == LBG_OK && dl_next < nz) st = download(dl_next, nz);
-                if (st == LBG_OK) st = download(0, std::min(steps, nz));
-            }
-        }
+    // one upload slab: H2D into a staging slot on `side`, re-pitched into A on the compute stream
+    auto upload = [&](int z0, int nzc) -> lbg_status {
+        const int slot = up_chunk % kJobSlots;
+        if (up_chunk >= kJobSlots) LBG_CUDA(cudaStreamWaitEvent(up, b->job_ev[1][slot], 0));  // slot unpacked
+        for (int q = 0; q < kQ; ++q)
+            LBG_CUDA(cudaMemcpyAsync(b->job_up[slot] + (size_t)q * nzc * run, host + ((size_t)q * L.pz + z0 + 1) * run,
+                                     sizeof(double) * nzc * run, cudaMemcpyHostToDevice, up));
+        LBG_CUDA(cudaEventRecord(b->job_ev[0][slot], up));
+        LBG_CUDA(cudaStreamWaitEvent(cs, b->job_ev[0][slot], 0));
+        job_unpack_kernel<<<dim3(gx, (unsigned)L.py, (unsigned)(kQ * nzc)), 128, 0, cs>>>(A, b->job_up[slot], L, z0, nzc);
+        LBG_LAUNCH_CHECK();
+        LBG_CUDA(cudaEventRecord(b->job_ev[1][slot], cs));
+        ++up_chunk;
+        return LBG_OK;
+    };
+    // step s-1's planes 0 and nz-1 into the neighbours' z ghosts (NCCL halo on step s-1's buffer)
+    auto seam = [&](int s) -> lbg_status {
+        const int cur0 = b->cur;
+        b->cur = (src_of(s) == b->buf[0]) ? 0 : 1;
+        lbg_status st = lbg_halo_begin(b);
+        if (st == LBG_OK) st = lbg_halo_complete(b);
+        b->cur = cur0;
         return st;
+    };
+
+    // the whole schedule (lbg_job_schedule.hpp) is enqueued by `schedule`; whatever it returns,
+    // every stream of the job is drained below before the host buffer is handed back (no copy
+    // may still target it)
+    auto schedule = [&]() -> lbg_status {
+        for (const job::Item& it : job::schedule(nz, steps, H, zcomm)) {
+            lbg_status st = LBG_OK;
+            switch (it.op) {
+                case job::Op::Upload: st = upload(it.z0, it.z1 - it.z0); break;
+                case job::Op::Sweep: st = sweep_planes(b, fl, src_of(it.s), dst_of(it.s), it.z0, it.z1, cs); break;
+                case job::Op::Seam: st = seam(it.s); break;
+                case job::Op::Download: st = download(it.z0, it.z1 - it.z0); break;
+            }
+            if (st != LBG_OK) return st;
+        }
+        return LBG_OK;
     };
     const lbg_status st = schedule();
     // drain every stream of the job before touching the host buffer or the block again
