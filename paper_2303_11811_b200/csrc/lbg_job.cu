@@ -31,6 +31,7 @@
 // exactly the operations of the whole-block sweep, so the result is bitwise that of
 // upload + steps x (sweep + swap) + download (tests/test_gpu_job.py).
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "lbg_internal.cuh"
@@ -206,7 +207,13 @@ extern "C" lbg_status lbg_run_host(lbg_block b, const lbg_fluid* fl, double* hos
     // every stream of the job is drained below before the host buffer is handed back (no copy
     // may still target it)
     auto schedule = [&]() -> lbg_status {
-        for (const job::Item& it : job::schedule(nz, steps, H, zcomm)) {
+        // LBG_JOB_TAIL=k: the last slab uploaded in pieces of H / k planes (A/B; default 0, whole
+        // slabs: measured no faster at 512^3, 20 steps — profiles/r02_ab_job.txt)
+        static const int tail = [] {
+            const char* e = std::getenv("LBG_JOB_TAIL");
+            return e ? std::atoi(e) : 0;
+        }();
+        for (const job::Item& it : job::schedule(nz, steps, H, zcomm, tail)) {
             lbg_status st = LBG_OK;
             switch (it.op) {
                 case job::Op::Upload: st = upload(it.z0, it.z1 - it.z0); break;

@@ -25,7 +25,11 @@ struct Item {
     int z0, z1;  // plane range
 };
 
-inline std::vector<Item> schedule(int nz, int steps, int slab, bool seam_halo) {
+// tail_split: the last slab's planes are uploaded in pieces of max(1, H / tail_split) — the
+// planes whose final step waits for the last upload (the last piece plus the 2 x steps seam
+// cone) are what goes down after the upload has ended, so a thinner last piece shortens that
+// D2H-only tail (0 or 1: whole slabs throughout)
+inline std::vector<Item> schedule(int nz, int steps, int slab, bool seam_halo, int tail_split = 0) {
     std::vector<Item> ops;
     if (nz <= 0 || steps < 0) return ops;
     const int H = std::max(1, std::min(slab, nz));
@@ -36,9 +40,17 @@ inline std::vector<Item> schedule(int nz, int steps, int slab, bool seam_halo) {
     for (int s = 0; s <= steps; ++s) F[s] = s;
     F[0] = 0;
     int dl_next = steps;  // the next final plane to download in the main phase
-    const int nchunks = (nz + H - 1) / H;
-    for (int c = 0; c < nchunks; ++c) {
-        const int z0 = c * H, z1 = std::min(nz, z0 + H);
+    std::vector<int> ends;  // upload chunk ends
+    const int tail0 = tail_split > 1 && nz > H ? nz - H : nz;
+    for (int z = H; z < tail0; z += H) ends.push_back(z);
+    if (tail0 < nz) {
+        if (ends.empty() || ends.back() != tail0) ends.push_back(tail0);
+        const int hs = std::max(1, H / tail_split);
+        for (int z = tail0 + hs; z < nz; z += hs) ends.push_back(z);
+    }
+    ends.push_back(nz);
+    for (size_t c = 0; c < ends.size(); ++c) {
+        const int z0 = c == 0 ? 0 : ends[c - 1], z1 = ends[c];
         ops.push_back({Op::Upload, 0, z0, z1});
         F[0] = z1;
         if (z1 < nz) {

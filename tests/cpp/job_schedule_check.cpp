@@ -17,8 +17,8 @@
 using lbg::job::Item;
 using lbg::job::Op;
 
-static int check(int nz, int steps, int slab, bool seam) {
-    const std::vector<Item> ops = lbg::job::schedule(nz, steps, slab, seam);
+static int check(int nz, int steps, int slab, bool seam, int tail = 0) {
+    const std::vector<Item> ops = lbg::job::schedule(nz, steps, slab, seam, tail);
     const int H = slab < 1 ? 1 : (slab > nz ? nz : slab);
     std::vector<int> val[2] = {std::vector<int>(nz, -1), std::vector<int>(nz, -1)};  // step held, -1 none
     std::vector<int> uploaded(nz, 0), downloaded(nz, 0), queued(nz, 0);
@@ -85,18 +85,19 @@ int main() {
     for (int nz = 1; nz <= 40; ++nz)
         for (int steps = 0; steps <= 24; ++steps)
             for (int slab : {1, 2, 3, 4, 5, 7, 8, 16, 40, 64})
-                for (int seam = 0; seam <= 1; ++seam) {
-                    if (seam && nz < 1) continue;
-                    const int r = check(nz, steps, slab, seam != 0);
-                    ++cases;
-                    if (r) {
-                        std::printf("fail %d: nz=%d steps=%d slab=%d seam=%d\n", r, nz, steps, slab, seam);
-                        return r;
+                for (int seam = 0; seam <= 1; ++seam)
+                    for (int tail : {0, 4}) {
+                        const int r = check(nz, steps, slab, seam != 0, tail);
+                        ++cases;
+                        if (r) {
+                            std::printf("fail %d: nz=%d steps=%d slab=%d seam=%d tail=%d\n", r, nz, steps, slab, seam,
+                                        tail);
+                            return r;
+                        }
                     }
-                }
     for (int steps : {0, 1, 20, 64})  // the benchmark's shape
         for (int seam = 0; seam <= 1; ++seam)
-            if (int r = check(512, steps, 16, seam != 0)) {
+            if (int r = check(512, steps, 16, seam != 0, 4)) {
                 std::printf("fail %d: nz=512 steps=%d\n", r, steps);
                 return r;
             }
