@@ -46,7 +46,7 @@ def main():
     ap.add_argument("--mode", choices=["weak", "strong"], default="weak")
     ap.add_argument("--blocks-per-gpu", type=int, default=0,
                     help="x-slab blocks per GPU (consecutive ids), one host worker each: spreads the host DEM "
-                         "(0: weak 4; strong one worker per host CPU, the largest power of two <= CPUs / GPUs, "
+                         "(0: weak up to 8 within the host CPUs; strong one worker per host CPU, the largest power of two <= CPUs / GPUs, "
                          "at most 16 per GPU — profiles/r02_c5blocks*.log)")
     args = ap.parse_args()
     if args.blocks_per_gpu <= 0:
@@ -58,7 +58,14 @@ def main():
                 bpg *= 2
             args.blocks_per_gpu = bpg
         else:
-            args.blocks_per_gpu = 4
+            # weak: up to 8 x-slab blocks per GPU within the host's CPUs (1 GPU: 23-31 ms per
+            # step with 8 vs 33 with 4 and 28-34 with 16, whose thin slabs cost more sweep —
+            # profiles/r02_c5weak_ab.log)
+            per = max(1, (os.cpu_count() or 4) // args.gpus)
+            bpg = 1
+            while 2 * bpg <= min(8, per):
+                bpg *= 2
+            args.blocks_per_gpu = bpg
     os.environ["LBDEM_GPU_SPREAD"] = "1"
     os.environ["LBDEM_GPU_HOST_MIRROR"] = "0"
     os.environ["LBDEM_GPU_BLOCKS_PER_DEVICE"] = str(args.blocks_per_gpu)
