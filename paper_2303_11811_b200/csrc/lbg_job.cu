@@ -27,7 +27,9 @@
 // is about one PCIe direction's transfer of the field plus the download of the last ~2 x steps
 // planes (the seam cone), instead of the sum of both directions.
 //
-// The sweeps are K1 (sweep_planes -> sweep_box_kernel) on plane ranges: every interior cell gets
+// The op sequence is lbg_job_schedule.hpp's (host-only; tests/test_job_schedule.py replays it
+// against these double-buffer rules for 40,000 cases). The sweeps are K1 (sweep_planes ->
+// sweep_box_kernel) on plane ranges: every interior cell gets
 // exactly the operations of the whole-block sweep, so the result is bitwise that of
 // upload + steps x (sweep + swap) + download (tests/test_gpu_job.py).
 #include <algorithm>
