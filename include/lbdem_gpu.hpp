@@ -205,6 +205,13 @@ public:
         check(lbg_fill_periodic(b_, p, full ? 1 : 0));
     }
     void swap() { check(lbg_swap(b_)); }
+    /// Simulation::run(steps) (sim.cpp:702-704) of a periodic fluid block on a host PdfField in
+    /// the reference layout (`host`, pinned for overlap), in place: lbg_run_host's pipelined
+    /// upload / sweeps / download; NumericError as the reference's end-of-sweep check.
+    void run_host(const lbm::FluidParams& p, double* host, int steps, int slab_planes = 0) {
+        const lbg_fluid f = to_fluid(p);
+        check(lbg_run_host(b_, &f, host, steps, slab_planes, nullptr));
+    }
 
     std::vector<psm::HydroPartial> finalize_hydro_forces(int mode = -1) {
         if (mode < 0) mode = fused_ ? LBG_REDUCE_FAST : LBG_REDUCE_PARITY;
